@@ -1,0 +1,22 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line(
+        "markers", "gpu: needs a CUDA device (B200) and the built extension")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import numpy as np
+    here = os.path.join(ROOT, "tests", "golden")
+    return {name: np.load(os.path.join(here, f"{name}.npz"))
+            for name in ("tables", "meshes", "operator", "heat",
+                         "trajectories")}
