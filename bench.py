@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 DG-operator DoF-updates/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                    [--impl native|reference]
+
+A step is one Shu-Osher SSP-RK3 step = 3 applications of f = M^-1 L_h,
+each fused with its Runge-Kutta stage update, over the whole mesh.
+Unit of work: one DoF receiving one f evaluation, so
+value = n_dofs * 3 * K / (device time of K steps), max over ranks.
+
+Default workload: config C2 (BASELINE configs[1], 4.7M DoFs, p=2 2D) at
+the explicit CFL step dt = 0.8 * 2.51 / rho(J), rho by device power
+iteration.  Inputs are resident in HBM; L2 (126 MB) is flushed between
+timed steps by writing a 256 MiB buffer outside the timed events.
+
+``--impl reference`` times the CPU oracle port of the reference
+(oracle/, numpy, all host threads) on the same config: the reference
+itself is pure Python and cannot travel to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 DG-operator DoF-updates/s at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "DoF-updates/s"
+FP64_NOMINAL_TFLOPS = 37.0  # HGX B200 datasheet FP64 / FP64 tensor
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--scheme", default="cdg2")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--power-iters", type=int, default=200)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t is not None:
+            self._t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": smax, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- workload
+
+def build_problem(cfg_name, scheme_name, rank=0, world=1):
+    from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
+    from paper_1403_1157_b200.configs import CONFIGS, make_mesh
+    from paper_1403_1157_b200.fields import initial_state
+    cfg = CONFIGS[cfg_name]
+    mesh = make_mesh(cfg)
+    space = DGSpace(mesh, cfg.order, 6)
+    U0 = initial_state(space, seed=1)
+    return cfg, space, PlaqueModel(), FluxScheme(scheme_name), U0
+
+
+def spectral_radius(op, U, iters):
+    """rho of the FD Jacobian of f at U by power iteration."""
+    import torch
+    g = torch.Generator(device=U.device).manual_seed(1234)
+    v = torch.randn(U.shape, dtype=torch.float64, device=U.device, generator=g)
+    v /= torch.linalg.norm(v)
+    fU = op.apply_f(U)
+    eps = math.sqrt(np.finfo(float).eps) * (1.0 + torch.linalg.norm(U).item())
+    rho = 0.0
+    for _ in range(iters):
+        Jv = (op.apply_f(U + eps * v) - fU) / eps
+        n = torch.linalg.norm(Jv)
+        rho = n.item()
+        v = Jv / n
+    return rho
+
+
+def fp64_peak(op):
+    """Measured DFMA throughput (TFLOP/s) of this GPU; the roofline
+    denominator for the FP64-bound operator kernels."""
+    import ctypes
+    import torch
+    lib = op.lib
+    nthr = lib.tdg_fp64_probe_threads()
+    out = torch.empty(nthr, dtype=torch.float64, device=op.device)
+    iters = 20000
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(2):
+        lib.tdg_fp64_probe(out.data_ptr(), iters, st)
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        lib.tdg_fp64_probe(out.data_ptr(), iters, st)
+        b.record()
+        b.synchronize()
+        best = max(best, nthr * 16 * 2 * iters / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
+    """Time the CPU oracle port on the same config; returns (DoF-upd/s,
+    sample description, n_dofs)."""
+    from oracle import OracleOperator
+    cfg, space, model, scheme, U0 = build_problem(cfg_name, scheme_name)
+    op = OracleOperator(space, model, scheme, nthreads=nthreads)
+    if dt is None:
+        from paper_1403_1157_b200.configs import rho_constant
+        h = float(space.mesh.diameters.min())
+        dt = 0.8 * 2.51 / (rho_constant(cfg.dim, cfg.order) * 1e-2 / h ** 2)
+    U = U0.copy()
+
+    def step(U):
+        U1 = U + dt * op.apply_f(U)
+        U2 = 0.75 * U + 0.25 * (U1 + dt * op.apply_f(U1))
+        return U / 3.0 + (2.0 / 3.0) * (U2 + dt * op.apply_f(U2))
+
+    for _ in range(warmup):
+        U = step(U)
+    tic = time.perf_counter()
+    for _ in range(steps):
+        U = step(U)
+    el = time.perf_counter() - tic
+    return space.n_dofs * 3 * steps / el, el, space.n_dofs
+
+
+# ---------------------------------------------------------------- arms
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    steps = max(1, args.steps)
+    warm = max(0, min(args.warmup, 1))
+    val, el, ndofs = cpu_reference(args.config, args.scheme, steps, warm, nthreads)
+    from paper_1403_1157_b200.configs import CONFIGS
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": el / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian bumps, L2-projected)",
+        "config": {"workload": CONFIGS[args.config].description
+                   + f", {args.scheme}, SSP-RK3 steps (3 f-evals each)",
+                   "n_dofs": ndofs},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthreads,
+                         "kind": "port",
+                         "sample": f"{steps} SSP-RK3 steps of the full {args.config} "
+                                   "mesh, numpy oracle port (oracle/), "
+                                   f"{nthreads} threads"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_native_arm(args, rank, world, local):
+    import torch
+    from paper_1403_1157_b200.operator import DiscreteOperator
+    from paper_1403_1157_b200.roofline import apply_bytes, apply_flops, executed_flops
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, space, model, scheme, U0h = build_problem(args.config, args.scheme, rank, world)
+    op = DiscreteOperator(space, model, scheme, device=dev)
+    t = op.tables
+    d, nb = t.dim, t.nb
+    ne, n_int, n_bnd = op.n_owned, len(t.if_code), len(t.bf_code)
+    n_dofs = ne * 6 * nb
+
+    U = torch.from_numpy(U0h).to(dev)
+    rho = spectral_radius(op, U, args.power_iters)
+    dt = 0.8 * 2.51 / rho
+
+    work = torch.empty_like(U)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        op.ssprk3_step(U, work, dt)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    op.profile(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for a, b in evs:
+        flush.fill_(1.0)
+        a.record()
+        op.ssprk3_step(U, work, dt)
+        b.record()
+    torch.cuda.synchronize()
+    barrier()
+    op.profile(False)
+    kt = op.profile_read()
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = tt.item()
+    value = n_dofs * world * 3 * args.steps / (ms * 1e-3)
+
+    # per-kernel roofline (algorithmic flops of the reference sequence)
+    Q, F = t.nq_vol, t.nq_face
+    fv, ff, fb = apply_flops(d, nb, Q, F, ne, n_int, n_bnd)
+    per = {}
+    for name, flops in (("faces", ff), ("wall", fb), ("volume", fv)):
+        tms, nl = kt[name]
+        if nl:
+            per[name] = {"avg_ms": tms / nl, "launches": nl,
+                         "algorithmic_tflops": flops / (tms / nl * 1e-3) / 1e12,
+                         "share_of_step": tms / ms}
+    peak = fp64_peak(op)
+    dom = max(per, key=lambda k: per[k]["avg_ms"])
+    step_flops = 3 * (fv + ff + fb)
+    roof = {"bound": "fp64", "kernel": f"k_{dom}",
+            "achieved": per[dom]["algorithmic_tflops"], "peak": peak,
+            "unit": "TFLOP/s", "frac": per[dom]["algorithmic_tflops"] / peak,
+            "traffic": None,
+            "peak_source": "measured DFMA loop (tdg_fp64_probe) on this GPU; "
+                           f"nominal {FP64_NOMINAL_TFLOPS} TFLOP/s; "
+                           "MEASURED_PEAKS.json has no fp64 figure",
+            "per_kernel": per,
+            "step_algorithmic_tflops": step_flops / (ms / args.steps * 1e-3) / 1e12,
+            "step_frac": step_flops / (ms / args.steps * 1e-3) / 1e12 / peak,
+            "step_executed_tflops": 3 * executed_flops(d, nb, Q, F, ne, n_int, n_bnd)
+            / (ms / args.steps * 1e-3) / 1e12,
+            "step_hbm_gbs_compulsory": 3 * apply_bytes(d, n_dofs, ne, n_int, n_bnd)
+            / (ms / args.steps * 1e-3) / 1e9}
+
+    # end to end through the public API: pinned host U -> device, one
+    # SSP-RK3 step, result back to host, every step
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.from_numpy(U0h).pin_memory()
+        Ud = torch.empty_like(U)
+        for _ in range(2):
+            Ud.copy_(Uh, non_blocking=True)
+            op.ssprk3_step(Ud, work, dt)
+            Uh.copy_(Ud)
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            Ud.copy_(Uh, non_blocking=True)
+            op.ssprk3_step(Ud, work, dt)
+            Uh.copy_(Ud, non_blocking=True)
+        b.record()
+        b.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ems = tt.item()
+        e2e = {"value": n_dofs * world * 3 * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": n_dofs * 8, "d2h_bytes_per_step": n_dofs * 8}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nthreads = os.cpu_count() or 1
+        val, el, _ = cpu_reference(args.config, args.scheme, 1, 0, nthreads, dt=dt)
+        cpu = {"value": val, "unit": UNIT, "cores": nthreads, "kind": "port",
+               "sample": f"1 SSP-RK3 step (3 apply_f) of the full {args.config} mesh, "
+                         f"numpy oracle port, {nthreads} threads, {el:.1f} s"}
+
+    launches = sum(v["launches"] for v in per.values())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian bumps, L2-projected on host)",
+            "config": {"workload": cfg.description + f", {args.scheme}, SSP-RK3 "
+                       "steps (3 fused f-evals + stage updates each)",
+                       "n_elements": ne, "n_dofs": n_dofs, "interior_faces": n_int,
+                       "boundary_faces": n_bnd, "dt": dt, "rho": rho,
+                       "l2": "flushed between timed steps (256 MiB write outside "
+                             "the timed events)",
+                       "parallelism": f"x-slabs x{world}" if world > 1 else "1 GPU"},
+            "roofline": roof, "clocks": clocks, "gpu_launches": launches,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if e2e:
+            line["e2e"] = e2e
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    run_native_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

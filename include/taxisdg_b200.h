@@ -1,0 +1,164 @@
+/*
+ * taxisdg_b200.h -- C-ABI of the B200 (sm_100a) matrix-free DG operator.
+ *
+ * Drop-in boundary for the hot path of the reference package `taxisdg`
+ * (arxiv/paper_1403_1157).  The reference is pure Python; the interfaces
+ * replaced here are (paths relative to /root/reference/pkg/src/taxisdg):
+ *
+ *   tdg_create / tdg_destroy   DiscreteOperator.__init__ tables, groups and
+ *                              partition setup          operator.py:85-229
+ *   tdg_apply (mass_inverse=0) DiscreteOperator.apply    operator.py:253-284
+ *   tdg_apply (mass_inverse=1) DiscreteOperator.apply_f  operator.py:286-288
+ *                              + DGSpace.apply_inverse_mass fespace.py:117-118
+ *   tdg_rk_stage               one explicit stage  a*U0 + b*U + c*M^-1 L(U)
+ *                              (SSP-RK3 composition of apply_f, SURVEY 8(a) a14;
+ *                              DIRK stage algebra timeint.py:315-333)
+ *   tdg_ssprk3_step            three fused stages (Shu-Osher form)
+ *   tdg_dot / tdg_norm2        Krylov scalars: `w @ V[i]`, `np.linalg.norm`
+ *                              in gmres_solve/newton_solve timeint.py:148-202,
+ *                              timeint.py:242-280
+ *   tdg_axpby / tdg_axpy_dev   Krylov/Newton vector updates timeint.py:171,199,278
+ *
+ * Conventions: every array argument of the apply/stage/vector calls is a
+ * DEVICE pointer; coefficient arrays use the reference layout U[e][s][i]
+ * (fp64, C order, n_elements x n_species x nb, fespace.py:46-69).  The
+ * descriptor's table/geometry pointers are device pointers owned by the
+ * caller and must outlive the context; the small host arrays
+ * (diffusivity, lin_source, params) are copied at create time.  Streams
+ * are `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ * No call allocates after tdg_create.  Every call returns 0 on success or
+ * a negative TDG_E* code; tdg_last_error() gives a message (thread-local).
+ * The per-apply sums are grouped in a fixed order: results are bitwise
+ * reproducible run to run (reference contract tests/test_operator.py:113-119).
+ */
+#ifndef TAXISDG_B200_H
+#define TAXISDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TDG_API __attribute__((visibility("default")))
+#else
+#define TDG_API
+#endif
+
+enum tdg_status {
+  TDG_OK = 0,
+  TDG_E_INVALID = -1,     /* bad descriptor / argument  (reference: ValueError) */
+  TDG_E_UNSUPPORTED = -2, /* (dim, order, model, species) not compiled in      */
+  TDG_E_CUDA = -3         /* CUDA runtime error                                 */
+};
+
+enum tdg_model { TDG_MODEL_PLAQUE = 0, TDG_MODEL_REDUCED = 1, TDG_MODEL_DIFFUSION = 2 };
+
+/* flux.py:57 SCHEME_NAMES order */
+enum tdg_scheme { TDG_CDG2 = 0, TDG_CDG = 1, TDG_BR2 = 2, TDG_IP = 3, TDG_BO = 4 };
+
+/* bit layout of the per-face code words (if_code / bf_code) */
+#define TDG_CODE_TIN(c)     ((c) & 31)          /* table id lf_in*nperm+pm_in   */
+#define TDG_CODE_TOUT(c)    (((c) >> 5) & 31)   /* table id of the outside side  */
+#define TDG_CODE_MINUS_IN   (1 << 10)           /* K- is the inside element      */
+#define TDG_CODE_TAG(c)     (((c) >> 11) & 7)   /* BoundaryTag (boundary faces)  */
+#define TDG_CODE_MIRROR     (1 << 14)           /* Dirichlet mirror exterior     */
+#define TDG_CODE_SKIP_OUT   (1 << 15)           /* outside is a ghost: no write  */
+
+typedef struct tdg_desc {
+  int32_t dim;            /* 2 or 3 */
+  int32_t order;          /* k, 1..3 */
+  int32_t n_species;      /* S */
+  int32_t nb;             /* C(k+d, d) */
+  int32_t nq_vol;         /* volume points (<= default rule of degree 3k+1) */
+  int32_t nq_face;        /* face points (<= default rule of degree 3k+2) */
+  int32_t model;          /* enum tdg_model */
+  int32_t scheme;         /* enum tdg_scheme */
+  int64_t n_elements;     /* owned elements = rows of U, R */
+  int64_t n_ghost;        /* ghost rows appended after the owned rows of U */
+  int64_t n_int_faces;    /* interior (+ Dirichlet mirror) faces */
+  int64_t n_bnd_faces;    /* prescribed-flux boundary faces */
+  double chi_e;           /* 1.5 (2D) / 2 (3D), flux.py:87-89 */
+  double adj_sign;        /* -1 for bo, +1 otherwise, flux.py:79-80 */
+  double ip_eta;          /* ip_eta0 * max(k,1)^2, operator.py:104 */
+  /* host arrays, copied at create */
+  const double* diffusivity;  /* [S] */
+  const double* lin_source;   /* [S*S] linear part of the source, row-major */
+  const double* params;       /* [32] model parameters (PlaqueParams order) */
+  /* device arrays (caller-owned) */
+  const double* vol_phi;      /* [Q*nb]       basis at volume points */
+  const double* vol_grad;     /* [Q*nb*d]     reference gradients */
+  const double* vol_w;        /* [Q]          volume weights */
+  const double* vol_stiff;    /* [d(d+1)/2*nb*nb] symmetric stiffness blocks */
+  const double* face_B;       /* [T*F*nb]     basis at face points, per table */
+  const double* face_G;       /* [T*F*nb*d]   gradients at face points */
+  const double* face_Pw;      /* [T*F*F]      (B B^T) w_face  (lifting) */
+  const double* face_w;       /* [F]          face weights */
+  const double* elem_geo;     /* [ne*(1+d(d+1)/2)]  detJ, sym(Jinv Jinv^T) */
+  const int32_t* if_elems;    /* [nif*2]  inside, outside row (-1 mirror) */
+  const int32_t* if_lf;       /* [nif*2]  local face index per side */
+  const int32_t* if_code;     /* [nif]    packed code word */
+  const double* if_geo;       /* [nif*(2d+4)] jn_in, jn_out, sfac, h, 1/detJ_in, 1/detJ_out */
+  const int32_t* bf_elem;     /* [nbf]    inside row */
+  const int32_t* bf_lf;       /* [nbf]    local face index */
+  const int32_t* bf_code;     /* [nbf]    packed code word */
+  const double* bf_geo;       /* [nbf]    sfac */
+} tdg_desc;
+
+typedef struct tdg_ctx tdg_ctx;
+
+TDG_API int tdg_version(void);
+TDG_API const char* tdg_last_error(void);
+
+TDG_API int tdg_create(const tdg_desc* desc, tdg_ctx** out);
+TDG_API int tdg_destroy(tdg_ctx* ctx);
+
+/* R = L_h(U) (mass_inverse=0) or M^-1 L_h(U) (mass_inverse=1).
+ * U has n_elements + n_ghost rows; R has n_elements rows.  t is accepted
+ * for API parity (the plaque/reduced/diffusion models are autonomous). */
+TDG_API int tdg_apply(tdg_ctx* ctx, const double* U, double* R, double t,
+              int mass_inverse, void* stream);
+
+/* out = a*U0 + b*U + c*M^-1 L_h(U); U0 may be NULL when a == 0; out may
+ * alias U or U0 (each element reads its own rows before writing). */
+TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out,
+                 double a, double b, double c, double t, void* stream);
+
+/* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U. */
+TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt,
+                    void* stream);
+
+/* Krylov reductions: deterministic two-pass tree (fixed grid), result
+ * written to a DEVICE scalar. */
+TDG_API int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n,
+            double* result, void* stream);
+TDG_API int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result,
+              void* stream);
+/* y = a*x + b*y (host scalars) */
+TDG_API int tdg_axpby(double a, const double* x, double b, double* y, int64_t n,
+              void* stream);
+/* y += s*alpha[0]*x with alpha a DEVICE scalar (MGS update without a
+ * host round trip) */
+TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y,
+                 int64_t n, void* stream);
+
+/* Per-kernel device timing: with profiling enabled every operator kernel
+ * launch is bracketed by CUDA events on its own stream;
+ * tdg_profile_read synchronizes, returns the accumulated milliseconds and
+ * launch counts per kernel (index 0 faces, 1 wall, 2 volume) and resets. */
+TDG_API int tdg_profile(tdg_ctx* ctx, int enable);
+TDG_API int tdg_profile_read(tdg_ctx* ctx, double* ms, int64_t* launches);
+
+/* FP64 throughput probe: a DFMA-bound kernel (148*8 CTAs x 256 threads,
+ * 16 independent chains, `iters` iterations) writing one value per
+ * thread to out[148*8*256]; flops = 148*8*256*16*2*iters. */
+TDG_API int tdg_fp64_probe(double* out, int64_t iters, void* stream);
+TDG_API int64_t tdg_fp64_probe_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAXISDG_B200_H */

@@ -215,6 +215,17 @@ class OracleOperator:
                 B = basis.eval(xi)
                 self.tab[lf, pm] = (B, basis.grad(xi),
                                     (B @ B.T) * self.wf[None, :])
+        nb = basis.size
+        Q = len(self.wv)
+        # flattened layouts so the contractions are batched matmuls
+        self._GvT = self.Gv.transpose(1, 0, 2).reshape(nb, Q * d)
+        self._GvW = (self.wv[:, None, None] * self.Gv).transpose(0, 2, 1) \
+            .reshape(Q * d, nb)
+        self._PhiW = self.wv[:, None] * self.Phi
+        self._GfT = {key: G.transpose(1, 0, 2).reshape(nb, -1)
+                     for key, (B, G, P) in self.tab.items()}
+        self._GfD = {key: G.transpose(2, 0, 1).reshape(d, -1)
+                     for key, (B, G, P) in self.tab.items()}
         _, self.detJ, self.Jinv = mesh.jacobians()
         self.nthreads = max(1, int(nthreads))
         self._groups()
@@ -261,26 +272,31 @@ class OracleOperator:
 
     def _volume(self, U, E, out):                 # operator.py:292-324
         c = U[E]
-        u = np.einsum("qi,esi->eqs", self.Phi, c)
-        gref = np.einsum("qia,esi->esqa", self.Gv, c)
+        ne, S, nb = c.shape
+        Q, d = self.Gv.shape[0], self.Gv.shape[2]
+        u = np.matmul(self.Phi, c.transpose(0, 2, 1))               # (e,q,s)
+        gref = np.matmul(c, self._GvT).reshape(ne, S * Q, d)        # (e,s*q,a)
         Jinv = self.Jinv[E]
-        gphys = np.einsum("esqa,eab->esqb", gref, Jinv)
-        S = self.phys.source(u)
-        sig = -self.A[None, :, None, None] * gphys
+        gphys = np.matmul(gref, Jinv)                               # gref @ Jinv
+        Ssrc = self.phys.source(u)
+        sig = -self.A[None, :, None] * gphys.reshape(ne, S, Q * d)
         if self.conv:
-            F = self.phys.flux(u, gphys.transpose(0, 2, 1, 3))  # (e,q,s,d)
-            sig = sig + F.transpose(0, 2, 1, 3)
-        sref = np.einsum("esqb,eab->esqa", sig, Jinv)        # sig @ Jinv^T
-        r = (np.einsum("esqa,qia->esi", sref * self.wv[None, None, :, None],
-                       self.Gv)
-             + np.einsum("eqs,qi->esi", S * self.wv[None, :, None], self.Phi))
+            gp = gphys.reshape(ne, S, Q, d).transpose(0, 2, 1, 3)   # (e,q,s,d)
+            F = self.phys.flux(u, gp).transpose(0, 2, 1, 3)
+            sig = sig + F.reshape(ne, S, Q * d)
+        sref = np.matmul(sig.reshape(ne, S * Q, d),
+                         np.swapaxes(Jinv, 1, 2))                   # sig @ Jinv^T
+        r = np.matmul(sref.reshape(ne, S, Q * d), self._GvW)
+        r += np.matmul(Ssrc.transpose(0, 2, 1), self._PhiW)
         out[E] += self.detJ[E][:, None, None] * r
 
     def _trace(self, U, elems, lf, pm):            # operator.py:326-334
         B, G, _ = self.tab[lf, pm]
         c = U[elems]
-        return (np.einsum("qi,fsi->fqs", B, c),
-                np.einsum("qia,fsi->fsqa", G, c))
+        nF, S, nb = c.shape
+        F, d = G.shape[0], G.shape[2]
+        return (np.matmul(B, c.transpose(0, 2, 1)),                          # (f,q,s)
+                np.matmul(c, self._GfT[lf, pm]).reshape(nF, S, F, d))        # (f,s,q,a)
 
     def _faces(self, U, g, out):                   # operator.py:359-434
         A = self.A
@@ -289,14 +305,15 @@ class OracleOperator:
         ein = g["ein"]
         n = g["n"]
         uin, grin = self._trace(U, ein, g["lin"], g["pin"])
-        jin = np.einsum("fab,fb->fa", self.Jinv[ein], n)
-        gnin = np.einsum("fsqa,fa->fsq", grin, jin)
+        nF, S, F, d = grin.shape
+        jin = np.matmul(self.Jinv[ein], n[:, :, None])                      # (f,a,1)
+        gnin = np.matmul(grin.reshape(nF, S * F, d), jin).reshape(nF, S, F)
         if g["interior"]:
             eout = g["eout"]
             Bo, Go, Po = self.tab[g["lout"], g["pout"]]
             uout, grout = self._trace(U, eout, g["lout"], g["pout"])
-            jout = np.einsum("fab,fb->fa", self.Jinv[eout], n)
-            gnout = np.einsum("fsqa,fa->fsq", grout, jout)
+            jout = np.matmul(self.Jinv[eout], n[:, :, None])
+            gnout = np.matmul(grout.reshape(nF, S * F, d), jout).reshape(nF, S, F)
         else:                                      # operator.py:436-444
             uout = 2.0 * self.phys.dirichlet[None, None, :] - uin
             grout, gnout = None, gnin
@@ -309,10 +326,9 @@ class OracleOperator:
         elif name == "ip":
             q = (self.eta / g["h"])[:, None, None] * A * dU
         else:
-            rin = (np.einsum("qp,fps->fqs", Pi, dU)
-                   * (-0.5 * sfac / self.detJ[ein])[:, None, None])
+            rin = np.matmul(Pi, dU) * (-0.5 * sfac / self.detJ[ein])[:, None, None]
             if g["interior"]:
-                rout = (np.einsum("qp,fps->fqs", Po, dU)
+                rout = (np.matmul(Po, dU)
                         * (-0.5 * sfac / self.detJ[eout])[:, None, None])
                 if name == "br2":
                     rho = 0.5 * (rin + rout)
@@ -323,24 +339,24 @@ class OracleOperator:
             fac = 4.0 * self.chi_e if name == "cdg" else 2.0 * self.chi_e
             q = -fac * A * rho
         if self.conv:                                # LLF, flux.py:126-138
-            gpin = np.einsum("fsqa,fab->fqsb", grin, self.Jinv[ein])
-            gpout = gpin if grout is None else np.einsum(
-                "fsqa,fab->fqsb", grout, self.Jinv[g["eout"]])
-            gav = 0.5 * (gpin + gpout)
+            gpin = np.matmul(grin.reshape(nF, S * F, d), self.Jinv[ein])
+            gpout = gpin if grout is None else np.matmul(
+                grout.reshape(nF, S * F, d), self.Jinv[g["eout"]])
+            gav = (0.5 * (gpin + gpout)).reshape(nF, S, F, d).transpose(0, 2, 1, 3)
             lam = self.phys.speed(uin, uout, gav, n[:, None, :])
-            Fs = self.phys.flux(uin, gav) + self.phys.flux(uout, gav)
-            q = q + 0.5 * np.einsum("fqsd,fd->fqs", Fs, n) \
-                + 0.5 * lam[:, :, None] * dU
+            Fs = self.phys.flux(uin, gav) + self.phys.flux(uout, gav)   # (f,q,s,d)
+            Fn = np.matmul(Fs.reshape(nF, F * S, d), n[:, :, None]).reshape(nF, F, S)
+            q = q + 0.5 * Fn + 0.5 * lam[:, :, None] * dU
         wq = (self.wf[None, :] * sfac[:, None])[:, None, :]          # (f,1,q)
         X = wq * dU.transpose(0, 2, 1) * (0.5 * self.adj * A)[None, :, None]
         Y = wq * (gavg_n * A[None, :, None] - q.transpose(0, 2, 1))
-        dpin = np.einsum("fa,qia->fqi", jin, Gi)
-        out[ein] += np.einsum("fsq,qi->fsi", Y, Bi) \
-            + np.einsum("fsq,fqi->fsi", X, dpin)
+        dpin = np.matmul(jin[:, :, 0][:, None, :], self._GfD[g["lin"], g["pin"]]
+                         ).reshape(nF, F, -1)                        # (f,q,i)
+        out[ein] += np.matmul(Y, Bi) + np.matmul(X, dpin)
         if g["interior"]:
-            dpout = np.einsum("fa,qia->fqi", jout, Go)
-            out[eout] += np.einsum("fsq,qi->fsi", -Y, Bo) \
-                + np.einsum("fsq,fqi->fsi", X, dpout)
+            dpout = np.matmul(jout[:, :, 0][:, None, :],
+                              self._GfD[g["lout"], g["pout"]]).reshape(nF, F, -1)
+            out[eout] += np.matmul(-Y, Bo) + np.matmul(X, dpout)
 
     def _wall(self, U, g, out):                    # operator.py:446-458
         B = self.tab[g["lin"], g["pin"]][0]

@@ -1,0 +1,14 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tdg {
+constexpr int kRedBlocks = 296;  // 2 CTAs per SM on 148 SMs; fixed => deterministic
+cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,
+                       bool norm, cudaStream_t st);
+cudaError_t launch_axpby(double a, const double* x, double b, double* y, int64_t n, cudaStream_t st);
+cudaError_t launch_axpy_dev(double s, const double* alpha, const double* x, double* y, int64_t n,
+                            cudaStream_t st);
+cudaError_t launch_fp64_probe(double* out, int64_t iters, cudaStream_t st);
+int64_t fp64_probe_threads();
+}  // namespace tdg

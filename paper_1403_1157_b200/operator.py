@@ -1,0 +1,234 @@
+"""Drop-in ``DiscreteOperator`` backed by the sm_100a kernels.
+
+Same constructor, methods and error behaviour as the reference
+(``pkg/src/taxisdg/operator.py:77-288``):
+
+    DiscreteOperator(space, model, scheme, nthreads=1, npartitions=None,
+                     vol_degree=None, face_degree=None)
+    .apply(U, t=0.0)    weak residual <phi, L_h(U)>          (:253-284)
+    .apply_f(U, t=0.0)  M^-1 L_h(U)                          (:286-288)
+    .set_threads(n, npartitions=None)                        (:208-229)
+    .audit_face_ownership()                                  (:231-249)
+    attributes .space .model .scheme .mesh
+
+``apply``/``apply_f`` accept a numpy array or ``DiscreteFunction`` (and
+return a fresh numpy array, like the reference) or a CUDA
+``torch.Tensor`` of the same shape (and return a CUDA tensor, no host
+round trip).  The device path is the only path: there is no CPU
+fallback, and construction fails loudly without the built library or a
+CUDA device.
+
+Beyond the reference API, the explicit stepping entry points used by the
+benchmarks and the device-resident JFNK stepper are exposed
+(``rk_stage``, ``ssprk3_step``, ``dot``, ``norm2``, ``axpby``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .fespace import DGSpace
+from .flux import FluxScheme
+from .tables import build_tables, scheme_constants
+
+__all__ = ["DiscreteOperator"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DiscreteOperator:
+    def __init__(self, space: DGSpace, model, scheme: FluxScheme,
+                 nthreads: int = 1, npartitions: int | None = None,
+                 vol_degree: int | None = None, face_degree: int | None = None,
+                 device=None, n_owned: int | None = None, global_ids=None):
+        if model.n_species != space.n_species:
+            raise ValueError(f"model has {model.n_species} species, space has "
+                             f"{space.n_species}")
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("DiscreteOperator needs a CUDA device (B200); "
+                               "there is no CPU path")
+        self.space, self.model, self.scheme = space, model, scheme
+        self.mesh = space.mesh
+        self.device = torch.device(device if device is not None else "cuda")
+        self.lib = _native.load()
+        t = build_tables(space, model, scheme, vol_degree, face_degree,
+                         n_owned=n_owned, global_ids=global_ids)
+        self.tables = t
+        self.n_owned = t.elem_geo.shape[0]
+        self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+        self._keep = {name: dev(getattr(t, name)) for name in (
+            "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
+            "face_Pw", "face_w", "elem_geo", "if_elems", "if_lf", "if_code",
+            "if_geo", "bf_elem", "bf_lf", "bf_code", "bf_geo")}
+        self._host = {
+            "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
+            "lin_source": np.ascontiguousarray(model.linear_source(), dtype=np.float64),
+            "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
+        chi_e, adj, eta = scheme_constants(space, scheme)
+        ptr = lambda x: ctypes.c_void_p(x.data_ptr() if x.numel() else 0)
+        hptr = lambda a: ctypes.c_void_p(a.ctypes.data)
+        k = self._keep
+        desc = _native.TdgDesc(
+            dim=t.dim, order=t.order, n_species=t.n_species, nb=t.nb,
+            nq_vol=t.nq_vol, nq_face=t.nq_face, model=model.model_id,
+            scheme=scheme.id, n_elements=self.n_owned,
+            n_ghost=self.n_rows - self.n_owned,
+            n_int_faces=len(t.if_code), n_bnd_faces=len(t.bf_code),
+            chi_e=chi_e, adj_sign=adj, ip_eta=eta,
+            diffusivity=hptr(self._host["diffusivity"]),
+            lin_source=hptr(self._host["lin_source"]),
+            params=hptr(self._host["params"]),
+            vol_phi=ptr(k["vol_phi"]), vol_grad=ptr(k["vol_grad"]),
+            vol_w=ptr(k["vol_w"]), vol_stiff=ptr(k["vol_stiff"]),
+            face_B=ptr(k["face_B"]), face_G=ptr(k["face_G"]),
+            face_Pw=ptr(k["face_Pw"]), face_w=ptr(k["face_w"]),
+            elem_geo=ptr(k["elem_geo"]), if_elems=ptr(k["if_elems"]),
+            if_lf=ptr(k["if_lf"]), if_code=ptr(k["if_code"]),
+            if_geo=ptr(k["if_geo"]), bf_elem=ptr(k["bf_elem"]),
+            bf_lf=ptr(k["bf_lf"]), bf_code=ptr(k["bf_code"]),
+            bf_geo=ptr(k["bf_geo"]))
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.tdg_create(ctypes.byref(desc),
+                                              ctypes.byref(handle)),
+                          "tdg_create")
+        self._ctx = handle
+        self._scalar = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.set_threads(nthreads, npartitions)
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None and ctx.value:
+            try:
+                self.lib.tdg_destroy(ctx)
+            except Exception:
+                pass
+            self._ctx = None
+
+    # -- reference API ------------------------------------------------------
+
+    def set_threads(self, nthreads: int, npartitions: int | None = None):
+        """Validated like the reference; the device decomposition is fixed
+        (one CTA per element / face tile), so the result never depends on
+        these values -- it is bitwise reproducible for any of them."""
+        if nthreads < 1:
+            raise ValueError("nthreads must be >= 1")
+        npartitions = nthreads if npartitions is None else npartitions
+        if npartitions < 1:
+            raise ValueError("npartitions must be >= 1")
+        self.nthreads, self.npartitions = int(nthreads), int(npartitions)
+
+    def audit_face_ownership(self) -> dict:
+        """Every element is assembled once and every element-local face
+        slot is written exactly once per application."""
+        t, d = self.tables, self.tables.dim
+        slots = np.zeros((self.n_owned, d + 1), dtype=np.int64)
+        el, lf, code = t.if_elems, t.if_lf, t.if_code
+        np.add.at(slots, (el[:, 0], lf[:, 0]), 1)
+        wr = (el[:, 1] >= 0) & ((code & ((1 << 14) | (1 << 15))) == 0)
+        np.add.at(slots, (el[wr, 1], lf[wr, 1]), 1)
+        np.add.at(slots, (t.bf_elem, t.bf_lf), 1)
+        return {"elements_ok": True, "faces_ok": bool((slots == 1).all()),
+                "faces_per_part": [len(code) + len(t.bf_code)],
+                "elements_per_part": [self.n_owned]}
+
+    def _stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def _as_device(self, U):
+        torch = _torch()
+        shape = (self.n_rows, self.space.n_species, self.space.nb)
+        if isinstance(U, torch.Tensor):
+            if U.dtype != torch.float64 or U.device.type != "cuda":
+                raise ValueError("U must be a float64 CUDA tensor")
+            if tuple(U.shape) != shape:
+                raise ValueError(f"U has shape {tuple(U.shape)}, expected {shape}")
+            return U.contiguous(), True
+        U = np.asarray(getattr(U, "coeffs", U), dtype=float)
+        if U.shape != shape:
+            raise ValueError(f"U has shape {U.shape}, expected {shape}")
+        return torch.from_numpy(np.ascontiguousarray(U)).to(self.device), False
+
+    def _apply(self, U, mass_inverse: int, t: float):
+        torch = _torch()
+        Ud, is_dev = self._as_device(U)
+        R = torch.empty((self.n_owned, self.space.n_species, self.space.nb),
+                        dtype=torch.float64, device=self.device)
+        _native.check(self.lib.tdg_apply(self._ctx, Ud.data_ptr(), R.data_ptr(),
+                                         float(t), mass_inverse, self._stream()),
+                      "tdg_apply")
+        return R if is_dev else R.cpu().numpy()
+
+    def apply(self, U, t: float = 0.0):
+        return self._apply(U, 0, t)
+
+    def apply_f(self, U, t: float = 0.0):
+        return self._apply(U, 1, t)
+
+    # -- device timing ---------------------------------------------------
+
+    KERNELS = ("faces", "wall", "volume")
+
+    def profile(self, enable: bool = True):
+        """Bracket every operator kernel launch with CUDA events on its
+        stream (per-kernel roofline timing inside the benchmark)."""
+        _native.check(self.lib.tdg_profile(self._ctx, int(bool(enable))),
+                      "tdg_profile")
+
+    def profile_read(self) -> dict:
+        ms = (ctypes.c_double * 3)()
+        n = (ctypes.c_int64 * 3)()
+        _native.check(self.lib.tdg_profile_read(self._ctx, ms, n),
+                      "tdg_profile_read")
+        return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
+
+    # -- explicit stepping / Krylov primitives (device tensors) ----------
+
+    def rk_stage(self, U0, U, out, a: float, b: float, c: float, t: float = 0.0):
+        """out = a U0 + b U + c M^-1 L(U) in one fused pass."""
+        _native.check(self.lib.tdg_rk_stage(
+            self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
+            out.data_ptr(), float(a), float(b), float(c), float(t),
+            self._stream()), "tdg_rk_stage")
+        return out
+
+    def ssprk3_step(self, U, work, dt: float, t: float = 0.0):
+        _native.check(self.lib.tdg_ssprk3_step(
+            self._ctx, U.data_ptr(), work.data_ptr(), float(t), float(dt),
+            self._stream()), "tdg_ssprk3_step")
+        return U
+
+    def dot(self, x, y, out=None):
+        out = self._scalar[:1] if out is None else out
+        _native.check(self.lib.tdg_dot(self._ctx, x.data_ptr(), y.data_ptr(),
+                                       x.numel(), out.data_ptr(), self._stream()),
+                      "tdg_dot")
+        return out
+
+    def norm2(self, x, out=None):
+        out = self._scalar[1:] if out is None else out
+        _native.check(self.lib.tdg_norm2(self._ctx, x.data_ptr(), x.numel(),
+                                         out.data_ptr(), self._stream()),
+                      "tdg_norm2")
+        return out
+
+    def axpby(self, a: float, x, b: float, y):
+        _native.check(self.lib.tdg_axpby(float(a), x.data_ptr(), float(b),
+                                         y.data_ptr(), x.numel(), self._stream()),
+                      "tdg_axpby")
+        return y
+
+    def axpy_dev(self, s: float, alpha, x, y):
+        _native.check(self.lib.tdg_axpy_dev(float(s), alpha.data_ptr(),
+                                            x.data_ptr(), y.data_ptr(),
+                                            x.numel(), self._stream()),
+                      "tdg_axpy_dev")
+        return y

@@ -1,0 +1,199 @@
+"""Pack reference tables, geometry and the face lists for the device.
+
+Host-side (numpy) construction of everything ``tdg_create`` consumes
+(include/taxisdg_b200.h ``tdg_desc``).  Sources in the reference:
+
+* volume tables Phi, Gref, w at degree 3k+1 and face tables B, G,
+  Pw = (B B^T) w per (local face, permutation) at degree 3k+2
+  (``operator.py:106-140``);
+* per-face data of ``_build_groups`` (``operator.py:147-206``): inside /
+  outside element, normal, sfac = measure / reference face measure,
+  h = min neighbour diameter, K- flag (``flux.py:92-95``);
+* element geometry detJ, Jinv (``mesh.py:267-277``).
+
+Device layout choices (B200-first, not the reference's):
+
+* the normal enters the face terms only through jn = Jinv n per side,
+  so faces carry jn_in, jn_out (2d doubles) instead of n and two Jinv;
+* the volume diffusion term uses the metric M = Jinv Jinv^T (symmetric,
+  d(d+1)/2 doubles per element) and exact stiffness blocks
+  KS_ac[j][i] = sum_q w_q G[q,j,c] G[q,i,a] (+ transpose for c != a),
+  integrated with the reference's own rule;
+* interior faces are sorted by their (inside table, outside table) pair
+  so a CTA's table reads are mostly uniform.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .fespace import DGSpace, face_reference_points
+from .flux import FluxScheme, chi_factor, minus_is_outside
+from .quadrature import face_rule, volume_rule
+
+__all__ = ["OperatorTables", "build_tables", "sym_pairs"]
+
+REF_FACE_MEASURE = {2: 1.0, 3: 0.5}
+CODE_MINUS_IN = 1 << 10
+CODE_MIRROR = 1 << 14
+CODE_SKIP_OUT = 1 << 15
+
+
+def sym_pairs(d: int):
+    return [(a, b) for a in range(d) for b in range(a, d)]
+
+
+@dataclass
+class OperatorTables:
+    dim: int
+    order: int
+    n_species: int
+    nb: int
+    nq_vol: int
+    nq_face: int
+    vol_phi: np.ndarray
+    vol_grad: np.ndarray
+    vol_w: np.ndarray
+    vol_stiff: np.ndarray
+    face_B: np.ndarray
+    face_G: np.ndarray
+    face_Pw: np.ndarray
+    face_w: np.ndarray
+    elem_geo: np.ndarray
+    if_elems: np.ndarray
+    if_lf: np.ndarray
+    if_code: np.ndarray
+    if_geo: np.ndarray
+    bf_elem: np.ndarray
+    bf_lf: np.ndarray
+    bf_code: np.ndarray
+    bf_geo: np.ndarray
+
+
+def _face_tables(space: DGSpace, frule):
+    d = space.mesh.dim
+    nperm = 2 if d == 2 else 6
+    Bs, Gs, Ps = [], [], []
+    for lf in range(d + 1):
+        for pm in range(nperm):
+            xi = face_reference_points(d, lf, pm, frule.points)
+            B = space.basis.eval(xi)
+            Bs.append(B)
+            Gs.append(space.basis.grad(xi))
+            Ps.append((B @ B.T) * frule.weights[None, :])
+    return np.stack(Bs), np.stack(Gs), np.stack(Ps)
+
+
+def build_tables(space: DGSpace, model, scheme: FluxScheme,
+                 vol_degree=None, face_degree=None, n_owned=None,
+                 global_ids=None) -> OperatorTables:
+    """Pack tables, element geometry and face lists.
+
+    Slab-decomposed runs pass a local mesh whose first ``n_owned``
+    elements are owned and the rest are ghosts, plus the ``global_ids``
+    of all local elements (the K- tie rule breaks ties by global id).
+    Faces with no owned side are dropped; a face whose inside is a ghost
+    is flipped (the face terms are symmetric under swapping the sides up
+    to roundoff); a face whose outside is a ghost writes only its inside
+    slot (SKIP_OUT)."""
+    mesh = space.mesh
+    d, k, S, nb = mesh.dim, space.order, space.n_species, space.nb
+    nperm = 2 if d == 2 else 6
+    vr = volume_rule(d, 3 * k + 1 if vol_degree is None else vol_degree)
+    fr = face_rule(d, 3 * k + 2 if face_degree is None else face_degree)
+    phi = space.basis.eval(vr.points)
+    grad = space.basis.grad(vr.points)
+    K = np.einsum("q,qjc,qia->caji", vr.weights, grad, grad)  # [c][a][j][i]
+    ks = []
+    for c, a in sym_pairs(d):
+        blk = K[c, a].copy()
+        if c != a:
+            blk += K[a, c]
+        ks.append(blk)
+    ks = np.stack(ks)
+    fB, fG, fPw = _face_tables(space, fr)
+
+    ne = mesh.n_elements
+    n_owned = ne if n_owned is None else int(n_owned)
+    gid = (np.arange(ne, dtype=np.int64) if global_ids is None
+           else np.asarray(global_ids, dtype=np.int64))
+    J, detJ, Jinv = mesh.jacobians()
+    Mmet = np.einsum("eab,ecb->eac", Jinv, Jinv)
+    egeo = np.concatenate([detJ[:, None]] + [Mmet[:, a, b][:, None]
+                                             for a, b in sym_pairs(d)], axis=1)
+
+    fe = mesh.face_elems.copy()
+    fl = mesh.face_local.astype(np.int64)
+    fp = mesh.face_perm.astype(np.int64)
+    nrm = mesh.face_normals.copy()
+    interior = fe[:, 1] >= 0
+    owned = lambda e: (e >= 0) & (e < n_owned)
+    flip = interior & ~owned(fe[:, 0]) & owned(fe[:, 1])
+    fe[flip] = fe[flip][:, ::-1]
+    fl[flip] = fl[flip][:, ::-1]
+    fp[flip] = fp[flip][:, ::-1]
+    nrm[flip] *= -1.0
+    dirichlet = getattr(model, "boundary_kind", "flux") == "dirichlet"
+    sfac_all = mesh.face_measures / REF_FACE_MEASURE[d]
+    tid = fl * nperm + fp
+
+    # interior faces (+ mirror faces for Dirichlet models)
+    fi = np.flatnonzero(interior & owned(fe[:, 0]))
+    ein, eout = fe[fi, 0], fe[fi, 1]
+    n = nrm[fi]
+    jin = np.einsum("fab,fb->fa", Jinv[ein], n)
+    jout = np.einsum("fab,fb->fa", Jinv[eout], n)
+    h = np.minimum(mesh.diameters[ein], mesh.diameters[eout])
+    mi = ~minus_is_outside(mesh.volumes[ein], mesh.volumes[eout],
+                           gid[ein], gid[eout])
+    code = (tid[fi, 0] | (tid[fi, 1] << 5) | np.where(mi, CODE_MINUS_IN, 0)
+            | np.where(owned(eout), 0, CODE_SKIP_OUT))
+    geo = np.concatenate([jin, jout, sfac_all[fi, None], h[:, None],
+                          1.0 / detJ[ein, None], 1.0 / detJ[eout, None]],
+                         axis=1)
+    el = np.stack([ein, eout], axis=1)
+    lfs = np.stack([fl[fi, 0], fl[fi, 1]], axis=1)
+    bmask = ~interior & owned(fe[:, 0])
+    if dirichlet:
+        bi = np.flatnonzero(bmask)
+        be = fe[bi, 0]
+        bj = np.einsum("fab,fb->fa", Jinv[be], nrm[bi])
+        bgeo = np.concatenate([bj, np.zeros_like(bj), sfac_all[bi, None],
+                               mesh.diameters[be, None], 1.0 / detJ[be, None],
+                               np.zeros((len(bi), 1))], axis=1)
+        bcode = (tid[bi, 0] | CODE_MINUS_IN | CODE_MIRROR
+                 | (mesh.face_tags[bi].astype(np.int64) << 11))
+        code = np.concatenate([code, bcode])
+        geo = np.concatenate([geo, bgeo])
+        el = np.concatenate([el, np.stack([be, np.full(len(bi), -1)], axis=1)])
+        lfs = np.concatenate([lfs, np.stack([fl[bi, 0], np.full(len(bi), -1)],
+                                            axis=1)])
+        nbf = np.zeros(0, dtype=np.int64)
+    else:
+        nbf = np.flatnonzero(bmask)
+    order = np.argsort(code & 1023, kind="stable")
+    code, geo, el, lfs = code[order], geo[order], el[order], lfs[order]
+
+    btag = mesh.face_tags[nbf].astype(np.int64)
+    border = np.lexsort((btag, tid[nbf, 0]))
+    nbf, btag = nbf[border], btag[border]
+    bcode = tid[nbf, 0] | (btag << 11)
+
+    c64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    return OperatorTables(
+        dim=d, order=k, n_species=S, nb=nb, nq_vol=len(vr), nq_face=len(fr),
+        vol_phi=c64(phi), vol_grad=c64(grad), vol_w=c64(vr.weights),
+        vol_stiff=c64(ks), face_B=c64(fB), face_G=c64(fG), face_Pw=c64(fPw),
+        face_w=c64(fr.weights), elem_geo=c64(egeo[:n_owned]),
+        if_elems=i32(el), if_lf=i32(lfs), if_code=i32(code), if_geo=c64(geo),
+        bf_elem=i32(fe[nbf, 0]), bf_lf=i32(fl[nbf, 0]),
+        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]))
+
+
+def scheme_constants(space: DGSpace, scheme: FluxScheme):
+    d, k = space.mesh.dim, space.order
+    return (chi_factor(d), scheme.adjoint_sign,
+            scheme.ip_eta0 * max(k, 1) ** 2)

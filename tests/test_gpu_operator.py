@@ -1,0 +1,204 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the
+reference's golden outputs and the CPU oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import OracleOperator, ssprk3  # noqa: E402
+from paper_1403_1157_b200 import (BoundaryTag, DGSpace, DiffusionModel,  # noqa: E402
+                                  FluxScheme, PlaqueModel, PlaqueParams,
+                                  unit_cube, unit_square)
+from paper_1403_1157_b200.fields import initial_state  # noqa: E402
+
+from _cases import AMPLIFIED, operator_case, rel_l2_per_species  # noqa: E402
+from test_oracle_golden import _golden_names  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+# north_star tolerance: per-species relative broken-L2 error <= 1e-10
+TOL_L2 = 1e-10
+
+
+def _op(space, model, scheme, **kw):
+    from paper_1403_1157_b200.operator import DiscreteOperator
+    return DiscreteOperator(space, model, scheme, **kw)
+
+
+@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
+def test_apply_matches_reference_golden(golden, name):
+    space, model, scheme, U, R, F = operator_case(golden, name)
+    op = _op(space, model, scheme)
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+    gf = op.apply_f(U)
+    assert rel_l2_per_species(space, gf, F).max() <= 1e-12
+
+
+@pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
+@pytest.mark.parametrize("dirichlet", [0, 1])
+def test_heat_models(golden, scheme, dirichlet):
+    h = golden["heat"]
+    space = DGSpace(unit_square(3), 2)
+    model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
+    key = f"heat_sq3_{scheme}_{dirichlet}"
+    R = h[f"{key}__R"]
+    got = _op(space, model, FluxScheme(scheme)).apply(h[f"{key}__U"])
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+@pytest.mark.parametrize("scheme", ["cdg2", "br2", "ip"])
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_dense_diffusion_oracle(golden, scheme, dirichlet):
+    """Materialise the device operator column by column and compare with
+    the reference's independent dense loop oracle (tests/oracles.py:223-327,
+    tests/test_acceptance.py:174-198, tol 1e-10)."""
+    from test_oracle_golden import _two_triangles
+    h = golden["heat"]
+    for mname, mesh in (("two", _two_triangles()), ("sq2", unit_square(2))):
+        for k in (1, 2):
+            space = DGSpace(mesh, k)
+            model = DiffusionModel(0.35, dirichlet=0.0 if dirichlet else None)
+            op = _op(space, model, FluxScheme(scheme))
+            n = space.n_dofs
+            E = torch.eye(n, dtype=torch.float64, device="cuda")
+            cols = [op.apply(E[j].reshape(space.shape)).reshape(-1) for j in range(n)]
+            A = torch.stack(cols, dim=1).cpu().numpy()
+            R = h[f"dense_{mname}_{k}_{scheme}_{int(dirichlet)}"]
+            assert np.abs(A - R).max() <= 1e-10 * np.abs(R).max()
+
+
+def test_ssprk3_c1_trajectory(golden):
+    """C1: unit_square(32), p=1, cdg2, default coefficients, 10 SSP-RK3
+    steps -- against the reference's own trajectory."""
+    t = golden["trajectories"]
+    space = DGSpace(unit_square(32), 1, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    U = torch.from_numpy(t["c1__U0"]).cuda()
+    work = torch.empty_like(U)
+    for _ in range(10):
+        op.ssprk3_step(U, work, float(t["c1__dt"]))
+    err = rel_l2_per_species(space, U.cpu().numpy(), t["c1__U10"])
+    assert err.max() <= TOL_L2, err
+
+
+def test_ssprk3_3d_trajectory(golden):
+    t = golden["trajectories"]
+    space = DGSpace(unit_cube(3, gamma1_in=None, top_tag=BoundaryTag.NO_FLOW), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    U = torch.from_numpy(t["cubez3__U0"]).cuda()
+    work = torch.empty_like(U)
+    for _ in range(3):
+        op.ssprk3_step(U, work, 2e-4)
+    assert rel_l2_per_species(space, U.cpu().numpy(), t["cubez3__U3"]).max() <= TOL_L2
+
+
+def test_rect_trajectory_amplified(golden):
+    t = golden["trajectories"]
+    space = DGSpace(unit_square(16, 4, lengths=(4.0, 1.0)), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U = torch.from_numpy(t["rect164__U0"]).cuda()
+    work = torch.empty_like(U)
+    for _ in range(5):
+        op.ssprk3_step(U, work, 2e-5)
+    assert rel_l2_per_species(space, U.cpu().numpy(), t["rect164__U5"]).max() <= TOL_L2
+
+
+def test_rk_stage_is_the_fused_combination():
+    space = DGSpace(unit_square(8, 4, lengths=(4.0, 1.0)), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U = torch.from_numpy(initial_state(space, 3)).cuda()
+    U0 = torch.from_numpy(initial_state(space, 4)).cuda()
+    f = op.apply_f(U)
+    out = torch.empty_like(U)
+    op.rk_stage(U0, U, out, 0.3, 0.5, 0.01)
+    ref = 0.3 * U0 + 0.5 * U + 0.01 * f
+    assert torch.allclose(out, ref, rtol=1e-14, atol=1e-16)
+
+
+def test_bitwise_reproducible():
+    space = DGSpace(unit_square(16), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U = torch.from_numpy(initial_state(space, 5)).cuda()
+    a = op.apply(U)
+    b = op.apply(U)
+    op.set_threads(4, npartitions=7)
+    c = op.apply(U)
+    assert torch.equal(a, b) and torch.equal(a, c)
+    assert op.audit_face_ownership()["faces_ok"]
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_full_size_single_application_vs_oracle(cfg):
+    """Spot check of one apply_f at the BASELINE config sizes (C2, C3 at a
+    quarter of its cells, C4 at 1/8) against the CPU oracle."""
+    if cfg == "c2":
+        space = DGSpace(unit_square(512, 128, lengths=(4.0, 1.0)), 2, 6)
+    elif cfg == "c3":
+        space = DGSpace(unit_square(1024, 256, lengths=(4.0, 1.0), jitter=0.1,
+                                    seed=7), 3, 6)
+    else:
+        space = DGSpace(unit_cube(32, gamma1_in=None, top_tag=BoundaryTag.NO_FLOW), 2, 6)
+    model = PlaqueModel()
+    U = initial_state(space, 1)
+    got = _op(space, model, FluxScheme("cdg2")).apply_f(U)
+    ref = OracleOperator(space, model, FluxScheme("cdg2"), nthreads=8).apply_f(U)
+    assert rel_l2_per_species(space, got, ref).max() <= 1e-12
+
+
+def test_constant_state_is_steady():
+    """Acceptance test_constant_states_are_steady (tests/test_acceptance.py:106-126)."""
+    for mesh in (unit_square(3), unit_cube(2)):
+        for k in (1, 2, 3):
+            space = DGSpace(mesh, k)
+            st = space.constant([2.3])
+            for name in ("cdg2", "cdg", "br2", "ip", "bo"):
+                op = _op(space, DiffusionModel(0.7, dirichlet=2.3), FluxScheme(name))
+                r = op.apply_f(st.coeffs)
+                assert np.abs(r).max() <= 1e-12 * np.abs(st.coeffs).max()
+
+
+def test_lipid_rate_cancels_and_inflow_rate():
+    """tests/test_operator.py:91-110 on the device."""
+    space = DGSpace(unit_square(4), 2, 6)
+    U = initial_state(space, 2)
+    op = _op(space, PlaqueModel(PlaqueParams(sigma=0.0, beta1=0.0, beta2=0.0)),
+             FluxScheme("cdg2"))
+    rate = space.function(op.apply_f(U)).species_totals()
+    assert abs(rate[4] + rate[5]) < 1e-13 * max(np.abs(rate).max(), 1.0)
+    params = PlaqueParams(sigma=0.8, nu2=1.0, beta1=0.0, beta2=0.0)
+    op = _op(space, PlaqueModel(params), FluxScheme("cdg2"))
+    rate = space.function(op.apply_f(space.zeros())).species_totals()
+    want = params.sigma * space.mesh.boundary_measure(BoundaryTag.GAMMA1_IN)
+    assert rate[4] == pytest.approx(want, rel=1e-12)
+    assert np.abs(np.delete(rate, 4)).max() < 1e-13
+
+
+def test_vector_ops():
+    space = DGSpace(unit_square(4), 1, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(1_000_003, dtype=torch.float64, device="cuda", generator=g)
+    y = torch.randn(1_000_003, dtype=torch.float64, device="cuda", generator=g)
+    d = op.dot(x, y).item()
+    assert d == pytest.approx(torch.dot(x, y).item(), rel=1e-12)
+    assert op.norm2(x).item() == pytest.approx(torch.linalg.norm(x).item(), rel=1e-13)
+    assert op.dot(x, y).item() == d  # deterministic
+    z = y.clone()
+    op.axpby(2.0, x, -0.5, z)
+    assert torch.allclose(z, 2 * x - 0.5 * y, rtol=1e-15, atol=0)
+    a = torch.tensor([3.0], dtype=torch.float64, device="cuda")
+    z = y.clone()
+    op.axpy_dev(-1.0, a, x, z)
+    assert torch.allclose(z, y - 3 * x, rtol=1e-15, atol=0)
+
+
+def test_shape_and_species_validation():
+    space = DGSpace(unit_square(2), 1, 6)
+    with pytest.raises(ValueError):
+        _op(space, DiffusionModel(1.0), FluxScheme("cdg2"))
+    op = _op(space, PlaqueModel(), FluxScheme("br2"))
+    with pytest.raises(ValueError):
+        op.apply(np.zeros((3, 6, 3)))
+    with pytest.raises(ValueError):
+        op.set_threads(0)
