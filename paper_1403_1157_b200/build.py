@@ -16,8 +16,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtaxisdg_b200.so")
-SOURCES = ["capi.cu", "vecops.cu"]
-HEADERS = ["common.cuh", "kernels.cuh", "models.cuh", "vecops.cuh"]
+SOURCES = ["capi.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
+           "inst_diffusion.cu"]
+HEADERS = ["common.cuh", "ctx.cuh", "kernels.cuh", "kernels_fast.cuh", "models.cuh",
+           "vecops.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
@@ -46,17 +48,20 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    logs = []
+    objs, procs = [], []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
                "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                            stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
+    logs = []
+    for src, pr in procs:
+        out, _ = pr.communicate()
+        logs.append(out)
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{out}")
     tmp = LIB + ".tmp"
     cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            *objs, "-o", tmp, "--cudart", "static"]

@@ -1,20 +1,14 @@
-// C-ABI entry points (include/taxisdg_b200.h) and instantiation dispatch.
+// C-ABI entry points (include/taxisdg_b200.h).
 #include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
-#include <utility>
-#include <vector>
 
-#include "taxisdg_b200.h"
-#include "common.cuh"
-#include "kernels.cuh"
-#include "models.cuh"
-#include "vecops.cuh"
+#include "ctx.cuh"
 
 using namespace tdg;
 
-namespace {
+namespace tdg {
 
 thread_local std::string g_err;
 
@@ -27,114 +21,14 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(TDG_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-struct Impl {
-  int (*configure)(int nqv);
-  int (*run)(tdg_ctx*, const double* U, const double* U0, double* out, double a, double b,
-             double c, int mode, cudaStream_t st);
-  int max_nqv, max_nqf;
-};
-
-}  // namespace
-
-struct tdg_ctx {
-  tdg_desc d;
-  OpParams p;
-  double* fc = nullptr;    // face-contribution slots [ne][d+1][S][nb]
-  double* part = nullptr;  // reduction partials
-  Impl impl;
-  // profiling: event pairs per kernel kind, drained by tdg_profile_read
-  bool profile = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
-  double ms[3] = {0, 0, 0};
-  int64_t launches[3] = {0, 0, 0};
-};
+}  // namespace tdg
 
 namespace {
 
-template <int D, int K, class M>
-int configure(int nqv) {
-  cudaError_t e;
-  e = cudaFuncSetAttribute(k_volume<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(VolumeTile<D, K, M>::smem(nqv)));
-  if (e != cudaSuccess) return cuda_fail(e, "configure volume");
-  e = cudaFuncSetAttribute(k_faces<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(FaceTile<D, K, M>::smem()));
-  if (e != cudaSuccess) return cuda_fail(e, "configure faces");
-  e = cudaFuncSetAttribute(k_wall<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(WallTile<D, K, M>::smem()));
-  if (e != cudaSuccess) return cuda_fail(e, "configure wall");
-  return TDG_OK;
-}
-
-struct KernelTimer {
-  tdg_ctx* ctx;
-  int kind;
-  cudaStream_t st;
-  cudaEvent_t a = nullptr, b = nullptr;
-  KernelTimer(tdg_ctx* c, int k, cudaStream_t s) : ctx(c), kind(k), st(s) {
-    if (!ctx->profile) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, st);
-  }
-  ~KernelTimer() {
-    if (!ctx->profile) return;
-    cudaEventRecord(b, st);
-    ctx->ev[kind].emplace_back(a, b);
-    ctx->launches[kind] += 1;
-  }
-};
-
-template <int D, int K, class M>
-int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
-        double c, int mode, cudaStream_t st) {
-  const OpParams& p = ctx->p;
-  if (p.nif > 0) {
-    KernelTimer kt(ctx, 0, st);
-    constexpr int TF = FaceTile<D, K, M>::TF;
-    const int64_t grid = (p.nif + TF - 1) / TF;
-    k_faces<D, K, M><<<unsigned(grid), kThreads, FaceTile<D, K, M>::smem(), st>>>(p, U, ctx->fc);
-  }
-  if (p.nbf > 0) {
-    KernelTimer kt(ctx, 1, st);
-    constexpr int TF = WallTile<D, K, M>::TF;
-    const int64_t grid = (p.nbf + TF - 1) / TF;
-    k_wall<D, K, M><<<unsigned(grid), kThreads, WallTile<D, K, M>::smem(), st>>>(p, U, ctx->fc);
-  }
-  if (p.ne > 0) {
-    KernelTimer kt(ctx, 2, st);
-    constexpr int TE = VolumeTile<D, K, M>::TE;
-    const int64_t grid = (p.ne + TE - 1) / TE;
-    k_volume<D, K, M><<<unsigned(grid), kThreads, VolumeTile<D, K, M>::smem(p.nqv), st>>>(
-        p, U, ctx->fc, U0, out, a, b, c, mode);
-  }
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
-}
-
-template <int D, int K, class M>
-Impl make_impl() {
-  return Impl{&configure<D, K, M>, &run<D, K, M>, Dims<D, K>::NQV, Dims<D, K>::NQF};
-}
-
-template <class M>
-bool pick_order(int dim, int order, Impl* out) {
-  switch (dim * 10 + order) {
-    case 21: *out = make_impl<2, 1, M>(); return true;
-    case 22: *out = make_impl<2, 2, M>(); return true;
-    case 23: *out = make_impl<2, 3, M>(); return true;
-    case 31: *out = make_impl<3, 1, M>(); return true;
-    case 32: *out = make_impl<3, 2, M>(); return true;
-    case 33: *out = make_impl<3, 3, M>(); return true;
-    default: return false;
-  }
-}
-
 bool pick(const tdg_desc& d, Impl* out) {
-  if (d.model == TDG_MODEL_PLAQUE && d.n_species == 6) return pick_order<PlaqueDev>(d.dim, d.order, out);
-  if (d.model == TDG_MODEL_REDUCED && d.n_species == 3) return pick_order<ReducedDev>(d.dim, d.order, out);
-  if (d.model == TDG_MODEL_DIFFUSION && d.n_species == 1)
-    return pick_order<DiffusionDev<1>>(d.dim, d.order, out);
+  if (d.model == TDG_MODEL_PLAQUE && d.n_species == 6) return pick_plaque(d.dim, d.order, out);
+  if (d.model == TDG_MODEL_REDUCED && d.n_species == 3) return pick_reduced(d.dim, d.order, out);
+  if (d.model == TDG_MODEL_DIFFUSION && d.n_species == 1) return pick_diffusion(d.dim, d.order, out);
   return false;
 }
 
@@ -298,6 +192,12 @@ int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y, int6
   if (!alpha || !x || !y) return fail(TDG_E_INVALID, "null argument");
   cudaError_t e = launch_axpy_dev(s, alpha, x, y, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "axpy_dev");
+}
+
+int tdg_set_variant(tdg_ctx* ctx, int generic) {
+  if (!ctx) return fail(TDG_E_INVALID, "null argument");
+  ctx->force_generic = generic != 0;
+  return TDG_OK;
 }
 
 int tdg_profile(tdg_ctx* ctx, int enable) {

@@ -1,0 +1,161 @@
+// Context object and the per-instantiation launch templates, shared by
+// the C-ABI translation unit (capi.cu) and the instantiation units
+// (inst_*.cu, compiled in parallel).
+#pragma once
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "taxisdg_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "kernels_fast.cuh"
+#include "models.cuh"
+#include "vecops.cuh"
+
+namespace tdg {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+struct Impl {
+  int (*configure)(int nqv);
+  int (*run)(tdg_ctx*, const double* U, const double* U0, double* out, double a, double b,
+             double c, int mode, cudaStream_t st);
+  int max_nqv, max_nqf;
+};
+
+bool pick_plaque(int dim, int order, Impl* out);
+bool pick_reduced(int dim, int order, Impl* out);
+bool pick_diffusion(int dim, int order, Impl* out);
+
+}  // namespace tdg
+
+struct tdg_ctx {
+  tdg_desc d;
+  tdg::OpParams p;
+  double* fc = nullptr;    // face-contribution slots [d+1][ne][S][nb]
+  double* part = nullptr;  // reduction partials
+  tdg::Impl impl;
+  // profiling: event pairs per kernel kind, drained by tdg_profile_read
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
+  double ms[3] = {0, 0, 0};
+  int64_t launches[3] = {0, 0, 0};
+  bool force_generic = false;  // testing: pin the CTA-staged kernels
+};
+
+namespace tdg {
+
+template <int D, int K, class M>
+int configure(int nqv) {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k_volume<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(VolumeTile<D, K, M>::smem(nqv)));
+  if (e != cudaSuccess) return cuda_fail(e, "configure volume");
+  e = cudaFuncSetAttribute(k_faces<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(FaceTile<D, K, M>::smem()));
+  if (e != cudaSuccess) return cuda_fail(e, "configure faces");
+  e = cudaFuncSetAttribute(k_wall<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(WallTile<D, K, M>::smem()));
+  if (e != cudaSuccess) return cuda_fail(e, "configure wall");
+  if constexpr (FastVol<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_volume_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(FastVol<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure volume_fast");
+  }
+  return TDG_OK;
+}
+
+struct KernelTimer {
+  tdg_ctx* ctx;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KernelTimer(tdg_ctx* c, int k, cudaStream_t s) : ctx(c), kind(k), st(s) {
+    if (!ctx->profile) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~KernelTimer() {
+    if (!ctx->profile) return;
+    cudaEventRecord(b, st);
+    ctx->ev[kind].emplace_back(a, b);
+    ctx->launches[kind] += 1;
+  }
+};
+
+template <int D, int K, class M>
+int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
+        double c, int mode, cudaStream_t st) {
+  const OpParams& p = ctx->p;
+  // register-resident kernels when the tables / working set fit and the
+  // default quadrature is in use; generic CTA-staged kernels otherwise
+  constexpr bool fast_face = FastFace<D, K, M>::ok;
+  constexpr bool fast_vol = FastVol<D, K, M>::ok;
+  const bool use_ff = fast_face && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
+  const bool use_fv = fast_vol && p.nqv == Dims<D, K>::NQV && !ctx->force_generic;
+  if (use_ff) {
+    if constexpr (fast_face) {
+      if (p.nif + p.nbf > 0) {
+        KernelTimer kt(ctx, 0, st);
+        using T = FastFace<D, K, M>;
+        const int64_t warps = (p.nif + T::FPW - 1) / T::FPW + (p.nbf + T::FPW - 1) / T::FPW;
+        const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+        k_faces_fast<D, K, M><<<unsigned(grid), 128, 0, st>>>(p, U, ctx->fc);
+      }
+    }
+  } else {
+    if (p.nif > 0) {
+      KernelTimer kt(ctx, 0, st);
+      constexpr int TF = FaceTile<D, K, M>::TF;
+      const int64_t grid = (p.nif + TF - 1) / TF;
+      k_faces<D, K, M><<<unsigned(grid), kThreads, FaceTile<D, K, M>::smem(), st>>>(p, U, ctx->fc);
+    }
+    if (p.nbf > 0) {
+      KernelTimer kt(ctx, 1, st);
+      constexpr int TF = WallTile<D, K, M>::TF;
+      const int64_t grid = (p.nbf + TF - 1) / TF;
+      k_wall<D, K, M><<<unsigned(grid), kThreads, WallTile<D, K, M>::smem(), st>>>(p, U, ctx->fc);
+    }
+  }
+  if (p.ne > 0) {
+    KernelTimer kt(ctx, 2, st);
+    if (use_fv) {
+      using T = FastVol<D, K, M>;
+      const int64_t grid = (p.ne + T::TE - 1) / T::TE;
+      if constexpr (fast_vol)
+        k_volume_fast<D, K, M><<<unsigned(grid), T::TE, T::smem(), st>>>(p, U, ctx->fc, U0, out,
+                                                                          a, b, c, mode);
+    } else {
+      constexpr int TE = VolumeTile<D, K, M>::TE;
+      const int64_t grid = (p.ne + TE - 1) / TE;
+      k_volume<D, K, M><<<unsigned(grid), kThreads, VolumeTile<D, K, M>::smem(p.nqv), st>>>(
+          p, U, ctx->fc, U0, out, a, b, c, mode);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
+}
+
+template <int D, int K, class M>
+Impl make_impl() {
+  return Impl{&configure<D, K, M>, &run<D, K, M>, Dims<D, K>::NQV, Dims<D, K>::NQF};
+}
+
+template <class M>
+bool pick_order(int dim, int order, Impl* out) {
+  switch (dim * 10 + order) {
+    case 21: *out = make_impl<2, 1, M>(); return true;
+    case 22: *out = make_impl<2, 2, M>(); return true;
+    case 23: *out = make_impl<2, 3, M>(); return true;
+    case 31: *out = make_impl<3, 1, M>(); return true;
+    case 32: *out = make_impl<3, 2, M>(); return true;
+    case 33: *out = make_impl<3, 3, M>(); return true;
+    default: return false;
+  }
+}
+
+}  // namespace tdg

@@ -6,7 +6,7 @@
 //   k_faces  interior (+ Dirichlet-mirror) faces   operator.py:359-444
 //   k_wall   prescribed-flux boundary faces        operator.py:446-458
 //            both write one contribution block per element-local face
-//            into FC[e][lf][s][i]; every (e, lf) slot is written exactly
+//            into FC[lf][e][s][i]; every (lf, e) slot is written exactly
 //            once per application, so the two-sided scatter is
 //            conflict-free without colouring or atomics;
 //   k_volume volume terms (operator.py:292-324) + sum over the element's
@@ -155,9 +155,9 @@ k_volume(OpParams p, const double* __restrict__ U, const double* __restrict__ FC
     for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
     const double detJ = ge[0];
     double rv = detJ * (acc - p.A[s] * dif + lin);
-    const double* fc = FC + (e0 + e) * (D + 1) * SN + r;
+    const double* fc = FC + (e0 + e) * SN + r;
 #pragma unroll
-    for (int lf = 0; lf <= D; ++lf) rv += fc[lf * SN];
+    for (int lf = 0; lf <= D; ++lf) rv += fc[lf * p.ne * SN];
     double o;
     if (mode == 0) o = rv;
     else if (mode == 1) o = rv / detJ;
@@ -338,7 +338,7 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
       acc = fma(sg * Y[q], __ldg(b + q * NB), acc);
       acc = fma(X[q], dp[q * NB], acc);
     }
-    const int64_t slot = int64_t(meta[f * 6 + 1 + side]) * (D + 1) + meta[f * 6 + 3 + side];
+    const int64_t slot = int64_t(meta[f * 6 + 3 + side]) * p.ne + meta[f * 6 + 1 + side];
     FC[slot * SN + si] = acc;
   }
 }
@@ -397,7 +397,7 @@ k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
     const double* b = p.fB + size_t(code_tin(code)) * nqf * NB + i;
     double acc = 0.0;
     for (int q = 0; q < nqf; ++q) acc = fma(yw[(f * S + s) * F + q], __ldg(b + q * NB), acc);
-    const int64_t slot = int64_t(meta[f * 4 + 1]) * (D + 1) + meta[f * 4 + 2];
+    const int64_t slot = int64_t(meta[f * 4 + 2]) * p.ne + meta[f * 4 + 1];
     FC[slot * SN + si] = acc;
   }
 }

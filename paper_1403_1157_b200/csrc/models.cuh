@@ -95,6 +95,36 @@ struct PlaqueDev {
     for (int s = 0; s < S; ++s) q[s] += 0.5 * lam * dU[s];
   }
 
+  // Lane-per-species form of face_conv: every lane of a face group calls
+  // it for its own species s; fetch(kind, sp) returns u_in (kind 0),
+  // u_out (1) or the averaged normal derivative (2) of species sp from the
+  // group's lanes (warp shuffles).  Returns q_s's convective part.
+  template <class Fetch>
+  __device__ __forceinline__ static double face_conv_lane(const double* P, int s, double dUs,
+                                                          Fetch fetch) {
+    const double g0 = fetch(2, 0), g3 = fetch(2, 3), g5 = fetch(2, 5);
+    double lam = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double n1 = fetch(side, 0), n2 = fetch(side, 1), c1 = fetch(side, 3),
+                   c3 = fetch(side, 5);
+      const double c1p = fmax(c1, 0.0);
+      const double k11 = P[C11A] * rcp(c1p + P[C11B]);
+      const double k13 = P[C13A] * rcp(fmax(c3, 0.0) + P[C13B]);
+      const double k21 = P[C21A] * rcp(c1p + P[C21B]);
+      const double k2n = P[C2NA] * rcp(fmax(n1, 0.0) + P[C2NB]);
+      const double v0 = k11 * g3 + k13 * g5;
+      const double v1 = k21 * g3 - k2n * g0;
+      lam = fmax(lam, fmax(fabs(v0), fabs(v1)));
+      f0 = fma(n1, v0, f0);
+      f1 = fma(n2, v1, f1);
+    }
+    double r = 0.5 * lam * dUs;
+    if (s == 0) r = fma(0.5, f0, r);
+    if (s == 1) r = fma(0.5, f1, r);
+    return r;
+  }
+
   // prescribed wall fluxes, inward-normal sign (model.py:194-209)
   __device__ __forceinline__ static void wall(const double* P, int tag, double c1, double* q) {
 #pragma unroll
@@ -102,6 +132,13 @@ struct PlaqueDev {
     if (tag == GAMMA1 || tag == GAMMA1_IN) q[0] = -P[MU1] * P[BETA1] * heaviside(c1 - P[C1S], P[EPSH]);
     if (tag == GAMMA1_IN) q[4] = -P[NU2] * P[SIGMA];
     if (tag == GAMMA2) q[1] = -P[MU2] * P[BETA2] * heaviside(c1 - P[C1SS], P[EPSH]);
+  }
+  __device__ __forceinline__ static double wall_lane(const double* P, int tag, int s, double c1) {
+    if (s == 0 && (tag == GAMMA1 || tag == GAMMA1_IN))
+      return -P[MU1] * P[BETA1] * heaviside(c1 - P[C1S], P[EPSH]);
+    if (s == 4 && tag == GAMMA1_IN) return -P[NU2] * P[SIGMA];
+    if (s == 1 && tag == GAMMA2) return -P[MU2] * P[BETA2] * heaviside(c1 - P[C1SS], P[EPSH]);
+    return 0.0;
   }
   __device__ __forceinline__ static double mirror_value(const double*, int) { return 0.0; }
 };
@@ -149,10 +186,31 @@ struct ReducedDev {
     for (int s = 0; s < S; ++s) q[s] += 0.5 * lam * dU[s];
   }
 
+  template <class Fetch>
+  __device__ __forceinline__ static double face_conv_lane(const double* P, int s, double dUs,
+                                                          Fetch fetch) {
+    const double g2 = fetch(2, 2);
+    double lam = 0.0, f0 = 0.0;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double v0 = P[C11A] * rcp(fmax(fetch(side, 2), 0.0) + P[C11B]) * g2;
+      lam = fmax(lam, fabs(v0));
+      f0 = fma(fetch(side, 0), v0, f0);
+    }
+    double r = 0.5 * lam * dUs;
+    if (s == 0) r = fma(0.5, f0, r);
+    return r;
+  }
+
   __device__ __forceinline__ static void wall(const double* P, int tag, double c1, double* q) {
 #pragma unroll
     for (int s = 0; s < S; ++s) q[s] = 0.0;
     if (tag == GAMMA1 || tag == GAMMA1_IN) q[0] = -P[MU1] * P[BETA1] * heaviside(c1 - P[C1S], P[EPSH]);
+  }
+  __device__ __forceinline__ static double wall_lane(const double* P, int tag, int s, double c1) {
+    if (s == 0 && (tag == GAMMA1 || tag == GAMMA1_IN))
+      return -P[MU1] * P[BETA1] * heaviside(c1 - P[C1S], P[EPSH]);
+    return 0.0;
   }
   __device__ __forceinline__ static double mirror_value(const double*, int) { return 0.0; }
 };
@@ -177,10 +235,15 @@ struct DiffusionDev {
                                                       double (*)[D], double*) {}
   __device__ __forceinline__ static void face_conv(const double*, const double*, const double*,
                                                    const double*, const double*, double*) {}
+  template <class Fetch>
+  __device__ __forceinline__ static double face_conv_lane(const double*, int, double, Fetch) {
+    return 0.0;
+  }
   __device__ __forceinline__ static void wall(const double*, int, double, double* q) {
 #pragma unroll
     for (int s = 0; s < S; ++s) q[s] = 0.0;
   }
+  __device__ __forceinline__ static double wall_lane(const double*, int, int, double) { return 0.0; }
   __device__ __forceinline__ static double mirror_value(const double* P, int s) { return P[s]; }
 };
 

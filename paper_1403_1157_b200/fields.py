@@ -46,5 +46,5 @@ def initial_state(space, seed: int, box=None) -> np.ndarray:
     mesh = space.mesh
     lo, hi = ((mesh.vertices.min(axis=0), mesh.vertices.max(axis=0))
               if box is None else box)
-    return space.project(bump_field(mesh.dim, space.n_species, seed,
-                                    np.asarray(lo), np.asarray(hi))).coeffs
+    return np.ascontiguousarray(space.project(bump_field(
+        mesh.dim, space.n_species, seed, np.asarray(lo), np.asarray(hi))).coeffs)

@@ -177,6 +177,12 @@ class DiscreteOperator:
 
     KERNELS = ("faces", "wall", "volume")
 
+    def set_variant(self, generic: bool):
+        """Pin the generic CTA-staged kernels (True) or let the library pick
+        the register-resident ones where compiled in (False, default)."""
+        _native.check(self.lib.tdg_set_variant(self._ctx, int(bool(generic))),
+                      "tdg_set_variant")
+
     def profile(self, enable: bool = True):
         """Bracket every operator kernel launch with CUDA events on its
         stream (per-kernel roofline timing inside the benchmark)."""
@@ -192,8 +198,23 @@ class DiscreteOperator:
 
     # -- explicit stepping / Krylov primitives (device tensors) ----------
 
+    def _check_vec(self, name, x, rows=None):
+        """Raw-pointer entry points need dense fp64 CUDA storage."""
+        torch = _torch()
+        if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 \
+                or x.device.type != "cuda" or not x.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+        if rows is not None and tuple(x.shape) != (rows, self.space.n_species,
+                                                   self.space.nb):
+            raise ValueError(f"{name} has shape {tuple(x.shape)}, expected "
+                             f"{(rows, self.space.n_species, self.space.nb)}")
+
     def rk_stage(self, U0, U, out, a: float, b: float, c: float, t: float = 0.0):
         """out = a U0 + b U + c M^-1 L(U) in one fused pass."""
+        self._check_vec("U", U, self.n_rows)
+        self._check_vec("out", out, self.n_owned)
+        if U0 is not None:
+            self._check_vec("U0", U0, self.n_owned)
         _native.check(self.lib.tdg_rk_stage(
             self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
             out.data_ptr(), float(a), float(b), float(c), float(t),
@@ -201,12 +222,18 @@ class DiscreteOperator:
         return out
 
     def ssprk3_step(self, U, work, dt: float, t: float = 0.0):
+        self._check_vec("U", U, self.n_rows)
+        self._check_vec("work", work, self.n_rows)
         _native.check(self.lib.tdg_ssprk3_step(
             self._ctx, U.data_ptr(), work.data_ptr(), float(t), float(dt),
             self._stream()), "tdg_ssprk3_step")
         return U
 
     def dot(self, x, y, out=None):
+        self._check_vec("x", x)
+        self._check_vec("y", y)
+        if x.numel() != y.numel():
+            raise ValueError("x and y differ in size")
         out = self._scalar[:1] if out is None else out
         _native.check(self.lib.tdg_dot(self._ctx, x.data_ptr(), y.data_ptr(),
                                        x.numel(), out.data_ptr(), self._stream()),
@@ -214,6 +241,7 @@ class DiscreteOperator:
         return out
 
     def norm2(self, x, out=None):
+        self._check_vec("x", x)
         out = self._scalar[1:] if out is None else out
         _native.check(self.lib.tdg_norm2(self._ctx, x.data_ptr(), x.numel(),
                                          out.data_ptr(), self._stream()),
@@ -221,12 +249,16 @@ class DiscreteOperator:
         return out
 
     def axpby(self, a: float, x, b: float, y):
+        self._check_vec("x", x)
+        self._check_vec("y", y)
         _native.check(self.lib.tdg_axpby(float(a), x.data_ptr(), float(b),
                                          y.data_ptr(), x.numel(), self._stream()),
                       "tdg_axpby")
         return y
 
     def axpy_dev(self, s: float, alpha, x, y):
+        self._check_vec("x", x)
+        self._check_vec("y", y)
         _native.check(self.lib.tdg_axpy_dev(float(s), alpha.data_ptr(),
                                             x.data_ptr(), y.data_ptr(),
                                             x.numel(), self._stream()),

@@ -35,6 +35,27 @@ def test_apply_matches_reference_golden(golden, name):
     assert rel_l2_per_species(space, gf, F).max() <= 1e-12
 
 
+@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
+def test_generic_kernels_match_reference_golden(golden, name):
+    """The CTA-staged generic kernels (used where the register-resident
+    ones are not compiled in) against the same golden outputs."""
+    space, model, scheme, U, R, F = operator_case(golden, name)
+    op = _op(space, model, scheme)
+    op.set_variant(generic=True)
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+def test_variants_agree_at_size():
+    space = DGSpace(unit_square(64, 16, lengths=(4.0, 1.0)), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U = torch.from_numpy(initial_state(space, 8)).cuda()
+    a = op.apply_f(U)
+    op.set_variant(generic=True)
+    b = op.apply_f(U)
+    assert rel_l2_per_species(space, a.cpu().numpy(), b.cpu().numpy()).max() <= 1e-13
+
+
 @pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
 @pytest.mark.parametrize("dirichlet", [0, 1])
 def test_heat_models(golden, scheme, dirichlet):
