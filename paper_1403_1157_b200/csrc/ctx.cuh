@@ -60,6 +60,11 @@ int configure(int nqv) {
   e = cudaFuncSetAttribute(k_wall<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(WallTile<D, K, M>::smem()));
   if (e != cudaSuccess) return cuda_fail(e, "configure wall");
+  if constexpr (FastFace<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_faces_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(FastFace<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_fast");
+  }
   if constexpr (FastVol<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_volume_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(FastVol<D, K, M>::smem()));
@@ -104,7 +109,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
         using T = FastFace<D, K, M>;
         const int64_t warps = (p.nif + T::FPW - 1) / T::FPW + (p.nbf + T::FPW - 1) / T::FPW;
         const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
-        k_faces_fast<D, K, M><<<unsigned(grid), 128, 0, st>>>(p, U, ctx->fc);
+        k_faces_fast<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, U, ctx->fc);
       }
     }
   } else {

@@ -34,7 +34,13 @@ struct FastFace {
   static constexpr int FPC = FPW * WARPS;     // faces per CTA
   static constexpr int TB = NT * F * NB, TG = NT * F * NB * D, TP = NT * F * F;
   static constexpr int TAB = TB + TG + TP + F;
-  static constexpr bool ok = F <= 8 && S >= 3 && S <= 8 && TAB * 8 <= 40 * 1024 && NB <= 10;
+  static constexpr int NCV = 1 + M::NFX;
+  // per-face scratch: normal-derivative tables (2 sides), the species
+  // transpose (u_in, u_out, avg d_n u at every point) and the coupled
+  // per-point results (wave speed, flux normals)
+  static constexpr int PF = 2 * F * NB + 3 * S * F + F * NCV;
+  static constexpr size_t smem() { return size_t(TAB + WARPS * FPW * PF) * 8; }
+  static constexpr bool ok = F <= 8 && S >= 3 && S <= 8 && NB <= 10 && smem() <= 100 * 1024;
 };
 
 template <int NB>
@@ -69,11 +75,11 @@ template <int D, int K, class M>
 __global__ void __launch_bounds__(128)
 k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
   using T = FastFace<D, K, M>;
-  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW, NCV = T::NCV;
   constexpr int NFG = Dims<D, K>::NFG;
-  __shared__ __align__(16) double tab[T::TAB];
-  double* tB = tab;
-  double* tG = tab + T::TB;
+  extern __shared__ __align__(16) double sm[];
+  double* tB = sm;
+  double* tG = tB + T::TB;
   double* tP = tG + T::TG;
   double* tw = tP + T::TP;
   for (int i = threadIdx.x; i < T::TB; i += 128) tB[i] = p.fB[i];
@@ -84,20 +90,25 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / S, s = lane - grp * S, base = grp * S;
+  const bool lane_ok = grp < FPW;
   // warps [0, wi) take interior faces, warps [wi, ...) wall faces: every
-  // warp is wholly interior or wholly wall, so the shuffles below are
-  // always executed by all 32 lanes
+  // warp is wholly interior or wholly wall (uniform __syncwarp/shuffles)
   const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
   const int64_t wi = (p.nif + FPW - 1) / FPW;
   const bool wall = gw >= wi;
   const int64_t f = wall ? p.nif + (gw - wi) * FPW + grp : gw * FPW + grp;
-  const bool active = grp < FPW && (wall ? f < p.nif + p.nbf : f < p.nif);
+  const bool active = lane_ok && (wall ? f < p.nif + p.nbf : f < p.nif);
   if (!__any_sync(0xffffffffu, active)) return;  // warp-uniform
 
+  double* scratch = sm + T::TAB + (warp * FPW + (lane_ok ? grp : 0)) * T::PF;
+  double* dph = scratch;                    // [2][F][NB]
+  double* xch = dph + 2 * F * NB;           // [3][S][F]
+  double* cvs = xch + 3 * S * F;            // [F][NCV]
+
   int code = 0, ein = 0, eout = -1, lfi = 0, lfo = 0;
-  double jin[D], jout[D], sfac = 0.0, h = 1.0, idi = 0.0, ido = 0.0;
+  double jn[2][D], sfac = 0.0, h = 1.0, idi = 0.0, ido = 0.0;
 #pragma unroll
-  for (int a = 0; a < D; ++a) jin[a] = jout[a] = 0.0;
+  for (int a = 0; a < D; ++a) jn[0][a] = jn[1][a] = 0.0;
   if (active && !wall) {
     code = p.ifcode[f];
     ein = p.ifel[2 * f];
@@ -107,8 +118,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
     const double* g = p.ifgeo + f * NFG;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      jin[a] = __ldg(g + a);
-      jout[a] = __ldg(g + D + a);
+      jn[0][a] = __ldg(g + a);
+      jn[1][a] = __ldg(g + D + a);
     }
     sfac = __ldg(g + 2 * D);
     h = __ldg(g + 2 * D + 1);
@@ -123,6 +134,7 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
   }
   const bool mirror = code_mirror(code);
   const int tin = code_tin(code), tout = code_tout(code);
+  const bool two = active && !wall && !mirror;
 
   double ci[NB], co[NB];
   if (active) load_row<NB>(U + int64_t(ein) * SN + s * NB, ci);
@@ -130,68 +142,89 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
 #pragma unroll
     for (int i = 0; i < NB; ++i) ci[i] = 0.0;
   }
-  const bool two = active && !wall && !mirror;
   if (two) load_row<NB>(U + int64_t(eout) * SN + s * NB, co);
   else {
 #pragma unroll
     for (int i = 0; i < NB; ++i) co[i] = 0.0;
   }
-
-  // traces at the face points: u and d_n u = sum_a jn_a (G_a . c)
-  double ui[F], uo[F], gi[F], go[F];
   const double* Bi = tB + tin * F * NB;
   const double* Bo = tB + tout * F * NB;
-  const double* Gi = tG + tin * F * NB * D;
-  const double* Go = tG + tout * F * NB * D;
-#pragma unroll
-  for (int q = 0; q < F; ++q) {
-    double u = 0.0, v = 0.0, ga[D], gb[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) ga[a] = gb[a] = 0.0;
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      u = fma(Bi[q * NB + i], ci[i], u);
-      v = fma(Bo[q * NB + i], co[i], v);
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        ga[a] = fma(Gi[(q * NB + i) * D + a], ci[i], ga[a]);
-        gb[a] = fma(Go[(q * NB + i) * D + a], co[i], gb[a]);
-      }
-    }
-    double x = 0.0, y = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      x = fma(jin[a], ga[a], x);
-      y = fma(jout[a], gb[a], y);
-    }
-    ui[q] = u;
-    gi[q] = x;
-    uo[q] = v;
-    go[q] = y;
-  }
 
   double ri[NB], ro[NB];
 #pragma unroll
   for (int i = 0; i < NB; ++i) ri[i] = ro[i] = 0.0;
 
   if (!wall) {
-    const double As = p.A[s];
-    const double gD = M::mirror_value(p.P, s);
-    if (mirror) {
+    // per-face normal-derivative test tables dphi.n = G . (Jinv n), shared
+    // by the S lanes of the face
+    if (lane_ok) {
+      for (int idx = s; idx < 2 * F * NB; idx += S) {
+        const int side = idx / (F * NB), qi = idx - side * F * NB;
+        const double* g = tG + ((side ? tout : tin) * F * NB + qi) * D;
+        double v = 0.0;
 #pragma unroll
-      for (int q = 0; q < F; ++q) {
-        uo[q] = 2.0 * gD - ui[q];
-        go[q] = gi[q];
+        for (int a = 0; a < D; ++a) v = fma(g[a], side ? jn[1][a] : jn[0][a], v);
+        dph[idx] = v;
       }
     }
-    double dU[F], gav[F], qv[F];
+    __syncwarp();
+    const double* dpi = dph;
+    const double* dpo = dph + F * NB;
+    double ui[F], uo[F], dU[F], gav[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) {
-      dU[q] = ui[q] - uo[q];
-      gav[q] = 0.5 * (gi[q] + go[q]);
-      qv[q] = 0.0;
+      double u = 0.0, v = 0.0, x = 0.0, y = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        u = fma(Bi[q * NB + i], ci[i], u);
+        x = fma(dpi[q * NB + i], ci[i], x);
+        v = fma(Bo[q * NB + i], co[i], v);
+        y = fma(dpo[q * NB + i], co[i], y);
+      }
+      if (mirror) {
+        v = 2.0 * M::mirror_value(p.P, s) - u;
+        y = x;
+      }
+      ui[q] = u;
+      uo[q] = v;
+      dU[q] = u - v;
+      gav[q] = 0.5 * (x + y);
     }
-    // penalty A_hat . n (operator.py:336-357)
+    const double As = p.A[s];
+    // coupled convective physics once per face point (smem transpose)
+    double conv[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) conv[q] = 0.0;
+    if constexpr (M::kConv) {
+      if (lane_ok) {
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          xch[(0 * S + s) * F + q] = ui[q];
+          xch[(1 * S + s) * F + q] = uo[q];
+          xch[(2 * S + s) * F + q] = gav[q];
+        }
+      }
+      __syncwarp();
+      if (lane_ok) {
+        for (int q = s; q < F; q += S) {
+          auto fetch = [&](int kind, int sp) { return xch[(kind * S + sp) * F + q]; };
+          M::face_point(p.P, fetch, cvs + q * NCV);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < F; ++q) {
+        double c = 0.5 * cvs[q * NCV] * dU[q];
+#pragma unroll
+        for (int k = 0; k < M::NFX; ++k)
+          if (s == k) c = fma(0.5, cvs[q * NCV + 1 + k], c);
+        conv[q] = c;
+      }
+    }
+    // penalty A_hat . n (operator.py:336-357), lifting on the needed side(s)
+    double qv[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) qv[q] = 0.0;
     if (p.scheme == IP) {
       const double c = p.eta / h * As;
 #pragma unroll
@@ -201,48 +234,39 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
       const bool use_in = mirror || br2 || code_minus_in(code);
       const bool use_out = !mirror && (br2 || !code_minus_in(code));
       const double wside = (br2 && !mirror) ? 0.5 : 1.0;
-      const double fac = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * As;
-      // -fac * A * rho, rho = -1/2 sfac/detJ * (Pw dU)
-      const double si = use_in ? fac * wside * 0.5 * sfac * idi : 0.0;
-      const double so = use_out ? fac * wside * 0.5 * sfac * ido : 0.0;
-      const double* Pi = tP + tin * F * F;
-      const double* Po = tP + tout * F * F;
+      // -fac A rho with rho = -1/2 sfac / detJ (Pw dU)
+      const double fac = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * As * wside * 0.5 * sfac;
+      if (use_in) {
+        const double* Pw = tP + tin * F * F;
 #pragma unroll
-      for (int q = 0; q < F; ++q) {
-        double a = 0.0, b = 0.0;
+        for (int q = 0; q < F; ++q) {
+          double a = 0.0;
 #pragma unroll
-        for (int pp = 0; pp < F; ++pp) {
-          a = fma(Pi[q * F + pp], dU[pp], a);
-          b = fma(Po[q * F + pp], dU[pp], b);
+          for (int pp = 0; pp < F; ++pp) a = fma(Pw[q * F + pp], dU[pp], a);
+          qv[q] = fma(fac * idi, a, qv[q]);
         }
-        qv[q] = si * a + so * b;
+      }
+      if (use_out) {
+        const double* Pw = tP + tout * F * F;
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int pp = 0; pp < F; ++pp) a = fma(Pw[q * F + pp], dU[pp], a);
+          qv[q] = fma(fac * ido, a, qv[q]);
+        }
       }
     }
     // projection onto both sides' test functions
 #pragma unroll
     for (int q = 0; q < F; ++q) {
-      double conv = 0.0;
-      if constexpr (M::kConv) {
-        const double mui = ui[q], muo = uo[q], mg = gav[q];
-        auto fetch = [&](int kind, int sp) {
-          const double v = kind == 0 ? mui : (kind == 1 ? muo : mg);
-          return __shfl_sync(0xffffffffu, v, base + sp);
-        };
-        conv = M::face_conv_lane(p.P, s, dU[q], fetch);
-      }
       const double wq = tw[q] * sfac;
-      const double Y = wq * (As * gav[q] - (qv[q] + conv));
+      const double Y = wq * (As * gav[q] - (qv[q] + conv[q]));
       const double X = wq * 0.5 * p.adj * As * dU[q];
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        double dpi = 0.0, dpo = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          dpi = fma(Gi[(q * NB + i) * D + a], jin[a], dpi);
-          dpo = fma(Go[(q * NB + i) * D + a], jout[a], dpo);
-        }
-        ri[i] = fma(Y, Bi[q * NB + i], fma(X, dpi, ri[i]));
-        ro[i] = fma(-Y, Bo[q * NB + i], fma(X, dpo, ro[i]));
+        ri[i] = fma(Y, Bi[q * NB + i], fma(X, dpi[q * NB + i], ri[i]));
+        ro[i] = fma(-Y, Bo[q * NB + i], fma(X, dpo[q * NB + i], ro[i]));
       }
     }
   } else {
@@ -250,7 +274,10 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
     const int tag = code_tag(code);
 #pragma unroll
     for (int q = 0; q < F; ++q) {
-      const double c1 = __shfl_sync(0xffffffffu, ui[q], base + M::WALL_SP);
+      double u = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) u = fma(Bi[q * NB + i], ci[i], u);
+      const double c1 = __shfl_sync(0xffffffffu, u, base + M::WALL_SP);
       const double Y = -tw[q] * sfac * M::wall_lane(p.P, tag, s, c1);
 #pragma unroll
       for (int i = 0; i < NB; ++i) ri[i] = fma(Y, Bi[q * NB + i], ri[i]);
@@ -265,6 +292,46 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
 
 // ------------------------------------------------------------------ volume
 
+// Coalesced copy of nt contiguous rows of SN doubles between global
+// memory and a padded shared tile (row stride SNP, odd => conflict-free
+// per-thread row access).  Uses 16-byte accesses when SN is even (the
+// tile base is 16-byte aligned because every row offset e0*SN*8 is).
+template <int SN, int SNP, int NTH>
+__device__ __forceinline__ void tile_load(const double* __restrict__ src, double* dst, int nt) {
+  if constexpr (SN % 2 == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    constexpr int H = SN / 2;
+    for (int idx = threadIdx.x; idx < nt * H; idx += NTH) {
+      const int e = idx / H, r = 2 * (idx - e * H);
+      const double2 v = __ldcs(s2 + idx);
+      dst[e * SNP + r] = v.x;
+      dst[e * SNP + r + 1] = v.y;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nt * SN; idx += NTH) {
+      const int e = idx / SN, r = idx - e * SN;
+      dst[e * SNP + r] = __ldcs(src + idx);
+    }
+  }
+}
+
+template <int SN, int SNP, int NTH>
+__device__ __forceinline__ void tile_store(double* dst, const double* src, int nt) {
+  if constexpr (SN % 2 == 0) {
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    constexpr int H = SN / 2;
+    for (int idx = threadIdx.x; idx < nt * H; idx += NTH) {
+      const int e = idx / H, r = 2 * (idx - e * H);
+      d2[idx] = make_double2(src[e * SNP + r], src[e * SNP + r + 1]);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nt * SN; idx += NTH) {
+      const int e = idx / SN, r = idx - e * SN;
+      dst[idx] = src[e * SNP + r];
+    }
+  }
+}
+
 template <int D, int K, class M>
 struct FastVol {
   using Dm = Dims<D, K>;
@@ -274,11 +341,12 @@ struct FastVol {
   static constexpr int TPHI = Q * NB, TGR = Q * NB * D, TKS = NSYM * NB * NB;
   static constexpr int TAB = TPHI + TGR + Q + TKS;
   static constexpr bool ok = SN <= 36 && TAB * 8 <= 24 * 1024;
+  static constexpr int MINB = 2;  // CTAs/SM the register budget targets
   static constexpr size_t smem() { return size_t(TAB + 2 * TE * SNP) * 8; }
 };
 
 template <int D, int K, class M>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FastVol<D, K, M>::MINB)
 k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
               const double* U0, double* out, double ca, double cb, double cc, int mode) {
   using T = FastVol<D, K, M>;
@@ -300,10 +368,7 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   for (int i = tid; i < Q; i += TE) tw[i] = p.wv[i];
   for (int i = tid; i < T::TKS; i += TE) tks[i] = p.ks[i];
   // coalesced tile load of U (owned rows are contiguous)
-  for (int idx = tid; idx < nt * SN; idx += TE) {
-    const int e = idx / SN, r = idx - e * SN;
-    bufA[e * SNP + r] = U[e0 * SN + idx];
-  }
+  tile_load<SN, SNP, TE>(U + e0 * SN, bufA, nt);
   __syncthreads();
   const bool act = tid < nt;
   double c[SN];
@@ -313,18 +378,49 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
 #pragma unroll
   for (int k = 0; k < NEG; ++k) ge[k] = act ? __ldg(p.egeo + (e0 + tid) * NEG + k) : (k == 0 ? 1.0 : 0.0);
 
-  // quadrature: taxis flux rows (pulled back) and the bilinear source
-  constexpr int NF = M::NFLUX, NL = M::NNL;
-  double af[NF > 0 ? NF : 1][NB], al[NL > 0 ? NL : 1][NB];
+  // output = base + scale * (residual rows), with the mode folded in:
+  //   mode 0: out = R;  1: out = R/detJ;  2: out = ca U0 + cb U + cc R/detJ
+  const double detJ = ge[0];
+  const double idet = 1.0 / detJ;
+  const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
+  double* row = bufA + tid * SNP;  // own row: no sync needed to overwrite
+
+  // (1) diffusion (exact stiffness) and linear source need every species;
+  //     afterwards only the quadrature species stay live in registers
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
+    double kc[NB];
 #pragma unroll
-    for (int k = 0; k < (NF > 0 ? NF : 1); ++k) af[k][i] = 0.0;
+    for (int j = 0; j < NB; ++j) {
+      double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][i] = 0.0;
+      for (int q = 0; q < NSYM; ++q) t = fma(ge[1 + q], tks[(q * NB + j) * NB + i], t);
+      kc[j] = t;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      double dif = 0.0, lin = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) dif = fma(c[s * NB + j], kc[j], dif);
+#pragma unroll
+      for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
+      const double rv = detJ * (lin - p.A[s] * dif);
+      row[s * NB + i] = mode == 2 ? fma(cb, c[s * NB + i], scale * rv) : scale * rv;
+    }
   }
+
+  // (2) quadrature: taxis flux rows (pulled back) and the bilinear source
+  constexpr int NF = M::NFLUX, NL = M::NNL;
   if constexpr (NF + NL > 0) {
-#pragma unroll 2
+    double af[NF > 0 ? NF : 1][NB], al[NL > 0 ? NL : 1][NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+      for (int k = 0; k < (NF > 0 ? NF : 1); ++k) af[k][i] = 0.0;
+#pragma unroll
+      for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][i] = 0.0;
+    }
+#pragma unroll 1
     for (int q = 0; q < Q; ++q) {
       const double* ph = tphi + q * NB;
       const double* gr = tgr + q * NB * D;
@@ -379,80 +475,35 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
         for (int k = 0; k < NL; ++k) al[k][i] = fma(nl[k], ph[i], al[k][i]);
       }
     }
+    const double sd = scale * detJ;
+#pragma unroll
+    for (int k = 0; k < NF; ++k)
+#pragma unroll
+      for (int i = 0; i < NB; ++i) row[M::flux_sp(k) * NB + i] += sd * af[k][i];
+#pragma unroll
+    for (int k = 0; k < NL; ++k)
+#pragma unroll
+      for (int i = 0; i < NB; ++i) row[M::nl_sp(k) * NB + i] += sd * al[k][i];
   }
 
-  // residual rows: detJ (quadrature terms + linear source - A diffusion)
-  const double detJ = ge[0];
-  double* row = bufA + tid * SNP;  // own row: no sync needed to overwrite
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    double kc[NB];
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < NSYM; ++q) t = fma(ge[1 + q], tks[(q * NB + j) * NB + i], t);
-      kc[j] = t;
-    }
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      double dif = 0.0, lin = 0.0;
-#pragma unroll
-      for (int j = 0; j < NB; ++j) dif = fma(c[s * NB + j], kc[j], dif);
-#pragma unroll
-      for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
-      double acc = lin - p.A[s] * dif;
-      if constexpr (NF > 0) {
-        const int fi = M::flux_index(s);
-        if (fi >= 0) acc += af[fi][i];
-      }
-      if constexpr (NL > 0) {
-        const int li = M::nl_index(s);
-        if (li >= 0) acc += al[li][i];
-      }
-      row[s * NB + i] = detJ * acc;
-    }
-  }
-  // face-slot tiles (FC[lf] rows of this tile are contiguous)
+  // (3) face-slot tiles (FC[lf] rows of this tile are contiguous)
 #pragma unroll 1
   for (int lf = 0; lf <= D; ++lf) {
     __syncthreads();
-    const double* src = FC + (int64_t(lf) * p.ne + e0) * SN;
-    for (int idx = tid; idx < nt * SN; idx += TE) {
-      const int e = idx / SN, r = idx - e * SN;
-      bufB[e * SNP + r] = src[idx];
-    }
+    tile_load<SN, SNP, TE>(FC + (int64_t(lf) * p.ne + e0) * SN, bufB, nt);
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < SN; ++r) row[r] += bufB[tid * SNP + r];
+    for (int r = 0; r < SN; ++r) row[r] = fma(scale, bufB[tid * SNP + r], row[r]);
   }
-  const bool need_u0 = mode == 2 && ca != 0.0;
-  if (need_u0) {
+  if (mode == 2 && ca != 0.0) {
     __syncthreads();
-    for (int idx = tid; idx < nt * SN; idx += TE) {
-      const int e = idx / SN, r = idx - e * SN;
-      bufB[e * SNP + r] = U0[e0 * SN + idx];
-    }
+    tile_load<SN, SNP, TE>(U0 + e0 * SN, bufB, nt);
     __syncthreads();
-  }
-  const double idet = 1.0 / detJ;
 #pragma unroll
-  for (int r = 0; r < SN; ++r) {
-    const double rv = row[r];
-    double o;
-    if (mode == 0) o = rv;
-    else if (mode == 1) o = rv * idet;
-    else {
-      o = fma(cb, c[r], cc * (rv * idet));
-      if (need_u0) o = fma(ca, bufB[tid * SNP + r], o);
-    }
-    row[r] = o;
+    for (int r = 0; r < SN; ++r) row[r] = fma(ca, bufB[tid * SNP + r], row[r]);
   }
   __syncthreads();
-  for (int idx = tid; idx < nt * SN; idx += TE) {
-    const int e = idx / SN, r = idx - e * SN;
-    out[e0 * SN + idx] = bufA[e * SNP + r];
-  }
+  tile_store<SN, SNP, TE>(out + e0 * SN, bufA, nt);
 }
 
 }  // namespace tdg

@@ -125,6 +125,36 @@ struct PlaqueDev {
     return r;
   }
 
+  // Coupled LLF physics once per face point.  fetch(kind, sp): u_in (0),
+  // u_out (1), avg d_n u (2) of species sp at this point.  cv[0] = wave
+  // speed lambda, cv[1 + s] = (F_s(u_in) + F_s(u_out)) . n for the flux
+  // species s < NFX; the species-s convective flux is then
+  // 1/2 cv[1+s] + 1/2 lambda (u_in - u_out)_s.
+  static constexpr int NFX = 2;
+  template <class Fetch>
+  __device__ __forceinline__ static void face_point(const double* P, Fetch fetch, double* cv) {
+    const double g0 = fetch(2, 0), g3 = fetch(2, 3), g5 = fetch(2, 5);
+    double lam = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double n1 = fetch(side, 0), n2 = fetch(side, 1), c1 = fetch(side, 3),
+                   c3 = fetch(side, 5);
+      const double c1p = fmax(c1, 0.0);
+      const double k11 = P[C11A] * rcp(c1p + P[C11B]);
+      const double k13 = P[C13A] * rcp(fmax(c3, 0.0) + P[C13B]);
+      const double k21 = P[C21A] * rcp(c1p + P[C21B]);
+      const double k2n = P[C2NA] * rcp(fmax(n1, 0.0) + P[C2NB]);
+      const double v0 = k11 * g3 + k13 * g5;
+      const double v1 = k21 * g3 - k2n * g0;
+      lam = fmax(lam, fmax(fabs(v0), fabs(v1)));
+      f0 = fma(n1, v0, f0);
+      f1 = fma(n2, v1, f1);
+    }
+    cv[0] = lam;
+    cv[1] = f0;
+    cv[2] = f1;
+  }
+
   // prescribed wall fluxes, inward-normal sign (model.py:194-209)
   __device__ __forceinline__ static void wall(const double* P, int tag, double c1, double* q) {
 #pragma unroll
@@ -202,6 +232,21 @@ struct ReducedDev {
     return r;
   }
 
+  static constexpr int NFX = 1;
+  template <class Fetch>
+  __device__ __forceinline__ static void face_point(const double* P, Fetch fetch, double* cv) {
+    const double g2 = fetch(2, 2);
+    double lam = 0.0, f0 = 0.0;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double v0 = P[C11A] * rcp(fmax(fetch(side, 2), 0.0) + P[C11B]) * g2;
+      lam = fmax(lam, fabs(v0));
+      f0 = fma(fetch(side, 0), v0, f0);
+    }
+    cv[0] = lam;
+    cv[1] = f0;
+  }
+
   __device__ __forceinline__ static void wall(const double* P, int tag, double c1, double* q) {
 #pragma unroll
     for (int s = 0; s < S; ++s) q[s] = 0.0;
@@ -239,6 +284,9 @@ struct DiffusionDev {
   __device__ __forceinline__ static double face_conv_lane(const double*, int, double, Fetch) {
     return 0.0;
   }
+  static constexpr int NFX = 0;
+  template <class Fetch>
+  __device__ __forceinline__ static void face_point(const double*, Fetch, double*) {}
   __device__ __forceinline__ static void wall(const double*, int, double, double* q) {
 #pragma unroll
     for (int s = 0; s < S; ++s) q[s] = 0.0;

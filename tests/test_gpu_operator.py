@@ -207,11 +207,11 @@ def test_vector_ops():
     assert op.dot(x, y).item() == d  # deterministic
     z = y.clone()
     op.axpby(2.0, x, -0.5, z)
-    assert torch.allclose(z, 2 * x - 0.5 * y, rtol=1e-15, atol=0)
+    assert torch.allclose(z, 2 * x - 0.5 * y, rtol=1e-14, atol=1e-15)
     a = torch.tensor([3.0], dtype=torch.float64, device="cuda")
     z = y.clone()
     op.axpy_dev(-1.0, a, x, z)
-    assert torch.allclose(z, y - 3 * x, rtol=1e-15, atol=0)
+    assert torch.allclose(z, y - 3 * x, rtol=1e-14, atol=1e-15)
 
 
 def test_shape_and_species_validation():
