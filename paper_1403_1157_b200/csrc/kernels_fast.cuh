@@ -33,12 +33,12 @@ struct FastFace {
   static constexpr int WARPS = 4;
   static constexpr int FPC = FPW * WARPS;     // faces per CTA
   static constexpr int TB = NT * F * NB, TG = NT * F * NB * D, TP = NT * F * F;
-  static constexpr int TAB = TB + TG + TP + F;
+  static constexpr int TAB = (TB + TG + TP + F + 1) & ~1;
   static constexpr int NCV = 1 + M::NFX;
   // per-face scratch: normal-derivative tables (2 sides), the species
   // transpose (u_in, u_out, avg d_n u at every point) and the coupled
   // per-point results (wave speed, flux normals)
-  static constexpr int PF = 2 * F * NB + 3 * S * F + F * NCV;
+  static constexpr int PF = (2 * F * NB + 3 * S * F + F * NCV + 1) & ~1;
   static constexpr size_t smem() { return size_t(TAB + WARPS * FPW * PF) * 8; }
   static constexpr bool ok = F <= 8 && S >= 3 && S <= 8 && NB <= 10 && smem() <= 100 * 1024;
 };
@@ -56,6 +56,24 @@ __device__ __forceinline__ void load_row(const double* __restrict__ src, double*
   } else {
 #pragma unroll
     for (int i = 0; i < NB; ++i) dst[i] = __ldg(src + i);
+  }
+}
+
+// row of NB doubles from shared memory, 16-byte loads when NB is even
+// (callers keep every row 16-byte aligned)
+template <int NB>
+__device__ __forceinline__ void smem_row(const double* src, double* dst) {
+  if constexpr (NB % 2 == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int i = 0; i < NB / 2; ++i) {
+      const double2 v = s2[i];
+      dst[2 * i] = v.x;
+      dst[2 * i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) dst[i] = src[i];
   }
 }
 
@@ -132,6 +150,12 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
     lfi = p.bflf[b];
     sfac = __ldg(p.bfgeo + b);
   }
+  // lanes without a face (tail of the list, lanes >= FPW*S) mirror the
+  // code word of lane 0 so every warp-uniform branch below stays uniform
+  {
+    const int c0 = __shfl_sync(0xffffffffu, code, 0);
+    if (!active) code = c0;
+  }
   const bool mirror = code_mirror(code);
   const int tin = code_tin(code), tout = code_tout(code);
   const bool two = active && !wall && !mirror;
@@ -174,12 +198,17 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
 #pragma unroll
     for (int q = 0; q < F; ++q) {
       double u = 0.0, v = 0.0, x = 0.0, y = 0.0;
+      double bi[NB], bo[NB], di[NB], dq[NB];
+      smem_row<NB>(Bi + q * NB, bi);
+      smem_row<NB>(Bo + q * NB, bo);
+      smem_row<NB>(dpi + q * NB, di);
+      smem_row<NB>(dpo + q * NB, dq);
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        u = fma(Bi[q * NB + i], ci[i], u);
-        x = fma(dpi[q * NB + i], ci[i], x);
-        v = fma(Bo[q * NB + i], co[i], v);
-        y = fma(dpo[q * NB + i], co[i], y);
+        u = fma(bi[i], ci[i], u);
+        x = fma(di[i], ci[i], x);
+        v = fma(bo[i], co[i], v);
+        y = fma(dq[i], co[i], y);
       }
       if (mirror) {
         v = 2.0 * M::mirror_value(p.P, s) - u;
@@ -263,10 +292,15 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
       const double wq = tw[q] * sfac;
       const double Y = wq * (As * gav[q] - (qv[q] + conv[q]));
       const double X = wq * 0.5 * p.adj * As * dU[q];
+      double bi[NB], bo[NB], di[NB], dq[NB];
+      smem_row<NB>(Bi + q * NB, bi);
+      smem_row<NB>(Bo + q * NB, bo);
+      smem_row<NB>(dpi + q * NB, di);
+      smem_row<NB>(dpo + q * NB, dq);
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        ri[i] = fma(Y, Bi[q * NB + i], fma(X, dpi[q * NB + i], ri[i]));
-        ro[i] = fma(-Y, Bo[q * NB + i], fma(X, dpo[q * NB + i], ro[i]));
+        ri[i] = fma(Y, bi[i], fma(X, di[i], ri[i]));
+        ro[i] = fma(-Y, bo[i], fma(X, dq[i], ro[i]));
       }
     }
   } else {
@@ -298,6 +332,22 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
 // tile base is 16-byte aligned because every row offset e0*SN*8 is).
 template <int SN, int SNP, int NTH>
 __device__ __forceinline__ void tile_load(const double* __restrict__ src, double* dst, int nt) {
+  constexpr int TE = NTH;  // one row per thread in the fast volume kernel
+  if (SN % 2 == 0 && nt == TE) {
+    // full tile: issue every load of this thread before any store
+    constexpr int H = SN / 2, PER = (TE * H) / NTH;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = __ldcs(s2 + threadIdx.x + k * NTH);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = threadIdx.x + k * NTH, e = idx / H, r = 2 * (idx - e * H);
+      dst[e * SNP + r] = v[k].x;
+      dst[e * SNP + r + 1] = v[k].y;
+    }
+    return;
+  }
   if constexpr (SN % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
     constexpr int H = SN / 2;
@@ -367,6 +417,15 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   for (int i = tid; i < T::TGR; i += TE) tgr[i] = p.grad[i];
   for (int i = tid; i < Q; i += TE) tw[i] = p.wv[i];
   for (int i = tid; i < T::TKS; i += TE) tks[i] = p.ks[i];
+  // the FC slot tiles and U0 are consumed after the quadrature loop: start
+  // pulling them into L2 now (bulk prefetch, one thread per tile)
+  if (tid <= D + 1) {
+    const double* src = tid <= D ? FC + (int64_t(tid) * p.ne + e0) * SN : U0 + e0 * SN;
+    if (tid <= D || (mode == 2 && ca != 0.0 && U0 != nullptr)) {
+      const unsigned bytes = unsigned(nt) * SN * 8u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes & ~15u) : "memory");
+    }
+  }
   // coalesced tile load of U (owned rows are contiguous)
   tile_load<SN, SNP, TE>(U + e0 * SN, bufA, nt);
   __syncthreads();
