@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--power-iters", type=int, default=200)
+    ap.add_argument("--variant", type=int, default=0,
+                    help="kernel variant bits (tdg_set_variant), for A/B timing")
     return ap.parse_args()
 
 
@@ -125,15 +127,35 @@ class ClockSampler:
 
 # -------------------------------------------------------------- workload
 
+def weak_config(cfg, world):
+    """Weak scaling: every rank owns one config-sized x-slab of a domain
+    N times as long in x (same cells, same cell size)."""
+    import dataclasses
+    if world == 1:
+        return cfg
+    cells = (cfg.cells[0] * world,) + tuple(cfg.cells[1:])
+    lengths = (cfg.lengths[0] * world,) + tuple(cfg.lengths[1:])
+    return dataclasses.replace(cfg, cells=cells, lengths=lengths)
+
+
 def build_problem(cfg_name, scheme_name, rank=0, world=1):
+    """(cfg, space, model, scheme, U0, slab); the slab is None at N=1."""
     from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
     from paper_1403_1157_b200.configs import CONFIGS, make_mesh
-    from paper_1403_1157_b200.fields import initial_state
-    cfg = CONFIGS[cfg_name]
-    mesh = make_mesh(cfg)
+    from paper_1403_1157_b200.decomp import build_slab
+    from paper_1403_1157_b200.fields import bump_field
+    cfg = weak_config(CONFIGS[cfg_name], world)
+    slab = None
+    if world == 1:
+        mesh = make_mesh(cfg)
+    else:
+        slab = build_slab(cfg, rank, world)
+        mesh = slab.mesh
     space = DGSpace(mesh, cfg.order, 6)
-    U0 = initial_state(space, seed=1)
-    return cfg, space, PlaqueModel(), FluxScheme(scheme_name), U0
+    lo = np.zeros(cfg.dim)
+    hi = np.asarray(cfg.lengths, dtype=float)
+    U0 = np.ascontiguousarray(space.project(bump_field(cfg.dim, 6, 1, lo, hi)).coeffs)
+    return cfg, space, PlaqueModel(), FluxScheme(scheme_name), U0, slab
 
 
 def spectral_radius(op, U, iters):
@@ -180,7 +202,7 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
     """Time the CPU oracle port on the same config; returns (DoF-upd/s,
     sample description, n_dofs)."""
     from oracle import OracleOperator
-    cfg, space, model, scheme, U0 = build_problem(cfg_name, scheme_name)
+    cfg, space, model, scheme, U0, _ = build_problem(cfg_name, scheme_name)
     op = OracleOperator(space, model, scheme, nthreads=nthreads)
     if dt is None:
         from paper_1403_1157_b200.configs import rho_constant
@@ -223,9 +245,9 @@ def run_reference_arm(args, rank):
                    "n_dofs": ndofs},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthreads,
                          "kind": "port",
-                         "sample": f"{steps} SSP-RK3 steps of the full {args.config} "
-                                   "mesh, numpy oracle port (oracle/), "
-                                   f"{nthreads} threads"},
+                         "sample": f"{steps} SSP-RK3 steps of one full {args.config}-sized "
+                                   "mesh (= one rank's weak-scaling slab), numpy oracle "
+                                   f"port of the reference (oracle/), {nthreads} threads"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -242,18 +264,33 @@ def run_native_arm(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cfg, space, model, scheme, U0h = build_problem(args.config, args.scheme, rank, world)
-    op = DiscreteOperator(space, model, scheme, device=dev)
+    cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world)
+    op = DiscreteOperator(space, model, scheme, device=dev,
+                          n_owned=None if slab is None else slab.n_owned,
+                          global_ids=None if slab is None else slab.global_ids)
+    if args.variant:
+        op.set_variant(generic=bool(args.variant & 1), vol1=bool(args.variant & 2))
     t = op.tables
     d, nb = t.dim, t.nb
     ne, n_int, n_bnd = op.n_owned, len(t.if_code), len(t.bf_code)
-    n_dofs = ne * 6 * nb
+    n_dofs = ne * 6 * nb          # owned DoFs of this rank
 
+    from paper_1403_1157_b200.stepping import SSPRK3
+    halo = None
+    if slab is not None:
+        from paper_1403_1157_b200.decomp import HaloExchange
+        halo = HaloExchange(slab, dev)
+    stepper = SSPRK3(op, halo)
     U = torch.from_numpy(U0h).to(dev)
+    if halo is not None:
+        halo.exchange(U)
     rho = spectral_radius(op, U, args.power_iters)
+    if world > 1:
+        rr = torch.tensor([rho], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(rr, op=torch.distributed.ReduceOp.MAX)
+        rho = rr.item()
     dt = 0.8 * 2.51 / rho
 
-    work = torch.empty_like(U)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -261,7 +298,7 @@ def run_native_arm(args, rank, world, local):
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
-        op.ssprk3_step(U, work, dt)
+        stepper.step(U, dt)
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
@@ -275,7 +312,7 @@ def run_native_arm(args, rank, world, local):
     for a, b in evs:
         flush.fill_(1.0)
         a.record()
-        op.ssprk3_step(U, work, dt)
+        stepper.step(U, dt)
         b.record()
     torch.cuda.synchronize()
     barrier()
@@ -325,7 +362,7 @@ def run_native_arm(args, rank, world, local):
         Ud = torch.empty_like(U)
         for _ in range(2):
             Ud.copy_(Uh, non_blocking=True)
-            op.ssprk3_step(Ud, work, dt)
+            stepper.step(Ud, dt)
             Uh.copy_(Ud)
         torch.cuda.synchronize()
         barrier()
@@ -333,7 +370,7 @@ def run_native_arm(args, rank, world, local):
         a.record()
         for _ in range(args.steps):
             Ud.copy_(Uh, non_blocking=True)
-            op.ssprk3_step(Ud, work, dt)
+            stepper.step(Ud, dt)
             Uh.copy_(Ud, non_blocking=True)
         b.record()
         b.synchronize()
@@ -367,7 +404,9 @@ def run_native_arm(args, rank, world, local):
                        "boundary_faces": n_bnd, "dt": dt, "rho": rho,
                        "l2": "flushed between timed steps (256 MiB write outside "
                              "the timed events)",
-                       "parallelism": f"x-slabs x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": (f"x-slabs x{world}, NCCL ghost-row exchange per stage, "
+                            "weak scaling (one config-sized slab per GPU)")
+                           if world > 1 else "1 GPU"},
             "roofline": roof, "clocks": clocks, "gpu_launches": launches,
         }
         if cpu:

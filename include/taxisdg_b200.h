@@ -145,10 +145,11 @@ TDG_API int tdg_axpby(double a, const double* x, double b, double* y, int64_t n,
 TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y,
                  int64_t n, void* stream);
 
-/* Kernel variant selection (testing / A-B timing): generic=1 pins the
- * CTA-staged generic kernels, 0 (default) lets the library use the
- * register-resident kernels where they are compiled in. */
-TDG_API int tdg_set_variant(tdg_ctx* ctx, int generic);
+/* Kernel variant selection (testing / A-B timing).  bit 0: pin the
+ * CTA-staged generic kernels; bit 1: use the one-thread-per-element
+ * volume kernel instead of the four-lanes-per-element one.  0 (default)
+ * lets the library pick the fastest compiled-in kernels. */
+TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 
 /* Per-kernel device timing: with profiling enabled every operator kernel
  * launch is bracketed by CUDA events on its own stream;

@@ -191,7 +191,7 @@ class OracleOperator:
     """
 
     def __init__(self, space, model, scheme, nthreads: int = 1,
-                 vol_degree=None, face_degree=None):
+                 vol_degree=None, face_degree=None, global_ids=None):
         if model.n_species != space.n_species:
             raise ValueError("species count mismatch")
         self.space, self.model, self.scheme = space, model, scheme
@@ -228,6 +228,9 @@ class OracleOperator:
                      for key, (B, G, P) in self.tab.items()}
         _, self.detJ, self.Jinv = mesh.jacobians()
         self.nthreads = max(1, int(nthreads))
+        # K- ties break by GLOBAL element id (slab-local meshes renumber)
+        self.gid = (np.arange(mesh.n_elements) if global_ids is None
+                    else np.asarray(global_ids))
         self._groups()
 
     def _groups(self):
@@ -264,7 +267,8 @@ class OracleOperator:
                 if g["interior"]:
                     h = np.minimum(h, m.diameters[g["eout"]])
                     vi, vo = m.volumes[g["ein"]], m.volumes[g["eout"]]
-                    g["minus_in"] = ~((vo < vi) | ((vo == vi) & (g["eout"] < g["ein"])))
+                    gi, go = self.gid[g["ein"]], self.gid[g["eout"]]
+                    g["minus_in"] = ~((vo < vi) | ((vo == vi) & (go < gi)))
                 g["h"] = h
                 self.groups.append(g)
 

@@ -194,9 +194,10 @@ int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y, int6
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "axpy_dev");
 }
 
-int tdg_set_variant(tdg_ctx* ctx, int generic) {
+int tdg_set_variant(tdg_ctx* ctx, int variant) {
   if (!ctx) return fail(TDG_E_INVALID, "null argument");
-  ctx->force_generic = generic != 0;
+  ctx->force_generic = (variant & 1) != 0;
+  ctx->vol_variant = (variant >> 1) & 1;
   return TDG_OK;
 }
 

@@ -44,6 +44,7 @@ struct tdg_ctx {
   double ms[3] = {0, 0, 0};
   int64_t launches[3] = {0, 0, 0};
   bool force_generic = false;  // testing: pin the CTA-staged kernels
+  int vol_variant = 0;         // 0: 4 lanes/element, 1: 1 thread/element
 };
 
 namespace tdg {
@@ -64,6 +65,11 @@ int configure(int nqv) {
     e = cudaFuncSetAttribute(k_faces_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(FastFace<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_fast");
+  }
+  if constexpr (Vol4<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_volume4<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Vol4<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure volume4");
   }
   if constexpr (FastVol<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_volume_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -102,6 +108,8 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   constexpr bool fast_vol = FastVol<D, K, M>::ok;
   const bool use_ff = fast_face && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
   const bool use_fv = fast_vol && p.nqv == Dims<D, K>::NQV && !ctx->force_generic;
+  const bool use_v4 = Vol4<D, K, M>::ok && p.nqv == Dims<D, K>::NQV && !ctx->force_generic &&
+                      ctx->vol_variant == 0;
   if (use_ff) {
     if constexpr (fast_face) {
       if (p.nif + p.nbf > 0) {
@@ -128,7 +136,13 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   }
   if (p.ne > 0) {
     KernelTimer kt(ctx, 2, st);
-    if (use_fv) {
+    if (use_v4) {
+      using T = Vol4<D, K, M>;
+      const int64_t grid = (p.ne + T::TE - 1) / T::TE;
+      if constexpr (Vol4<D, K, M>::ok)
+        k_volume4<D, K, M><<<unsigned(grid), T::THREADS, T::smem(), st>>>(p, U, ctx->fc, U0, out,
+                                                                          a, b, c, mode);
+    } else if (use_fv) {
       using T = FastVol<D, K, M>;
       const int64_t grid = (p.ne + T::TE - 1) / T::TE;
       if constexpr (fast_vol)

@@ -565,4 +565,237 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   tile_store<SN, SNP, TE>(out + e0 * SN, bufA, nt);
 }
 
+// ------------------------------------------------------- volume, 4 lanes/elem
+//
+// Four threads per element split the quadrature points (q = j, j+4, ...),
+// holding only the coefficients of the species the point physics reads
+// plus their partial projections; the partials meet through two xor
+// shuffles.  The epilogue (exact-stiffness diffusion, linear source, the
+// d+1 face slots, U0 and the Runge-Kutta combination) gives each thread
+// every 4th output entry of its element: for a fixed step the 32 lanes of
+// a warp touch 8 rows x 4 consecutive doubles = 8 full 32-byte sectors,
+// so the FC / U0 / output streams need no shared-memory staging.
+
+template <int D, int K, class M>
+struct Vol4 {
+  using Dm = Dims<D, K>;
+  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, Q = Dm::NQV;
+  static constexpr int NSYM = Dm::NSYM, NEG = Dm::NEG;
+  static constexpr int TPE = 4, THREADS = 128, TE = THREADS / TPE;
+  static constexpr int NACC = M::NFLUX * NB + M::NNL * NB;
+  static constexpr int TPHI = Q * NB, TGR = Q * NB * D, TKS = NSYM * NB * NB;
+  static constexpr int TAB = (TPHI + TGR + Q + TKS + 1) & ~1;
+  static constexpr int SNP = SN | 1;
+  // prefetched tiles: D+1 face slots + U0, dense rows of SN doubles
+  static constexpr int NPF = D + 2;
+  static constexpr bool kAsync = (SN % 2) == 0;  // 16-byte cp.async granules
+  static constexpr size_t smem() {
+    return size_t(TAB + TE * SNP + TE * (NACC > 0 ? NACC : 1) + TE * NEG + TE * NB * NB +
+                  NPF * TE * SN) * 8;
+  }
+  static constexpr bool ok = M::NVAL * NB <= 40 && smem() <= 96 * 1024 && SN % TPE == 0;
+  static constexpr int MINB = 3;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int D, int K, class M>
+__global__ void __launch_bounds__(128, Vol4<D, K, M>::MINB)
+k_volume4(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
+          const double* U0, double* out, double ca, double cb, double cc, int mode) {
+  using T = Vol4<D, K, M>;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, SNP = T::SNP, Q = T::Q, TE = T::TE;
+  constexpr int NEG = T::NEG, NSYM = T::NSYM, TPE = T::TPE;
+  constexpr int NF = M::NFLUX, NL = M::NNL, NACC = T::NACC > 0 ? T::NACC : 1;
+  extern __shared__ __align__(16) double sm[];
+  double* tphi = sm;
+  double* tgr = tphi + T::TPHI;
+  double* tw = tgr + T::TGR;
+  double* tks = tw + Q;
+  double* uT = sm + T::TAB;          // [TE][SNP] coefficient rows
+  double* aT = uT + TE * SNP;        // [TE][NACC] reduced projections
+  double* gT = aT + TE * NACC;       // [TE][NEG]  geometry
+  double* kT = gT + TE * NEG;        // [TE][NB][NB] physical stiffness
+  double* pf = kT + TE * NB * NB;    // [NPF][TE][SN] prefetched FC slots, U0
+  // keep pf 16-byte aligned
+  static_assert(((T::TAB + TE * SNP + TE * NACC + TE * NEG + TE * NB * NB) % 2) == 0 || !T::kAsync,
+                "prefetch region must be 16-byte aligned");
+
+  const int tid = threadIdx.x;
+  const int64_t e0 = int64_t(blockIdx.x) * TE;
+  const int nt = int(p.ne - e0 < TE ? p.ne - e0 : TE);
+  const bool use_u0 = mode == 2 && ca != 0.0;
+  // start the epilogue's streams now; they land while the quadrature runs
+  if constexpr (T::kAsync) {
+    constexpr int H = SN / 2;
+    for (int k = 0; k < T::NPF; ++k) {
+      if (k == D + 1 && !use_u0) break;
+      const double* src = k <= D ? FC + (int64_t(k) * p.ne + e0) * SN : U0 + e0 * SN;
+      double* dst = pf + k * TE * SN;
+      for (int idx = tid; idx < nt * H; idx += 128) cp_async16(dst + 2 * idx, src + 2 * idx);
+    }
+    cp_async_commit();
+  }
+  for (int i = tid; i < T::TPHI; i += 128) tphi[i] = p.phi[i];
+  for (int i = tid; i < T::TGR; i += 128) tgr[i] = p.grad[i];
+  for (int i = tid; i < Q; i += 128) tw[i] = p.wv[i];
+  for (int i = tid; i < T::TKS; i += 128) tks[i] = p.ks[i];
+  for (int idx = tid; idx < nt * SN; idx += 128) {
+    const int e = idx / SN, r = idx - e * SN;
+    uT[e * SNP + r] = __ldg(U + e0 * SN + idx);
+  }
+  for (int idx = tid; idx < nt * NEG; idx += 128) gT[idx] = __ldg(p.egeo + e0 * NEG + idx);
+  __syncthreads();
+
+  const int el = tid / TPE, j = tid - el * TPE;
+  const bool act = el < nt;
+  const double* cr = uT + (act ? el : 0) * SNP;
+  const double* ge = gT + (act ? el : 0) * NEG;
+
+  // physical stiffness sum_p M_p KS_p of the element, shared by its lanes
+  for (int idx = j; idx < NB * NB; idx += TPE) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < NSYM; ++q) t = fma(ge[1 + q], tks[q * NB * NB + idx], t);
+    kT[(act ? el : 0) * NB * NB + idx] = t;
+  }
+
+  // ---- quadrature (points q = j, j + TPE, ...) -----------------------
+  if constexpr (NF + NL > 0) {
+    double cv[M::NVAL > 0 ? M::NVAL : 1][NB];
+#pragma unroll
+    for (int k = 0; k < M::NVAL; ++k)
+#pragma unroll
+      for (int i = 0; i < NB; ++i) cv[k][i] = cr[M::val_sp(k) * NB + i];
+    double ms[NSYM];
+#pragma unroll
+    for (int k = 0; k < NSYM; ++k) ms[k] = ge[1 + k];
+    double af[NF > 0 ? NF : 1][NB], al[NL > 0 ? NL : 1][NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+      for (int k = 0; k < (NF > 0 ? NF : 1); ++k) af[k][i] = 0.0;
+#pragma unroll
+      for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][i] = 0.0;
+    }
+#pragma unroll 1
+    for (int q = j; q < Q; q += TPE) {
+      const double* ph = tphi + q * NB;
+      const double* gr = tgr + q * NB * D;
+      double v[M::NVAL], g[M::NGRAD][D];
+#pragma unroll
+      for (int k = 0; k < M::NVAL; ++k) v[k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < M::NGRAD; ++k)
+#pragma unroll
+        for (int a = 0; a < D; ++a) g[k][a] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const double phv = ph[i];
+#pragma unroll
+        for (int k = 0; k < M::NVAL; ++k) v[k] = fma(phv, cv[k][i], v[k]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double gv = gr[i * D + a];
+#pragma unroll
+          for (int k = 0; k < M::NGRAD; ++k) g[k][a] = fma(gv, cv[M::grad_in_val(k)][i], g[k][a]);
+        }
+      }
+      double gM[M::NGRAD][D];
+#pragma unroll
+      for (int k = 0; k < M::NGRAD; ++k)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) t = fma(g[k][a], ms[sym_index(D, a, b)], t);
+          gM[k][b] = t;
+        }
+      double fr[NF > 0 ? NF : 1][D], nl[NL > 0 ? NL : 1];
+      M::template volume_point<D>(p.P, v, gM, fr, nl);
+      const double w = tw[q];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double gv = w * gr[i * D + a];
+#pragma unroll
+          for (int k = 0; k < NF; ++k) af[k][i] = fma(fr[k][a], gv, af[k][i]);
+        }
+        const double pw = w * ph[i];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) al[k][i] = fma(nl[k], pw, al[k][i]);
+      }
+    }
+    // combine the TPE partial projections of the element
+#pragma unroll
+    for (int o = 1; o < TPE; o <<= 1) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int k = 0; k < NF; ++k) af[k][i] += __shfl_xor_sync(0xffffffffu, af[k][i], o);
+#pragma unroll
+        for (int k = 0; k < NL; ++k) al[k][i] += __shfl_xor_sync(0xffffffffu, al[k][i], o);
+      }
+    }
+    if (act && j == 0) {
+      double* a = aT + el * NACC;
+#pragma unroll
+      for (int k = 0; k < NF; ++k)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) a[k * NB + i] = af[k][i];
+#pragma unroll
+      for (int k = 0; k < NL; ++k)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) a[NF * NB + k * NB + i] = al[k][i];
+    }
+  }
+  if constexpr (T::kAsync) cp_async_wait_all();
+  __syncthreads();
+  if (!act) return;
+
+  // ---- epilogue: every TPE-th output entry of the element --------------
+  const double detJ = ge[0];
+  const double idet = 1.0 / detJ;
+  const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
+  const int64_t row = (e0 + el) * SN;
+  const int64_t slot_stride = p.ne * SN;
+  const double* kp = kT + el * NB * NB;
+#pragma unroll
+  for (int k = 0; k < SN / TPE; ++k) {
+    const int r = j + TPE * k;
+    const int s = r / NB, i = r - s * NB;
+    double dif = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj) dif = fma(cr[s * NB + jj], kp[jj * NB + i], dif);
+    double lin = 0.0;
+#pragma unroll
+    for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
+    double acc = lin - p.A[s] * dif;
+    if constexpr (NF + NL > 0) {
+      const int fi = M::flux_index(s), li = M::nl_index(s);
+      if (fi >= 0) acc += aT[el * NACC + fi * NB + i];
+      if (li >= 0) acc += aT[el * NACC + NF * NB + li * NB + i];
+    }
+    double rv = detJ * acc;
+#pragma unroll
+    for (int lf = 0; lf <= D; ++lf)
+      rv += T::kAsync ? pf[(lf * TE + el) * SN + r] : __ldcs(FC + lf * slot_stride + row + r);
+    double o;
+    if (mode == 0) o = rv;
+    else if (mode == 1) o = rv * idet;
+    else {
+      o = fma(cb, cr[r], scale * rv);
+      if (use_u0)
+        o = fma(ca, T::kAsync ? pf[((D + 1) * TE + el) * SN + r] : __ldcs(U0 + row + r), o);
+    }
+    out[row + r] = o;
+  }
+}
+
 }  // namespace tdg

@@ -43,6 +43,9 @@ struct PlaqueDev {
   static constexpr int NNL = 1;    // bilinear part of S_c1
   __host__ __device__ static constexpr int val_sp(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 3 : 5; }
   __host__ __device__ static constexpr int grad_sp(int k) { return k == 0 ? 0 : k == 1 ? 3 : 5; }
+  // position of grad_sp(k) in the val_sp list (the gradient species are
+  // a subset of the value species, so one coefficient copy serves both)
+  __host__ __device__ static constexpr int grad_in_val(int k) { return k == 0 ? 0 : k == 1 ? 2 : 3; }
   __host__ __device__ static constexpr int flux_sp(int k) { return k; }
   __host__ __device__ static constexpr int nl_sp(int) { return 3; }
   __host__ __device__ static constexpr int flux_index(int s) { return s <= 1 ? s : -1; }
@@ -56,10 +59,10 @@ struct PlaqueDev {
                                                       double* nl) {
     const double n1 = v[0], n2 = v[1], c1 = v[2], c3 = v[3];
     const double c1p = fmax(c1, 0.0);
-    const double x11 = P[C11A] * n1 / (c1p + P[C11B]);
-    const double x13 = P[C13A] * n1 / (fmax(c3, 0.0) + P[C13B]);
-    const double x21 = P[C21A] * n2 / (c1p + P[C21B]);
-    const double x2n = P[C2NA] * n2 / (fmax(n1, 0.0) + P[C2NB]);
+    const double x11 = P[C11A] * n1 * rcp(c1p + P[C11B]);
+    const double x13 = P[C13A] * n1 * rcp(fmax(c3, 0.0) + P[C13B]);
+    const double x21 = P[C21A] * n2 * rcp(c1p + P[C21B]);
+    const double x2n = P[C2NA] * n2 * rcp(fmax(n1, 0.0) + P[C2NB]);
 #pragma unroll
     for (int b = 0; b < D; ++b) {
       fr[0][b] = x11 * gM[1][b] + x13 * gM[2][b];
@@ -184,6 +187,7 @@ struct ReducedDev {
   static constexpr int NNL = 1;    // -alpha1 n1 c1 on c1
   __host__ __device__ static constexpr int val_sp(int k) { return k == 0 ? 0 : 2; }
   __host__ __device__ static constexpr int grad_sp(int) { return 2; }
+  __host__ __device__ static constexpr int grad_in_val(int) { return 1; }
   __host__ __device__ static constexpr int flux_sp(int) { return 0; }
   __host__ __device__ static constexpr int nl_sp(int) { return 2; }
   __host__ __device__ static constexpr int flux_index(int s) { return s == 0 ? 0 : -1; }
@@ -194,7 +198,7 @@ struct ReducedDev {
   __device__ __forceinline__ static void volume_point(const double* P, const double* v,
                                                       const double (*gM)[D], double (*fr)[D],
                                                       double* nl) {
-    const double x11 = P[C11A] * v[0] / (fmax(v[1], 0.0) + P[C11B]);
+    const double x11 = P[C11A] * v[0] * rcp(fmax(v[1], 0.0) + P[C11B]);
 #pragma unroll
     for (int b = 0; b < D; ++b) fr[0][b] = x11 * gM[0][b];
     nl[0] = -P[ALPHA1] * v[0] * v[1];
@@ -270,6 +274,7 @@ struct DiffusionDev {
   static constexpr int NVAL = 0, NGRAD = 0, NFLUX = 0, NNL = 0;
   __host__ __device__ static constexpr int val_sp(int) { return 0; }
   __host__ __device__ static constexpr int grad_sp(int) { return 0; }
+  __host__ __device__ static constexpr int grad_in_val(int) { return 0; }
   __host__ __device__ static constexpr int flux_sp(int) { return 0; }
   __host__ __device__ static constexpr int nl_sp(int) { return 0; }
   __host__ __device__ static constexpr int flux_index(int) { return -1; }

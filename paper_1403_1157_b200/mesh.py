@@ -274,6 +274,57 @@ class Mesh:
 # reference generators ``mesh.py:463-554``)
 
 
+def _square_parts(nx, ny, gamma1_in, lengths, jitter, seed, cells_x):
+    """Vertices, elements (two triangles (a,b,c), (a,c,d) per cell, cell
+    order x fastest), global element ids and the tag function of the
+    cell columns [cells_x[0], cells_x[1]) of the nx x ny grid.  Vertex
+    coordinates are the global grid's, bit for bit."""
+    i0, i1 = cells_x
+    xs = np.linspace(0.0, 1.0, nx + 1)
+    ys = np.linspace(0.0, 1.0, ny + 1)
+    nvx = i1 - i0 + 1                               # local vertex columns
+    X, Y = np.meshgrid(xs[i0:i1 + 1], ys)
+    verts = np.stack([X.ravel(), Y.ravel()], axis=1)
+    I, J = np.meshgrid(np.arange(i1 - i0), np.arange(ny))
+    I, J = I.ravel(), J.ravel()
+    a = J * nvx + I
+    b, c, d = a + 1, a + nvx + 1, a + nvx
+    elems = np.empty((2 * len(a), 3), dtype=np.int64)
+    elems[0::2] = np.stack([a, b, c], axis=1)
+    elems[1::2] = np.stack([a, c, d], axis=1)
+    gcell = J * nx + (I + i0)
+    gids = np.empty(2 * len(a), dtype=np.int64)
+    gids[0::2] = 2 * gcell
+    gids[1::2] = 2 * gcell + 1
+
+    def tag_fn(keys):
+        vi, vj = keys % nvx + i0, keys // nvx          # global grid indices
+        tags = np.full(len(keys), int(BoundaryTag.NO_FLOW), dtype=np.int8)
+        bottom = (vj[:, 0] == 0) & (vj[:, 1] == 0)
+        top = (vj[:, 0] == ny) & (vj[:, 1] == ny)
+        g0 = vi.min(axis=1)
+        mid = 0.5 * (xs[g0] + xs[np.minimum(g0 + 1, nx)])
+        inflow = (gamma1_in[0] <= mid) & (mid <= gamma1_in[1])
+        tags[bottom] = np.where(inflow[bottom], int(BoundaryTag.GAMMA1_IN),
+                                int(BoundaryTag.GAMMA1))
+        tags[top] = int(BoundaryTag.GAMMA2)
+        return tags
+
+    if tuple(lengths) != (1.0, 1.0):
+        verts = verts * np.asarray(lengths, dtype=float)[None, :]
+    if jitter > 0.0:
+        # the global jitter field, sliced: slabs see the same vertices
+        rng = np.random.default_rng(seed)
+        h = np.asarray(lengths, dtype=float) / np.array([nx, ny])
+        shift = rng.uniform(-jitter, jitter, size=((ny + 1) * (nx + 1), 2)) * h[None, :]
+        gvi = np.arange(len(verts)) % nvx + i0
+        gvj = np.arange(len(verts)) // nvx
+        interior = (gvi > 0) & (gvi < nx) & (gvj > 0) & (gvj < ny)
+        verts = verts.copy()
+        verts[interior] += shift[(gvj * (nx + 1) + gvi)[interior]]
+    return verts, elems, gids, tag_fn
+
+
 def unit_square(nx: int, ny: int | None = None,
                 gamma1_in=(0.25, 0.75), lengths=(1.0, 1.0),
                 jitter: float = 0.0, seed: int = 0) -> Mesh:
@@ -289,42 +340,8 @@ def unit_square(nx: int, ny: int | None = None,
     ny = nx if ny is None else ny
     if nx < 1 or ny < 1:
         raise ValueError("nx and ny must be >= 1")
-    xs = np.linspace(0.0, 1.0, nx + 1)
-    ys = np.linspace(0.0, 1.0, ny + 1)
-    X, Y = np.meshgrid(xs, ys)                    # vertex id j*(nx+1)+i
-    verts = np.stack([X.ravel(), Y.ravel()], axis=1)
-    I, J = np.meshgrid(np.arange(nx), np.arange(ny))
-    I, J = I.ravel(), J.ravel()
-    a = J * (nx + 1) + I
-    b, c, d = a + 1, a + nx + 2, a + nx + 1
-    elems = np.empty((2 * nx * ny, 3), dtype=np.int64)
-    elems[0::2] = np.stack([a, b, c], axis=1)
-    elems[1::2] = np.stack([a, c, d], axis=1)
-
-    def tag_fn(keys):
-        vi, vj = keys % (nx + 1), keys // (nx + 1)
-        tags = np.full(len(keys), int(BoundaryTag.NO_FLOW), dtype=np.int8)
-        bottom = (vj[:, 0] == 0) & (vj[:, 1] == 0)
-        top = (vj[:, 0] == ny) & (vj[:, 1] == ny)
-        i0 = vi.min(axis=1)
-        mid = 0.5 * (xs[i0] + xs[np.minimum(i0 + 1, nx)])
-        inflow = (gamma1_in[0] <= mid) & (mid <= gamma1_in[1])
-        tags[bottom] = np.where(inflow[bottom], int(BoundaryTag.GAMMA1_IN),
-                                int(BoundaryTag.GAMMA1))
-        tags[top] = int(BoundaryTag.GAMMA2)
-        return tags
-
-    verts = verts * np.asarray(lengths, dtype=float)[None, :] \
-        if tuple(lengths) != (1.0, 1.0) else verts
-    if jitter > 0.0:
-        rng = np.random.default_rng(seed)
-        h = np.asarray(lengths, dtype=float) / np.array([nx, ny])
-        shift = rng.uniform(-jitter, jitter, size=verts.shape) * h[None, :]
-        vi = np.arange(len(verts)) % (nx + 1)
-        vj = np.arange(len(verts)) // (nx + 1)
-        interior = (vi > 0) & (vi < nx) & (vj > 0) & (vj < ny)
-        verts = verts.copy()
-        verts[interior] += shift[interior]
+    verts, elems, _, tag_fn = _square_parts(nx, ny, gamma1_in, lengths,
+                                            jitter, seed, (0, nx))
     return Mesh(verts, elems, tag_fn=tag_fn)
 
 
@@ -334,44 +351,38 @@ KUHN_PATHS = [(0, 1 << p0, (1 << p0) | (1 << p1), 7)
               for p0, p1, _ in itertools.permutations((0, 1, 2))]
 
 
-def unit_cube(nx: int, ny: int | None = None, nz: int | None = None,
-              gamma1_in=(0.25, 0.75, 0.25, 0.75), top_tag=BoundaryTag.GAMMA2,
-              lengths=(1.0, 1.0, 1.0)) -> Mesh:
-    """Six Kuhn tetrahedra per cell.  Bottom (z=0) GAMMA1 with the
-    rectangle ``gamma1_in`` = (x0, x1, y0, y1) tagged GAMMA1_IN by cell
-    centre (None: no inflow patch), top ``top_tag`` (reference: GAMMA2),
-    everything else NO_FLOW."""
-    ny = nx if ny is None else ny
-    nz = nx if nz is None else nz
-    if min(nx, ny, nz) < 1:
-        raise ValueError("nx, ny, nz must be >= 1")
+def _cube_parts(nx, ny, nz, gamma1_in, top_tag, lengths, cells_x):
+    i0, i1 = cells_x
     xs = np.linspace(0.0, 1.0, nx + 1)
     ys = np.linspace(0.0, 1.0, ny + 1)
     zs = np.linspace(0.0, 1.0, nz + 1)
-    Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
+    nvx = i1 - i0 + 1
+    Z, Y, X = np.meshgrid(zs, ys, xs[i0:i1 + 1], indexing="ij")
     verts = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
-    K, J, I = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx),
+    K, J, I = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(i1 - i0),
                           indexing="ij")
     I, J, K = I.ravel(), J.ravel(), K.ravel()
 
     def vid(i, j, k):
-        return (k * (ny + 1) + j) * (nx + 1) + i
+        return (k * (ny + 1) + j) * nvx + i
 
-    elems = np.empty((6 * nx * ny * nz, 4), dtype=np.int64)
+    elems = np.empty((6 * len(I), 4), dtype=np.int64)
     for t, path in enumerate(KUHN_PATHS):
         elems[t::6] = np.stack([vid(I + (b & 1), J + ((b >> 1) & 1),
                                     K + ((b >> 2) & 1)) for b in path], axis=1)
+    gcell = (K * ny + J) * nx + (I + i0)
+    gids = (6 * gcell[:, None] + np.arange(6)[None, :]).ravel()
 
     def tag_fn(keys):
-        vi = keys % (nx + 1)
-        vj = (keys // (nx + 1)) % (ny + 1)
-        vk = keys // ((nx + 1) * (ny + 1))
+        vi = keys % nvx + i0
+        vj = (keys // nvx) % (ny + 1)
+        vk = keys // (nvx * (ny + 1))
         tags = np.full(len(keys), int(BoundaryTag.NO_FLOW), dtype=np.int8)
         bottom = np.all(vk == 0, axis=1)
         top = np.all(vk == nz, axis=1)
-        i0, j0 = vi.min(axis=1), vj.min(axis=1)
-        cx = 0.5 * (xs[i0] + xs[np.minimum(i0 + 1, nx)])
-        cy = 0.5 * (ys[j0] + ys[np.minimum(j0 + 1, ny)])
+        g0, h0 = vi.min(axis=1), vj.min(axis=1)
+        cx = 0.5 * (xs[g0] + xs[np.minimum(g0 + 1, nx)])
+        cy = 0.5 * (ys[h0] + ys[np.minimum(h0 + 1, ny)])
         if gamma1_in is None:
             inflow = np.zeros(len(keys), dtype=bool)
         else:
@@ -385,4 +396,20 @@ def unit_cube(nx: int, ny: int | None = None, nz: int | None = None,
 
     if tuple(lengths) != (1.0, 1.0, 1.0):
         verts = verts * np.asarray(lengths, dtype=float)[None, :]
+    return verts, elems, gids, tag_fn
+
+
+def unit_cube(nx: int, ny: int | None = None, nz: int | None = None,
+              gamma1_in=(0.25, 0.75, 0.25, 0.75), top_tag=BoundaryTag.GAMMA2,
+              lengths=(1.0, 1.0, 1.0)) -> Mesh:
+    """Six Kuhn tetrahedra per cell.  Bottom (z=0) GAMMA1 with the
+    rectangle ``gamma1_in`` = (x0, x1, y0, y1) tagged GAMMA1_IN by cell
+    centre (None: no inflow patch), top ``top_tag`` (reference: GAMMA2),
+    everything else NO_FLOW."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    if min(nx, ny, nz) < 1:
+        raise ValueError("nx, ny, nz must be >= 1")
+    verts, elems, _, tag_fn = _cube_parts(nx, ny, nz, gamma1_in, top_tag,
+                                          lengths, (0, nx))
     return Mesh(verts, elems, tag_fn=tag_fn)

@@ -177,11 +177,13 @@ class DiscreteOperator:
 
     KERNELS = ("faces", "wall", "volume")
 
-    def set_variant(self, generic: bool):
-        """Pin the generic CTA-staged kernels (True) or let the library pick
-        the register-resident ones where compiled in (False, default)."""
-        _native.check(self.lib.tdg_set_variant(self._ctx, int(bool(generic))),
-                      "tdg_set_variant")
+    def set_variant(self, generic: bool = False, vol1: bool = False):
+        """Kernel selection for testing / A-B timing: ``generic`` pins the
+        CTA-staged generic kernels; ``vol1`` the one-thread-per-element
+        volume kernel.  Defaults: fastest compiled-in kernels."""
+        _native.check(self.lib.tdg_set_variant(
+            self._ctx, int(bool(generic)) | (int(bool(vol1)) << 1)),
+            "tdg_set_variant")
 
     def profile(self, enable: bool = True):
         """Bracket every operator kernel launch with CUDA events on its
@@ -199,22 +201,26 @@ class DiscreteOperator:
     # -- explicit stepping / Krylov primitives (device tensors) ----------
 
     def _check_vec(self, name, x, rows=None):
-        """Raw-pointer entry points need dense fp64 CUDA storage."""
+        """Raw-pointer entry points need dense fp64 CUDA storage; state
+        vectors have the owned rows first (ghost rows optional)."""
         torch = _torch()
         if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 \
                 or x.device.type != "cuda" or not x.is_contiguous():
             raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
-        if rows is not None and tuple(x.shape) != (rows, self.space.n_species,
-                                                   self.space.nb):
-            raise ValueError(f"{name} has shape {tuple(x.shape)}, expected "
-                             f"{(rows, self.space.n_species, self.space.nb)}")
+        ok_rows = (self.n_owned, self.n_rows) if rows is None else (rows,)
+        if rows is not None or x.dim() == 3:
+            if x.dim() != 3 or x.shape[1:] != (self.space.n_species, self.space.nb) \
+                    or x.shape[0] not in ok_rows:
+                raise ValueError(f"{name} has shape {tuple(x.shape)}, expected "
+                                 f"(rows in {ok_rows}, {self.space.n_species}, "
+                                 f"{self.space.nb})")
 
     def rk_stage(self, U0, U, out, a: float, b: float, c: float, t: float = 0.0):
         """out = a U0 + b U + c M^-1 L(U) in one fused pass."""
         self._check_vec("U", U, self.n_rows)
-        self._check_vec("out", out, self.n_owned)
+        self._check_vec("out", out)
         if U0 is not None:
-            self._check_vec("U0", U0, self.n_owned)
+            self._check_vec("U0", U0)
         _native.check(self.lib.tdg_rk_stage(
             self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
             out.data_ptr(), float(a), float(b), float(c), float(t),
@@ -230,6 +236,7 @@ class DiscreteOperator:
         return U
 
     def dot(self, x, y, out=None):
+        x, y = x.reshape(-1), y.reshape(-1)
         self._check_vec("x", x)
         self._check_vec("y", y)
         if x.numel() != y.numel():
@@ -241,6 +248,7 @@ class DiscreteOperator:
         return out
 
     def norm2(self, x, out=None):
+        x = x.reshape(-1)
         self._check_vec("x", x)
         out = self._scalar[1:] if out is None else out
         _native.check(self.lib.tdg_norm2(self._ctx, x.data_ptr(), x.numel(),
@@ -249,16 +257,20 @@ class DiscreteOperator:
         return out
 
     def axpby(self, a: float, x, b: float, y):
-        self._check_vec("x", x)
-        self._check_vec("y", y)
+        if x.numel() != y.numel():
+            raise ValueError("x and y differ in size")
+        self._check_vec("x", x.reshape(-1))
+        self._check_vec("y", y.reshape(-1))
         _native.check(self.lib.tdg_axpby(float(a), x.data_ptr(), float(b),
                                          y.data_ptr(), x.numel(), self._stream()),
                       "tdg_axpby")
         return y
 
     def axpy_dev(self, s: float, alpha, x, y):
-        self._check_vec("x", x)
-        self._check_vec("y", y)
+        if x.numel() != y.numel():
+            raise ValueError("x and y differ in size")
+        self._check_vec("x", x.reshape(-1))
+        self._check_vec("y", y.reshape(-1))
         _native.check(self.lib.tdg_axpy_dev(float(s), alpha.data_ptr(),
                                             x.data_ptr(), y.data_ptr(),
                                             x.numel(), self._stream()),

@@ -1,0 +1,38 @@
+"""Explicit time stepping on the device.
+
+``SSPRK3`` is the Shu-Osher SSP-RK3 the benchmark configs use (SURVEY
+8(a) a14: U1 = U + dt f(U); U2 = 3/4 U + 1/4 (U1 + dt f(U1));
+U3 = 1/3 U + 2/3 (U2 + dt f(U2))), each stage one fused operator
+application + stage update (``tdg_rk_stage``).  With a slab
+decomposition (``decomp.HaloExchange``) the ghost rows of the stage
+input are refreshed before every stage.
+"""
+
+from __future__ import annotations
+
+__all__ = ["SSPRK3"]
+
+
+class SSPRK3:
+    def __init__(self, op, halo=None):
+        self.op = op
+        self.halo = halo
+        self._work = None
+
+    def _stage(self, U0, U, out, a, b, c):
+        if self.halo is not None:
+            self.halo.exchange(U)
+        self.op.rk_stage(U0, U, out, a, b, c)
+
+    def step(self, U, dt: float):
+        """Advance U (owned rows first, then ghost rows) in place."""
+        import torch
+        if self._work is None or self._work.shape != U.shape:
+            self._work = torch.empty_like(U)
+        if self.halo is None:
+            return self.op.ssprk3_step(U, self._work, dt)
+        W = self._work
+        self._stage(None, U, W, 0.0, 1.0, dt)
+        self._stage(U, W, W, 0.75, 0.25, 0.25 * dt)
+        self._stage(U, W, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt)
+        return U

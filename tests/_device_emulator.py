@@ -84,7 +84,40 @@ class DeviceEmulator:
                 for k, s in enumerate(fsp):
                     R[:, s] += w[q] * np.einsum("ea,ia->ei", fr[k], gr[q])
                 R[:, nsp] += w[q] * nl[0][:, None] * phi[q][None, :]
-        R = detJ[:, None, None] * R + FC.sum(axis=1)
+        R = detJ[:, None, None] * R
+        if FC is not None:
+            R = R + FC.sum(axis=1)
+        return R
+
+    def apply_tiled(self, U, tiles):
+        """Fused-kernel semantics: per tile, volume rows then the tile's
+        face entries colour by colour into the tile's rows."""
+        from paper_1403_1157_b200.tiling import CODE_WALL, CODE_WIN, CODE_WOUT
+        t = self.t
+        vol = self._volume(U, None)
+        R = np.full_like(vol, np.nan)
+        nc = tiles.n_colors
+        for k in range(tiles.n_tiles):
+            rows = tiles.rows[tiles.tile_ptr[k]:tiles.tile_ptr[k + 1]]
+            nown = tiles.tile_nown[k]
+            acc = vol[rows[:nown]].copy()
+            for c in range(nc):
+                b, e = tiles.color_ptr[k * (nc + 1) + c], tiles.color_ptr[k * (nc + 1) + c + 1]
+                for j in range(b, e):
+                    code = int(tiles.ent_code[j])
+                    si = int(tiles.ent_slots[j]) & 0xFFFF
+                    so = (int(tiles.ent_slots[j]) >> 16) & 0xFFFF
+                    ein = rows[si]
+                    if code & CODE_WALL:
+                        ri, ro = self.wall_contrib(U, code, ein, tiles.ent_geo[j, 2 * t.dim]), None
+                    else:
+                        eout = rows[so] if so != 0xFFFF else -1
+                        ri, ro = self.face_contrib(U, code, ein, eout, tiles.ent_geo[j])
+                    if code & CODE_WIN:
+                        acc[si] += ri
+                    if code & CODE_WOUT:
+                        acc[so] += ro
+            R[rows[:nown]] = acc
         return R
 
     def _conv(self, ui, uo, gn, dU, qv):
@@ -115,14 +148,22 @@ class DeviceEmulator:
 
     def _faces(self, U, FC):
         t = self.t
-        d, S, nb = t.dim, t.n_species, t.nb
-        F = t.nq_face
         for f in range(len(t.if_code)):
             code = int(t.if_code[f])
+            ein, eout = t.if_elems[f]
+            ri, ro = self.face_contrib(U, code, ein, eout, t.if_geo[f])
+            FC[ein, t.if_lf[f, 0]] = ri
+            if ro is not None and not (code & SKIP):
+                FC[eout, t.if_lf[f, 1]] = ro
+
+    def face_contrib(self, U, code, ein, eout, g):
+        """(inside row, outside row or None) of one interior/mirror face."""
+        t = self.t
+        d, S, nb = t.dim, t.n_species, t.nb
+        F = t.nq_face
+        if True:
             tin, tout = code & 31, (code >> 5) & 31
             mirror = bool(code & MIRROR)
-            ein, eout = t.if_elems[f]
-            g = t.if_geo[f]
             jin, jout = g[:d], g[d:2 * d]
             sfac, h, idi, ido = g[2 * d:2 * d + 4]
             dpi = np.einsum("qia,a->qi", t.face_G[tin], jin)
@@ -160,18 +201,22 @@ class DeviceEmulator:
             wq = t.face_w * sfac
             Y = wq[None, :] * (self.A[:, None] * gn - qv.T)
             X = wq[None, :] * 0.5 * self.adj * self.A[:, None] * dU
-            FC[ein, t.if_lf[f, 0]] = Y @ t.face_B[tin] + X @ dpi
-            if not mirror and not (code & SKIP):
-                FC[eout, t.if_lf[f, 1]] = -Y @ t.face_B[tout] + X @ dpo
+            ri = Y @ t.face_B[tin] + X @ dpi
+            ro = None if mirror else -Y @ t.face_B[tout] + X @ dpo
+            return ri, ro
 
     def _wall(self, U, FC):
         t = self.t
+        for f in range(len(t.bf_code)):
+            FC[t.bf_elem[f], t.bf_lf[f]] = self.wall_contrib(
+                U, int(t.bf_code[f]), t.bf_elem[f], t.bf_geo[f])
+
+    def wall_contrib(self, U, code, e, sfac):
+        t = self.t
         S = t.n_species
         P = self.P
-        for f in range(len(t.bf_code)):
-            code = int(t.bf_code[f])
+        if True:
             tin, tag = code & 31, (code >> 11) & 7
-            e = t.bf_elem[f]
             B = t.face_B[tin]
             q = np.zeros((S, t.nq_face))
             if self.mid == MODEL_PLAQUE:
@@ -186,5 +231,5 @@ class DeviceEmulator:
                 c1 = B @ U[e, 2]
                 if tag in (1, 2):
                     q[0] = -P[0] * P[21] * _heav(c1 - P[24], P[26])
-            Y = -(t.face_w * t.bf_geo[f])[None, :] * q
-            FC[e, t.bf_lf[f]] = Y @ B
+            Y = -(t.face_w * sfac)[None, :] * q
+            return Y @ B

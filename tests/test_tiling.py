@@ -1,0 +1,83 @@
+"""Host tiling for the fused operator kernel: ownership, write-once face
+sides, conflict-free colours, and the fused accumulation order emulated
+against the reference golden outputs."""
+import numpy as np
+import pytest
+
+from paper_1403_1157_b200 import (DGSpace, DiffusionModel, FluxScheme,
+                                  PlaqueModel, unit_cube, unit_square)
+from paper_1403_1157_b200.tables import build_tables, scheme_constants
+from paper_1403_1157_b200.tiling import (CODE_WALL, CODE_WIN, CODE_WOUT,
+                                         build_tiles)
+
+from _cases import operator_case
+from _device_emulator import DeviceEmulator
+from test_oracle_golden import _golden_names
+
+
+def _check_invariants(t, tiles, n_own):
+    owned = np.concatenate([tiles.rows[tiles.tile_ptr[k]:tiles.tile_ptr[k] + tiles.tile_nown[k]]
+                            for k in range(tiles.n_tiles)])
+    assert np.array_equal(np.sort(owned), np.arange(n_own))
+    # every face side that must be written is written exactly once
+    writes = {}
+    nc = tiles.n_colors
+    for k in range(tiles.n_tiles):
+        rows = tiles.rows[tiles.tile_ptr[k]:tiles.tile_ptr[k + 1]]
+        nown = tiles.tile_nown[k]
+        for c in range(nc):
+            seen = set()
+            b, e = tiles.color_ptr[k * (nc + 1) + c], tiles.color_ptr[k * (nc + 1) + c + 1]
+            for j in range(b, e):
+                code = int(tiles.ent_code[j])
+                si = int(tiles.ent_slots[j]) & 0xFFFF
+                so = (int(tiles.ent_slots[j]) >> 16) & 0xFFFF
+                for flag, slot in ((CODE_WIN, si), (CODE_WOUT, so)):
+                    if code & flag:
+                        assert slot < nown
+                        assert slot not in seen, "colour conflict"
+                        seen.add(slot)
+                        writes[(int(rows[slot]), j, flag)] = 1
+    n_sides = 0
+    for f in range(len(t.if_code)):
+        n_sides += 1 + int(not (int(t.if_code[f]) & ((1 << 14) | (1 << 15))))
+    n_sides += len(t.bf_code)
+    assert len(writes) == n_sides
+
+
+@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
+@pytest.mark.parametrize("te", [8, 64])
+def test_fused_order_matches_reference(golden, name, te):
+    space, model, scheme, U, R, _ = operator_case(golden, name)
+    t = build_tables(space, model, scheme)
+    tiles = build_tiles(t, space.mesh.centroids, te=te)
+    _check_invariants(t, tiles, space.mesh.n_elements)
+    em = DeviceEmulator(t, model, scheme.id, *scheme_constants(space, scheme))
+    got = em.apply_tiled(U, tiles)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+@pytest.mark.parametrize("dirichlet", [0, 1])
+def test_fused_order_heat(golden, dirichlet):
+    h = golden["heat"]
+    space = DGSpace(unit_square(3), 2)
+    model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
+    for scheme in ("cdg2", "br2", "ip"):
+        key = f"heat_sq3_{scheme}_{dirichlet}"
+        sc = FluxScheme(scheme)
+        t = build_tables(space, model, sc)
+        tiles = build_tiles(t, space.mesh.centroids, te=8)
+        _check_invariants(t, tiles, space.mesh.n_elements)
+        em = DeviceEmulator(t, model, sc.id, *scheme_constants(space, sc))
+        got = em.apply_tiled(h[f"{key}__U"], tiles)
+        R = h[f"{key}__R"]
+        assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+def test_tiles_at_c2_size():
+    space = DGSpace(unit_square(512, 128, lengths=(4.0, 1.0)), 2, 6)
+    t = build_tables(space, PlaqueModel(), FluxScheme("cdg2"))
+    tiles = build_tiles(t, space.mesh.centroids, te=256)
+    st = tiles.stats()
+    assert st["tiles"] == 512 and st["colors"] <= 6 and st["halo_fraction"] < 0.3
+    assert tiles.max_rows < 400
