@@ -269,7 +269,7 @@ def run_native_arm(args, rank, world, local):
                           n_owned=None if slab is None else slab.n_owned,
                           global_ids=None if slab is None else slab.global_ids)
     if args.variant:
-        op.set_variant(generic=bool(args.variant & 1), vol1=bool(args.variant & 2))
+        op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2))
     t = op.tables
     d, nb = t.dim, t.nb
     ne, n_int, n_bnd = op.n_owned, len(t.if_code), len(t.bf_code)
@@ -338,11 +338,18 @@ def run_native_arm(args, rank, world, local):
                          "share_of_step": tms / ms}
     peak = fp64_peak(op)
     dom = max(per, key=lambda k: per[k]["avg_ms"])
+    traffic = None
+    try:  # dram read+write bytes per launch from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh)["bytes_per_launch"].get(f"k_{dom}")
+    except (OSError, ValueError, KeyError):
+        traffic = None
     step_flops = 3 * (fv + ff + fb)
     roof = {"bound": "fp64", "kernel": f"k_{dom}",
             "achieved": per[dom]["algorithmic_tflops"], "peak": peak,
             "unit": "TFLOP/s", "frac": per[dom]["algorithmic_tflops"] / peak,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full dram bytes/launch)",
             "peak_source": "measured DFMA loop (tdg_fp64_probe) on this GPU; "
                            f"nominal {FP64_NOMINAL_TFLOPS} TFLOP/s; "
                            "MEASURED_PEAKS.json has no fp64 figure",

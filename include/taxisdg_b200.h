@@ -146,8 +146,8 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
                  int64_t n, void* stream);
 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
- * CTA-staged generic kernels; bit 1: use the one-thread-per-element
- * volume kernel instead of the four-lanes-per-element one.  0 (default)
+ * CTA-staged generic kernels; bit 1: use the four-lanes-per-element
+ * volume kernel instead of the one-thread-per-element one.  0 (default)
  * lets the library pick the fastest compiled-in kernels. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 

@@ -44,7 +44,7 @@ struct tdg_ctx {
   double ms[3] = {0, 0, 0};
   int64_t launches[3] = {0, 0, 0};
   bool force_generic = false;  // testing: pin the CTA-staged kernels
-  int vol_variant = 0;         // 0: 4 lanes/element, 1: 1 thread/element
+  int vol_variant = 0;         // 0: 1 thread/element (default), 1: 4 lanes/element
 };
 
 namespace tdg {
@@ -109,7 +109,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   const bool use_ff = fast_face && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
   const bool use_fv = fast_vol && p.nqv == Dims<D, K>::NQV && !ctx->force_generic;
   const bool use_v4 = Vol4<D, K, M>::ok && p.nqv == Dims<D, K>::NQV && !ctx->force_generic &&
-                      ctx->vol_variant == 0;
+                      ctx->vol_variant == 1;
   if (use_ff) {
     if constexpr (fast_face) {
       if (p.nif + p.nbf > 0) {

@@ -177,12 +177,12 @@ class DiscreteOperator:
 
     KERNELS = ("faces", "wall", "volume")
 
-    def set_variant(self, generic: bool = False, vol1: bool = False):
+    def set_variant(self, generic: bool = False, vol4: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
-        CTA-staged generic kernels; ``vol1`` the one-thread-per-element
+        CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel.  Defaults: fastest compiled-in kernels."""
         _native.check(self.lib.tdg_set_variant(
-            self._ctx, int(bool(generic)) | (int(bool(vol1)) << 1)),
+            self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)),
             "tdg_set_variant")
 
     def profile(self, enable: bool = True):
