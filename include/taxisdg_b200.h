@@ -123,11 +123,13 @@ TDG_API int tdg_apply(tdg_ctx* ctx, const double* U, double* R, double t,
               int mass_inverse, void* stream);
 
 /* out = a*U0 + b*U + c*M^-1 L_h(U); U0 may be NULL when a == 0; out may
- * alias U or U0 (each element reads its own rows before writing). */
+ * alias U0.  out may alias U too, but then the volume part cannot overlap
+ * the face kernel (serial schedule). */
 TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out,
                  double a, double b, double c, double t, void* stream);
 
-/* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U. */
+/* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U (a
+ * second stage vector is allocated by the library on first use). */
 TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt,
                     void* stream);
 
@@ -147,14 +149,17 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
  * CTA-staged generic kernels; bit 1: use the four-lanes-per-element
- * volume kernel instead of the one-thread-per-element one.  0 (default)
- * lets the library pick the fastest compiled-in kernels. */
+ * volume kernel instead of the one-thread-per-element one; bit 2: run
+ * volume and faces serially on the caller's stream instead of the
+ * overlapped two-stream schedule.  0 (default) lets the library pick the
+ * fastest compiled-in kernels and schedule. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 
 /* Per-kernel device timing: with profiling enabled every operator kernel
  * launch is bracketed by CUDA events on its own stream;
  * tdg_profile_read synchronizes, returns the accumulated milliseconds and
- * launch counts per kernel (index 0 faces, 1 wall, 2 volume) and resets. */
+ * launch counts per kernel (ms[4], launches[4]: 0 faces, 1 wall, 2 volume,
+ * 3 face-slot sum of the overlapped path) and resets. */
 TDG_API int tdg_profile(tdg_ctx* ctx, int enable);
 TDG_API int tdg_profile_read(tdg_ctx* ctx, double* ms, int64_t* launches);
 
@@ -163,6 +168,9 @@ TDG_API int tdg_profile_read(tdg_ctx* ctx, double* ms, int64_t* launches);
  * thread to out[148*8*256]; flops = 148*8*256*16*2*iters. */
 TDG_API int tdg_fp64_probe(double* out, int64_t iters, void* stream);
 TDG_API int64_t tdg_fp64_probe_threads(void);
+/* FP64 tensor-core (DMMA m8n8k4) probe on the same grid: per warp 4
+ * independent 8x8x4 MMAs per iteration, flops = threads/32*iters*4*512. */
+TDG_API int tdg_dmma_probe(double* out, int64_t iters, void* stream);
 
 #ifdef __cplusplus
 }

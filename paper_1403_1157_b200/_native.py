@@ -67,7 +67,8 @@ def load(path: str = LIB):
     lib.tdg_profile_read.argtypes = [_p, ctypes.POINTER(_d), ctypes.POINTER(_i64)]
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
-    for name in ("tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
+    for name in ("tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev"):

@@ -105,6 +105,13 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.bfcode = d.bf_code;
   p.bfgeo = d.bf_geo;
 
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+      ctx->num_sms = sms;
+    cudaGetLastError();
+  }
   int rc = impl.configure(d.nq_vol);
   if (rc != TDG_OK) {
     delete ctx;
@@ -123,6 +130,12 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     delete ctx;
     return cuda_fail(e, "cudaMalloc reduction workspace");
   }
+  if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_vol, cudaEventDisableTiming) != cudaSuccess) {
+    ctx->overlap = false;  // serial path still works
+    cudaGetLastError();
+  }
   *out = ctx;
   return TDG_OK;
 }
@@ -136,6 +149,10 @@ int tdg_destroy(tdg_ctx* ctx) {
     }
   cudaFree(ctx->fc);
   cudaFree(ctx->part);
+  if (ctx->work2) cudaFree(ctx->work2);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_vol) cudaEventDestroy(ctx->ev_vol);
   delete ctx;
   return TDG_OK;
 }
@@ -158,14 +175,29 @@ int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out, d
 int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, void* stream) {
   if (!ctx || !U || !work) return fail(TDG_E_INVALID, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  (void)t;
+  const int64_t rows = ctx->d.n_elements + ctx->d.n_ghost;
+  const size_t n = size_t(rows) * ctx->d.n_species * ctx->d.nb;
+  // the overlapped application must not write its own input: stage 2
+  // goes to a second (library-owned) work vector
+  if (!ctx->work2 || ctx->work2_n < n) {
+    if (ctx->work2) cudaFree(ctx->work2);
+    ctx->work2 = nullptr;
+    ctx->work2_n = 0;
+    if (cudaMalloc(&ctx->work2, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TDG_E_CUDA, "cudaMalloc ssprk3 work");
+    }
+    ctx->work2_n = n;
+  }
+  double* w2 = ctx->work2;
   int rc = ctx->impl.run(ctx, U, nullptr, work, 0.0, 1.0, dt, 2, st);  // U1 = U + dt f(U)
   if (rc) return rc;
-  // U2 = 3/4 U + 1/4 (U1 + dt f(U1)), in place on work
-  rc = ctx->impl.run(ctx, work, U, work, 0.75, 0.25, 0.25 * dt, 2, st);
+  // U2 = 3/4 U + 1/4 (U1 + dt f(U1))
+  rc = ctx->impl.run(ctx, work, U, w2, 0.75, 0.25, 0.25 * dt, 2, st);
   if (rc) return rc;
-  // U3 = 1/3 U + 2/3 (U2 + dt f(U2)), in place on U
-  (void)t;
-  return ctx->impl.run(ctx, work, U, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, st);
+  // U3 = 1/3 U + 2/3 (U2 + dt f(U2)), written over U (U is only U0 here)
+  return ctx->impl.run(ctx, w2, U, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, st);
 }
 
 int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* result,
@@ -198,6 +230,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   if (!ctx) return fail(TDG_E_INVALID, "null argument");
   ctx->force_generic = (variant & 1) != 0;
   ctx->vol_variant = (variant >> 1) & 1;
+  ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   return TDG_OK;
 }
 
@@ -209,7 +242,7 @@ int tdg_profile(tdg_ctx* ctx, int enable) {
 
 int tdg_profile_read(tdg_ctx* ctx, double* ms, int64_t* launches) {
   if (!ctx || !ms || !launches) return fail(TDG_E_INVALID, "null argument");
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     for (auto& pr : ctx->ev[k]) {
       cudaError_t e = cudaEventSynchronize(pr.second);
       if (e != cudaSuccess) return cuda_fail(e, "profile_read");
@@ -235,5 +268,11 @@ int tdg_fp64_probe(double* out, int64_t iters, void* stream) {
 }
 
 int64_t tdg_fp64_probe_threads(void) { return fp64_probe_threads(); }
+
+int tdg_dmma_probe(double* out, int64_t iters, void* stream) {
+  if (!out || iters < 1) return fail(TDG_E_INVALID, "bad argument");
+  cudaError_t e = launch_dmma_probe(out, iters, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "dmma_probe");
+}
 
 }  // extern "C"

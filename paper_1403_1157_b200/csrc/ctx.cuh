@@ -40,10 +40,18 @@ struct tdg_ctx {
   tdg::Impl impl;
   // profiling: event pairs per kernel kind, drained by tdg_profile_read
   bool profile = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
-  double ms[3] = {0, 0, 0};
-  int64_t launches[3] = {0, 0, 0};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
+  double ms[4] = {0, 0, 0, 0};
+  int64_t launches[4] = {0, 0, 0, 0};
   bool force_generic = false;  // testing: pin the CTA-staged kernels
+  int num_sms = 148;
+  // overlapped application: volume part on `aux` concurrent with the
+  // face kernel on the caller's stream, then the face-slot sum
+  bool overlap = true;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_vol = nullptr;
+  double* work2 = nullptr;  // second SSP-RK3 stage vector (library-owned)
+  size_t work2_n = 0;
   int vol_variant = 0;         // 0: 1 thread/element (default), 1: 4 lanes/element
 };
 
@@ -98,18 +106,13 @@ struct KernelTimer {
   }
 };
 
+template <class M, int D, int K>
+constexpr int SN_of() { return M::S * Dims<D, K>::NB; }
+
 template <int D, int K, class M>
-int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
-        double c, int mode, cudaStream_t st) {
+void run_faces(tdg_ctx* ctx, const double* U, cudaStream_t st, bool use_ff) {
   const OpParams& p = ctx->p;
-  // register-resident kernels when the tables / working set fit and the
-  // default quadrature is in use; generic CTA-staged kernels otherwise
   constexpr bool fast_face = FastFace<D, K, M>::ok;
-  constexpr bool fast_vol = FastVol<D, K, M>::ok;
-  const bool use_ff = fast_face && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
-  const bool use_fv = fast_vol && p.nqv == Dims<D, K>::NQV && !ctx->force_generic;
-  const bool use_v4 = Vol4<D, K, M>::ok && p.nqv == Dims<D, K>::NQV && !ctx->force_generic &&
-                      ctx->vol_variant == 1;
   if (use_ff) {
     if constexpr (fast_face) {
       if (p.nif + p.nbf > 0) {
@@ -134,6 +137,49 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
       k_wall<D, K, M><<<unsigned(grid), kThreads, WallTile<D, K, M>::smem(), st>>>(p, U, ctx->fc);
     }
   }
+}
+
+template <int D, int K, class M>
+int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
+        double c, int mode, cudaStream_t st) {
+  const OpParams& p = ctx->p;
+  // register-resident kernels when the tables / working set fit and the
+  // default quadrature is in use; generic CTA-staged kernels otherwise
+  constexpr bool fast_face = FastFace<D, K, M>::ok;
+  constexpr bool fast_vol = FastVol<D, K, M>::ok;
+  const bool use_ff = fast_face && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
+  const bool use_fv = fast_vol && p.nqv == Dims<D, K>::NQV && !ctx->force_generic;
+  const bool use_v4 = Vol4<D, K, M>::ok && p.nqv == Dims<D, K>::NQV && !ctx->force_generic &&
+                      ctx->vol_variant == 1;
+  // overlapped path: fast volume kernel (without the face-slot sum) on the
+  // aux stream while the face kernel runs; out must not alias U (the face
+  // kernel still reads U), U0 may alias out (read before written per row)
+  const bool overlap = use_fv && use_ff && ctx->overlap && ctx->aux && out != U && p.ne > 0 &&
+                       (SN_of<M, D, K>() % 2 == 0);
+  if (overlap) {
+    if constexpr (fast_vol && (SN_of<M, D, K>() % 2 == 0)) {
+      using T = FastVol<D, K, M>;
+      cudaEventRecord(ctx->ev_in, st);
+      cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
+      {
+        KernelTimer kt(ctx, 2, ctx->aux);
+        const int64_t grid = (p.ne + T::TE - 1) / T::TE;
+        k_volume_fast<D, K, M><<<unsigned(grid), T::TE, T::smem(), ctx->aux>>>(
+            p, U, ctx->fc, U0, out, a, b, c, mode | 4);
+      }
+      cudaEventRecord(ctx->ev_vol, ctx->aux);
+      run_faces<D, K, M>(ctx, U, st, use_ff);
+      cudaStreamWaitEvent(st, ctx->ev_vol, 0);
+      KernelTimer kt(ctx, 3, st);
+      const int64_t n2 = p.ne * (SN_of<M, D, K>() / 2);
+      const int grid = int(n2 / 256 + 1 < 148 * 8 ? n2 / 256 + 1 : 148 * 8);
+      k_fc_add<D, SN_of<M, D, K>(), Dims<D, K>::NEG><<<grid, 256, 0, st>>>(
+          ctx->fc, p.egeo, p.ne, out, c, mode);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
+  }
+  run_faces<D, K, M>(ctx, U, st, use_ff);
   if (p.ne > 0) {
     KernelTimer kt(ctx, 2, st);
     if (use_v4) {

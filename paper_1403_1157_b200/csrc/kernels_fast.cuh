@@ -41,6 +41,7 @@ struct FastFace {
   static constexpr int PF = (2 * F * NB + 3 * S * F + F * NCV + 1) & ~1;
   static constexpr size_t smem() { return size_t(TAB + WARPS * FPW * PF) * 8; }
   static constexpr bool ok = F <= 8 && S >= 3 && S <= 8 && NB <= 10 && smem() <= 100 * 1024;
+  static constexpr int MINB = NB <= 6 ? 4 : 3;  // register budget: 128 / 168
 };
 
 template <int NB>
@@ -89,8 +90,75 @@ __device__ __forceinline__ void store_row(double* dst, const double* v) {
   }
 }
 
+template <int D, int NB>
+struct FaceRec {
+  int code, ein, eout, lfi, lfo;
+  bool active, wall;
+  double jn[2][D], sfac, h, idi, ido;
+  double ci[NB], co[NB];
+};
+
+// Face record and the two coefficient rows of species s for warp-group gw.
 template <int D, int K, class M>
-__global__ void __launch_bounds__(128)
+__device__ __forceinline__ void load_face_group(const OpParams& p, const double* __restrict__ U,
+                                                int64_t gw, int64_t wi, int grp, int s, bool lane_ok,
+                                                FaceRec<D, Dims<D, K>::NB>& r) {
+  using T = FastFace<D, K, M>;
+  constexpr int NB = T::NB, SN = T::SN, FPW = T::FPW, NFG = Dims<D, K>::NFG;
+  r.wall = gw >= wi;
+  const int64_t f = r.wall ? p.nif + (gw - wi) * FPW + grp : gw * FPW + grp;
+  r.active = lane_ok && (r.wall ? f < p.nif + p.nbf : f < p.nif);
+  r.code = 0;
+  r.ein = 0;
+  r.eout = -1;
+  r.lfi = 0;
+  r.lfo = 0;
+  r.sfac = 0.0;
+  r.h = 1.0;
+  r.idi = 0.0;
+  r.ido = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) r.jn[0][a] = r.jn[1][a] = 0.0;
+  if (r.active && !r.wall) {
+    r.code = __ldg(p.ifcode + f);
+    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
+    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
+    r.ein = el.x;
+    r.eout = el.y;
+    r.lfi = lf.x;
+    r.lfo = lf.y;
+    const double* g = p.ifgeo + f * NFG;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      r.jn[0][a] = __ldg(g + a);
+      r.jn[1][a] = __ldg(g + D + a);
+    }
+    r.sfac = __ldg(g + 2 * D);
+    r.h = __ldg(g + 2 * D + 1);
+    r.idi = __ldg(g + 2 * D + 2);
+    r.ido = __ldg(g + 2 * D + 3);
+  } else if (r.active) {
+    const int64_t b = f - p.nif;
+    r.code = __ldg(p.bfcode + b);
+    r.ein = __ldg(p.bfel + b);
+    r.lfi = __ldg(p.bflf + b);
+    r.sfac = __ldg(p.bfgeo + b);
+  }
+  if (r.active) load_row<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
+  else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) r.ci[i] = 0.0;
+  }
+  const bool two = r.active && !r.wall && !code_mirror(r.code);
+  if (two) load_row<NB>(U + int64_t(r.eout) * SN + s * NB, r.co);
+  else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) r.co[i] = 0.0;
+  }
+}
+
+template <int D, int K, class M>
+__global__ void __launch_bounds__(128, FastFace<D, K, M>::MINB)
 k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
   using T = FastFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW, NCV = T::NCV;
@@ -109,67 +177,40 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / S, s = lane - grp * S, base = grp * S;
   const bool lane_ok = grp < FPW;
-  // warps [0, wi) take interior faces, warps [wi, ...) wall faces: every
-  // warp is wholly interior or wholly wall (uniform __syncwarp/shuffles)
-  const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
-  const int64_t wi = (p.nif + FPW - 1) / FPW;
-  const bool wall = gw >= wi;
-  const int64_t f = wall ? p.nif + (gw - wi) * FPW + grp : gw * FPW + grp;
-  const bool active = lane_ok && (wall ? f < p.nif + p.nbf : f < p.nif);
-  if (!__any_sync(0xffffffffu, active)) return;  // warp-uniform
-
   double* scratch = sm + T::TAB + (warp * FPW + (lane_ok ? grp : 0)) * T::PF;
   double* dph = scratch;                    // [2][F][NB]
   double* xch = dph + 2 * F * NB;           // [3][S][F]
   double* cvs = xch + 3 * S * F;            // [F][NCV]
 
-  int code = 0, ein = 0, eout = -1, lfi = 0, lfo = 0;
-  double jn[2][D], sfac = 0.0, h = 1.0, idi = 0.0, ido = 0.0;
-#pragma unroll
-  for (int a = 0; a < D; ++a) jn[0][a] = jn[1][a] = 0.0;
-  if (active && !wall) {
-    code = p.ifcode[f];
-    ein = p.ifel[2 * f];
-    eout = p.ifel[2 * f + 1];
-    lfi = p.iflf[2 * f];
-    lfo = p.iflf[2 * f + 1];
-    const double* g = p.ifgeo + f * NFG;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      jn[0][a] = __ldg(g + a);
-      jn[1][a] = __ldg(g + D + a);
-    }
-    sfac = __ldg(g + 2 * D);
-    h = __ldg(g + 2 * D + 1);
-    idi = __ldg(g + 2 * D + 2);
-    ido = __ldg(g + 2 * D + 3);
-  } else if (active) {
-    const int64_t b = f - p.nif;
-    code = p.bfcode[b];
-    ein = p.bfel[b];
-    lfi = p.bflf[b];
-    sfac = __ldg(p.bfgeo + b);
-  }
-  // lanes without a face (tail of the list, lanes >= FPW*S) mirror the
-  // code word of lane 0 so every warp-uniform branch below stays uniform
+  const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
+  const int64_t wi = (p.nif + FPW - 1) / FPW;
+  FaceRec<D, NB> cur;
+  load_face_group<D, K, M>(p, U, gw, wi, grp, s, lane_ok, cur);
+  const bool wall = cur.wall, active = cur.active;
+  if (!__any_sync(0xffffffffu, active)) return;  // warp-uniform
+  int code = cur.code;
+  // lanes without a face copy lane 0's code word so every warp-uniform
+  // branch below stays uniform
   {
     const int c0 = __shfl_sync(0xffffffffu, code, 0);
     if (!active) code = c0;
   }
+  const int ein = cur.ein, eout = cur.eout, lfi = cur.lfi, lfo = cur.lfo;
+  const double sfac = cur.sfac, h = cur.h, idi = cur.idi, ido = cur.ido;
+  double jn[2][D];
+#pragma unroll
+  for (int a2 = 0; a2 < D; ++a2) {
+    jn[0][a2] = cur.jn[0][a2];
+    jn[1][a2] = cur.jn[1][a2];
+  }
   const bool mirror = code_mirror(code);
   const int tin = code_tin(code), tout = code_tout(code);
   const bool two = active && !wall && !mirror;
-
   double ci[NB], co[NB];
-  if (active) load_row<NB>(U + int64_t(ein) * SN + s * NB, ci);
-  else {
 #pragma unroll
-    for (int i = 0; i < NB; ++i) ci[i] = 0.0;
-  }
-  if (two) load_row<NB>(U + int64_t(eout) * SN + s * NB, co);
-  else {
-#pragma unroll
-    for (int i = 0; i < NB; ++i) co[i] = 0.0;
+  for (int i = 0; i < NB; ++i) {
+    ci[i] = cur.ci[i];
+    co[i] = cur.co[i];
   }
   const double* Bi = tB + tin * F * NB;
   const double* Bo = tB + tout * F * NB;
@@ -181,14 +222,24 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
   if (!wall) {
     // per-face normal-derivative test tables dphi.n = G . (Jinv n), shared
     // by the S lanes of the face
+    // lane s builds modes i = s, s+S, ... of both sides' tables
     if (lane_ok) {
-      for (int idx = s; idx < 2 * F * NB; idx += S) {
-        const int side = idx / (F * NB), qi = idx - side * F * NB;
-        const double* g = tG + ((side ? tout : tin) * F * NB + qi) * D;
-        double v = 0.0;
 #pragma unroll
-        for (int a = 0; a < D; ++a) v = fma(g[a], side ? jn[1][a] : jn[0][a], v);
-        dph[idx] = v;
+      for (int k = 0; k < (NB + S - 1) / S; ++k) {
+        const int i = s + k * S;
+        if (i < NB) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            const double* g = tG + ((side ? tout : tin) * F * NB + i) * D;
+#pragma unroll
+            for (int q = 0; q < F; ++q) {
+              double v = 0.0;
+#pragma unroll
+              for (int a = 0; a < D; ++a) v = fma(g[q * NB * D + a], jn[side][a], v);
+              dph[(side * F + q) * NB + i] = v;
+            }
+          }
+        }
       }
     }
     __syncwarp();
@@ -210,9 +261,11 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
         v = fma(bo[i], co[i], v);
         y = fma(dq[i], co[i], y);
       }
-      if (mirror) {
-        v = 2.0 * M::mirror_value(p.P, s) - u;
-        y = x;
+      if constexpr (M::kMirror) {
+        if (mirror) {
+          v = 2.0 * M::mirror_value(p.P, s) - u;
+          y = x;
+        }
       }
       ui[q] = u;
       uo[q] = v;
@@ -236,7 +289,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
       __syncwarp();
       if (lane_ok) {
         for (int q = s; q < F; q += S) {
-          auto fetch = [&](int kind, int sp) { return xch[(kind * S + sp) * F + q]; };
+          const double* xq = xch + q;
+          auto fetch = [xq](int kind, int sp) { return xq[(kind * S + sp) * F]; };
           M::face_point(p.P, fetch, cvs + q * NCV);
         }
       }
@@ -409,6 +463,9 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   double* tks = tw + Q;
   double* bufA = sm + T::TAB;
   double* bufB = bufA + TE * SNP;
+  // mode bit 2: the face-slot sum is added by k_fc_add (overlapped run)
+  const bool with_fc = (mode & 4) == 0;
+  mode &= 3;
   const int tid = threadIdx.x;
   const int64_t e0 = int64_t(blockIdx.x) * TE;
   const int nt = int(p.ne - e0 < TE ? p.ne - e0 : TE);
@@ -421,7 +478,7 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   // pulling them into L2 now (bulk prefetch, one thread per tile)
   if (tid <= D + 1) {
     const double* src = tid <= D ? FC + (int64_t(tid) * p.ne + e0) * SN : U0 + e0 * SN;
-    if (tid <= D || (mode == 2 && ca != 0.0 && U0 != nullptr)) {
+    if ((tid <= D && with_fc) || (tid == D + 1 && (mode & 3) == 2 && ca != 0.0 && U0 != nullptr)) {
       const unsigned bytes = unsigned(nt) * SN * 8u;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes & ~15u) : "memory");
     }
@@ -547,7 +604,7 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
 
   // (3) face-slot tiles (FC[lf] rows of this tile are contiguous)
 #pragma unroll 1
-  for (int lf = 0; lf <= D; ++lf) {
+  for (int lf = 0; lf <= (with_fc ? D : -1); ++lf) {
     __syncthreads();
     tile_load<SN, SNP, TE>(FC + (int64_t(lf) * p.ne + e0) * SN, bufB, nt);
     __syncthreads();
@@ -563,6 +620,40 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   }
   __syncthreads();
   tile_store<SN, SNP, TE>(out + e0 * SN, bufA, nt);
+}
+
+// out += scale(e) * sum_lf FC[lf][e]: the face-slot sum of an overlapped
+// application (volume part on a second stream, concurrent with the face
+// kernel).  Pure streaming: 16-byte loads/stores, grid-stride.
+template <int D, int SN, int NEG>
+__global__ void __launch_bounds__(256)
+k_fc_add(const double* __restrict__ FC, const double* __restrict__ egeo, int64_t ne,
+         double* __restrict__ out, double cc, int mode) {
+  static_assert(SN % 2 == 0, "16-byte path");
+  constexpr int H = SN / 2;
+  const int64_t n2 = ne * H;
+  const double2* f2 = reinterpret_cast<const double2*>(FC);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  for (int64_t idx = int64_t(blockIdx.x) * 256 + threadIdx.x; idx < n2;
+       idx += int64_t(gridDim.x) * 256) {
+    const int64_t e = idx / H;
+    double sc = 1.0;
+    if (mode != 0) {
+      const double idet = 1.0 / __ldg(egeo + e * NEG);
+      sc = mode == 1 ? idet : cc * idet;
+    }
+    double2 acc = __ldcs(f2 + idx);
+#pragma unroll
+    for (int lf = 1; lf <= D; ++lf) {
+      const double2 v = __ldcs(f2 + lf * n2 + idx);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    double2 o = o2[idx];
+    o.x = fma(sc, acc.x, o.x);
+    o.y = fma(sc, acc.y, o.y);
+    o2[idx] = o;
+  }
 }
 
 // ------------------------------------------------------- volume, 4 lanes/elem

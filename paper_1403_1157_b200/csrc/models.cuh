@@ -36,6 +36,7 @@ __device__ __forceinline__ double heaviside(double s, double eps) {
 struct PlaqueDev {
   static constexpr int S = 6;
   static constexpr bool kConv = true;
+  static constexpr bool kMirror = false;  // closed by prescribed fluxes only
   // volume point inputs/outputs
   static constexpr int NVAL = 4;   // n1 n2 c1 c3
   static constexpr int NGRAD = 3;  // n1 c1 c3
@@ -181,6 +182,7 @@ struct PlaqueDev {
 struct ReducedDev {
   static constexpr int S = 3;
   static constexpr bool kConv = true;
+  static constexpr bool kMirror = false;
   static constexpr int NVAL = 2;   // n1 c1
   static constexpr int NGRAD = 1;  // c1
   static constexpr int NFLUX = 1;  // row n1
@@ -271,6 +273,7 @@ template <int NS>
 struct DiffusionDev {
   static constexpr int S = NS;
   static constexpr bool kConv = false;
+  static constexpr bool kMirror = true;
   static constexpr int NVAL = 0, NGRAD = 0, NFLUX = 0, NNL = 0;
   __host__ __device__ static constexpr int val_sp(int) { return 0; }
   __host__ __device__ static constexpr int grad_sp(int) { return 0; }

@@ -127,4 +127,29 @@ cudaError_t launch_fp64_probe(double* out, int64_t iters, cudaStream_t st) {
 
 int64_t fp64_probe_threads() { return int64_t(kProbeBlocks) * kProbeThreads; }
 
+// FP64 tensor-core probe: mma.sync.m8n8k4 f64 (DMMA), 4 independent
+// accumulator tiles per warp; flops = blocks*8 warps*iters*4*2*8*8*4.
+__global__ void __launch_bounds__(256) k_dmma_probe(double* out, int64_t iters) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + 1e-9 * lane, b = 1.0 - 1e-9 * lane;
+  double c[4][2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k][0] = c[k][1] = 0.001 * k;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+  out[int64_t(blockIdx.x) * 256 + threadIdx.x] = s;
+}
+
+cudaError_t launch_dmma_probe(double* out, int64_t iters, cudaStream_t st) {
+  k_dmma_probe<<<kProbeBlocks, 256, 0, st>>>(out, iters);
+  return cudaGetLastError();
+}
+
 }  // namespace tdg

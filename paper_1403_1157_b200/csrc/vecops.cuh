@@ -11,4 +11,5 @@ cudaError_t launch_axpy_dev(double s, const double* alpha, const double* x, doub
                             cudaStream_t st);
 cudaError_t launch_fp64_probe(double* out, int64_t iters, cudaStream_t st);
 int64_t fp64_probe_threads();
+cudaError_t launch_dmma_probe(double* out, int64_t iters, cudaStream_t st);
 }  // namespace tdg

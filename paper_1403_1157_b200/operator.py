@@ -175,15 +175,17 @@ class DiscreteOperator:
 
     # -- device timing ---------------------------------------------------
 
-    KERNELS = ("faces", "wall", "volume")
+    KERNELS = ("faces", "wall", "volume", "fc_add")
 
-    def set_variant(self, generic: bool = False, vol4: bool = False):
+    def set_variant(self, generic: bool = False, vol4: bool = False,
+                    serial: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
-        volume kernel.  Defaults: fastest compiled-in kernels."""
+        volume kernel; ``serial`` disables the two-stream overlap of the
+        volume part with the face kernel.  Defaults: fastest."""
         _native.check(self.lib.tdg_set_variant(
-            self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)),
-            "tdg_set_variant")
+            self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
+            | (int(bool(serial)) << 2)), "tdg_set_variant")
 
     def profile(self, enable: bool = True):
         """Bracket every operator kernel launch with CUDA events on its
@@ -192,8 +194,8 @@ class DiscreteOperator:
                       "tdg_profile")
 
     def profile_read(self) -> dict:
-        ms = (ctypes.c_double * 3)()
-        n = (ctypes.c_int64 * 3)()
+        ms = (ctypes.c_double * 4)()
+        n = (ctypes.c_int64 * 4)()
         _native.check(self.lib.tdg_profile_read(self._ctx, ms, n),
                       "tdg_profile_read")
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}

@@ -55,7 +55,15 @@ def test_variants_agree_at_size():
     b = op.apply_f(U)
     op.set_variant(vol4=True)
     c = op.apply_f(U)
-    for x in (b, c):
+    op.set_variant(serial=True)
+    d = op.apply_f(U)
+    out = torch.empty_like(U)
+    op.set_variant()
+    op.rk_stage(U, U, out, 0.25, 0.5, 1e-3)      # overlapped (out != U)
+    out2 = U.clone()
+    op.rk_stage(U, out2, out2, 0.25, 0.5, 1e-3)   # in place: serial path
+    assert torch.allclose(out, out2, rtol=1e-14, atol=1e-16)
+    for x in (b, c, d):
         assert rel_l2_per_species(space, a.cpu().numpy(), x.cpu().numpy()).max() <= 1e-13
 
 
