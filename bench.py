@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--power-iters", type=int, default=200)
+    ap.add_argument("--integrator", default="ssprk3", choices=["ssprk3", "sdirk3"],
+                    help="sdirk3: the reference's default SDIRK3 + JFNK at --dt")
+    ap.add_argument("--dt", type=float, default=0.01)
     ap.add_argument("--variant", type=int, default=0,
                     help="kernel variant bits (tdg_set_variant), for A/B timing")
     return ap.parse_args()
@@ -428,11 +431,49 @@ def run_native_arm(args, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def run_implicit(args, rank, world, local):
+    """C2 with the reference's default integrator: SDIRK3 + JFNK (dt 0.01,
+    Newton 1e-8/1e-12/25, GMRES 1e-4/30/200; reference config.py:74-83).
+    DoF-updates counted per actual f evaluation."""
+    import torch
+    from paper_1403_1157_b200.operator import DiscreteOperator
+    from paper_1403_1157_b200.timeint import integrate
+    torch.cuda.set_device(local)
+    cfg, space, model, scheme, U0h, _ = build_problem(args.config, args.scheme)
+    op = DiscreteOperator(space, model, scheme)
+    U = torch.from_numpy(U0h).cuda()
+    nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
+          "gmres_restart": 30, "gmres_maxiter": 200}
+    integrate(op, U, 0.0, 1.0, args.dt, order=3, n_steps=max(1, args.warmup),
+              newton_kwargs=nk)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    res = integrate(op, U, 0.0, 1.0, args.dt, order=3, n_steps=args.steps, newton_kwargs=nk)
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b)
+    n_dofs = space.n_dofs
+    line = {"metric": METRIC, "value": n_dofs * res.f_evaluations / (ms * 1e-3),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.description + f", {args.scheme}, SDIRK3 + JFNK "
+                       f"(reference defaults), dt {args.dt}",
+                       "f_evaluations": res.f_evaluations,
+                       "newton_iterations": res.newton_iterations,
+                       "gmres_iterations": res.gmres_iterations}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference_arm(args, rank)
+        return
+    if args.integrator == "sdirk3":
+        run_implicit(args, rank, world, local)
         return
     run_native_arm(args, rank, world, local)
 

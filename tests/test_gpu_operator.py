@@ -267,3 +267,57 @@ def test_two_slabs_on_one_gpu_match_global(name, cells):
             own = gid[:sl.n_owned]
             assert torch.allclose(out[:sl.n_owned], ref.index_select(0, own),
                                   rtol=1e-13, atol=1e-15)
+
+
+def test_sdirk3_jfnk_matches_reference_trajectory(golden):
+    """Device SDIRK3 + JFNK + GMRES (timeint.py:137-380) against the
+    reference's own integrate() run (tightened tolerances)."""
+    from paper_1403_1157_b200.timeint import integrate
+    t = golden["trajectories"]
+    space = DGSpace(unit_square(4), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    res = integrate(op, t["sdirk__U0"], 0.0, 1.0, 0.01, order=3, n_steps=2,
+                    newton_kwargs={"rtol": 1e-11, "atol": 1e-13, "gmres_rtol": 1e-6})
+    err = rel_l2_per_species(space, res.U, t["sdirk__U2"])
+    assert err.max() <= 1e-9, err
+    assert res.f_evaluations > 0 and res.gmres_iterations > 0
+
+
+def test_sdirk_failure_raises_solver_error():
+    from paper_1403_1157_b200.timeint import SolverError, integrate
+    space = DGSpace(unit_square(4), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    U0 = initial_state(space, 3)
+    with pytest.raises(SolverError) as exc:
+        integrate(op, U0, 0.0, 1.0, 0.01, order=3, n_steps=1,
+                  newton_kwargs={"maxiter": 1, "rtol": 1e-14, "atol": 0.0})
+    assert exc.value.diagnostics["stage"] == 0
+
+
+@pytest.mark.parametrize("order", [2, 4])
+def test_sdirk_orders_match_oracle_composition(order):
+    """SDIRK2/4 tableaux on the device vs the same integrator composed on
+    the CPU oracle (timeint.py:71-101 tableaux)."""
+    from oracle.taxis_oracle import _gmres, _newton  # noqa: F401
+    from paper_1403_1157_b200.timeint import dirk_tableau, integrate
+    space = DGSpace(unit_square(4), 1, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme("cdg2"))
+    U0 = initial_state(space, 5)
+    nk = {"rtol": 1e-12, "atol": 1e-14, "gmres_rtol": 1e-8}
+    res = integrate(op, U0, 0.0, 1.0, 2e-3, order=order, n_steps=2, newton_kwargs=nk)
+    # oracle composition with the same tableau
+    ref = OracleOperator(space, model, FluxScheme("cdg2"))
+    tab = dirk_tableau(order)
+    U = U0.copy()
+    for _ in range(2):
+        K = []
+        for i in range(tab.n_stages):
+            base = U + 2e-3 * sum(tab.A[i, j] * K[j] for j in range(i))
+            aii = tab.A[i, i]
+            G = lambda v, base=base, aii=aii: (v.reshape(U.shape) - base - 2e-3 * aii
+                                               * ref.apply_f(v.reshape(U.shape))).ravel()
+            V = _newton(G, base.ravel(), **nk).reshape(U.shape)
+            K.append((V - base) / (2e-3 * aii))
+        U = U + 2e-3 * sum(tab.b[i] * K[i] for i in range(tab.n_stages))
+    assert rel_l2_per_species(space, res.U, U).max() <= 1e-9
