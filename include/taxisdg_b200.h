@@ -106,6 +106,9 @@ typedef struct tdg_desc {
   const int32_t* bf_lf;       /* [nbf]    local face index */
   const int32_t* bf_code;     /* [nbf]    packed code word */
   const double* bf_geo;       /* [nbf]    sfac */
+  /* optional: zero-padded per-signature operand tables of the tensor-core
+   * (DMMA) face kernel, layout of tables.mma_face_tables (NULL disables it) */
+  const double* face_mma;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -151,8 +154,9 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * CTA-staged generic kernels; bit 1: use the four-lanes-per-element
  * volume kernel instead of the one-thread-per-element one; bit 2: run
  * volume and faces serially on the caller's stream instead of the
- * overlapped two-stream schedule.  0 (default) lets the library pick the
- * fastest compiled-in kernels and schedule. */
+ * overlapped two-stream schedule; bit 3: flip the face-kernel choice
+ * between the tensor-core (DMMA) kernel and the SIMT kernel.  0 (default)
+ * lets the library pick the fastest compiled-in kernels and schedule. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 
 /* Per-kernel device timing: with profiling enabled every operator kernel

@@ -18,7 +18,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtaxisdg_b200.so")
 SOURCES = ["capi.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
            "inst_diffusion.cu"]
-HEADERS = ["common.cuh", "ctx.cuh", "kernels.cuh", "kernels_fast.cuh", "models.cuh",
+HEADERS = ["common.cuh", "ctx.cuh", "kernels.cuh", "kernels_fast.cuh", "kernels_mma.cuh",
+           "models.cuh",
            "vecops.cuh"]
 
 NVCC_FLAGS = [

@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "kernels_fast.cuh"
+#include "kernels_mma.cuh"
 #include "models.cuh"
 #include "vecops.cuh"
 
@@ -45,6 +46,7 @@ struct tdg_ctx {
   int64_t launches[4] = {0, 0, 0, 0};
   bool force_generic = false;  // testing: pin the CTA-staged kernels
   int num_sms = 148;
+  bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -69,6 +71,11 @@ int configure(int nqv) {
   e = cudaFuncSetAttribute(k_wall<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(WallTile<D, K, M>::smem()));
   if (e != cudaSuccess) return cuda_fail(e, "configure wall");
+  if constexpr (MmaFace<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_faces_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(MmaFace<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_mma");
+  }
   if constexpr (FastFace<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_faces_fast<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(FastFace<D, K, M>::smem()));
@@ -113,6 +120,22 @@ template <int D, int K, class M>
 void run_faces(tdg_ctx* ctx, const double* U, cudaStream_t st, bool use_ff) {
   const OpParams& p = ctx->p;
   constexpr bool fast_face = FastFace<D, K, M>::ok;
+  // tensor-core face kernel: default in 3D, opt-in (flip) in 2D
+  constexpr bool mma_ok = MmaFace<D, K, M>::ok;
+  bool use_mma = mma_ok && p.fmma != nullptr && p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
+  use_mma = use_mma && ((D == 3) != ctx->flip_mma);
+  if (use_mma) {
+    if constexpr (mma_ok) {
+      using T = MmaFace<D, K, M>;
+      if (p.nif + p.nbf > 0) {
+        KernelTimer kt(ctx, 0, st);
+        const int64_t warps = (p.nif + T::NFW - 1) / T::NFW + (p.nbf + T::NFW - 1) / T::NFW;
+        const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+        k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.fmma, U, ctx->fc);
+      }
+    }
+    return;
+  }
   if (use_ff) {
     if constexpr (fast_face) {
       if (p.nif + p.nbf > 0) {

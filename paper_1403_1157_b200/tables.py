@@ -193,6 +193,38 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]))
 
 
+def _ceil(x, m):
+    return (x + m - 1) // m * m
+
+
+def mma_face_tables(t: OperatorTables) -> np.ndarray:
+    """Zero-padded per-signature operand tables of the tensor-core face
+    kernel (csrc/kernels_mma.cuh), concatenated per table id:
+
+    TB   [FP][NBK]     B[q][k]                    traces u = B c
+    TG   [FP][KG]      G[q][k][a] at col k*d + a  traces d_n u = G (c x jn)
+    TBW  [NBM][FP]     w_q B[q][i]                modal lifting m = (wB)^T dU
+    TBT  [NBM][FP]     B[q][i]                    projection of Y
+    TGT  [NBM][FP*d]   G[q][i][a] at col q*d + a  projection of X jn
+    with FP = ceil8(F), NBK = ceil4(nb), NBM = ceil8(nb), KG = ceil4(nb d).
+    Returns the flat array and the per-table stride."""
+    d, nb, F = t.dim, t.nb, t.nq_face
+    FP, NBK, NBM, KG = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8), _ceil(nb * d, 4)
+    NT = t.face_B.shape[0]
+    parts = []
+    for k in range(NT):
+        B, G = t.face_B[k], t.face_G[k]                    # (F, nb), (F, nb, d)
+        TB = np.zeros((FP, NBK)); TB[:F, :nb] = B
+        TG = np.zeros((FP, KG)); TG[:F, :nb * d] = G.reshape(F, nb * d)
+        TBW = np.zeros((NBM, FP)); TBW[:nb, :F] = (t.face_w[:, None] * B).T
+        TBT = np.zeros((NBM, FP)); TBT[:nb, :F] = B.T
+        TGT = np.zeros((NBM, FP * d))
+        TGT[:nb, :F * d] = G.transpose(1, 0, 2).reshape(nb, F * d)
+        parts.append(np.concatenate([x.ravel() for x in (TB, TG, TBW, TBT, TGT)]))
+    stride = len(parts[0])
+    return np.ascontiguousarray(np.concatenate(parts)), stride
+
+
 def scheme_constants(space: DGSpace, scheme: FluxScheme):
     d, k = space.mesh.dim, space.order
     return (chi_factor(d), scheme.adjoint_sign,

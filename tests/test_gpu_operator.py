@@ -46,6 +46,31 @@ def test_generic_kernels_match_reference_golden(golden, name):
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
 
+@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
+def test_flipped_face_kernel_matches_reference_golden(golden, name):
+    """The other face kernel (tensor-core DMMA in 2D, SIMT/generic in 3D)
+    against the same golden outputs."""
+    space, model, scheme, U, R, F = operator_case(golden, name)
+    op = _op(space, model, scheme)
+    op.set_variant(flip_mma=True)
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+@pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
+@pytest.mark.parametrize("dirichlet", [0, 1])
+def test_heat_models_mma(golden, scheme, dirichlet):
+    h = golden["heat"]
+    space = DGSpace(unit_square(3), 2)
+    model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
+    key = f"heat_sq3_{scheme}_{dirichlet}"
+    R = h[f"{key}__R"]
+    op = _op(space, model, FluxScheme(scheme))
+    op.set_variant(flip_mma=True)
+    got = op.apply(h[f"{key}__U"])
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
 def test_variants_agree_at_size():
     space = DGSpace(unit_square(64, 16, lengths=(4.0, 1.0)), 2, 6)
     op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
