@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--integrator", default="ssprk3", choices=["ssprk3", "sdirk3"],
                     help="sdirk3: the reference's default SDIRK3 + JFNK at --dt")
     ap.add_argument("--dt", type=float, default=0.01)
+    ap.add_argument("--force-slab", action="store_true",
+                    help="use the slab/halo code path even at N=1 (testing)")
     ap.add_argument("--variant", type=int, default=0,
                     help="kernel variant bits (tdg_set_variant), for A/B timing")
     return ap.parse_args()
@@ -141,15 +143,16 @@ def weak_config(cfg, world):
     return dataclasses.replace(cfg, cells=cells, lengths=lengths)
 
 
-def build_problem(cfg_name, scheme_name, rank=0, world=1):
-    """(cfg, space, model, scheme, U0, slab); the slab is None at N=1."""
+def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False):
+    """(cfg, space, model, scheme, U0, slab); the slab is None at N=1
+    unless ``force_slab``."""
     from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
     from paper_1403_1157_b200.configs import CONFIGS, make_mesh
     from paper_1403_1157_b200.decomp import build_slab
     from paper_1403_1157_b200.fields import bump_field
     cfg = weak_config(CONFIGS[cfg_name], world)
     slab = None
-    if world == 1:
+    if world == 1 and not force_slab:
         mesh = make_mesh(cfg)
     else:
         slab = build_slab(cfg, rank, world)
@@ -264,10 +267,11 @@ def run_native_arm(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world)
+    cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
+                                                         args.force_slab)
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
                           global_ids=None if slab is None else slab.global_ids)
@@ -289,7 +293,7 @@ def run_native_arm(args, rank, world, local):
     if halo is not None:
         halo.exchange(U)
     rho = spectral_radius(op, U, args.power_iters)
-    if world > 1:
+    if dist_on:
         rr = torch.tensor([rho], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(rr, op=torch.distributed.ReduceOp.MAX)
         rho = rr.item()
@@ -297,8 +301,10 @@ def run_native_arm(args, rank, world, local):
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
+
     def barrier():
-        if world > 1:
+        if dist_on:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
@@ -324,7 +330,7 @@ def run_native_arm(args, rank, world, local):
     kt = op.profile_read()
     clocks = sampler.stop()
     ms = sum(a.elapsed_time(b) for a, b in evs)
-    if world > 1:
+    if dist_on:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = tt.item()
@@ -388,7 +394,7 @@ def run_native_arm(args, rank, world, local):
         b.record()
         b.synchronize()
         ems = a.elapsed_time(b)
-        if world > 1:
+        if dist_on:
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             ems = tt.item()
@@ -427,7 +433,7 @@ def run_native_arm(args, rank, world, local):
         if e2e:
             line["e2e"] = e2e
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         torch.distributed.destroy_process_group()
 
 

@@ -47,40 +47,42 @@ struct MmaFace {
   using Dm = Dims<D, K>;
   static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, F = Dm::NQF, NFG = Dm::NFG;
   static constexpr int FP = ceil_to(F, 8), NBK = ceil_to(NB, 4), NBM = ceil_to(NB, 8);
-  static constexpr int KG = ceil_to(NB * D, 4);
   static constexpr int NFW = S == 6 ? 4 : 8;          // faces per warp
   static constexpr int NC = NFW * S;                  // columns (face, species)
   static constexpr int NT = (NC + 7) / 8;             // n-tiles
   static constexpr int NCP = NT * 8;                  // padded columns
-  static constexpr int MT = FP / 8, KT = NBK / 4, KGT = KG / 4, IT = NBM / 8;
+  static constexpr int MT = FP / 8, KT = NBK / 4, IT = NBM / 8;
   static constexpr int NCV = 1 + M::NFX;
   // one signature's table block (doubles), see tables.mma_face_tables
-  static constexpr int OB = 0, OG = OB + FP * NBK, OBW = OG + FP * KG, OBT = OBW + NBM * FP,
-                       OGT = OBT + NBM * FP, TSTRIDE = OGT + NBM * FP * D;
+  static constexpr int OB = 0, OG = OB + FP * NBK, OBW = OG + D * FP * NBK, OBT = OBW + NBM * FP,
+                       OGT = OBT + NBM * FP, TSTRIDE = OGT + D * NBM * FP;
   // per-warp shared memory (doubles)
   static constexpr int SC = 2 * NBK * NCP;   // coefficients [side][k][n]
   static constexpr int SDU = 8 * NCP;        // jump chunk [ql][n]
   static constexpr int SMK = 2 * NBM * NCP;  // scaled modal lifting [side][i][n]
-  static constexpr int SST = 3 * 8 * NCP;    // stage [u_in|Y, u_out|X, avg d_n u][ql][n]
+  static constexpr int SST = 3 * 8 * NCP;    // stage [u_in|Y, u_out, avg d_n u][ql][n]
+  static constexpr int SX = D * 8 * NCP;     // X jn_a of the side being projected [a][ql][n]
   static constexpr int SCV = NFW * 8 * NCV;  // coupled physics [f][ql][cv]
-  static constexpr int SOUT = 2 * NBM * NCP; // projected rows [side][i][n]
+  static constexpr int SOUT = 2 * NBM * NCP; // projected rows [side][i][n] (aliases SDU..)
   static constexpr int SFD = NFW * NFG;      // face doubles
   static constexpr int SFI = NFW * 4;        // face ints (code, ein, eout, lf) as doubles
-  static constexpr int PW = SC + SDU + SMK + SST + SCV + SOUT + SFD + SFI;
+  static constexpr int SALIAS = (SDU + SMK + SST + SX) > SOUT ? 0 : SOUT - (SDU + SMK + SST + SX);
+  static constexpr int PW = SC + SDU + SMK + SST + SX + SALIAS + SCV + SFD + SFI;
   static constexpr int WARPS = 4;
   static constexpr size_t smem() { return size_t(WARPS) * PW * 8; }
   static constexpr bool ok = S >= 1 && S <= 8 && smem() <= 200 * 1024;
+  static constexpr int MINB = smem() <= 72 * 1024 ? 3 : 2;
 };
 
 template <int D, int K, class M>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, MmaFace<D, K, M>::MINB)
 k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
             double* __restrict__ FC) {
   using T = MmaFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
   constexpr int NFW = T::NFW, NC = T::NC, NT = T::NT, NCP = T::NCP;
-  constexpr int MT = T::MT, KT = T::KT, KGT = T::KGT, IT = T::IT, NBK = T::NBK;
-  constexpr int NBM = T::NBM, KG = T::KG, FP = T::FP, NCV = T::NCV, TS = T::TSTRIDE;
+  constexpr int MT = T::MT, KT = T::KT, IT = T::IT, NBK = T::NBK;
+  constexpr int NBM = T::NBM, FP = T::FP, NCV = T::NCV, TS = T::TSTRIDE;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
@@ -89,9 +91,10 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
   double* dUS = cS + T::SC;          // [8][NCP]
   double* mKS = dUS + T::SDU;        // [2][NBM][NCP]
   double* stS = mKS + T::SMK;        // [3][8][NCP]
-  double* cvS = stS + T::SST;        // [NFW][8][NCV]
-  double* outS = cvS + T::SCV;       // [2][NBM][NCP]
-  double* fD = outS + T::SOUT;       // [NFW][NFG]
+  double* xS = stS + T::SST;         // [D][8][NCP]
+  double* cvS = xS + T::SX + T::SALIAS;  // [NFW][8][NCV]
+  double* outS = dUS;                // [2][NBM][NCP], aliases dUS..xS (dead by then)
+  double* fD = cvS + T::SCV;         // [NFW][NFG]
   int* fI = reinterpret_cast<int*>(fD + T::SFD);  // [NFW][8]: code ein eout lfi lfo valid
 
   const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
@@ -187,6 +190,10 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
     const double* TBi = tabs + size_t(tin) * TS;
     const double* TBo = tabs + size_t(tout) * TS;
     auto member_col = [&](int n) { return n < NC && ((members >> col_face(n)) & 1); };
+    // B-fragment columns of this lane (col g of every n-tile)
+    bool bmask[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bmask[nt] = member_col(8 * nt + g);
 
     // which lifting sides the member faces use (operator.py:336-357)
     bool any_in = false, any_out = false, any_two = false;
@@ -214,7 +221,8 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
       return fac * p.A[col_sp(n)] * wside * 0.5 * d[2 * D] * (sd == 0 ? d[2 * D + 2] : d[2 * D + 3]);
     };
 
-    // traces of one point chunk: u (and d_n u when grads) for both sides
+    // traces of one point chunk: u (and d_n u = sum_a jn_a (G_a c)) for
+    // both sides; B operands are plain shared-memory loads
     auto traces = [&](int c, double (&ui)[NT][2], double (&uo)[NT][2], double (&gi)[NT][2],
                       double (&go)[NT][2], bool grads, bool out_side) {
 #pragma unroll
@@ -229,33 +237,39 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int n = 8 * nt + g;
-          const bool mc = member_col(n);
-          const double bi = mc ? cS[(0 * NBK + k) * NCP + n] : 0.0;
-          dmma(ui[nt][0], ui[nt][1], ai, bi);
-          if (out_side) {
-            const double bo = mc ? cS[(1 * NBK + k) * NCP + n] : 0.0;
-            dmma(uo[nt][0], uo[nt][1], ao, bo);
-          }
+          dmma(ui[nt][0], ui[nt][1], ai, bmask[nt] ? cS[k * NCP + n] : 0.0);
+          if (out_side) dmma(uo[nt][0], uo[nt][1], ao, bmask[nt] ? cS[(NBK + k) * NCP + n] : 0.0);
         }
       }
       if (!grads) return;
-#pragma unroll 2
-      for (int kg = 0; kg < KGT; ++kg) {
-        const int kk = 4 * kg + tq, k = kk / D, a = kk - k * D;
-        const bool kv = kk < NB * D;
-        const double ai = kv ? __ldg(TBi + T::OG + row * KG + kk) : 0.0;
-        const double ao = (kv && out_side) ? __ldg(TBo + T::OG + row * KG + kk) : 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int n = 8 * nt + g;
-          const bool mc = kv && member_col(n);
-          const double bi = mc ? cS[(0 * NBK + k) * NCP + n] * jn_of(0, a, n) : 0.0;
-          dmma(gi[nt][0], gi[nt][1], ai, bi);
-          if (out_side) {
-            const double bo = mc ? cS[(1 * NBK + k) * NCP + n] * jn_of(1, a, n) : 0.0;
-            dmma(go[nt][0], go[nt][1], ao, bo);
+      for (int a = 0; a < D; ++a) {
+        double ti[NT][2], to[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) ti[nt][0] = ti[nt][1] = to[nt][0] = to[nt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int k = 4 * kt + tq;
+          const double ai = __ldg(TBi + T::OG + (a * FP + row) * NBK + k);
+          const double ao = out_side ? __ldg(TBo + T::OG + (a * FP + row) * NBK + k) : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int n = 8 * nt + g;
+            dmma(ti[nt][0], ti[nt][1], ai, bmask[nt] ? cS[k * NCP + n] : 0.0);
+            if (out_side) dmma(to[nt][0], to[nt][1], ao, bmask[nt] ? cS[(NBK + k) * NCP + n] : 0.0);
           }
         }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int n = 8 * nt + 2 * tq + j;
+            if (n < NC) {
+              const double* d = fD + col_face(n) * NFG;
+              gi[nt][j] = fma(d[a], ti[nt][j], gi[nt][j]);
+              go[nt][j] = fma(d[D + a], to[nt][j], go[nt][j]);
+            }
+          }
       }
     };
 
@@ -267,7 +281,8 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mI[it][nt][0] = mI[it][nt][1] = mO[it][nt][0] = mO[it][nt][1] = 0.0;
       if (any_in || any_out) {
-        for (int c = 0; c < MT; ++c) {
+#pragma unroll 1
+      for (int c = 0; c < MT; ++c) {
           double ui[NT][2], uo[NT][2], gi[NT][2], go[NT][2];
           traces(c, ui, uo, gi, go, false, any_two);
 #pragma unroll
@@ -317,6 +332,7 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
       }
 
       // ---- pass 2: traces, physics, projection ---------------------------
+#pragma unroll 1
       for (int c = 0; c < MT; ++c) {
         double ui[NT][2], uo[NT][2], gi[NT][2], go[NT][2];
         traces(c, ui, uo, gi, go, true, any_two);
@@ -368,7 +384,8 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
           }
           __syncwarp();
         }
-        // Y, X at the chunk's points (operator.py:413-418) -> stage
+        // Y, X at the chunk's points (operator.py:413-418)
+        double Xr[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -393,14 +410,24 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
               Y = wq * (As * gav[nt][j] - qv);
               X = wq * 0.5 * p.adj * As * dU[nt][j];
             }
-            stS[(0 * 8 + g) * NCP + n] = Y;
-            stS[(1 * 8 + g) * NCP + n] = X;
+            stS[g * NCP + n] = Y;
+            Xr[nt][j] = X;
           }
-        __syncwarp();
         // projection onto both sides' test functions
 #pragma unroll
         for (int sd = 0; sd < 2; ++sd) {
           if (sd == 1 && !any_two) break;
+          // X jn_a of this side -> shared (B operands)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int n = 8 * nt + 2 * tq + j;
+              const double* d = fD + (n < NC ? col_face(n) : 0) * NFG + sd * D;
+#pragma unroll
+              for (int a2 = 0; a2 < D; ++a2) xS[(a2 * 8 + g) * NCP + n] = n < NC ? Xr[nt][j] * d[a2] : 0.0;
+            }
+          __syncwarp();
           const double* TBs = sd ? TBo : TBi;
           const double sgn = sd ? -1.0 : 1.0;
 #pragma unroll
@@ -408,35 +435,31 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
             const int ql = 4 * ks + tq;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-              const double a = __ldg(TBs + T::OBT + (8 * it + g) * FP + 8 * c + ql);
+              const double ay = sgn * __ldg(TBs + T::OBT + (8 * it + g) * FP + 8 * c + ql);
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) {
-                const double b = sgn * stS[(0 * 8 + ql) * NCP + 8 * nt + g];
-                if (sd) dmma(rO[it][nt][0], rO[it][nt][1], a, b);
-                else dmma(rI[it][nt][0], rI[it][nt][1], a, b);
+                const double b = stS[ql * NCP + 8 * nt + g];
+                if (sd) dmma(rO[it][nt][0], rO[it][nt][1], ay, b);
+                else dmma(rI[it][nt][0], rI[it][nt][1], ay, b);
+              }
+#pragma unroll
+              for (int a2 = 0; a2 < D; ++a2) {
+                const double ax = __ldg(TBs + T::OGT + (a2 * NBM + 8 * it + g) * FP + 8 * c + ql);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                  const double b = xS[(a2 * 8 + ql) * NCP + 8 * nt + g];
+                  if (sd) dmma(rO[it][nt][0], rO[it][nt][1], ax, b);
+                  else dmma(rI[it][nt][0], rI[it][nt][1], ax, b);
+                }
               }
             }
           }
-#pragma unroll
-          for (int kx = 0; kx < 2 * D; ++kx) {
-            const int kk = 4 * kx + tq, ql = kk / D, a2 = kk - ql * D;
-#pragma unroll
-            for (int it = 0; it < IT; ++it) {
-              const double a = __ldg(TBs + T::OGT + (8 * it + g) * (FP * D) + 8 * c * D + kk);
-#pragma unroll
-              for (int nt = 0; nt < NT; ++nt) {
-                const int n = 8 * nt + g;
-                const double b = stS[(1 * 8 + ql) * NCP + n] * jn_of(sd, a2, n);
-                if (sd) dmma(rO[it][nt][0], rO[it][nt][1], a, b);
-                else dmma(rI[it][nt][0], rI[it][nt][1], a, b);
-              }
-            }
-          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     } else {
       // ---- prescribed-flux wall faces: Y = -w sfac q_s(c1) on the inside -
+#pragma unroll 1
       for (int c = 0; c < MT; ++c) {
         double ui[NT][2], uo[NT][2], gi[NT][2], go[NT][2];
         traces(c, ui, uo, gi, go, false, false);

@@ -197,29 +197,28 @@ def _ceil(x, m):
     return (x + m - 1) // m * m
 
 
-def mma_face_tables(t: OperatorTables) -> np.ndarray:
+def mma_face_tables(t: OperatorTables):
     """Zero-padded per-signature operand tables of the tensor-core face
     kernel (csrc/kernels_mma.cuh), concatenated per table id:
 
-    TB   [FP][NBK]     B[q][k]                    traces u = B c
-    TG   [FP][KG]      G[q][k][a] at col k*d + a  traces d_n u = G (c x jn)
-    TBW  [NBM][FP]     w_q B[q][i]                modal lifting m = (wB)^T dU
-    TBT  [NBM][FP]     B[q][i]                    projection of Y
-    TGT  [NBM][FP*d]   G[q][i][a] at col q*d + a  projection of X jn
-    with FP = ceil8(F), NBK = ceil4(nb), NBM = ceil8(nb), KG = ceil4(nb d).
-    Returns the flat array and the per-table stride."""
+    TB   [FP][NBK]        B[q][k]               traces u = B c
+    TGa  [d][FP][NBK]     G[q][k][a]            traces d_n u = sum_a jn_a (G_a c)
+    TBW  [NBM][FP]        w_q B[q][i]           modal lifting m = (wB)^T dU
+    TBT  [NBM][FP]        B[q][i]               projection of Y
+    TGTa [d][NBM][FP]     G[q][i][a]            projection of X jn_a
+    with FP = ceil8(F), NBK = ceil4(nb), NBM = ceil8(nb).  Returns the
+    flat array and the per-table stride."""
     d, nb, F = t.dim, t.nb, t.nq_face
-    FP, NBK, NBM, KG = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8), _ceil(nb * d, 4)
+    FP, NBK, NBM = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
     NT = t.face_B.shape[0]
     parts = []
     for k in range(NT):
         B, G = t.face_B[k], t.face_G[k]                    # (F, nb), (F, nb, d)
         TB = np.zeros((FP, NBK)); TB[:F, :nb] = B
-        TG = np.zeros((FP, KG)); TG[:F, :nb * d] = G.reshape(F, nb * d)
+        TG = np.zeros((d, FP, NBK)); TG[:, :F, :nb] = G.transpose(2, 0, 1)
         TBW = np.zeros((NBM, FP)); TBW[:nb, :F] = (t.face_w[:, None] * B).T
         TBT = np.zeros((NBM, FP)); TBT[:nb, :F] = B.T
-        TGT = np.zeros((NBM, FP * d))
-        TGT[:nb, :F * d] = G.transpose(1, 0, 2).reshape(nb, F * d)
+        TGT = np.zeros((d, NBM, FP)); TGT[:, :nb, :F] = G.transpose(2, 1, 0)
         parts.append(np.concatenate([x.ravel() for x in (TB, TG, TBW, TBT, TGT)]))
     stride = len(parts[0])
     return np.ascontiguousarray(np.concatenate(parts)), stride
