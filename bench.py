@@ -270,6 +270,7 @@ def run_native_arm(args, rank, world, local):
     if world > 1 or "RANK" in os.environ:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
     cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
                                                          args.force_slab)
     op = DiscreteOperator(space, model, scheme, device=dev,
@@ -300,8 +301,6 @@ def run_native_arm(args, rank, world, local):
     dt = 0.8 * 2.51 / rho
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
 
     def barrier():
         if dist_on:
