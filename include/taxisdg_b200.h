@@ -109,6 +109,9 @@ typedef struct tdg_desc {
   /* optional: zero-padded per-signature operand tables of the tensor-core
    * (DMMA) face kernel, layout of tables.mma_face_tables (NULL disables it) */
   const double* face_mma;
+  /* optional: padded operand tables of the tensor-core volume kernel
+   * (tables.mma_volume_tables, NULL disables it) */
+  const double* vol_mma;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -155,7 +158,8 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * volume kernel instead of the one-thread-per-element one; bit 2: run
  * volume and faces serially on the caller's stream instead of the
  * overlapped two-stream schedule; bit 3: flip the face-kernel choice
- * between the tensor-core (DMMA) kernel and the SIMT kernel.  0 (default)
+ * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
+ * the SIMT volume kernels instead of the tensor-core one.  0 (default)
  * lets the library pick the fastest compiled-in kernels and schedule. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 

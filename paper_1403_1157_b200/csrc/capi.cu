@@ -105,6 +105,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.bfcode = d.bf_code;
   p.bfgeo = d.bf_geo;
   p.fmma = d.face_mma;
+  p.vmma = d.vol_mma;
 
   {
     int dev = 0, sms = 0;
@@ -233,6 +234,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->vol_variant = (variant >> 1) & 1;
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
+  ctx->no_vmma = ((variant >> 4) & 1) != 0;
   return TDG_OK;
 }
 

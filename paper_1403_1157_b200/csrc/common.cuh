@@ -62,6 +62,7 @@ struct OpParams {
   const int32_t* __restrict__ bfcode;
   const double* __restrict__ bfgeo;
   const double* __restrict__ fmma;  // tensor-core face tables (may be null)
+  const double* __restrict__ vmma;  // tensor-core volume tables (may be null)
 };
 
 // code-word layout, mirrors include/taxisdg_b200.h

@@ -47,6 +47,7 @@ struct tdg_ctx {
   bool force_generic = false;  // testing: pin the CTA-staged kernels
   int num_sms = 148;
   bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
+  bool no_vmma = false;   // testing: SIMT volume kernels instead of the tensor-core one
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -71,6 +72,11 @@ int configure(int nqv) {
   e = cudaFuncSetAttribute(k_wall<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(WallTile<D, K, M>::smem()));
   if (e != cudaSuccess) return cuda_fail(e, "configure wall");
+  if constexpr (MmaVol<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_volume_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(MmaVol<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure volume_mma");
+  }
   if constexpr (MmaFace<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_faces_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(MmaFace<D, K, M>::smem()));
@@ -162,6 +168,28 @@ void run_faces(tdg_ctx* ctx, const double* U, cudaStream_t st, bool use_ff) {
   }
 }
 
+// fast volume kernel: tensor-core (use_vm) or one thread per element
+template <int D, int K, class M>
+void launch_volume(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a,
+                   double b, double c, int mode, cudaStream_t st, bool use_vm) {
+  const OpParams& p = ctx->p;
+  if (use_vm) {
+    if constexpr (MmaVol<D, K, M>::ok) {
+      using T = MmaVol<D, K, M>;
+      const int64_t grid = (p.ne + T::TE - 1) / T::TE;
+      k_volume_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.vmma, U, ctx->fc, U0, out,
+                                                                    a, b, c, mode);
+    }
+    return;
+  }
+  if constexpr (FastVol<D, K, M>::ok) {
+    using T = FastVol<D, K, M>;
+    const int64_t grid = (p.ne + T::TE - 1) / T::TE;
+    k_volume_fast<D, K, M><<<unsigned(grid), T::TE, T::smem(), st>>>(p, U, ctx->fc, U0, out, a,
+                                                                      b, c, mode);
+  }
+}
+
 template <int D, int K, class M>
 int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
         double c, int mode, cudaStream_t st) {
@@ -177,18 +205,18 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   // overlapped path: fast volume kernel (without the face-slot sum) on the
   // aux stream while the face kernel runs; out must not alias U (the face
   // kernel still reads U), U0 may alias out (read before written per row)
-  const bool overlap = use_fv && use_ff && ctx->overlap && ctx->aux && out != U && p.ne > 0 &&
-                       (SN_of<M, D, K>() % 2 == 0);
+  constexpr bool vmma_ok = MmaVol<D, K, M>::ok;
+  const bool use_vm = vmma_ok && p.vmma != nullptr && p.nqv == Dims<D, K>::NQV &&
+                      !ctx->force_generic && !ctx->no_vmma;
+  const bool overlap = (use_fv || use_vm) && use_ff && ctx->overlap && ctx->aux && out != U &&
+                       p.ne > 0 && (SN_of<M, D, K>() % 2 == 0);
   if (overlap) {
-    if constexpr (fast_vol && (SN_of<M, D, K>() % 2 == 0)) {
-      using T = FastVol<D, K, M>;
+    if constexpr ((fast_vol || vmma_ok) && (SN_of<M, D, K>() % 2 == 0)) {
       cudaEventRecord(ctx->ev_in, st);
       cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
       {
         KernelTimer kt(ctx, 2, ctx->aux);
-        const int64_t grid = (p.ne + T::TE - 1) / T::TE;
-        k_volume_fast<D, K, M><<<unsigned(grid), T::TE, T::smem(), ctx->aux>>>(
-            p, U, ctx->fc, U0, out, a, b, c, mode | 4);
+        launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, use_vm);
       }
       cudaEventRecord(ctx->ev_vol, ctx->aux);
       run_faces<D, K, M>(ctx, U, st, use_ff);
@@ -203,7 +231,10 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
     return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
   }
   run_faces<D, K, M>(ctx, U, st, use_ff);
-  if (p.ne > 0) {
+  if (p.ne > 0 && use_vm) {
+    KernelTimer kt(ctx, 2, st);
+    launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode, st, true);
+  } else if (p.ne > 0) {
     KernelTimer kt(ctx, 2, st);
     if (use_v4) {
       using T = Vol4<D, K, M>;

@@ -224,6 +224,25 @@ def mma_face_tables(t: OperatorTables):
     return np.ascontiguousarray(np.concatenate(parts)), stride
 
 
+def mma_volume_tables(t: OperatorTables) -> np.ndarray:
+    """Zero-padded operand tables of the tensor-core volume kernel
+    (csrc/kernels_mma.cuh, k_volume_mma), concatenated:
+
+    TPhi  [QP][NBK]        Phi[q][k]          point values  u = Phi c
+    TGa   [d][QP][NBK]     G[q][k][a]         reference gradients
+    TGaT  [d][NBM][QP]     G[q][i][a]         projection of the flux rows
+    TPhiT [NBM][QP]        Phi[q][i]          projection of the bilinear source
+    with QP = ceil8(Q), NBK = ceil4(nb), NBM = ceil8(nb)."""
+    d, nb = t.dim, t.nb
+    Q = t.vol_phi.shape[0]
+    QP, NBK, NBM = _ceil(Q, 8), _ceil(nb, 4), _ceil(nb, 8)
+    TPhi = np.zeros((QP, NBK)); TPhi[:Q, :nb] = t.vol_phi
+    TG = np.zeros((d, QP, NBK)); TG[:, :Q, :nb] = t.vol_grad.transpose(2, 0, 1)
+    TGT = np.zeros((d, NBM, QP)); TGT[:, :nb, :Q] = t.vol_grad.transpose(2, 1, 0)
+    TPT = np.zeros((NBM, QP)); TPT[:nb, :Q] = t.vol_phi.T
+    return np.ascontiguousarray(np.concatenate([x.ravel() for x in (TPhi, TG, TGT, TPT)]))
+
+
 def scheme_constants(space: DGSpace, scheme: FluxScheme):
     d, k = space.mesh.dim, space.order
     return (chi_factor(d), scheme.adjoint_sign,

@@ -55,6 +55,9 @@ def test_flipped_face_kernel_matches_reference_golden(golden, name):
     op.set_variant(flip_mma=True)
     got = op.apply(U)
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+    op.set_variant(simt_volume=True)
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
 
 @pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
@@ -82,13 +85,15 @@ def test_variants_agree_at_size():
     c = op.apply_f(U)
     op.set_variant(serial=True)
     d = op.apply_f(U)
+    op.set_variant(simt_volume=True)
+    e_ = op.apply_f(U)
     out = torch.empty_like(U)
     op.set_variant()
     op.rk_stage(U, U, out, 0.25, 0.5, 1e-3)      # overlapped (out != U)
     out2 = U.clone()
     op.rk_stage(U, out2, out2, 0.25, 0.5, 1e-3)   # in place: serial path
     assert torch.allclose(out, out2, rtol=1e-14, atol=1e-16)
-    for x in (b, c, d):
+    for x in (b, c, d, e_):
         assert rel_l2_per_species(space, a.cpu().numpy(), x.cpu().numpy()).max() <= 1e-13
 
 
