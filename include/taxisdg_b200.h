@@ -112,6 +112,8 @@ typedef struct tdg_desc {
   /* optional: padded operand tables of the tensor-core volume kernel
    * (tables.mma_volume_tables, NULL disables it) */
   const double* vol_mma;
+  /* the last n_cut_faces interior faces touch ghost rows (slab runs) */
+  int64_t n_cut_faces;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -133,6 +135,14 @@ TDG_API int tdg_apply(tdg_ctx* ctx, const double* U, double* R, double t,
  * the face kernel (serial schedule). */
 TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out,
                  double a, double b, double c, double t, void* stream);
+
+/* A stage split around a ghost-row exchange (slab-decomposed runs):
+ * part 1 launches everything that reads owned rows only (volume terms,
+ * non-cut faces, walls); part 2, issued after the ghost rows of U are in
+ * place, launches the cut faces and the final sum.  Same arguments and
+ * result as tdg_rk_stage. */
+TDG_API int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out,
+                              double a, double b, double c, double t, int part, void* stream);
 
 /* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U (a
  * second stage vector is allocated by the library on first use). */
@@ -159,7 +169,7 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * volume and faces serially on the caller's stream instead of the
  * overlapped two-stream schedule; bit 3: flip the face-kernel choice
  * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
- * the SIMT volume kernels instead of the tensor-core one.  0 (default)
+ * the tensor-core volume kernel instead of the SIMT one.  0 (default)
  * lets the library pick the fastest compiled-in kernels and schedule. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 

@@ -47,8 +47,9 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   if (d.dim != 2 && d.dim != 3) return fail(TDG_E_INVALID, "dim must be 2 or 3");
   if (d.n_species < 1 || d.n_species > kMaxS) return fail(TDG_E_INVALID, "n_species out of range");
   if (d.scheme < TDG_CDG2 || d.scheme > TDG_BO) return fail(TDG_E_INVALID, "unknown scheme");
-  if (d.n_elements < 0 || d.n_ghost < 0 || d.n_int_faces < 0 || d.n_bnd_faces < 0)
-    return fail(TDG_E_INVALID, "negative size");
+  if (d.n_elements < 0 || d.n_ghost < 0 || d.n_int_faces < 0 || d.n_bnd_faces < 0 ||
+      d.n_cut_faces < 0 || d.n_cut_faces > d.n_int_faces)
+    return fail(TDG_E_INVALID, "negative size / bad cut-face count");
   if (d.n_elements + d.n_ghost > (int64_t(1) << 31) - 1)
     return fail(TDG_E_INVALID, "element rows must fit int32");
   Impl impl;
@@ -174,6 +175,15 @@ int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out, d
   return ctx->impl.run(ctx, U, U0, out, a, b, c, 2, static_cast<cudaStream_t>(stream));
 }
 
+int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out, double a,
+                      double b, double c, double t, int part, void* stream) {
+  (void)t;
+  if (!ctx || !U || !out) return fail(TDG_E_INVALID, "null argument");
+  if (a != 0.0 && !U0) return fail(TDG_E_INVALID, "U0 required when a != 0");
+  if (part < 1 || part > 2) return fail(TDG_E_INVALID, "part must be 1 (begin) or 2 (end)");
+  return ctx->impl.run(ctx, U, U0, out, a, b, c, 2 | (part << 8), static_cast<cudaStream_t>(stream));
+}
+
 int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, void* stream) {
   if (!ctx || !U || !work) return fail(TDG_E_INVALID, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -234,7 +244,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->vol_variant = (variant >> 1) & 1;
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
-  ctx->no_vmma = ((variant >> 4) & 1) != 0;
+  ctx->use_vmma = ((variant >> 4) & 1) != 0;
   return TDG_OK;
 }
 

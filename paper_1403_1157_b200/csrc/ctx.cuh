@@ -47,7 +47,7 @@ struct tdg_ctx {
   bool force_generic = false;  // testing: pin the CTA-staged kernels
   int num_sms = 148;
   bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
-  bool no_vmma = false;   // testing: SIMT volume kernels instead of the tensor-core one
+  bool use_vmma = false;  // A/B: tensor-core volume kernel (slower than SIMT at C2)
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -123,8 +123,7 @@ template <class M, int D, int K>
 constexpr int SN_of() { return M::S * Dims<D, K>::NB; }
 
 template <int D, int K, class M>
-void run_faces(tdg_ctx* ctx, const double* U, cudaStream_t st, bool use_ff) {
-  const OpParams& p = ctx->p;
+void run_faces(tdg_ctx* ctx, const OpParams& p, const double* U, cudaStream_t st, bool use_ff) {
   constexpr bool fast_face = FastFace<D, K, M>::ok;
   // tensor-core face kernel: default in 3D, opt-in (flip) in 2D
   constexpr bool mma_ok = MmaFace<D, K, M>::ok;
@@ -193,7 +192,34 @@ void launch_volume(tdg_ctx* ctx, const double* U, const double* U0, double* out,
 template <int D, int K, class M>
 int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
         double c, int mode, cudaStream_t st) {
+  // mode bits 8-9: 0 whole application; 1 "begin" (everything that does
+  // not read ghost rows); 2 "end" (cut faces + what depends on them).  A
+  // slab-decomposed stage runs begin, the NCCL ghost exchange, end.
+  const int part = (mode >> 8) & 3;
+  mode &= 0xff;
   const OpParams& p = ctx->p;
+  const int64_t ncut = ctx->d.n_cut_faces;
+  // faces split: [0, nif-ncut) + walls need owned rows only; the last ncut
+  // interior faces touch ghost rows
+  auto faces = [&](int which, bool use_ff_) {
+    if (which == 0 && part == 0) {
+      run_faces<D, K, M>(ctx, p, U, st, use_ff_);
+      return;
+    }
+    OpParams pp = p;
+    if (which == 1) {
+      pp.nif = p.nif - ncut;
+    } else {
+      const int64_t off = p.nif - ncut;
+      pp.ifel = p.ifel + 2 * off;
+      pp.iflf = p.iflf + 2 * off;
+      pp.ifcode = p.ifcode + off;
+      pp.ifgeo = p.ifgeo + off * Dims<D, K>::NFG;
+      pp.nif = ncut;
+      pp.nbf = 0;
+    }
+    if (pp.nif + pp.nbf > 0) run_faces<D, K, M>(ctx, pp, U, st, use_ff_);
+  };
   // register-resident kernels when the tables / working set fit and the
   // default quadrature is in use; generic CTA-staged kernels otherwise
   constexpr bool fast_face = FastFace<D, K, M>::ok;
@@ -207,19 +233,26 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   // kernel still reads U), U0 may alias out (read before written per row)
   constexpr bool vmma_ok = MmaVol<D, K, M>::ok;
   const bool use_vm = vmma_ok && p.vmma != nullptr && p.nqv == Dims<D, K>::NQV &&
-                      !ctx->force_generic && !ctx->no_vmma;
+                      !ctx->force_generic && ctx->use_vmma;
   const bool overlap = (use_fv || use_vm) && use_ff && ctx->overlap && ctx->aux && out != U &&
                        p.ne > 0 && (SN_of<M, D, K>() % 2 == 0);
   if (overlap) {
     if constexpr ((fast_vol || vmma_ok) && (SN_of<M, D, K>() % 2 == 0)) {
-      cudaEventRecord(ctx->ev_in, st);
-      cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
-      {
-        KernelTimer kt(ctx, 2, ctx->aux);
-        launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, use_vm);
+      if (part != 2) {
+        cudaEventRecord(ctx->ev_in, st);
+        cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
+        {
+          KernelTimer kt(ctx, 2, ctx->aux);
+          launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, use_vm);
+        }
+        cudaEventRecord(ctx->ev_vol, ctx->aux);
+        faces(part == 0 ? 0 : 1, use_ff);
       }
-      cudaEventRecord(ctx->ev_vol, ctx->aux);
-      run_faces<D, K, M>(ctx, U, st, use_ff);
+      if (part == 1) {
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
+      }
+      if (part == 2) faces(2, use_ff);
       cudaStreamWaitEvent(st, ctx->ev_vol, 0);
       KernelTimer kt(ctx, 3, st);
       const int64_t n2 = p.ne * (SN_of<M, D, K>() / 2);
@@ -230,7 +263,14 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
   }
-  run_faces<D, K, M>(ctx, U, st, use_ff);
+  if (part == 0) faces(0, use_ff);
+  else if (part == 1) {
+    faces(1, use_ff);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
+  } else {
+    faces(2, use_ff);
+  }
   if (p.ne > 0 && use_vm) {
     KernelTimer kt(ctx, 2, st);
     launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode, st, true);

@@ -98,7 +98,7 @@ class DiscreteOperator:
             if_geo=ptr(k["if_geo"]), bf_elem=ptr(k["bf_elem"]),
             bf_lf=ptr(k["bf_lf"]), bf_code=ptr(k["bf_code"]),
             bf_geo=ptr(k["bf_geo"]), face_mma=ptr(k["face_mma"]),
-            vol_mma=ptr(k["vol_mma"]))
+            vol_mma=ptr(k["vol_mma"]), n_cut_faces=t.n_cut)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _native.check(self.lib.tdg_create(ctypes.byref(desc),
@@ -183,7 +183,7 @@ class DiscreteOperator:
 
     def set_variant(self, generic: bool = False, vol4: bool = False,
                     serial: bool = False, flip_mma: bool = False,
-                    simt_volume: bool = False):
+                    mma_volume: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
@@ -191,7 +191,7 @@ class DiscreteOperator:
         _native.check(self.lib.tdg_set_variant(
             self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
             | (int(bool(serial)) << 2) | (int(bool(flip_mma)) << 3)
-            | (int(bool(simt_volume)) << 4)),
+            | (int(bool(mma_volume)) << 4)),
             "tdg_set_variant")
 
     def profile(self, enable: bool = True):
@@ -234,6 +234,21 @@ class DiscreteOperator:
             self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
             out.data_ptr(), float(a), float(b), float(c), float(t),
             self._stream()), "tdg_rk_stage")
+        return out
+
+    def rk_stage_part(self, U0, U, out, a: float, b: float, c: float, part: int,
+                      t: float = 0.0):
+        """Half of ``rk_stage`` around a ghost exchange: part 1 = work on
+        owned rows only, part 2 = cut faces + final sum (issue after the
+        ghost rows of U are filled)."""
+        self._check_vec("U", U, self.n_rows)
+        self._check_vec("out", out)
+        if U0 is not None:
+            self._check_vec("U0", U0)
+        _native.check(self.lib.tdg_rk_stage_part(
+            self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
+            out.data_ptr(), float(a), float(b), float(c), float(t), int(part),
+            self._stream()), "tdg_rk_stage_part")
         return out
 
     def ssprk3_step(self, U, work, dt: float, t: float = 0.0):

@@ -20,19 +20,22 @@ class SSPRK3:
         self._work = None
 
     def _stage(self, U0, U, out, a, b, c):
-        if self.halo is not None:
-            self.halo.exchange(U)
-        self.op.rk_stage(U0, U, out, a, b, c)
+        # pack + post the exchange first (its kernels and NCCL ops then run
+        # beside the owned-row work), fill the ghosts, finish the cut faces
+        self.halo.start(U)
+        self.op.rk_stage_part(U0, U, out, a, b, c, 1)
+        self.halo.wait()
+        self.op.rk_stage_part(U0, U, out, a, b, c, 2)
 
     def step(self, U, dt: float):
         """Advance U (owned rows first, then ghost rows) in place."""
         import torch
-        if self._work is None or self._work.shape != U.shape:
-            self._work = torch.empty_like(U)
+        if self._work is None or self._work.shape != (2,) + tuple(U.shape):
+            self._work = torch.empty((2,) + tuple(U.shape), dtype=U.dtype, device=U.device)
         if self.halo is None:
-            return self.op.ssprk3_step(U, self._work, dt)
-        W = self._work
-        self._stage(None, U, W, 0.0, 1.0, dt)
-        self._stage(U, W, W, 0.75, 0.25, 0.25 * dt)
-        self._stage(U, W, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt)
+            return self.op.ssprk3_step(U, self._work[0], dt)
+        W1, W2 = self._work[0], self._work[1]   # no stage writes its own input
+        self._stage(None, U, W1, 0.0, 1.0, dt)
+        self._stage(U, W1, W2, 0.75, 0.25, 0.25 * dt)
+        self._stage(U, W2, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt)
         return U

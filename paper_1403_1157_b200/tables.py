@@ -70,6 +70,7 @@ class OperatorTables:
     bf_lf: np.ndarray
     bf_code: np.ndarray
     bf_geo: np.ndarray
+    n_cut: int = 0
 
 
 def _face_tables(space: DGSpace, frule):
@@ -173,8 +174,12 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         nbf = np.zeros(0, dtype=np.int64)
     else:
         nbf = np.flatnonzero(bmask)
-    order = np.argsort(code & 1023, kind="stable")
+    # faces touching a ghost row (SKIP_OUT) last, so a slab stage can run
+    # the others while the ghost exchange is in flight
+    cut = (code & CODE_SKIP_OUT) != 0
+    order = np.lexsort((code & 1023, cut))
     code, geo, el, lfs = code[order], geo[order], el[order], lfs[order]
+    n_cut = int(cut.sum())
 
     btag = mesh.face_tags[nbf].astype(np.int64)
     border = np.lexsort((btag, tid[nbf, 0]))
@@ -190,7 +195,7 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         face_w=c64(fr.weights), elem_geo=c64(egeo[:n_owned]),
         if_elems=i32(el), if_lf=i32(lfs), if_code=i32(code), if_geo=c64(geo),
         bf_elem=i32(fe[nbf, 0]), bf_lf=i32(fl[nbf, 0]),
-        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]))
+        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]), n_cut=n_cut)
 
 
 def _ceil(x, m):

@@ -55,7 +55,7 @@ def test_flipped_face_kernel_matches_reference_golden(golden, name):
     op.set_variant(flip_mma=True)
     got = op.apply(U)
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
-    op.set_variant(simt_volume=True)
+    op.set_variant(mma_volume=True)
     got = op.apply(U)
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
@@ -85,7 +85,7 @@ def test_variants_agree_at_size():
     c = op.apply_f(U)
     op.set_variant(serial=True)
     d = op.apply_f(U)
-    op.set_variant(simt_volume=True)
+    op.set_variant(mma_volume=True)
     e_ = op.apply_f(U)
     out = torch.empty_like(U)
     op.set_variant()
@@ -297,6 +297,65 @@ def test_two_slabs_on_one_gpu_match_global(name, cells):
             own = gid[:sl.n_owned]
             assert torch.allclose(out[:sl.n_owned], ref.index_select(0, own),
                                   rtol=1e-13, atol=1e-15)
+            # split stage around the ghost exchange: part 1 must not read
+            # ghost rows (NaN while it runs), part 2 sees them filled
+            out2 = torch.empty_like(U)
+            U2 = U.clone()
+            U2[sl.n_owned:] = float("nan")
+            op.rk_stage_part(U2, U2, out2, 0.5, 0.5, 1e-3, 1)
+            U2[sl.n_owned:] = U[sl.n_owned:]
+            op.rk_stage_part(U2, U2, out2, 0.5, 0.5, 1e-3, 2)
+            assert torch.equal(out2[:sl.n_owned], out[:sl.n_owned])
+            assert op.tables.n_cut > 0
+
+
+class _ReplayHalo:
+    """Stands in for HaloExchange on one GPU: ``start`` poisons the ghost
+    rows, ``wait`` fills them with the neighbour values of the matching
+    global stage input (what NCCL would deliver)."""
+
+    def __init__(self, stage_inputs, ghost_gid, n_owned):
+        self.stage_inputs, self.gid, self.n_owned = stage_inputs, ghost_gid, n_owned
+        self.k = 0
+
+    def start(self, U):
+        self._U = U
+        U[self.n_owned:] = float("nan")
+
+    def wait(self):
+        src = self.stage_inputs[self.k % 3]
+        self._U[self.n_owned:] = src.index_select(0, self.gid)
+        self.k += 1
+
+
+@pytest.mark.parametrize("name,cells", [("c2", (12, 4)), ("c4", (4, 2, 2))])
+def test_slab_ssprk3_step_with_overlapped_exchange(name, cells):
+    """stepping.SSPRK3 over slabs (begin / exchange / end per stage, three
+    buffers) == the undecomposed SSP-RK3 step on the owned rows."""
+    from paper_1403_1157_b200.configs import CONFIGS, make_mesh
+    from paper_1403_1157_b200.decomp import build_slab
+    from paper_1403_1157_b200.fields import bump_field
+    from paper_1403_1157_b200.stepping import SSPRK3
+    cfg, order, dt = CONFIGS[name], 2, 2e-4
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    gspace = DGSpace(make_mesh(cfg, cells=cells), order, 6)
+    fn = bump_field(cfg.dim, 6, 3, np.zeros(cfg.dim), np.asarray(cfg.lengths, float))
+    Ug = torch.from_numpy(np.ascontiguousarray(gspace.project(fn).coeffs)).cuda()
+    gop = _op(gspace, model, FluxScheme("cdg2"))
+    W1, W2, Un = (torch.empty_like(Ug) for _ in range(3))
+    gop.rk_stage(None, Ug, W1, 0.0, 1.0, dt)
+    gop.rk_stage(Ug, W1, W2, 0.75, 0.25, 0.25 * dt)
+    gop.rk_stage(Ug, W2, Un, 1 / 3, 2 / 3, 2 / 3 * dt)
+    for r in range(2):
+        sl = build_slab(cfg, r, 2, cells=cells)
+        op = _op(DGSpace(sl.mesh, order, 6), model, FluxScheme("cdg2"),
+                 n_owned=sl.n_owned, global_ids=sl.global_ids)
+        gid = torch.as_tensor(sl.global_ids, device="cuda")
+        U = Ug.index_select(0, gid).contiguous()
+        halo = _ReplayHalo([Ug, W1, W2], gid[sl.n_owned:], sl.n_owned)
+        SSPRK3(op, halo).step(U, dt)
+        assert torch.allclose(U[:sl.n_owned], Un.index_select(0, gid[:sl.n_owned]),
+                              rtol=1e-13, atol=1e-15)
 
 
 def test_sdirk3_jfnk_matches_reference_trajectory(golden):
