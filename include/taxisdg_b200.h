@@ -149,6 +149,12 @@ TDG_API int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, d
 TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt,
                     void* stream);
 
+/* Species totals int u_s over the owned elements, written to totals[S]
+ * (device): sqrt(|ref simplex|) * sum_e detJ_e U[e,s,0].  Replaces
+ * DiscreteFunction.species_totals (reference fespace.py:170-174).
+ * Deterministic (fixed-order two-pass reduction). */
+TDG_API int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stream);
+
 /* Krylov reductions: deterministic two-pass tree (fixed grid), result
  * written to a DEVICE scalar. */
 TDG_API int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n,

@@ -127,7 +127,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     delete ctx;
     return cuda_fail(e, "cudaMalloc face slots");
   }
-  e = cudaMalloc(&ctx->part, kRedBlocks * sizeof(double));
+  e = cudaMalloc(&ctx->part, kRedBlocks * kMaxTotS * sizeof(double));
   if (e != cudaSuccess) {
     cudaFree(ctx->fc);
     delete ctx;
@@ -217,6 +217,17 @@ int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* r
   if (!ctx || !x || !y || !result) return fail(TDG_E_INVALID, "null argument");
   cudaError_t e = launch_dot(x, y, n, ctx->part, result, false, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "dot");
+}
+
+int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stream) {
+  if (!ctx || !U || !totals) return fail(TDG_E_INVALID, "null argument");
+  const tdg_desc& d = ctx->d;
+  const int neg = 1 + d.dim * (d.dim + 1) / 2;
+  // sqrt(|reference simplex|): 1/2 in 2D, 1/6 in 3D
+  const double scale = sqrt(d.dim == 2 ? 0.5 : 1.0 / 6.0);
+  cudaError_t e = launch_totals(U, ctx->p.egeo, d.n_elements, d.n_species, d.nb, neg, scale,
+                                ctx->part, totals, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "species_totals");
 }
 
 int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result, void* stream) {

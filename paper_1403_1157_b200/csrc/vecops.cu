@@ -59,6 +59,41 @@ __global__ void __launch_bounds__(kRedThreads) k_sum_final(const double* __restr
   if (threadIdx.x == 0) *out = sqrt_out ? sqrt(s) : s;
 }
 
+// species totals (fespace.py:170-174): int u_s = scale * sum_e detJ_e U[e,s,0].
+// Same fixed-order two-pass scheme as the dot; block b writes part[b*S+s].
+__global__ void __launch_bounds__(kRedThreads) k_totals_partial(
+    const double* __restrict__ U, const double* __restrict__ egeo, int64_t ne, int S, int nb,
+    int neg, double* __restrict__ part) {
+  double acc[kMaxTotS];
+#pragma unroll
+  for (int s = 0; s < kMaxTotS; ++s) acc[s] = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  for (int64_t e = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; e < ne; e += stride) {
+    const double dj = __ldg(egeo + e * neg);
+    const double* row = U + e * int64_t(S) * nb;
+#pragma unroll
+    for (int s = 0; s < kMaxTotS; ++s)
+      if (s < S) acc[s] = fma(dj, __ldg(row + s * nb), acc[s]);
+  }
+  for (int s = 0; s < S; ++s) {
+    const double v = block_sum(acc[s]);
+    if (threadIdx.x == 0) part[blockIdx.x * S + s] = v;
+    __syncthreads();  // block_sum's shared scratch is reused
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_totals_final(const double* __restrict__ part,
+                                                              int np, int S, double scale,
+                                                              double* __restrict__ out) {
+  for (int s = 0; s < S; ++s) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < np; i += kRedThreads) acc += part[i * S + s];
+    const double v = block_sum(acc);
+    if (threadIdx.x == 0) out[s] = scale * v;
+    __syncthreads();
+  }
+}
+
 __global__ void k_axpby(double a, const double* __restrict__ x, double b, double* __restrict__ y,
                         int64_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -78,6 +113,13 @@ static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = 148 * 16;
   return int(g < 1 ? 1 : g > cap ? cap : g);
+}
+
+cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S, int nb, int neg,
+                          double scale, double* part, double* out, cudaStream_t st) {
+  k_totals_partial<<<kRedBlocks, kRedThreads, 0, st>>>(U, egeo, ne, S, nb, neg, part);
+  k_totals_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, S, scale, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,

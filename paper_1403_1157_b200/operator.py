@@ -259,6 +259,17 @@ class DiscreteOperator:
             self._stream()), "tdg_ssprk3_step")
         return U
 
+    def species_totals(self, U, out=None):
+        """Device int u_s over the owned elements (reference
+        ``fespace.py:170-174``); returns a CUDA tensor of S values."""
+        torch = _torch()
+        self._check_vec("U", U)
+        if out is None:
+            out = torch.empty(self.space.n_species, dtype=torch.float64, device=self.device)
+        _native.check(self.lib.tdg_species_totals(self._ctx, U.data_ptr(), out.data_ptr(),
+                                                  self._stream()), "tdg_species_totals")
+        return out
+
     def dot(self, x, y, out=None):
         x, y = x.reshape(-1), y.reshape(-1)
         self._check_vec("x", x)

@@ -410,3 +410,18 @@ def test_sdirk_orders_match_oracle_composition(order):
             K.append((V - base) / (2e-3 * aii))
         U = U + 2e-3 * sum(tab.b[i] * K[i] for i in range(tab.n_stages))
     assert rel_l2_per_species(space, res.U, U).max() <= 1e-9
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_species_totals_on_device(dim):
+    """tdg_species_totals == DiscreteFunction.species_totals (reference
+    fespace.py:170-174) on a jittered / 3D mesh."""
+    from paper_1403_1157_b200.fespace import DiscreteFunction
+    mesh = unit_square(6, 4, jitter=0.1, seed=3) if dim == 2 else unit_cube(2)
+    space = DGSpace(mesh, 2, 6)
+    rng = np.random.default_rng(7)
+    U = rng.standard_normal((mesh.n_elements, 6, space.nb))
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    got = op.species_totals(torch.from_numpy(U).cuda()).cpu().numpy()
+    ref = DiscreteFunction(space, U).species_totals()
+    assert np.allclose(got, ref, rtol=1e-13, atol=1e-14)
