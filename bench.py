@@ -133,17 +133,25 @@ class ClockSampler:
 # -------------------------------------------------------------- workload
 
 def weak_config(cfg, world):
-    """Weak scaling: every rank owns one config-sized x-slab of a domain
-    N times as long in x (same cells, same cell size)."""
+    """Weak scaling: every rank owns one x-slab of cfg.cells[0] /
+    cfg.weak_div cell columns (same cell size) of a domain N times that
+    long in x -- C2 at N GPUs is N side-by-side C2 domains; C5 (weak_div
+    8) at N = 8 is exactly C5."""
     import dataclasses
-    if world == 1:
+    if world == 1 and cfg.weak_div == 1:
         return cfg
-    cells = (cfg.cells[0] * world,) + tuple(cfg.cells[1:])
-    lengths = (cfg.lengths[0] * world,) + tuple(cfg.lengths[1:])
-    return dataclasses.replace(cfg, cells=cells, lengths=lengths)
+    cx = cfg.cells[0] // cfg.weak_div
+    lx = cfg.lengths[0] / cfg.weak_div
+    cells = (cx * world,) + tuple(cfg.cells[1:])
+    lengths = (lx * world,) + tuple(cfg.lengths[1:])
+    desc = cfg.description
+    if cfg.weak_div > 1:
+        desc += f" -- weak unit {cx}x" + "x".join(map(str, cfg.cells[1:])) + \
+            f" cells per GPU ({world}/{cfg.weak_div} of the config)"
+    return dataclasses.replace(cfg, cells=cells, lengths=lengths, description=desc)
 
 
-def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False):
+def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, device=None):
     """(cfg, space, model, scheme, U0, slab); the slab is None at N=1
     unless ``force_slab``."""
     from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
@@ -160,7 +168,13 @@ def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False):
     space = DGSpace(mesh, cfg.order, 6)
     lo = np.zeros(cfg.dim)
     hi = np.asarray(cfg.lengths, dtype=float)
-    U0 = np.ascontiguousarray(space.project(bump_field(cfg.dim, 6, 1, lo, hi)).coeffs)
+    fn = bump_field(cfg.dim, 6, 1, lo, hi)
+    if cfg.dim == 3 and device is not None:
+        # host projection costs ~0.4 ms/tet at p=3: project on the GPU
+        from paper_1403_1157_b200.fields import project_bumps_device
+        U0 = project_bumps_device(space, fn, device).cpu().numpy()
+    else:
+        U0 = np.ascontiguousarray(space.project(fn).coeffs)
     return cfg, space, PlaqueModel(), FluxScheme(scheme_name), U0, slab
 
 
@@ -260,6 +274,13 @@ def run_reference_arm(args, rank):
     print(json.dumps(line), flush=True)
 
 
+_T0 = time.time()
+
+
+def log(msg):
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def run_native_arm(args, rank, world, local):
     import torch
     from paper_1403_1157_b200.operator import DiscreteOperator
@@ -272,10 +293,12 @@ def run_native_arm(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
     cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
-                                                         args.force_slab)
+                                                         args.force_slab, dev)
+    log(f"problem built: {space.mesh.n_elements} elements")
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
                           global_ids=None if slab is None else slab.global_ids)
+    log("operator created")
     if args.variant:
         op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),
                        serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
@@ -300,6 +323,7 @@ def run_native_arm(args, rank, world, local):
         torch.distributed.all_reduce(rr, op=torch.distributed.ReduceOp.MAX)
         rho = rr.item()
     dt = 0.8 * 2.51 / rho
+    log(f"rho {rho:.4e}")
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -453,7 +477,7 @@ def run_implicit(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
     cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
-                                                         args.force_slab)
+                                                         args.force_slab, dev)
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
                           global_ids=None if slab is None else slab.global_ids)

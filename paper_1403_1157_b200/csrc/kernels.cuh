@@ -152,7 +152,8 @@ k_volume(OpParams p, const double* __restrict__ U, const double* __restrict__ FC
     }
     double lin = 0.0;
 #pragma unroll
-    for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
+    for (int t = 0; t < S; ++t)
+      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
     const double detJ = ge[0];
     double rv = detJ * (acc - p.A[s] * dif + lin);
     const double* fc = FC + (e0 + e) * SN + r;

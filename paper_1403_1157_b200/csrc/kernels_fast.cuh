@@ -441,16 +441,18 @@ struct FastVol {
   using Dm = Dims<D, K>;
   static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, SNP = SN | 1, Q = Dm::NQV;
   static constexpr int NSYM = Dm::NSYM, NEG = Dm::NEG;
-  static constexpr int TE = 128;
+  // 64 elements (2 warps) per CTA: 4 small CTAs per SM desynchronise
+  // their load / compute / store phases better than 2 large ones
+  static constexpr int TE = 64;
   static constexpr int TPHI = Q * NB, TGR = Q * NB * D, TKS = NSYM * NB * NB;
   static constexpr int TAB = TPHI + TGR + Q + TKS;
   static constexpr bool ok = SN <= 36 && TAB * 8 <= 24 * 1024;
-  static constexpr int MINB = 2;  // CTAs/SM the register budget targets
+  static constexpr int MINB = 4;  // CTAs/SM the register budget targets
   static constexpr size_t smem() { return size_t(TAB + 2 * TE * SNP) * 8; }
 };
 
 template <int D, int K, class M>
-__global__ void __launch_bounds__(128, FastVol<D, K, M>::MINB)
+__global__ void __launch_bounds__(FastVol<D, K, M>::TE, FastVol<D, K, M>::MINB)
 k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
               const double* U0, double* out, double ca, double cb, double cc, int mode) {
   using T = FastVol<D, K, M>;
@@ -519,7 +521,8 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
 #pragma unroll
       for (int j = 0; j < NB; ++j) dif = fma(c[s * NB + j], kc[j], dif);
 #pragma unroll
-      for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
+      for (int t = 0; t < S; ++t)
+      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
       const double rv = detJ * (lin - p.A[s] * dif);
       row[s * NB + i] = mode == 2 ? fma(cb, c[s * NB + i], scale * rv) : scale * rv;
     }
@@ -536,7 +539,7 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
 #pragma unroll
       for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][i] = 0.0;
     }
-#pragma unroll 1
+#pragma unroll 2
     for (int q = 0; q < Q; ++q) {
       const double* ph = tphi + q * NB;
       const double* gr = tgr + q * NB * D;
@@ -866,7 +869,8 @@ k_volume4(OpParams p, const double* __restrict__ U, const double* __restrict__ F
     for (int jj = 0; jj < NB; ++jj) dif = fma(cr[s * NB + jj], kp[jj * NB + i], dif);
     double lin = 0.0;
 #pragma unroll
-    for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
+    for (int t = 0; t < S; ++t)
+      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
     double acc = lin - p.A[s] * dif;
     if constexpr (NF + NL > 0) {
       const int fi = M::flux_index(s), li = M::nl_index(s);

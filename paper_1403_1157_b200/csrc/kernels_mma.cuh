@@ -797,7 +797,8 @@ k_volume_mma(OpParams p, const double* __restrict__ vtab, const double* __restri
     for (int jj = 0; jj < NB; ++jj) dif = fma(cr[s * NB + jj], kp[jj * NB + i], dif);
     double lin = 0.0;
 #pragma unroll
-    for (int t = 0; t < S; ++t) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
+    for (int t = 0; t < S; ++t)
+      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
     double acc = lin - p.A[s] * dif;
     if constexpr (NF + NL > 0) {
       const int fi = M::flux_index(s), li = M::nl_index(s);

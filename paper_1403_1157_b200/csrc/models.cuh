@@ -35,6 +35,12 @@ __device__ __forceinline__ double heaviside(double s, double eps) {
 // species n1 n2 n3 c1 c2 c3  (model.py:133)
 struct PlaqueDev {
   static constexpr int S = 6;
+  // nonzeros of the modal linear-source matrix (model.py linear_source;
+  // tables.py checks the host matrix against this pattern)
+  __host__ __device__ static constexpr bool lin_nz(int s, int t) {
+    return (s == 0 && t == 0) || (s == 1 && t == 1) || (s == 2 && t <= 1) || (s == 3 && t == 2) ||
+           (s >= 4 && t == 4);
+  }
   static constexpr bool kConv = true;
   static constexpr bool kMirror = false;  // closed by prescribed fluxes only
   // volume point inputs/outputs
@@ -181,6 +187,9 @@ struct PlaqueDev {
 // species n1 n3 c1  (model.py:212-264)
 struct ReducedDev {
   static constexpr int S = 3;
+  __host__ __device__ static constexpr bool lin_nz(int s, int t) {
+    return (s == 1 && t == 0) || (s == 2 && t == 1);
+  }
   static constexpr bool kConv = true;
   static constexpr bool kMirror = false;
   static constexpr int NVAL = 2;   // n1 c1
@@ -272,6 +281,7 @@ struct ReducedDev {
 template <int NS>
 struct DiffusionDev {
   static constexpr int S = NS;
+  __host__ __device__ static constexpr bool lin_nz(int, int) { return false; }
   static constexpr bool kConv = false;
   static constexpr bool kMirror = true;
   static constexpr int NVAL = 0, NGRAD = 0, NFLUX = 0, NNL = 0;

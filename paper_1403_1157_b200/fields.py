@@ -14,7 +14,7 @@ import numpy as np
 
 from .model import gaussian_bump
 
-__all__ = ["bump_field", "initial_state"]
+__all__ = ["bump_field", "initial_state", "project_bumps_device"]
 
 
 def bump_field(dim, n_species, seed, box_lo, box_hi, nbumps=None):
@@ -37,7 +37,43 @@ def bump_field(dim, n_species, seed, box_lo, box_hi, nbumps=None):
                 out[..., s] += 0.05 * f(x)
         return out
 
+    # the draws, for the device projection (same order as above)
+    rng = np.random.default_rng(seed)
+    fn.params = [[(rng.uniform(box_lo, box_hi), rng.uniform(0.05, 0.15), rng.uniform(0.5, 1.0))
+                  for _ in range(nbumps)] for _ in range(n_species)]
     return fn
+
+
+def project_bumps_device(space, fn, device, chunk: int = 1 << 15):
+    """``space.project(fn)`` for a ``bump_field`` on the GPU (torch fp64,
+    element chunks): the same quadrature (degree 2k+4), basis values and
+    geometry as the host projection, for meshes where the host version
+    is too slow (3D p=3: ~0.4 ms/tet).  Returns a CUDA tensor (ne, S, nb)."""
+    import torch
+    from .quadrature import volume_rule
+    mesh = space.mesh
+    rule = volume_rule(mesh.dim, 2 * space.order + 4)
+    dt = torch.float64
+    phi = torch.as_tensor(space.basis.eval(rule.points), dtype=dt, device=device)   # (q, nb)
+    wq = torch.as_tensor(rule.weights, dtype=dt, device=device)
+    ref = torch.as_tensor(rule.points, dtype=dt, device=device)                     # (q, d)
+    J, _, _ = mesh.jacobians()
+    v0 = mesh.vertices[mesh.elements[:, 0]]
+    ne, S = mesh.n_elements, len(fn.params)
+    out = torch.empty((ne, S, space.nb), dtype=dt, device=device)
+    wphi = wq[:, None] * phi                                                         # (q, nb)
+    for a in range(0, ne, chunk):
+        b = min(ne, a + chunk)
+        Jc = torch.as_tensor(J[a:b], dtype=dt, device=device)
+        x = torch.as_tensor(v0[a:b], dtype=dt, device=device)[:, None, :] + \
+            torch.einsum("eij,qj->eqi", Jc, ref)                                     # (e, q, d)
+        vals = torch.full(x.shape[:2] + (S,), 0.1, dtype=dt, device=device)
+        for s, row in enumerate(fn.params):
+            for c, w, amp in row:
+                r2 = ((x - torch.as_tensor(c, dtype=dt, device=device)) ** 2).sum(-1)
+                vals[..., s] += 0.05 * (amp * torch.exp(-r2 / (2.0 * w * w)))
+        out[a:b] = torch.einsum("eqs,qi->esi", vals, wphi)
+    return out
 
 
 def initial_state(space, seed: int, box=None) -> np.ndarray:

@@ -37,6 +37,25 @@ from .tables import build_tables, scheme_constants
 __all__ = ["DiscreteOperator"]
 
 
+# nonzero patterns of the modal linear source the kernels are compiled
+# for (models.cuh lin_nz); entries outside them are never read
+_LIN_PATTERN = {
+    0: [(0, 0), (1, 1), (2, 0), (2, 1), (3, 2), (4, 4), (5, 4)],   # plaque
+    1: [(1, 0), (2, 1)],                                           # reduced
+    2: [],                                                         # diffusion
+}
+
+
+def _checked_linear_source(model) -> np.ndarray:
+    L = np.ascontiguousarray(model.linear_source(), dtype=np.float64)
+    mask = np.zeros(L.shape, dtype=bool)
+    for s, t in _LIN_PATTERN[model.model_id]:
+        mask[s, t] = True
+    if np.any(L[~mask] != 0.0):
+        raise ValueError("linear source has entries outside the compiled sparsity pattern")
+    return L
+
+
 def _torch():
     import torch
     return torch
@@ -73,7 +92,7 @@ class DiscreteOperator:
             "if_geo", "bf_elem", "bf_lf", "bf_code", "bf_geo")})
         self._host = {
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
-            "lin_source": np.ascontiguousarray(model.linear_source(), dtype=np.float64),
+            "lin_source": _checked_linear_source(model),
             "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
         chi_e, adj, eta = scheme_constants(space, scheme)
         ptr = lambda x: ctypes.c_void_p(x.data_ptr() if x.numel() else 0)

@@ -425,3 +425,16 @@ def test_species_totals_on_device(dim):
     got = op.species_totals(torch.from_numpy(U).cuda()).cpu().numpy()
     ref = DiscreteFunction(space, U).species_totals()
     assert np.allclose(got, ref, rtol=1e-13, atol=1e-14)
+
+
+@pytest.mark.parametrize("dim,order", [(2, 2), (3, 3)])
+def test_device_projection_matches_host(dim, order):
+    """fields.project_bumps_device == DGSpace.project (reference
+    fespace.py:90-111) for the seeded bump fields."""
+    from paper_1403_1157_b200.fields import bump_field, project_bumps_device
+    mesh = unit_square(6, 4, jitter=0.1, seed=2) if dim == 2 else unit_cube(2)
+    space = DGSpace(mesh, order, 6)
+    fn = bump_field(dim, 6, 5, np.zeros(dim), np.ones(dim))
+    ref = space.project(fn).coeffs
+    got = project_bumps_device(space, fn, "cuda", chunk=7).cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
