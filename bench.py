@@ -302,7 +302,8 @@ def run_native_arm(args, rank, world, local):
     if args.variant:
         op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),
                        serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
-                       mma_volume=bool(args.variant & 16))
+                       mma_volume=bool(args.variant & 16),
+                       face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb
     ne, n_int, n_bnd = op.n_owned, len(t.if_code), len(t.bf_code)

@@ -256,6 +256,12 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
+  // bits 8-11: CTAs per SM of the face kernel's grid-stride grid (0 = the
+  // resident count; 15 = one group per warp, no grid cap)
+  {
+    const int f = (variant >> 8) & 15;
+    ctx->face_ctas_per_sm = f == 15 ? -1 : f;
+  }
   return TDG_OK;
 }
 

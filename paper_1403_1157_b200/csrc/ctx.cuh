@@ -56,6 +56,7 @@ struct tdg_ctx {
   double* work2 = nullptr;  // second SSP-RK3 stage vector (library-owned)
   size_t work2_n = 0;
   int vol_variant = 0;         // 0: 1 thread/element (default), 1: 4 lanes/element
+  int face_ctas_per_sm = 0;    // face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
 };
 
 namespace tdg {
@@ -147,8 +148,15 @@ void run_faces(tdg_ctx* ctx, const OpParams& p, const double* U, cudaStream_t st
         KernelTimer kt(ctx, 0, st);
         using T = FastFace<D, K, M>;
         const int64_t warps = (p.nif + T::FPW - 1) / T::FPW + (p.nbf + T::FPW - 1) / T::FPW;
-        const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
-        k_faces_fast<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, U, ctx->fc);
+        int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+        // persistent-style grid: face_ctas_per_sm CTAs per SM loop over
+        // the groups (tables staged once per CTA); 0 = one group per warp
+        if (ctx->face_ctas_per_sm >= 0) {
+          const int per = ctx->face_ctas_per_sm > 0 ? ctx->face_ctas_per_sm : T::MINB;
+          const int64_t cap = int64_t(ctx->num_sms) * per;
+          grid = grid < cap ? grid : cap;
+        }
+        k_faces_fast<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, U, ctx->fc, warps);
       }
     }
   } else {

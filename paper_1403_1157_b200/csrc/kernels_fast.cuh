@@ -1,7 +1,8 @@
 // Register-resident operator kernels for the small-table cases (2D, and
 // any (d, k, model) whose per-lane working set fits in registers).
 //
-// k_faces_fast  one lane per (face, species): a warp holds 32/S faces;
+// k_faces_fast  one lane per (face, species): a warp holds 32/S faces
+//               per group and loops over groups (grid-stride);
 //               the S lanes of a face read the face's two contiguous
 //               S*nb coefficient blocks coalesced, evaluate u and d_n u
 //               at all face points in registers, exchange the few values
@@ -99,6 +100,9 @@ struct FaceRec {
 };
 
 // Face record and the two coefficient rows of species s for warp-group gw.
+// Interior groups load unconditionally from a clamped face index (lanes
+// past the end recompute the last face and never store), so the common
+// path has no predicated loads or zero fills.
 template <int D, int K, class M>
 __device__ __forceinline__ void load_face_group(const OpParams& p, const double* __restrict__ U,
                                                 int64_t gw, int64_t wi, int grp, int s, bool lane_ok,
@@ -106,28 +110,18 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
   using T = FastFace<D, K, M>;
   constexpr int NB = T::NB, SN = T::SN, FPW = T::FPW, NFG = Dims<D, K>::NFG;
   r.wall = gw >= wi;
-  const int64_t f = r.wall ? p.nif + (gw - wi) * FPW + grp : gw * FPW + grp;
-  r.active = lane_ok && (r.wall ? f < p.nif + p.nbf : f < p.nif);
-  r.code = 0;
-  r.ein = 0;
-  r.eout = -1;
-  r.lfi = 0;
-  r.lfo = 0;
-  r.sfac = 0.0;
-  r.h = 1.0;
-  r.idi = 0.0;
-  r.ido = 0.0;
-#pragma unroll
-  for (int a = 0; a < D; ++a) r.jn[0][a] = r.jn[1][a] = 0.0;
-  if (r.active && !r.wall) {
-    r.code = __ldg(p.ifcode + f);
-    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
-    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
+  if (!r.wall) {
+    const int64_t f = gw * FPW + grp;
+    r.active = lane_ok && f < p.nif;
+    const int64_t fc = f < p.nif ? f : p.nif - 1;
+    r.code = __ldg(p.ifcode + fc);
+    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + fc);
+    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + fc);
     r.ein = el.x;
     r.eout = el.y;
     r.lfi = lf.x;
     r.lfo = lf.y;
-    const double* g = p.ifgeo + f * NFG;
+    const double* g = p.ifgeo + fc * NFG;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       r.jn[0][a] = __ldg(g + a);
@@ -137,29 +131,33 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
     r.h = __ldg(g + 2 * D + 1);
     r.idi = __ldg(g + 2 * D + 2);
     r.ido = __ldg(g + 2 * D + 3);
-  } else if (r.active) {
-    const int64_t b = f - p.nif;
-    r.code = __ldg(p.bfcode + b);
-    r.ein = __ldg(p.bfel + b);
-    r.lfi = __ldg(p.bflf + b);
-    r.sfac = __ldg(p.bfgeo + b);
+    load_row<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
+    // mirror faces (Dirichlet models only) have no outside element
+    const int eo = (M::kMirror && r.eout < 0) ? r.ein : r.eout;
+    load_row<NB>(U + int64_t(eo) * SN + s * NB, r.co);
+    return;
   }
-  if (r.active) load_row<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
-  else {
+  const int64_t b = (gw - wi) * FPW + grp;
+  r.active = lane_ok && b < p.nbf;
+  const int64_t bc = b < p.nbf ? b : p.nbf - 1;
+  r.code = __ldg(p.bfcode + bc);
+  r.ein = __ldg(p.bfel + bc);
+  r.eout = -1;
+  r.lfi = __ldg(p.bflf + bc);
+  r.lfo = 0;
+  r.sfac = __ldg(p.bfgeo + bc);
+  r.h = 1.0;
+  r.idi = r.ido = 0.0;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) r.ci[i] = 0.0;
-  }
-  const bool two = r.active && !r.wall && !code_mirror(r.code);
-  if (two) load_row<NB>(U + int64_t(r.eout) * SN + s * NB, r.co);
-  else {
+  for (int a = 0; a < D; ++a) r.jn[0][a] = r.jn[1][a] = 0.0;
+  load_row<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
 #pragma unroll
-    for (int i = 0; i < NB; ++i) r.co[i] = 0.0;
-  }
+  for (int i = 0; i < NB; ++i) r.co[i] = 0.0;
 }
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(128, FastFace<D, K, M>::MINB)
-k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
+k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, int64_t ngroups) {
   using T = FastFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW, NCV = T::NCV;
   constexpr int NFG = Dims<D, K>::NFG;
@@ -182,12 +180,14 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
   double* xch = dph + 2 * F * NB;           // [3][S][F]
   double* cvs = xch + 3 * S * F;            // [F][NCV]
 
-  const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
   const int64_t wi = (p.nif + FPW - 1) / FPW;
+  // grid-stride over face groups: the tables above are staged once per CTA
+  for (int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp; gw < ngroups;
+       gw += int64_t(gridDim.x) * T::WARPS) {
   FaceRec<D, NB> cur;
   load_face_group<D, K, M>(p, U, gw, wi, grp, s, lane_ok, cur);
   const bool wall = cur.wall, active = cur.active;
-  if (!__any_sync(0xffffffffu, active)) return;  // warp-uniform
+  if (!__any_sync(0xffffffffu, active)) continue;  // warp-uniform
   int code = cur.code;
   // lanes without a face copy lane 0's code word so every warp-uniform
   // branch below stays uniform
@@ -375,6 +375,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC) 
     store_row<NB>(FC + (int64_t(lfi) * p.ne + ein) * SN + s * NB, ri);
     if (two && !code_skip_out(code))
       store_row<NB>(FC + (int64_t(lfo) * p.ne + eout) * SN + s * NB, ro);
+  }
+  __syncwarp();  // the warp's scratch is rewritten by the next group
   }
 }
 
