@@ -175,7 +175,9 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * volume and faces serially on the caller's stream instead of the
  * overlapped two-stream schedule; bit 3: flip the face-kernel choice
  * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
- * the tensor-core volume kernel instead of the SIMT one; bits 8-11: CTAs
+ * the tensor-core volume kernel instead of the SIMT one; bit 5: launch
+ * tdg_ssprk3_step's kernels directly instead of replaying its cached CUDA
+ * graph; bits 8-11: CTAs
  * per SM of the register-resident face kernel's grid-stride grid (0 =
  * default, 15 = uncapped, one face group per warp).  0 (default) lets the
  * library pick the fastest compiled-in kernels and schedule. */

@@ -152,6 +152,10 @@ int tdg_destroy(tdg_ctx* ctx) {
     }
   cudaFree(ctx->fc);
   cudaFree(ctx->part);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->gev_a) cudaEventDestroy(ctx->gev_a);
+  if (ctx->gev_b) cudaEventDestroy(ctx->gev_b);
   if (ctx->work2) cudaFree(ctx->work2);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
@@ -203,13 +207,54 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, 
     ctx->work2_n = n;
   }
   double* w2 = ctx->work2;
-  int rc = ctx->impl.run(ctx, U, nullptr, work, 0.0, 1.0, dt, 2, st);  // U1 = U + dt f(U)
-  if (rc) return rc;
-  // U2 = 3/4 U + 1/4 (U1 + dt f(U1))
-  rc = ctx->impl.run(ctx, work, U, w2, 0.75, 0.25, 0.25 * dt, 2, st);
-  if (rc) return rc;
-  // U3 = 1/3 U + 2/3 (U2 + dt f(U2)), written over U (U is only U0 here)
-  return ctx->impl.run(ctx, w2, U, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, st);
+  auto stages = [&](cudaStream_t s) {
+    int rc = ctx->impl.run(ctx, U, nullptr, work, 0.0, 1.0, dt, 2, s);  // U1 = U + dt f(U)
+    if (rc) return rc;
+    // U2 = 3/4 U + 1/4 (U1 + dt f(U1))
+    rc = ctx->impl.run(ctx, work, U, w2, 0.75, 0.25, 0.25 * dt, 2, s);
+    if (rc) return rc;
+    // U3 = 1/3 U + 2/3 (U2 + dt f(U2)), written over U (U is only U0 here)
+    return ctx->impl.run(ctx, w2, U, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, s);
+  };
+  if (!ctx->use_graph || ctx->profile) return stages(st);
+  // graph path: the nine launches and their cross-stream events replay as
+  // one graph on gstream, ordered after / before the caller's stream
+  if (!ctx->gexec || ctx->g_U != U || ctx->g_work != work || ctx->g_dt != dt) {
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+    if (!ctx->gstream) {
+      if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->gev_a, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->gev_b, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "graph stream");
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "begin capture");
+    const int rc = stages(ctx->gstream);
+    e = cudaStreamEndCapture(ctx->gstream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "end capture");
+    e = cudaGraphInstantiate(&ctx->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      ctx->gexec = nullptr;
+      return cuda_fail(e, "graph instantiate");
+    }
+    ctx->g_U = U;
+    ctx->g_work = work;
+    ctx->g_dt = dt;
+  }
+  cudaEventRecord(ctx->gev_a, st);
+  cudaStreamWaitEvent(ctx->gstream, ctx->gev_a, 0);
+  cudaError_t e = cudaGraphLaunch(ctx->gexec, ctx->gstream);
+  if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  cudaEventRecord(ctx->gev_b, ctx->gstream);
+  cudaStreamWaitEvent(st, ctx->gev_b, 0);
+  return TDG_OK;
 }
 
 int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* result,
@@ -256,6 +301,11 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
+  ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
+  if (ctx->gexec) {  // kernel choice changed: re-capture
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
   // bits 8-11: CTAs per SM of the face kernel's grid-stride grid (0 = the
   // resident count; 15 = one group per warp, no grid cap)
   {

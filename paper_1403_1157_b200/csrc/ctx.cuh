@@ -56,6 +56,16 @@ struct tdg_ctx {
   double* work2 = nullptr;  // second SSP-RK3 stage vector (library-owned)
   size_t work2_n = 0;
   int vol_variant = 0;         // 0: 1 thread/element (default), 1: 4 lanes/element
+  // SSP-RK3 step replayed from a CUDA graph (captured on gstream, joined
+  // to the caller's stream with events); re-captured when U / work / dt
+  // change.  Not used while profiling (per-kernel events).
+  bool use_graph = true;
+  cudaStream_t gstream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t gev_a = nullptr, gev_b = nullptr;
+  const double* g_U = nullptr;
+  const double* g_work = nullptr;
+  double g_dt = 0.0;
   int face_ctas_per_sm = 0;    // face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
 };
 

@@ -202,7 +202,8 @@ class DiscreteOperator:
 
     def set_variant(self, generic: bool = False, vol4: bool = False,
                     serial: bool = False, flip_mma: bool = False,
-                    mma_volume: bool = False, face_ctas_per_sm: int = 0):
+                    mma_volume: bool = False, face_ctas_per_sm: int = 0,
+                    no_graph: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
@@ -212,7 +213,8 @@ class DiscreteOperator:
         _native.check(self.lib.tdg_set_variant(
             self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
             | (int(bool(serial)) << 2) | (int(bool(flip_mma)) << 3)
-            | (int(bool(mma_volume)) << 4) | ((int(face_ctas_per_sm) & 15) << 8)),
+            | (int(bool(mma_volume)) << 4) | (int(bool(no_graph)) << 5)
+            | ((int(face_ctas_per_sm) & 15) << 8)),
             "tdg_set_variant")
 
     def profile(self, enable: bool = True):

@@ -438,3 +438,23 @@ def test_device_projection_matches_host(dim, order):
     ref = space.project(fn).coeffs
     got = project_bumps_device(space, fn, "cuda", chunk=7).cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_ssprk3_graph_replay_is_bitwise_equal_to_direct_launches():
+    """tdg_ssprk3_step replays a cached CUDA graph; re-captured when dt or
+    the buffers change; identical bits to the direct launch sequence."""
+    space = DGSpace(unit_square(16, 8, lengths=(2.0, 1.0)), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U0 = torch.from_numpy(initial_state(space, 4)).cuda()
+    runs = []
+    for no_graph in (False, True):
+        op.set_variant(no_graph=no_graph)
+        U, W = U0.clone(), torch.empty_like(U0)
+        for dt in (1e-4, 1e-4, 2e-4, 1e-4):
+            op.ssprk3_step(U, W, dt)
+        U2, W2 = U0.clone(), torch.empty_like(U0)      # new buffers
+        op.ssprk3_step(U2, W2, 1e-4)
+        torch.cuda.synchronize()
+        runs.append((U.clone(), U2.clone()))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
+    assert not torch.equal(runs[0][0], U0)
