@@ -169,8 +169,8 @@ def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, devi
     lo = np.zeros(cfg.dim)
     hi = np.asarray(cfg.lengths, dtype=float)
     fn = bump_field(cfg.dim, 6, 1, lo, hi)
-    if cfg.dim == 3 and device is not None:
-        # host projection costs ~0.4 ms/tet at p=3: project on the GPU
+    if device is not None and (cfg.dim == 3 or mesh.n_elements > 500_000):
+        # host projection is slow at scale (~0.4 ms/tet at 3D p=3): on the GPU
         from paper_1403_1157_b200.fields import project_bumps_device
         U0 = project_bumps_device(space, fn, device).cpu().numpy()
     else:
@@ -304,6 +304,7 @@ def run_native_arm(args, rank, world, local):
                        serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
                        mma_volume=bool(args.variant & 16),
                        no_graph=bool(args.variant & 32),
+                       tc_volume=bool(args.variant & 4096),
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb

@@ -114,6 +114,9 @@ typedef struct tdg_desc {
   const double* vol_mma;
   /* the last n_cut_faces interior faces touch ghost rows (slab runs) */
   int64_t n_cut_faces;
+  /* operand tables of the transposed tensor-core volume kernel
+   * (tables.tc_volume_tables; may be NULL) */
+  const double* vol_tc;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -177,7 +180,9 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
  * the tensor-core volume kernel instead of the SIMT one; bit 5: launch
  * tdg_ssprk3_step's kernels directly instead of replaying its cached CUDA
- * graph; bits 8-11: CTAs
+ * graph; bit 12: use the transposed tensor-core volume kernel wherever it
+ * compiles (default only where the one-thread-per-element kernel does not
+ * fit); bits 8-11: CTAs
  * per SM of the register-resident face kernel's grid-stride grid (0 =
  * default, 15 = uncapped, one face group per warp).  0 (default) lets the
  * library pick the fastest compiled-in kernels and schedule. */

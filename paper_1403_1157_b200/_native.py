@@ -36,7 +36,7 @@ class TdgDesc(ctypes.Structure):
         ("elem_geo", _p),
         ("if_elems", _p), ("if_lf", _p), ("if_code", _p), ("if_geo", _p),
         ("bf_elem", _p), ("bf_lf", _p), ("bf_code", _p), ("bf_geo", _p),
-        ("face_mma", _p), ("vol_mma", _p), ("n_cut_faces", _i64),
+        ("face_mma", _p), ("vol_mma", _p), ("n_cut_faces", _i64), ("vol_tc", _p),
     ]
 
 

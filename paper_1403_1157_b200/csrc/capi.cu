@@ -107,6 +107,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.bfgeo = d.bf_geo;
   p.fmma = d.face_mma;
   p.vmma = d.vol_mma;
+  p.vtc = d.vol_tc;
 
   {
     int dev = 0, sms = 0;
@@ -301,6 +302,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
+  ctx->force_tc = ((variant >> 12) & 1) != 0;  // bit 12: transposed tensor-core volume everywhere
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
   if (ctx->gexec) {  // kernel choice changed: re-capture
     cudaGraphExecDestroy(ctx->gexec);

@@ -63,6 +63,7 @@ struct OpParams {
   const double* __restrict__ bfgeo;
   const double* __restrict__ fmma;  // tensor-core face tables (may be null)
   const double* __restrict__ vmma;  // tensor-core volume tables (may be null)
+  const double* __restrict__ vtc;   // transposed tensor-core volume tables (may be null)
 };
 
 // code-word layout, mirrors include/taxisdg_b200.h

@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "kernels_fast.cuh"
 #include "kernels_mma.cuh"
+#include "kernels_tc.cuh"
 #include "models.cuh"
 #include "vecops.cuh"
 
@@ -48,6 +49,7 @@ struct tdg_ctx {
   int num_sms = 148;
   bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
   bool use_vmma = false;  // A/B: tensor-core volume kernel (slower than SIMT at C2)
+  bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -87,6 +89,11 @@ int configure(int nqv) {
     e = cudaFuncSetAttribute(k_volume_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(MmaVol<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure volume_mma");
+  }
+  if constexpr (TcVol<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_volume_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TcVol<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure volume_tc");
   }
   if constexpr (MmaFace<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_faces_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -185,12 +192,25 @@ void run_faces(tdg_ctx* ctx, const OpParams& p, const double* U, cudaStream_t st
   }
 }
 
-// fast volume kernel: tensor-core (use_vm) or one thread per element
+// fast volume kernels: vk 0 one thread per element, 1 tensor-core
+// (element-local GEMMs), 2 tensor-core transposed (elements x points)
 template <int D, int K, class M>
 void launch_volume(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a,
-                   double b, double c, int mode, cudaStream_t st, bool use_vm) {
+                   double b, double c, int mode, cudaStream_t st, int vk) {
   const OpParams& p = ctx->p;
-  if (use_vm) {
+  if (vk == 2) {
+    if constexpr (TcVol<D, K, M>::ok) {
+      using T = TcVol<D, K, M>;
+      const int64_t tasks = (p.ne + T::EW - 1) / T::EW;
+      int64_t grid = (tasks + T::WARPS - 1) / T::WARPS;
+      const int64_t cap = int64_t(ctx->num_sms) * T::MINB;
+      grid = grid < cap ? grid : cap;
+      k_volume_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.vtc, U, ctx->fc, U0, out,
+                                                                   a, b, c, mode);
+    }
+    return;
+  }
+  if (vk == 1) {
     if constexpr (MmaVol<D, K, M>::ok) {
       using T = MmaVol<D, K, M>;
       const int64_t grid = (p.ne + T::TE - 1) / T::TE;
@@ -252,16 +272,22 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   constexpr bool vmma_ok = MmaVol<D, K, M>::ok;
   const bool use_vm = vmma_ok && p.vmma != nullptr && p.nqv == Dims<D, K>::NQV &&
                       !ctx->force_generic && ctx->use_vmma;
-  const bool overlap = (use_fv || use_vm) && use_ff && ctx->overlap && ctx->aux && out != U &&
-                       p.ne > 0 && (SN_of<M, D, K>() % 2 == 0);
+  // transposed tensor-core volume kernel: default where the one-thread-
+  // per-element kernel does not fit (2D k=3, 3D)
+  constexpr bool tc_ok = TcVol<D, K, M>::ok;
+  const bool use_tc = tc_ok && !use_vm && p.vtc != nullptr && p.nqv == Dims<D, K>::NQV &&
+                      !ctx->force_generic && (ctx->force_tc || !use_fv);
+  const int vk = use_vm ? 1 : (use_tc ? 2 : 0);
+  const bool overlap = (use_fv || use_vm || use_tc) && use_ff && ctx->overlap && ctx->aux &&
+                       out != U && p.ne > 0 && (SN_of<M, D, K>() % 2 == 0);
   if (overlap) {
-    if constexpr ((fast_vol || vmma_ok) && (SN_of<M, D, K>() % 2 == 0)) {
+    if constexpr ((fast_vol || vmma_ok || tc_ok) && (SN_of<M, D, K>() % 2 == 0)) {
       if (part != 2) {
         cudaEventRecord(ctx->ev_in, st);
         cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
         {
           KernelTimer kt(ctx, 2, ctx->aux);
-          launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, use_vm);
+          launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, vk);
         }
         cudaEventRecord(ctx->ev_vol, ctx->aux);
         faces(part == 0 ? 0 : 1, use_ff);
@@ -289,9 +315,9 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   } else {
     faces(2, use_ff);
   }
-  if (p.ne > 0 && use_vm) {
+  if (p.ne > 0 && (use_vm || use_tc)) {
     KernelTimer kt(ctx, 2, st);
-    launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode, st, true);
+    launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode, st, vk);
   } else if (p.ne > 0) {
     KernelTimer kt(ctx, 2, st);
     if (use_v4) {

@@ -1,0 +1,243 @@
+// Volume terms + M^-1 + Runge-Kutta stage on the FP64 tensor cores, for
+// the larger (d, k) where one thread per element cannot hold an element
+// in registers (2D k=3, 3D k=2/3): C3, C4, C5.
+//
+// Layout: a warp owns EW = 8 elements, the M dimension of every
+// mma.sync.m8n8k4.f64 (DMMA).  With g = lane>>2, t = lane&3:
+//
+//   A fragment  A[g][t]        element g, basis k = 4 kt + t   (coefficients,
+//                              loaded straight from U: 32 contiguous bytes
+//                              per element and k-step)
+//   B fragment  B[t][g]        tables, n = point or output column
+//   accumulator C[g][2t + j]   element g, column 2t + j
+//
+//   point values   V_s[e][q]   = sum_k c_s[e][k] Phi[q][k]      (B = Phi^T)
+//   ref. gradients G_sa[e][q]  = sum_k c_s[e][k] d_a Phi[q][k]
+//   flux rows      R_f[e][n]  += sum_q Fr_fa[e][q] w_q d_a Phi[q][pi(n)]
+//   bilinear src   R_l[e][n]  += sum_q Nl[e][q]    w_q Phi[q][pi(n)]
+//   diffusion      D_s[e][n]   = sum_p M_p[e] sum_k c_s[e][k] KS_p[k][pi(n)]
+//
+// The point physics runs on the accumulator layout (each lane holds every
+// species at its two (element, point) pairs), and the projection's A
+// operand is that same accumulator taken one point parity at a time (k-step
+// ks uses points 8qt + 2t + ks): no lane exchange anywhere.  The output
+// columns are permuted, pi(8nt + 2t + j) = 4(2nt + j) + t, so a lane's
+// output entries are exactly the basis indices of its A fragments: the
+// linear source, the U / U0 / face-slot reads and the output stores are
+// lane-local, 32-byte-contiguous accesses.  Formulas as k_volume
+// (reference operator.py:292-324, model.py:147-170); tables built by
+// tables.tc_volume_tables.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "kernels_mma.cuh"
+#include "models.cuh"
+
+namespace tdg {
+
+template <int D, int K, class M>
+struct TcVol {
+  using Dm = Dims<D, K>;
+  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, Q = Dm::NQV;
+  static constexpr int NEG = Dm::NEG, NSYM = Dm::NSYM;
+  static constexpr int QP = ceil_to(Q, 8), QT = QP / 8;
+  static constexpr int KT = (NB + 3) / 4, NBK = 4 * KT;
+  static constexpr int NNT = (NB + 7) / 8, NBN = 8 * NNT;
+  static constexpr int NV = M::NVAL, NG = M::NGRAD, NF = M::NFLUX, NL = M::NNL;
+  // table offsets (doubles)
+  static constexpr int OPHT = 0;                         // [NBK][QP]
+  static constexpr int OGT = OPHT + NBK * QP;            // [D][NBK][QP]
+  static constexpr int OPP = OGT + D * NBK * QP;         // [QP][NBN]
+  static constexpr int OPG = OPP + QP * NBN;             // [D][QP][NBN]
+  static constexpr int OKS = OPG + D * QP * NBN;         // [NSYM][NBK][NBN]
+  static constexpr int TAB = OKS + NSYM * NBK * NBN;
+  static constexpr int WARPS = 4, EW = 8;
+  static constexpr bool kSmemTables = TAB * 8 <= 64 * 1024;
+  static constexpr size_t smem() { return kSmemTables ? size_t(TAB) * 8 : 0; }
+  static constexpr int MINB = 2;
+  static constexpr bool ok = S <= kMaxS && D >= 2;
+};
+
+template <int D, int K, class M>
+__global__ void __launch_bounds__(128, TcVol<D, K, M>::MINB)
+k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
+            const double* __restrict__ FC, const double* U0, double* out, double ca, double cb,
+            double cc, int mode) {
+  using T = TcVol<D, K, M>;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, NEG = T::NEG, NSYM = T::NSYM;
+  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NBK = T::NBK, NNT = T::NNT, NBN = T::NBN;
+  constexpr int NV = T::NV, NG = T::NG, NF = T::NF, NL = T::NL;
+  extern __shared__ __align__(16) double sm[];
+  const double* tb = tabs;
+  if constexpr (T::kSmemTables) {
+    for (int i = threadIdx.x; i < T::TAB; i += 128) sm[i] = __ldg(tabs + i);
+    __syncthreads();
+    tb = sm;
+  }
+  // mode bit 2: the face-slot sum is added by k_fc_add (overlapped run)
+  const bool with_fc = (mode & 4) == 0;
+  mode &= 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntask = (p.ne + T::EW - 1) / T::EW;
+
+  for (int64_t task = int64_t(blockIdx.x) * T::WARPS + warp; task < ntask;
+       task += int64_t(gridDim.x) * T::WARPS) {
+    const int64_t e = task * T::EW + g;
+    const bool valid = e < p.ne;
+    const int64_t ec = valid ? e : p.ne - 1;
+    double ge[NEG];
+#pragma unroll
+    for (int k = 0; k < NEG; ++k) ge[k] = __ldg(p.egeo + ec * NEG + k);
+    // A fragments: every species, every k-step (basis 4 kt + t)
+    double cf[S][KT];
+    const double* urow = U + ec * SN;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+        cf[s][kt] = (4 * kt + t < NB) ? __ldg(urow + s * NB + 4 * kt + t) : 0.0;
+
+    double af[NF > 0 ? NF : 1][NNT][2], al[NL > 0 ? NL : 1][NNT][2];
+#pragma unroll
+    for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int k = 0; k < (NF > 0 ? NF : 1); ++k) af[k][nt][j] = 0.0;
+#pragma unroll
+        for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][nt][j] = 0.0;
+      }
+
+    if constexpr (NF + NL > 0) {
+#pragma unroll 1
+      for (int qt = 0; qt < QT; ++qt) {
+        // point values and reference gradients of the quadrature species
+        double v[NV > 0 ? NV : 1][2], gr[NG > 0 ? NG : 1][D][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+          for (int k = 0; k < (NV > 0 ? NV : 1); ++k) v[k][j] = 0.0;
+#pragma unroll
+          for (int k = 0; k < (NG > 0 ? NG : 1); ++k)
+#pragma unroll
+            for (int a = 0; a < D; ++a) gr[k][a][j] = 0.0;
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int kr = 4 * kt + t, qc = 8 * qt + g;
+          const double bphi = tb[T::OPHT + kr * QP + qc];
+#pragma unroll
+          for (int k = 0; k < NV; ++k) dmma(v[k][0], v[k][1], cf[M::val_sp(k)][kt], bphi);
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double bg = tb[T::OGT + (a * NBK + kr) * QP + qc];
+#pragma unroll
+            for (int k = 0; k < NG; ++k) dmma(gr[k][a][0], gr[k][a][1], cf[M::grad_sp(k)][kt], bg);
+          }
+        }
+        // point physics at (element g, point 8qt + 2t + j)
+        double fr[NF > 0 ? NF : 1][D][2], nl[NL > 0 ? NL : 1][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double vv[NV > 0 ? NV : 1], gM[NG > 0 ? NG : 1][D];
+#pragma unroll
+          for (int k = 0; k < NV; ++k) vv[k] = v[k][j];
+#pragma unroll
+          for (int k = 0; k < NG; ++k)
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              double s = 0.0;
+#pragma unroll
+              for (int a = 0; a < D; ++a) s = fma(gr[k][a][j], ge[1 + sym_index(D, a, b)], s);
+              gM[k][b] = s;
+            }
+          double f[NF > 0 ? NF : 1][D], n1[NL > 0 ? NL : 1];
+          M::template volume_point<D>(p.P, vv, gM, f, n1);
+#pragma unroll
+          for (int k = 0; k < NF; ++k)
+#pragma unroll
+            for (int a = 0; a < D; ++a) fr[k][a][j] = f[k][a];
+#pragma unroll
+          for (int k = 0; k < NL; ++k) nl[k][j] = n1[k];
+        }
+        // projection: k-step ks takes the points of parity ks
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int qr = 8 * qt + 2 * t + ks;
+#pragma unroll
+          for (int nt = 0; nt < NNT; ++nt) {
+            const int nc = 8 * nt + g;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              const double bp = tb[T::OPG + (a * QP + qr) * NBN + nc];
+#pragma unroll
+              for (int k = 0; k < NF; ++k) dmma(af[k][nt][0], af[k][nt][1], fr[k][a][ks], bp);
+            }
+            if constexpr (NL > 0) {
+              const double bq = tb[T::OPP + qr * NBN + nc];
+#pragma unroll
+              for (int k = 0; k < NL; ++k) dmma(al[k][nt][0], al[k][nt][1], nl[k][ks], bq);
+            }
+          }
+        }
+      }
+    }
+
+    // epilogue per species: diffusion GEMM, linear source, face slots, RK
+    const double detJ = ge[0];
+    const double idet = 1.0 / detJ;
+    const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      double dif[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) dif[nt][0] = dif[nt][1] = 0.0;
+#pragma unroll
+      for (int pq = 0; pq < NSYM; ++pq)
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const double a = cf[s][kt] * ge[1 + pq];
+#pragma unroll
+          for (int nt = 0; nt < NNT; ++nt)
+            dmma(dif[nt][0], dif[nt][1], a,
+                 tb[T::OKS + (pq * NBK + 4 * kt + t) * NBN + 8 * nt + g]);
+        }
+      const int fi = M::flux_index(s), li = M::nl_index(s);
+      const double As = p.A[s];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int kt = 2 * nt + j, i = 4 * kt + t;
+          if (kt >= KT || i >= NB) continue;
+          double lin = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < S; ++s2)
+            if (M::lin_nz(s, s2)) lin = fma(p.L[s * kMaxS + s2], cf[s2][kt], lin);
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < NF; ++k)
+            if (fi == k) acc = af[k][nt][j];
+#pragma unroll
+          for (int k = 0; k < NL; ++k)
+            if (li == k) acc += al[k][nt][j];
+          double rv = detJ * (acc - As * dif[nt][j] + lin);
+          const int64_t off = ec * SN + s * NB + i;
+          if (with_fc) {
+#pragma unroll
+            for (int lf = 0; lf <= D; ++lf) rv += __ldcs(FC + int64_t(lf) * p.ne * SN + off);
+          }
+          double o = scale * rv;
+          if (mode == 2) {
+            o = fma(cb, cf[s][kt], o);
+            if (ca != 0.0) o = fma(ca, U0[off], o);
+          }
+          if (valid) out[off] = o;
+        }
+    }
+  }
+}
+
+}  // namespace tdg

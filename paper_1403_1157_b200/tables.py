@@ -248,6 +248,36 @@ def mma_volume_tables(t: OperatorTables) -> np.ndarray:
     return np.ascontiguousarray(np.concatenate([x.ravel() for x in (TPhi, TG, TGT, TPT)]))
 
 
+def tc_volume_tables(t: OperatorTables) -> np.ndarray:
+    """Operand tables of the transposed tensor-core volume kernel
+    (csrc/kernels_tc.cuh, k_volume_tc), concatenated:
+
+    PHT [NBK][QP]        Phi[q][k]                    B of the point values
+    GT  [d][NBK][QP]     G[q][k][a]                   B of the reference gradients
+    PP  [QP][NBN]        w_q Phi[q][pi(n)]            projection of the bilinear source
+    PG  [d][QP][NBN]     w_q G[q][pi(n)][a]           projection of the flux rows
+    KS  [nsym][NBK][NBN] KS_p[k][pi(n)]               diffusion stiffness blocks
+    with QP = ceil8(Q), NBK = ceil4(nb), NBN = ceil8(nb) and the output
+    column permutation pi(8 nt + 2 t + j) = 4 (2 nt + j) + t (entries with
+    pi(n) >= nb are zero)."""
+    d, nb = t.dim, t.nb
+    Q = t.vol_phi.shape[0]
+    QP, NBK, NBN = _ceil(Q, 8), _ceil(nb, 4), _ceil(nb, 8)
+    nsym = d * (d + 1) // 2
+    n = np.arange(NBN)
+    pi = 4 * (2 * (n // 8) + (n % 8) % 2) + (n % 8) // 2
+    ok = pi < nb
+    pic = np.where(ok, pi, 0)
+    w = t.vol_w
+    PHT = np.zeros((NBK, QP)); PHT[:nb, :Q] = t.vol_phi.T
+    GT = np.zeros((d, NBK, QP)); GT[:, :nb, :Q] = t.vol_grad.transpose(2, 1, 0)
+    PP = np.zeros((QP, NBN)); PP[:Q] = (w[:, None] * t.vol_phi)[:, pic] * ok
+    PG = np.zeros((d, QP, NBN))
+    PG[:, :Q] = (w[:, None, None] * t.vol_grad).transpose(2, 0, 1)[:, :, pic] * ok
+    KS = np.zeros((nsym, NBK, NBN)); KS[:, :nb] = t.vol_stiff[:, :, pic] * ok
+    return np.ascontiguousarray(np.concatenate([x.ravel() for x in (PHT, GT, PP, PG, KS)]))
+
+
 def scheme_constants(space: DGSpace, scheme: FluxScheme):
     d, k = space.mesh.dim, space.order
     return (chi_factor(d), scheme.adjoint_sign,

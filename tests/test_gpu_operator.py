@@ -60,6 +60,24 @@ def test_flipped_face_kernel_matches_reference_golden(golden, name):
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
 
+@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
+def test_tc_volume_kernel_matches_reference_golden(golden, name):
+    """The transposed tensor-core volume kernel (default for 2D k=3 and
+    3D), forced on every golden case, incl. the overlapped schedule."""
+    space, model, scheme, U, R, F = operator_case(golden, name)
+    op = _op(space, model, scheme)
+    op.set_variant(tc_volume=True)
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+    gf = op.apply_f(U)
+    assert rel_l2_per_species(space, gf, F).max() <= 1e-12
+    Ut = torch.from_numpy(np.ascontiguousarray(U)).cuda()
+    out = torch.empty_like(Ut)
+    op.rk_stage(Ut, Ut, out, 0.5, 0.25, 1e-3)
+    ref = 0.75 * U + 1e-3 * F
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
 @pytest.mark.parametrize("dirichlet", [0, 1])
 def test_heat_models_mma(golden, scheme, dirichlet):
