@@ -115,7 +115,7 @@ typedef struct tdg_desc {
   /* the last n_cut_faces interior faces touch ghost rows (slab runs) */
   int64_t n_cut_faces;
   /* operand tables of the transposed tensor-core volume kernel
-   * (tables.tc_volume_tables; may be NULL) */
+   * (tables.tc_volume_tables, may be NULL) */
   const double* vol_tc;
 } tdg_desc;
 
