@@ -117,6 +117,14 @@ typedef struct tdg_desc {
   /* operand tables of the transposed tensor-core volume kernel
    * (tables.tc_volume_tables, may be NULL) */
   const double* vol_tc;
+  /* transposed tensor-core face kernel (3D): per-signature operand tables
+   * (tables.tc_face_tables, stride from the compiled sizes) and blocks of up
+   * to 8 interior faces of one signature, int32 [n_face_blocks][2] = (first
+   * face, count), the last n_face_blocks_cut of them cut faces (may be NULL) */
+  const double* face_tc;
+  const int32_t* face_blocks;
+  int64_t n_face_blocks;
+  int64_t n_face_blocks_cut;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -180,7 +188,8 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
  * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
  * the tensor-core volume kernel instead of the SIMT one; bit 5: launch
  * tdg_ssprk3_step's kernels directly instead of replaying its cached CUDA
- * graph; bit 12: use the transposed tensor-core volume kernel wherever it
+ * graph; bit 13: in 3D, use the element-local DMMA face kernel for interior
+ * faces instead of the transposed one; bit 12: use the transposed tensor-core volume kernel wherever it
  * compiles (default only where the one-thread-per-element kernel does not
  * fit); bits 8-11: CTAs
  * per SM of the register-resident face kernel's grid-stride grid (0 =

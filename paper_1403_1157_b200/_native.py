@@ -37,6 +37,7 @@ class TdgDesc(ctypes.Structure):
         ("if_elems", _p), ("if_lf", _p), ("if_code", _p), ("if_geo", _p),
         ("bf_elem", _p), ("bf_lf", _p), ("bf_code", _p), ("bf_geo", _p),
         ("face_mma", _p), ("vol_mma", _p), ("n_cut_faces", _i64), ("vol_tc", _p),
+        ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64), ("n_face_blocks_cut", _i64),
     ]
 
 

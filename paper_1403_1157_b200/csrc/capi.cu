@@ -108,6 +108,8 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.fmma = d.face_mma;
   p.vmma = d.vol_mma;
   p.vtc = d.vol_tc;
+  p.ftc = d.face_tc;
+  p.fblk = d.face_blocks;
 
   {
     int dev = 0, sms = 0;
@@ -302,7 +304,8 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
-  ctx->force_tc = ((variant >> 12) & 1) != 0;  // bit 12: transposed tensor-core volume everywhere
+  ctx->force_tc = ((variant >> 12) & 1) != 0;
+  ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)  // bit 12: transposed tensor-core volume everywhere
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
   if (ctx->gexec) {  // kernel choice changed: re-capture
     cudaGraphExecDestroy(ctx->gexec);

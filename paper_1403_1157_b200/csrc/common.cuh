@@ -64,6 +64,8 @@ struct OpParams {
   const double* __restrict__ fmma;  // tensor-core face tables (may be null)
   const double* __restrict__ vmma;  // tensor-core volume tables (may be null)
   const double* __restrict__ vtc;   // transposed tensor-core volume tables (may be null)
+  const double* __restrict__ ftc;   // transposed tensor-core face tables (may be null)
+  const int32_t* __restrict__ fblk; // interior-face blocks [n][2] (first, count)
 };
 
 // code-word layout, mirrors include/taxisdg_b200.h

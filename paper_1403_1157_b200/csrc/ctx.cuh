@@ -13,6 +13,7 @@
 #include "kernels_fast.cuh"
 #include "kernels_mma.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_tcf.cuh"
 #include "models.cuh"
 #include "vecops.cuh"
 
@@ -50,6 +51,7 @@ struct tdg_ctx {
   bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
   bool use_vmma = false;  // A/B: tensor-core volume kernel (slower than SIMT at C2)
   bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
+  bool no_tcf = false;    // A/B: element-local DMMA face kernel instead of the transposed one
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -89,6 +91,11 @@ int configure(int nqv) {
     e = cudaFuncSetAttribute(k_volume_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(MmaVol<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure volume_mma");
+  }
+  if constexpr (TcFace<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_faces_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TcFace<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_tc");
   }
   if constexpr (TcVol<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_volume_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -239,7 +246,42 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   const int64_t ncut = ctx->d.n_cut_faces;
   // faces split: [0, nif-ncut) + walls need owned rows only; the last ncut
   // interior faces touch ghost rows
+  // transposed tensor-core interior-face kernel (3D): blocks of faces of
+  // one signature; walls on the element-local DMMA kernel
+  constexpr bool tcf_ok = TcFace<D, K, M>::ok && MmaFace<D, K, M>::ok;
+  const bool use_tcf = tcf_ok && p.ftc != nullptr && p.fblk != nullptr && p.fmma != nullptr &&
+                       p.nqf == Dims<D, K>::NQF && !ctx->force_generic && !ctx->no_tcf &&
+                       !ctx->flip_mma;
+  auto faces_tc = [&](int which) {
+    if constexpr (tcf_ok) {
+      const int64_t nblk = ctx->d.n_face_blocks, ncb = ctx->d.n_face_blocks_cut;
+      const int64_t b0 = which == 2 ? nblk - ncb : 0;
+      const int64_t b1 = which == 1 ? nblk - ncb : nblk;
+      if (b1 > b0) {
+        KernelTimer kt(ctx, 0, st);
+        using T = TcFace<D, K, M>;
+        int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
+        const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 4;
+        grid = grid < cap ? grid : cap;
+        k_faces_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1, U,
+                                                                    ctx->fc);
+      }
+      if (which != 2 && p.nbf > 0) {
+        KernelTimer kt(ctx, 1, st);
+        using T = MmaFace<D, K, M>;
+        OpParams pw = p;
+        pw.nif = 0;
+        const int64_t warps = (p.nbf + T::NFW - 1) / T::NFW;
+        const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+        k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(pw, pw.fmma, U, ctx->fc);
+      }
+    }
+  };
   auto faces = [&](int which, bool use_ff_) {
+    if (use_tcf) {
+      faces_tc(part == 0 ? 0 : which);
+      return;
+    }
     if (which == 0 && part == 0) {
       run_faces<D, K, M>(ctx, p, U, st, use_ff_);
       return;

@@ -1,0 +1,316 @@
+// Interior faces on the FP64 tensor cores, transposed (3D).
+//
+// A warp owns a block of up to 8 interior faces with one trace-table
+// signature (tables.tc_face_blocks): the faces are the M dimension of
+// every mma.sync.m8n8k4.f64, so the signature's tables are the shared B
+// operands and the per-face geometry (jn = Jinv n, lifting weight) scales
+// the A operands lane by lane.  With g = lane>>2, t = lane&3 a lane owns
+// face g; its accumulators hold columns 2t + j of the 8-column tiles:
+//
+//   traces      u[f][q]   = sum_k c[f][k] B[q][k]                  (B^T tables)
+//               d_n u     = sum_a sum_k (jn_a c)[f][k] G_a[q][k]
+//   lifting     m[f][n]   = kappa_f sum_q dU[f][q] w_q B[q][pi(n)]  (modal)
+//               rho[f][q] = sum_i m[f][i] B[q][i]
+//   projection  R[f][n]  += sum_q Y[f][q] B[q][pi(n)] + sum_qa (X jn_a)[f][q] G_a[q][pi(n)]
+//
+// Point quantities come out in the accumulator layout (face g, points
+// 8qt + 2t + j) and feed the next GEMM as A operands one point parity at a
+// time (k-step ks takes points 8qt + 2t + ks); the lifting coefficients
+// feed rho the same way through the column permutation pi(8nt + 2t + j) =
+// 4(2nt + j) + t.  No lane exchange, no warp barrier: pass A evaluates the
+// coupled LLF physics (wave speed, taxis flux normals) per (face, point)
+// into a lane-private shared-memory slice; pass B runs species by species
+// (jumps -> modal lifting; traces, flux, projection) and writes the two
+// face-slot rows.  Formulas as k_faces_fast / k_faces_mma (reference
+// operator.py:326-434, flux.py:92-138); wall faces stay on k_faces_mma.
+#pragma once
+
+#include "common.cuh"
+#include "kernels_mma.cuh"
+#include "models.cuh"
+
+namespace tdg {
+
+template <int D, int K, class M>
+struct TcFace {
+  using Dm = Dims<D, K>;
+  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, F = Dm::NQF, NFG = Dm::NFG;
+  static constexpr int QP = ceil_to(F, 8), QT = QP / 8;
+  static constexpr int KT = (NB + 3) / 4, NBK = 4 * KT;
+  static constexpr int NNT = (NB + 7) / 8, NBN = 8 * NNT;
+  static constexpr int NCV = 1 + M::NFX;
+  // per-signature table offsets (doubles), see tables.tc_face_tables
+  static constexpr int OBT = 0, OGT = OBT + NBK * QP, OBP = OGT + D * NBK * QP,
+                       OGP = OBP + QP * NBN, OWB = OGP + D * QP * NBN, TS = OWB + QP * NBN;
+  static constexpr int WARPS = 4;
+  static constexpr int PWS = 8 * QP * NCV;  // per-warp point-physics slice
+  static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
+  static constexpr int MINB = 2;
+  static constexpr bool ok = D == 3 && S <= kMaxS && smem() <= 96 * 1024;
+};
+
+// species the face point physics reads (values / averaged normal
+// derivatives); the model's face_point fetches them by species index
+template <class M>
+struct TcfPhys {
+  static constexpr int NV = M::NVAL, NG = M::NGRAD;
+  __host__ __device__ static constexpr int val(int k) { return M::val_sp(k); }
+  __host__ __device__ static constexpr int grad(int k) { return M::grad_sp(k); }
+};
+template <>
+struct TcfPhys<PlaqueDev> {  // LLF wave speed needs n1 n2 c1 c3; d_n of n1 c1 c3
+  static constexpr int NV = 4, NG = 3;
+  __host__ __device__ static constexpr int val(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 3 : 5; }
+  __host__ __device__ static constexpr int grad(int k) { return k == 0 ? 0 : k == 1 ? 3 : 5; }
+};
+
+template <class M>
+struct TcfPoint {
+  double v[3][M::S];
+  __device__ __forceinline__ double operator()(int kind, int sp) const { return v[kind][sp]; }
+};
+
+template <int D, int K, class M>
+__global__ void __launch_bounds__(128, TcFace<D, K, M>::MINB)
+k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
+           int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ FC) {
+  using T = TcFace<D, K, M>;
+  using PH = TcfPhys<M>;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
+  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NBK = T::NBK, NNT = T::NNT, NBN = T::NBN;
+  constexpr int NCV = T::NCV, TS = T::TS;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double* cvS = sm + warp * T::PWS + g * QP * NCV;  // this lane's face
+
+  for (int64_t blk = blk0 + int64_t(blockIdx.x) * T::WARPS + warp; blk < blk1;
+       blk += int64_t(gridDim.x) * T::WARPS) {
+    const int2 bd = __ldg(reinterpret_cast<const int2*>(blocks) + blk);
+    const bool active = g < bd.y;
+    const int64_t f = int64_t(bd.x) + (active ? g : 0);
+    const int code = __ldg(p.ifcode + f);
+    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
+    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
+    const double* gg = p.ifgeo + f * NFG;
+    double jn[2][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      jn[0][a] = __ldg(gg + a);
+      jn[1][a] = __ldg(gg + D + a);
+    }
+    const double sfac = __ldg(gg + 2 * D), h = __ldg(gg + 2 * D + 1);
+    const double idi = __ldg(gg + 2 * D + 2), ido = __ldg(gg + 2 * D + 3);
+    const bool mirror = M::kMirror && code_mirror(code);
+    // signature of the block (uniform): the B operands
+    const int sig = __shfl_sync(0xffffffffu, code, 0) & 1023;
+    const double* Ti = tabs + size_t(sig & 31) * TS;
+    const double* To = tabs + size_t((sig >> 5) & 31) * TS;
+    const double* ui_row = U + int64_t(el.x) * SN;
+    const double* uo_row = U + int64_t(mirror ? el.x : el.y) * SN;
+
+    // ---- pass A: coupled point physics -> lane-private slice -----------
+    if constexpr (M::kConv) {
+      constexpr int NV = PH::NV, NG = PH::NG;
+      double ci[NV][KT], co[NV][KT];
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const bool in = 4 * kt + t < NB;
+          ci[k][kt] = in ? __ldg(ui_row + PH::val(k) * NB + 4 * kt + t) : 0.0;
+          co[k][kt] = in ? __ldg(uo_row + PH::val(k) * NB + 4 * kt + t) : 0.0;
+        }
+#pragma unroll 1
+      for (int qt = 0; qt < QT; ++qt) {
+        double vi[NV][2], vo[NV][2], di[NG][2], dq[NG][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) vi[k][j] = vo[k][j] = 0.0;
+#pragma unroll
+          for (int k = 0; k < NG; ++k) di[k][j] = dq[k][j] = 0.0;
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int kr = 4 * kt + t, qc = 8 * qt + g;
+          const double bi = __ldg(Ti + T::OBT + kr * QP + qc);
+          const double bo = __ldg(To + T::OBT + kr * QP + qc);
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            dmma(vi[k][0], vi[k][1], ci[k][kt], bi);
+            dmma(vo[k][0], vo[k][1], co[k][kt], bo);
+          }
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double gi = __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc);
+            const double go = __ldg(To + T::OGT + (a * NBK + kr) * QP + qc);
+#pragma unroll
+            for (int k = 0; k < NG; ++k) {
+              int kv = 0;
+#pragma unroll
+              for (int j2 = 0; j2 < NV; ++j2)
+                if (PH::val(j2) == PH::grad(k)) kv = j2;
+              dmma(di[k][0], di[k][1], ci[kv][kt] * jn[0][a], gi);
+              dmma(dq[k][0], dq[k][1], co[kv][kt] * jn[1][a], go);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          TcfPoint<M> pt;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            pt.v[0][PH::val(k)] = vi[k][j];
+            pt.v[1][PH::val(k)] = mirror ? 2.0 * M::mirror_value(p.P, PH::val(k)) - vi[k][j] : vo[k][j];
+          }
+#pragma unroll
+          for (int k = 0; k < NG; ++k)
+            pt.v[2][PH::grad(k)] = mirror ? di[k][j] : 0.5 * (di[k][j] + dq[k][j]);
+          double cv[NCV];
+          M::face_point(p.P, pt, cv);
+          const int q = 8 * qt + 2 * t + j;
+#pragma unroll
+          for (int c = 0; c < NCV; ++c) cvS[q * NCV + c] = cv[c];
+        }
+      }
+    }
+
+    // lifting weights per side (operator.py:336-357)
+    const bool br2 = p.scheme == BR2;
+    const bool lift = p.scheme != IP && p.scheme != BO;
+    const bool use_in = lift && (mirror || br2 || code_minus_in(code));
+    const bool use_out = lift && !mirror && (br2 || !code_minus_in(code));
+    const double wside = (br2 && !mirror) ? 0.5 : 1.0;
+    const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac;
+    const bool skip_out = !active || mirror || code_skip_out(code);
+    double* fci = FC + (int64_t(lf.x) * p.ne + el.x) * SN;
+    double* fco = FC + (int64_t(lf.y) * p.ne + el.y) * SN;
+
+    // ---- pass B: species by species ------------------------------------
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) {
+      const double As = p.A[s];
+      const double gs = M::kMirror ? M::mirror_value(p.P, s) : 0.0;
+      double ci[KT], co[KT];
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const bool in = 4 * kt + t < NB;
+        ci[kt] = in ? __ldg(ui_row + s * NB + 4 * kt + t) : 0.0;
+        co[kt] = in ? __ldg(uo_row + s * NB + 4 * kt + t) : 0.0;
+      }
+      // B1: jumps -> modal lifting coefficients m_in, m_out
+      double mi[NNT][2], mo[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) mi[nt][0] = mi[nt][1] = mo[nt][0] = mo[nt][1] = 0.0;
+      if (lift) {
+#pragma unroll 1
+        for (int qt = 0; qt < QT; ++qt) {
+          double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0};
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const int kr = 4 * kt + t, qc = 8 * qt + g;
+            dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + kr * QP + qc));
+            dmma(uo[0], uo[1], co[kt], __ldg(To + T::OBT + kr * QP + qc));
+          }
+          double du[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) du[j] = mirror ? 2.0 * (ui[j] - gs) : ui[j] - uo[j];
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int qr = 8 * qt + 2 * t + ks;
+#pragma unroll
+            for (int nt = 0; nt < NNT; ++nt) {
+              dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + T::OWB + qr * NBN + 8 * nt + g));
+              dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + T::OWB + qr * NBN + 8 * nt + g));
+            }
+          }
+        }
+        const double ki = use_in ? fac0 * As * idi : 0.0;
+        const double ko = use_out ? fac0 * As * ido : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            mi[nt][j] *= ki;
+            mo[nt][j] *= ko;
+          }
+      }
+      // B2: traces, flux, projection
+      double ri[NNT][2], ro[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) ri[nt][0] = ri[nt][1] = ro[nt][0] = ro[nt][1] = 0.0;
+#pragma unroll 1
+      for (int qt = 0; qt < QT; ++qt) {
+        double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0}, di[2] = {0.0, 0.0}, dq[2] = {0.0, 0.0};
+        double rho[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int kr = 4 * kt + t, qc = 8 * qt + g;
+          const double bi = __ldg(Ti + T::OBT + kr * QP + qc);
+          const double bo = __ldg(To + T::OBT + kr * QP + qc);
+          dmma(ui[0], ui[1], ci[kt], bi);
+          dmma(uo[0], uo[1], co[kt], bo);
+          if (lift) {
+            // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
+            dmma(rho[0], rho[1], mi[kt / 2][kt % 2], bi);
+            dmma(rho[0], rho[1], mo[kt / 2][kt % 2], bo);
+          }
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            dmma(di[0], di[1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc));
+            dmma(dq[0], dq[1], co[kt] * jn[1][a], __ldg(To + T::OGT + (a * NBK + kr) * QP + qc));
+          }
+        }
+        double Y[2], X[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 8 * qt + 2 * t + j;
+          const double uoj = mirror ? 2.0 * gs - ui[j] : uo[j];
+          const double du = ui[j] - uoj;
+          const double gav = mirror ? di[j] : 0.5 * (di[j] + dq[j]);
+          double qv = rho[j];
+          if (p.scheme == IP) qv = p.eta / h * As * du;
+          if constexpr (M::kConv) {
+            double cnv = 0.5 * cvS[q * NCV] * du;
+#pragma unroll
+            for (int k = 0; k < M::NFX; ++k)
+              if (s == k) cnv = fma(0.5, cvS[q * NCV + 1 + k], cnv);
+            qv += cnv;
+          }
+          const double wq = q < F ? __ldg(p.fw + q) * sfac : 0.0;
+          Y[j] = wq * (As * gav - qv);
+          X[j] = wq * 0.5 * p.adj * As * du;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int qr = 8 * qt + 2 * t + ks;
+#pragma unroll
+          for (int nt = 0; nt < NNT; ++nt) {
+            const int nc = 8 * nt + g;
+            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + T::OBP + qr * NBN + nc));
+            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + qr * NBN + nc));
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              dmma(ri[nt][0], ri[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (a * QP + qr) * NBN + nc));
+              dmma(ro[nt][0], ro[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (a * QP + qr) * NBN + nc));
+            }
+          }
+        }
+      }
+      // face-slot rows: lane entries (face g, basis 4 (2nt + j) + t)
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 4 * (2 * nt + j) + t;
+          if (i < NB) {
+            if (active) fci[s * NB + i] = ri[nt][j];
+            if (!skip_out) fco[s * NB + i] = ro[nt][j];
+          }
+        }
+    }
+  }
+}
+
+}  // namespace tdg

@@ -83,10 +83,13 @@ class DiscreteOperator:
         self.n_owned = t.elem_geo.shape[0]
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
-        from .tables import mma_face_tables, mma_volume_tables, tc_volume_tables
+        from .tables import (mma_face_tables, mma_volume_tables, tc_face_blocks,
+                             tc_face_tables, tc_volume_tables)
         mma, self._mma_stride = mma_face_tables(t)
+        blocks, n_cut_blocks = tc_face_blocks(t)
         self._keep = {"face_mma": dev(mma), "vol_mma": dev(mma_volume_tables(t)),
-                      "vol_tc": dev(tc_volume_tables(t))}
+                      "vol_tc": dev(tc_volume_tables(t)), "face_tc": dev(tc_face_tables(t)[0]),
+                      "face_blocks": dev(blocks)}
         self._keep.update({name: dev(getattr(t, name)) for name in (
             "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
             "face_Pw", "face_w", "elem_geo", "if_elems", "if_lf", "if_code",
@@ -118,7 +121,9 @@ class DiscreteOperator:
             if_geo=ptr(k["if_geo"]), bf_elem=ptr(k["bf_elem"]),
             bf_lf=ptr(k["bf_lf"]), bf_code=ptr(k["bf_code"]),
             bf_geo=ptr(k["bf_geo"]), face_mma=ptr(k["face_mma"]),
-            vol_mma=ptr(k["vol_mma"]), n_cut_faces=t.n_cut, vol_tc=ptr(k["vol_tc"]))
+            vol_mma=ptr(k["vol_mma"]), n_cut_faces=t.n_cut, vol_tc=ptr(k["vol_tc"]),
+            face_tc=ptr(k["face_tc"]), face_blocks=ptr(k["face_blocks"]),
+            n_face_blocks=len(blocks), n_face_blocks_cut=n_cut_blocks)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _native.check(self.lib.tdg_create(ctypes.byref(desc),
@@ -204,7 +209,8 @@ class DiscreteOperator:
     def set_variant(self, generic: bool = False, vol4: bool = False,
                     serial: bool = False, flip_mma: bool = False,
                     mma_volume: bool = False, face_ctas_per_sm: int = 0,
-                    no_graph: bool = False, tc_volume: bool = False):
+                    no_graph: bool = False, tc_volume: bool = False,
+                    no_tc_faces: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
@@ -215,7 +221,7 @@ class DiscreteOperator:
             self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
             | (int(bool(serial)) << 2) | (int(bool(flip_mma)) << 3)
             | (int(bool(mma_volume)) << 4) | (int(bool(no_graph)) << 5)
-            | (int(bool(tc_volume)) << 12)
+            | (int(bool(tc_volume)) << 12) | (int(bool(no_tc_faces)) << 13)
             | ((int(face_ctas_per_sm) & 15) << 8)),
             "tdg_set_variant")
 

@@ -229,6 +229,65 @@ def mma_face_tables(t: OperatorTables):
     return np.ascontiguousarray(np.concatenate(parts)), stride
 
 
+def _pi_cols(nb: int):
+    """Output-column permutation of the transposed tensor-core kernels:
+    pi(8 nt + 2 t + j) = 4 (2 nt + j) + t; returns (pi clipped, valid)."""
+    NBN = _ceil(nb, 8)
+    n = np.arange(NBN)
+    pi = 4 * (2 * (n // 8) + (n % 8) % 2) + (n % 8) // 2
+    ok = pi < nb
+    return np.where(ok, pi, 0), ok
+
+
+def tc_face_tables(t: OperatorTables):
+    """Per-signature operand tables of the transposed tensor-core face
+    kernel (csrc/kernels_tcf.cuh), concatenated per table id:
+
+    BT  [NBK][QP]        B[q][k]                 traces u = c B^T, rho = m B^T
+    GT  [d][NBK][QP]     G[q][k][a]              traces d_n u = sum_a (jn_a c) G_a^T
+    BP  [QP][NBN]        B[q][pi(n)]             projection of Y
+    GP  [d][QP][NBN]     G[q][pi(n)][a]          projection of X jn_a
+    WB  [QP][NBN]        w_q B[q][pi(n)]         modal lifting m = dU (w B)
+    with QP = ceil8(F), NBK = ceil4(nb), NBN = ceil8(nb).  Returns the flat
+    array and the per-signature stride."""
+    d, nb, F = t.dim, t.nb, t.nq_face
+    QP, NBK, NBN = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
+    pic, ok = _pi_cols(nb)
+    parts = []
+    for k in range(t.face_B.shape[0]):
+        B, G = t.face_B[k], t.face_G[k]                    # (F, nb), (F, nb, d)
+        BT = np.zeros((NBK, QP)); BT[:nb, :F] = B.T
+        GT = np.zeros((d, NBK, QP)); GT[:, :nb, :F] = G.transpose(2, 1, 0)
+        BP = np.zeros((QP, NBN)); BP[:F] = B[:, pic] * ok
+        GP = np.zeros((d, QP, NBN)); GP[:, :F] = G.transpose(2, 0, 1)[:, :, pic] * ok
+        WB = np.zeros((QP, NBN)); WB[:F] = (t.face_w[:, None] * B)[:, pic] * ok
+        parts.append(np.concatenate([x.ravel() for x in (BT, GT, BP, GP, WB)]))
+    stride = len(parts[0])
+    return np.ascontiguousarray(np.concatenate(parts)), stride
+
+
+def tc_face_blocks(t: OperatorTables, block: int = 8):
+    """Blocks of up to ``block`` consecutive interior faces with one trace-
+    table signature each (the M dimension of the transposed face kernel),
+    never straddling the non-cut / cut boundary.  Returns (int32 [nblk][2]
+    = (first face, count), number of blocks of cut faces at the end)."""
+    nif = len(t.if_code)
+    if nif == 0:
+        return np.zeros((0, 2), np.int32), 0
+    sig = (t.if_code.astype(np.int64) & 1023) + (np.arange(nif) >= nif - t.n_cut) * 1024
+    brk = np.flatnonzero(np.diff(sig)) + 1
+    starts = np.concatenate([[0], brk])
+    lens = np.diff(np.concatenate([starts, [nif]]))
+    nblk = (lens + block - 1) // block
+    rs = np.repeat(starts, nblk)
+    j = np.arange(nblk.sum()) - np.repeat(np.cumsum(nblk) - nblk, nblk)
+    first = rs + block * j
+    cnt = np.minimum(block, np.repeat(starts + lens, nblk) - first)
+    blocks = np.ascontiguousarray(np.stack([first, cnt], axis=1), dtype=np.int32)
+    n_cut_blocks = int((first >= nif - t.n_cut).sum()) if t.n_cut else 0
+    return blocks, n_cut_blocks
+
+
 def mma_volume_tables(t: OperatorTables) -> np.ndarray:
     """Zero-padded operand tables of the tensor-core volume kernel
     (csrc/kernels_mma.cuh, k_volume_mma), concatenated:
@@ -264,10 +323,7 @@ def tc_volume_tables(t: OperatorTables) -> np.ndarray:
     Q = t.vol_phi.shape[0]
     QP, NBK, NBN = _ceil(Q, 8), _ceil(nb, 4), _ceil(nb, 8)
     nsym = d * (d + 1) // 2
-    n = np.arange(NBN)
-    pi = 4 * (2 * (n // 8) + (n % 8) % 2) + (n % 8) // 2
-    ok = pi < nb
-    pic = np.where(ok, pi, 0)
+    pic, ok = _pi_cols(nb)
     w = t.vol_w
     PHT = np.zeros((NBK, QP)); PHT[:nb, :Q] = t.vol_phi.T
     GT = np.zeros((d, NBK, QP)); GT[:, :nb, :Q] = t.vol_grad.transpose(2, 1, 0)

@@ -58,6 +58,9 @@ def test_flipped_face_kernel_matches_reference_golden(golden, name):
     op.set_variant(mma_volume=True)
     got = op.apply(U)
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+    op.set_variant(no_tc_faces=True)       # 3D: element-local DMMA interior faces
+    got = op.apply(U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
 
 @pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
