@@ -237,13 +237,19 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           }
       }
       // B2: traces, flux, projection
-      double ri[NNT][2], ro[NNT][2];
+      // separate accumulators for the Y and X terms (shorter DMMA chains)
+      double ri[NNT][2], ro[NNT][2], rix[NNT][2], rox[NNT][2];
 #pragma unroll
-      for (int nt = 0; nt < NNT; ++nt) ri[nt][0] = ri[nt][1] = ro[nt][0] = ro[nt][1] = 0.0;
+      for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) ri[nt][j] = ro[nt][j] = rix[nt][j] = rox[nt][j] = 0.0;
 #pragma unroll 1
       for (int qt = 0; qt < QT; ++qt) {
-        double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0}, di[2] = {0.0, 0.0}, dq[2] = {0.0, 0.0};
-        double rho[2] = {0.0, 0.0};
+        double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0};
+        double dia[D][2], dqa[D][2];
+        double rhi[2] = {0.0, 0.0}, rho_[2] = {0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) dia[a][0] = dia[a][1] = dqa[a][0] = dqa[a][1] = 0.0;
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
           const int kr = 4 * kt + t, qc = 8 * qt + g;
@@ -253,14 +259,26 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           dmma(uo[0], uo[1], co[kt], bo);
           if (lift) {
             // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
-            dmma(rho[0], rho[1], mi[kt / 2][kt % 2], bi);
-            dmma(rho[0], rho[1], mo[kt / 2][kt % 2], bo);
+            dmma(rhi[0], rhi[1], mi[kt / 2][kt % 2], bi);
+            dmma(rho_[0], rho_[1], mo[kt / 2][kt % 2], bo);
           }
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            dmma(di[0], di[1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc));
-            dmma(dq[0], dq[1], co[kt] * jn[1][a], __ldg(To + T::OGT + (a * NBK + kr) * QP + qc));
+            dmma(dia[a][0], dia[a][1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc));
+            dmma(dqa[a][0], dqa[a][1], co[kt] * jn[1][a], __ldg(To + T::OGT + (a * NBK + kr) * QP + qc));
           }
+        }
+        double di[2], dq[2], rho[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          di[j] = dia[0][j];
+          dq[j] = dqa[0][j];
+#pragma unroll
+          for (int a = 1; a < D; ++a) {
+            di[j] += dia[a][j];
+            dq[j] += dqa[a][j];
+          }
+          rho[j] = rhi[j] + rho_[j];
         }
         double Y[2], X[2];
 #pragma unroll
@@ -292,8 +310,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
             dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + qr * NBN + nc));
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-              dmma(ri[nt][0], ri[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (a * QP + qr) * NBN + nc));
-              dmma(ro[nt][0], ro[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (a * QP + qr) * NBN + nc));
+              dmma(rix[nt][0], rix[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (a * QP + qr) * NBN + nc));
+              dmma(rox[nt][0], rox[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (a * QP + qr) * NBN + nc));
             }
           }
         }
@@ -305,8 +323,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
         for (int j = 0; j < 2; ++j) {
           const int i = 4 * (2 * nt + j) + t;
           if (i < NB) {
-            if (active) fci[s * NB + i] = ri[nt][j];
-            if (!skip_out) fco[s * NB + i] = ro[nt][j];
+            if (active) fci[s * NB + i] = ri[nt][j] + rix[nt][j];
+            if (!skip_out) fco[s * NB + i] = ro[nt][j] + rox[nt][j];
           }
         }
     }
