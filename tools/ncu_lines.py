@@ -10,7 +10,7 @@ from collections import Counter
 
 rep, cubin, fun = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+raw = subprocess.run(["ncu", "-i", rep] + (["-k", "regex:" + sys.argv[5]] if len(sys.argv) > 5 else []) + ["--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, counts = None, []
