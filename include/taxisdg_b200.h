@@ -167,7 +167,8 @@ TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, dou
 TDG_API int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stream);
 
 /* Krylov reductions: deterministic two-pass tree (fixed grid), result
- * written to a DEVICE scalar. */
+ * written to a DEVICE scalar.  Operands must be 16-byte aligned
+ * (TDG_E_INVALID otherwise). */
 TDG_API int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n,
             double* result, void* stream);
 TDG_API int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result,
@@ -179,6 +180,16 @@ TDG_API int tdg_axpby(double a, const double* x, double b, double* y, int64_t n,
  * host round trip) */
 TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y,
                  int64_t n, void* stream);
+
+/* One modified Gram-Schmidt sweep of GMRES's Arnoldi step (reference
+ * timeint.py:162-170): for i = 0..j, h[i] = w . V_i then w -= h[i] V_i;
+ * finally h[j+1] = ||w||.  V holds rows of length n with leading dimension
+ * ldv; h (j+2 doubles) and everything else are device pointers.  Each
+ * axpy is fused with the next dot (same element order and reduction tree
+ * as tdg_dot / tdg_axpy_dev, so bitwise the same results), one call per
+ * Arnoldi step, no host round trip. */
+TDG_API int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w, int64_t n,
+                    double* h, void* stream);
 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
  * CTA-staged generic kernels; bit 1: use the four-lanes-per-element

@@ -260,9 +260,12 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, 
   return TDG_OK;
 }
 
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* result,
             void* stream) {
   if (!ctx || !x || !y || !result) return fail(TDG_E_INVALID, "null argument");
+  if (!aligned16(x) || !aligned16(y)) return fail(TDG_E_INVALID, "dot operands must be 16-byte aligned");
   cudaError_t e = launch_dot(x, y, n, ctx->part, result, false, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "dot");
 }
@@ -280,6 +283,7 @@ int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stre
 
 int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result, void* stream) {
   if (!ctx || !x || !result) return fail(TDG_E_INVALID, "null argument");
+  if (!aligned16(x)) return fail(TDG_E_INVALID, "norm operand must be 16-byte aligned");
   cudaError_t e = launch_dot(x, x, n, ctx->part, result, true, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "norm2");
 }
@@ -288,6 +292,16 @@ int tdg_axpby(double a, const double* x, double b, double* y, int64_t n, void* s
   if (!x || !y) return fail(TDG_E_INVALID, "null argument");
   cudaError_t e = launch_axpby(a, x, b, y, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "axpby");
+}
+
+int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w, int64_t n, double* h,
+            void* stream) {
+  if (!ctx || !V || !w || !h) return fail(TDG_E_INVALID, "null argument");
+  if (j < 0 || n < 0 || ldv < n) return fail(TDG_E_INVALID, "bad mgs sizes");
+  if (!aligned16(V) || !aligned16(w) || (ldv & 1))
+    return fail(TDG_E_INVALID, "mgs operands must be 16-byte aligned (even ldv)");
+  cudaError_t e = launch_mgs(V, ldv, j, w, n, h, ctx->part, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "mgs");
 }
 
 int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y, int64_t n,

@@ -32,22 +32,54 @@ __device__ __forceinline__ double block_sum(double v) {
   return v;
 }
 
-template <bool SQ>
-__global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __restrict__ x,
-                                                             const double* __restrict__ y,
-                                                             int64_t n, double* __restrict__ part) {
-  double acc = 0.0;
+// Partial reductions over a fixed grid (kRedBlocks CTAs): each thread
+// walks the vector in 16-byte pairs, two pairs per iteration (grid stride
+// 2*stride), so ~10 MB of loads are in flight per array (HBM needs ~7 MB);
+// lanes accumulate in a fixed order, then a fixed tree -> deterministic.
+//   MODE 0: x . y    1: x . x    2: x -= h v_prev, then x . y
+//   MODE 3: x -= h v_prev, then x . x        (the fused MGS steps)
+// Element order and per-thread accumulators depend only on n and the grid,
+// so a fused axpy+dot is bitwise an axpy followed by a dot.  Vectors must
+// be 16-byte aligned (torch allocations and rows of an even-length V).
+template <int MODE>
+__global__ void __launch_bounds__(kRedThreads) k_red_partial(
+    const double* __restrict__ h_prev, const double* __restrict__ vprev, double* x,
+    const double* __restrict__ y, int64_t n, double* __restrict__ part) {
+  constexpr bool AXPY = MODE >= 2, SQ = MODE == 1 || MODE == 3;
+  const double a = AXPY ? -1.0 * __ldg(h_prev) : 0.0;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  const int64_t n2 = n >> 1;
   const int64_t stride = int64_t(gridDim.x) * kRedThreads;
-  int64_t i = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
-  // two independent accumulators to keep two loads in flight per thread
-  double acc2 = 0.0;
-  for (; i + stride < n; i += 2 * stride) {
-    const double a = __ldg(x + i), b = __ldg(x + i + stride);
-    acc = fma(a, SQ ? a : __ldg(y + i), acc);
-    acc2 = fma(b, SQ ? b : __ldg(y + i + stride), acc2);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  const double2* p2 = reinterpret_cast<const double2*>(vprev);
+  auto step = [&](int64_t k, double& s0, double& s1) {
+    double2 xv = x2[k];
+    if constexpr (AXPY) {
+      const double2 pv = __ldg(p2 + k);
+      xv.x = fma(a, pv.x, xv.x);
+      xv.y = fma(a, pv.y, xv.y);
+      x2[k] = xv;
+    }
+    const double2 yv = SQ ? xv : __ldg(y2 + k);
+    s0 = fma(xv.x, yv.x, s0);
+    s1 = fma(xv.y, yv.y, s1);
+  };
+  int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+  for (; k + stride < n2; k += 2 * stride) {
+    step(k, acc0, acc1);
+    step(k + stride, acc2, acc3);
   }
-  if (i < n) acc = fma(__ldg(x + i), SQ ? __ldg(x + i) : __ldg(y + i), acc);
-  const double s = block_sum(acc + acc2);
+  if (k < n2) step(k, acc0, acc1);
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+    double xv = x[n - 1];
+    if constexpr (AXPY) {
+      xv = fma(a, __ldg(vprev + n - 1), xv);
+      x[n - 1] = xv;
+    }
+    acc0 = fma(xv, SQ ? xv : __ldg(y + n - 1), acc0);
+  }
+  const double s = block_sum((acc0 + acc1) + (acc2 + acc3));
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
@@ -122,13 +154,30 @@ cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S
   return cudaGetLastError();
 }
 
+// x is only read in MODE 0/1 (the cast drops const for the shared kernel)
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,
                        bool norm, cudaStream_t st) {
+  double* xm = const_cast<double*>(x);
   if (norm)
-    k_dot_partial<true><<<kRedBlocks, kRedThreads, 0, st>>>(x, x, n, part);
+    k_red_partial<1><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, x, n, part);
   else
-    k_dot_partial<false><<<kRedBlocks, kRedThreads, 0, st>>>(x, y, n, part);
+    k_red_partial<0><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, y, n, part);
   k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, out, norm ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n, double* h,
+                       double* part, cudaStream_t st) {
+  // h[0] = w . V_0;  h[i] = (w -= h[i-1] V_{i-1}) . V_i;  h[j+1] = ||w -= h[j] V_j||
+  k_red_partial<0><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, w, V, n, part);
+  k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h, 0);
+  for (int i = 1; i <= j; ++i) {
+    k_red_partial<2><<<kRedBlocks, kRedThreads, 0, st>>>(h + i - 1, V + (i - 1) * ldv, w,
+                                                         V + i * ldv, n, part);
+    k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h + i, 0);
+  }
+  k_red_partial<3><<<kRedBlocks, kRedThreads, 0, st>>>(h + j, V + j * ldv, w, w, n, part);
+  k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h + j + 1, 1);
   return cudaGetLastError();
 }
 

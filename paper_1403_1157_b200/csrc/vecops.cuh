@@ -3,12 +3,14 @@
 #include <stdint.h>
 
 namespace tdg {
-constexpr int kRedBlocks = 296;  // 2 CTAs per SM on 148 SMs; fixed => deterministic
+constexpr int kRedBlocks = 1184;  // 8 CTAs per SM on 148 SMs; fixed => deterministic
 constexpr int kMaxTotS = 8;      // species of the totals reduction
 cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S, int nb, int neg,
                           double scale, double* part, double* out, cudaStream_t st);
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,
                        bool norm, cudaStream_t st);
+cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n, double* h,
+                       double* part, cudaStream_t st);
 cudaError_t launch_axpby(double a, const double* x, double b, double* y, int64_t n, cudaStream_t st);
 cudaError_t launch_axpy_dev(double s, const double* alpha, const double* x, double* y, int64_t n,
                             cudaStream_t st);

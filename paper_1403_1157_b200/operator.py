@@ -301,6 +301,19 @@ class DiscreteOperator:
                                                   self._stream()), "tdg_species_totals")
         return out
 
+    def mgs(self, V, j: int, w, h):
+        """One modified Gram-Schmidt sweep (GMRES Arnoldi step, reference
+        ``timeint.py:162-170``) against rows V[0..j]: h[i] = w.V_i,
+        w -= h[i] V_i, h[j+1] = ||w||; all on the device, one call."""
+        if V.dim() != 2 or not V.is_contiguous() or not w.is_contiguous():
+            raise ValueError("mgs needs a contiguous 2-D V and a contiguous w")
+        n = w.numel()
+        if V.shape[1] != n or j + 1 > V.shape[0] or h.numel() < j + 2:
+            raise ValueError("mgs: inconsistent sizes")
+        _native.check(self.lib.tdg_mgs(self._ctx, V.data_ptr(), V.stride(0), int(j), w.data_ptr(),
+                                       n, h.data_ptr(), self._stream()), "tdg_mgs")
+        return h
+
     def dot(self, x, y, out=None):
         x, y = x.reshape(-1), y.reshape(-1)
         self._check_vec("x", x)

@@ -479,3 +479,33 @@ def test_ssprk3_graph_replay_is_bitwise_equal_to_direct_launches():
         runs.append((U.clone(), U2.clone()))
     assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
     assert not torch.equal(runs[0][0], U0)
+
+
+def test_fused_mgs_is_bitwise_the_dot_axpy_sequence():
+    """tdg_mgs (axpy fused with the next dot) == the per-vector
+    tdg_dot / tdg_axpy_dev sweep, bit for bit (reference timeint.py:162-170)."""
+    space = DGSpace(unit_square(8, 4), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n = 100_002                     # even: 16-byte aligned rows
+    V = torch.randn(7, n, generator=g, dtype=torch.float64, device="cuda")
+    w0 = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    for j in (0, 1, 5):
+        w1, h1 = w0.clone(), torch.zeros(j + 2, dtype=torch.float64, device="cuda")
+        op.mgs(V, j, w1, h1)
+        w2, h2 = w0.clone(), torch.zeros(j + 2, dtype=torch.float64, device="cuda")
+        for i in range(j + 1):
+            op.dot(w2, V[i], h2[i:i + 1])
+            op.axpy_dev(-1.0, h2[i:i + 1], V[i], w2)
+        op.norm2(w2, h2[j + 1:j + 2])
+        assert torch.equal(w1, w2) and torch.equal(h1, h2)
+    with pytest.raises(ValueError):
+        op.mgs(V, 7, w0.clone(), torch.zeros(9, dtype=torch.float64, device="cuda"))
+    # odd lengths (tail element) and misaligned operands
+    x = torch.randn(100_003, generator=g, dtype=torch.float64, device="cuda")
+    y = torch.randn(100_003, generator=g, dtype=torch.float64, device="cuda")
+    d = op.dot(x, y).item()
+    assert d == pytest.approx(float((x * y).sum()), rel=1e-12)
+    assert op.norm2(x).item() == pytest.approx(float(x.norm()), rel=1e-13)
+    with pytest.raises(ValueError):
+        op.dot(x[1:], y[1:])
