@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-implicit", action="store_true",
+                    help="skip the extra SDIRK3+JFNK figure of the explicit C2 run")
     ap.add_argument("--power-iters", type=int, default=200)
     ap.add_argument("--integrator", default="ssprk3", choices=["ssprk3", "sdirk3"],
                     help="sdirk3: the reference's default SDIRK3 + JFNK at --dt")
@@ -450,6 +452,31 @@ def run_native_arm(args, rank, world, local):
         e2e = {"value": n_dofs * world * 3 * args.steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": n_dofs * 8, "d2h_bytes_per_step": n_dofs * 8}
 
+    # the reference's default integrator on the same state:
+    # one SDIRK3 + JFNK step at dt 0.01 (C2) with the reference's Newton /
+    # GMRES settings; DoF-updates counted per actual f evaluation
+    implicit = None
+    if world == 1 and slab is None and not args.no_implicit and cfg.dim == 2 and cfg.order == 2:
+        from paper_1403_1157_b200.timeint import integrate
+        nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
+              "gmres_restart": 30, "gmres_maxiter": 200}
+        Ui = torch.from_numpy(U0h).to(dev)
+        integrate(op, Ui, 0.0, 1.0, 0.01, order=3, n_steps=1, newton_kwargs=nk)  # warm-up
+        torch.cuda.synchronize()
+        ia, ib = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ia.record()
+        res = integrate(op, Ui, 0.0, 1.0, 0.01, order=3, n_steps=1, newton_kwargs=nk)
+        ib.record()
+        ib.synchronize()
+        ims = ia.elapsed_time(ib)
+        implicit = {"value": n_dofs * res.f_evaluations / (ims * 1e-3), "unit": UNIT,
+                    "integrator": "SDIRK3 + JFNK (reference defaults: Newton 1e-8/1e-12/25, "
+                                  "GMRES(30) 1e-4/200), dt 0.01, 1 step from U0 after 1 warm-up step",
+                    "ms_per_step": ims, "f_evaluations": res.f_evaluations,
+                    "newton_iterations": res.newton_iterations,
+                    "gmres_iterations": res.gmres_iterations}
+        del Ui
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nthreads = os.cpu_count() or 1
@@ -476,6 +503,7 @@ def run_native_arm(args, rank, world, local):
                             "weak scaling (one config-sized slab per GPU)")
                            if world > 1 else "1 GPU"},
             "roofline": roof, "clocks": clocks, "gpu_launches": launches,
+            **({"implicit": implicit} if implicit else {}),
         }
         if cpu:
             line["cpu_baseline"] = cpu
