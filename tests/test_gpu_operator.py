@@ -509,3 +509,32 @@ def test_fused_mgs_is_bitwise_the_dot_axpy_sequence():
     assert op.norm2(x).item() == pytest.approx(float(x.norm()), rel=1e-13)
     with pytest.raises(ValueError):
         op.dot(x[1:], y[1:])
+
+
+def _tiny_meshes():
+    from paper_1403_1157_b200.mesh import Mesh
+    one = Mesh([[0.0, 0.0], [1.0, 0.0], [0.2, 0.9]], [[0, 1, 2]],
+               {(0, 1): BoundaryTag.GAMMA1, (1, 2): BoundaryTag.GAMMA2})
+    tet = Mesh([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.1, 0.2, 0.8]],
+               [[0, 1, 2, 3]], {(0, 1, 2): BoundaryTag.GAMMA1_IN})
+    return {"one_triangle": one, "square1": unit_square(1), "square_3x1": unit_square(3, 1),
+            "one_tet": tet, "cube1": unit_cube(1)}
+
+
+@pytest.mark.parametrize("mesh_name", ["one_triangle", "square1", "square_3x1", "one_tet", "cube1"])
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("scheme", ["cdg2", "br2", "ip"])
+def test_tiny_meshes_match_oracle(mesh_name, order, scheme):
+    """Edge cases: a single element (no interior face, wall faces only),
+    one interior face, ragged face groups -- every default kernel path
+    against the oracle (reference operator.py:253-288)."""
+    mesh = _tiny_meshes()[mesh_name]
+    space = DGSpace(mesh, order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    U = initial_state(space, 11)
+    ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
+    for variant in ({}, {"generic": True}, {"serial": True}):
+        op = _op(space, model, FluxScheme(scheme))
+        op.set_variant(**variant)
+        got = op.apply_f(U)
+        assert rel_l2_per_species(space, got, ref).max() <= 1e-12, variant
