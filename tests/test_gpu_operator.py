@@ -538,3 +538,22 @@ def test_tiny_meshes_match_oracle(mesh_name, order, scheme):
         op.set_variant(**variant)
         got = op.apply_f(U)
         assert rel_l2_per_species(space, got, ref).max() <= 1e-12, variant
+
+
+@pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
+@pytest.mark.parametrize("dirichlet", [False, True])
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_heat_3d_tensor_core_kernels_match_oracle(scheme, dirichlet, order):
+    """3D heat model (Dirichlet mirror faces or zero-flux walls) through the
+    transposed tensor-core face and volume kernels (default in 3D) and
+    the element-local DMMA face kernel, vs the oracle
+    (reference operator.py:436-444, tests/oracles.py:192-220)."""
+    space = DGSpace(unit_cube(2), order, 1)
+    model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
+    U = initial_state(space, 21)
+    ref = OracleOperator(space, model, FluxScheme(scheme)).apply(U)
+    for variant in ({}, {"no_tc_faces": True}, {"tc_volume": True}):
+        op = _op(space, model, FluxScheme(scheme))
+        op.set_variant(**variant)
+        got = op.apply(U)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), variant
