@@ -181,16 +181,23 @@ def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, devi
 
 
 def spectral_radius(op, U, iters):
-    """rho of the FD Jacobian of f at U by power iteration."""
+    """rho of the FD Jacobian of f at U by power iteration.
+    Slab runs (ghost rows after the owned ones) iterate on the owned rows
+    with the ghost rows held at U (a per-slab estimate; the caller takes
+    the max over ranks)."""
     import torch
+    n_own = op.n_owned
     g = torch.Generator(device=U.device).manual_seed(1234)
-    v = torch.randn(U.shape, dtype=torch.float64, device=U.device, generator=g)
+    v = torch.randn((n_own,) + tuple(U.shape[1:]), dtype=torch.float64, device=U.device,
+                    generator=g)
     v /= torch.linalg.norm(v)
     fU = op.apply_f(U)
-    eps = math.sqrt(np.finfo(float).eps) * (1.0 + torch.linalg.norm(U).item())
+    eps = math.sqrt(np.finfo(float).eps) * (1.0 + torch.linalg.norm(U[:n_own]).item())
     rho = 0.0
+    Up = U.clone()
     for _ in range(iters):
-        Jv = (op.apply_f(U + eps * v) - fU) / eps
+        Up[:n_own] = U[:n_own] + eps * v
+        Jv = (op.apply_f(Up) - fU) / eps
         n = torch.linalg.norm(Jv)
         rho = n.item()
         v = Jv / n

@@ -557,3 +557,28 @@ def test_heat_3d_tensor_core_kernels_match_oracle(scheme, dirichlet, order):
         op.set_variant(**variant)
         got = op.apply(U)
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), variant
+
+
+def test_bench_spectral_radius_on_a_slab():
+    """bench.spectral_radius on a slab operator (ghost rows present) runs and
+    matches the undecomposed estimate (dt selection at N > 1)."""
+    import importlib.util
+    import os
+    from paper_1403_1157_b200.configs import CONFIGS, make_mesh
+    from paper_1403_1157_b200.decomp import build_slab
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cfg, cells = CONFIGS["c2"], (16, 8)
+    model = PlaqueModel()
+    gspace = DGSpace(make_mesh(cfg, cells=cells), 2, 6)
+    Ug = torch.from_numpy(initial_state(gspace, 3)).cuda()
+    rho_g = bench.spectral_radius(_op(gspace, model, FluxScheme("cdg2")), Ug, 60)
+    sl = build_slab(cfg, 0, 2, cells=cells)
+    op = _op(DGSpace(sl.mesh, 2, 6), model, FluxScheme("cdg2"), n_owned=sl.n_owned,
+             global_ids=sl.global_ids)
+    U = Ug.index_select(0, torch.as_tensor(sl.global_ids, device="cuda")).contiguous()
+    assert op.n_rows > op.n_owned
+    rho = bench.spectral_radius(op, U, 60)
+    assert 0.8 * rho_g <= rho <= 1.05 * rho_g
