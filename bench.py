@@ -328,6 +328,10 @@ def run_native_arm(args, rank, world, local):
         halo = HaloExchange(slab, dev)
     stepper = SSPRK3(op, halo)
     U = torch.from_numpy(U0h).to(dev)
+    if dist_on:
+        # initialise the NCCL communicator with a collective before the
+        # first batched point-to-point exchange
+        torch.distributed.barrier()
     if halo is not None:
         halo.exchange(U)
     rho = spectral_radius(op, U, args.power_iters)
@@ -546,6 +550,8 @@ def run_implicit(args, rank, world, local):
         from paper_1403_1157_b200.decomp import HaloExchange
         halo = HaloExchange(slab, dev)
     U = torch.from_numpy(U0h).to(dev)
+    if dist_on:
+        torch.distributed.barrier()
     nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
           "gmres_restart": 30, "gmres_maxiter": 200}
     integrate(op, U, 0.0, 1.0, args.dt, order=3, n_steps=max(1, args.warmup),
