@@ -388,7 +388,12 @@ def run_native_arm(args, rank, world, local):
     op.profile(False)
     kt = op.profile_read()
     ms_prof = sum(a.elapsed_time(b) for a, b in pevs)
-    value = n_dofs * world * 3 * args.steps / (ms * 1e-3)
+    total_dofs = n_dofs
+    if dist_on:  # whole-job DoFs (owned rows of every rank)
+        td = torch.tensor([float(n_dofs)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(td, op=torch.distributed.ReduceOp.SUM)
+        total_dofs = int(td.item())
+    value = total_dofs * 3 * args.steps / (ms * 1e-3)
 
     # per-kernel roofline (algorithmic flops of the reference sequence)
     Q, F = t.nq_vol, t.nq_face
@@ -460,8 +465,8 @@ def run_native_arm(args, rank, world, local):
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             ems = tt.item()
-        e2e = {"value": n_dofs * world * 3 * args.steps / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": n_dofs * 8, "d2h_bytes_per_step": n_dofs * 8}
+        e2e = {"value": total_dofs * 3 * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": Uh.numel() * 8, "d2h_bytes_per_step": Uh.numel() * 8}
 
     # the reference's default integrator on the same state:
     # one SDIRK3 + JFNK step at dt 0.01 (C2) with the reference's Newton /
