@@ -166,6 +166,14 @@ TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, dou
  * Deterministic (fixed-order two-pass reduction). */
 TDG_API int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stream);
 
+/* Broken L2 norm per species of U - V over the owned elements (V may be
+ * NULL: the norm of U), written to out[S] (device): sqrt(sum_e detJ_e
+ * sum_i (U - V)[e,s,i]^2) -- exact for the orthonormal basis; the parity
+ * metric of the DG-vs-DG comparisons (the reference's l2_error,
+ * analysis.py:30-50, for two fields on the same space). */
+TDG_API int tdg_species_l2(tdg_ctx* ctx, const double* U, const double* V, double* out,
+                           void* stream);
+
 /* Krylov reductions: deterministic two-pass tree (fixed grid), result
  * written to a DEVICE scalar.  Operands must be 16-byte aligned
  * (TDG_E_INVALID otherwise). */

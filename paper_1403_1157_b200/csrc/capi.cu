@@ -281,6 +281,15 @@ int tdg_species_totals(tdg_ctx* ctx, const double* U, double* totals, void* stre
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "species_totals");
 }
 
+int tdg_species_l2(tdg_ctx* ctx, const double* U, const double* V, double* out, void* stream) {
+  if (!ctx || !U || !out) return fail(TDG_E_INVALID, "null argument");
+  const tdg_desc& d = ctx->d;
+  const int neg = 1 + d.dim * (d.dim + 1) / 2;
+  cudaError_t e = launch_l2(U, V, ctx->p.egeo, d.n_elements, d.n_species, d.nb, neg, ctx->part,
+                            out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "species_l2");
+}
+
 int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result, void* stream) {
   if (!ctx || !x || !result) return fail(TDG_E_INVALID, "null argument");
   if (!aligned16(x)) return fail(TDG_E_INVALID, "norm operand must be 16-byte aligned");

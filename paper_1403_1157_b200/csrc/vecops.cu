@@ -114,6 +114,42 @@ __global__ void __launch_bounds__(kRedThreads) k_totals_partial(
   }
 }
 
+__global__ void k_sqrt_inplace(double* x, int n) {
+  if (threadIdx.x < n) x[threadIdx.x] = sqrt(x[threadIdx.x]);
+}
+
+// broken L2 norm per species of U - V (V may be null): the orthonormal
+// basis makes it exact, ||W||_s^2 = sum_e detJ_e sum_i W[e,s,i]^2
+// (SURVEY 8(c) parity metric; fespace.py:1-5).  Block b writes part[b*S+s].
+__global__ void __launch_bounds__(kRedThreads) k_l2_partial(
+    const double* __restrict__ U, const double* __restrict__ V, const double* __restrict__ egeo,
+    int64_t ne, int S, int nb, int neg, double* __restrict__ part) {
+  double acc[kMaxTotS];
+#pragma unroll
+  for (int s = 0; s < kMaxTotS; ++s) acc[s] = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  for (int64_t e = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; e < ne; e += stride) {
+    const double dj = __ldg(egeo + e * neg);
+    const double* ru = U + e * int64_t(S) * nb;
+    const double* rv = V ? V + e * int64_t(S) * nb : nullptr;
+#pragma unroll
+    for (int s = 0; s < kMaxTotS; ++s) {
+      if (s >= S) break;
+      double q = 0.0;
+      for (int i = 0; i < nb; ++i) {
+        const double w = __ldg(ru + s * nb + i) - (rv ? __ldg(rv + s * nb + i) : 0.0);
+        q = fma(w, w, q);
+      }
+      acc[s] = fma(dj, q, acc[s]);
+    }
+  }
+  for (int s = 0; s < S; ++s) {
+    const double v = block_sum(acc[s]);
+    if (threadIdx.x == 0) part[blockIdx.x * S + s] = v;
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kRedThreads) k_totals_final(const double* __restrict__ part,
                                                               int np, int S, double scale,
                                                               double* __restrict__ out) {
@@ -145,6 +181,14 @@ static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = 148 * 16;
   return int(g < 1 ? 1 : g > cap ? cap : g);
+}
+
+cudaError_t launch_l2(const double* U, const double* V, const double* egeo, int64_t ne, int S,
+                      int nb, int neg, double* part, double* out, cudaStream_t st) {
+  k_l2_partial<<<kRedBlocks, kRedThreads, 0, st>>>(U, V, egeo, ne, S, nb, neg, part);
+  k_totals_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, S, 1.0, out);
+  k_sqrt_inplace<<<1, 32, 0, st>>>(out, S);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S, int nb, int neg,

@@ -5,6 +5,8 @@
 namespace tdg {
 constexpr int kRedBlocks = 1184;  // 8 CTAs per SM on 148 SMs; fixed => deterministic
 constexpr int kMaxTotS = 8;      // species of the totals reduction
+cudaError_t launch_l2(const double* U, const double* V, const double* egeo, int64_t ne, int S,
+                      int nb, int neg, double* part, double* out, cudaStream_t st);
 cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S, int nb, int neg,
                           double scale, double* part, double* out, cudaStream_t st);
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,

@@ -301,6 +301,22 @@ class DiscreteOperator:
                                                   self._stream()), "tdg_species_totals")
         return out
 
+    def species_l2(self, U, V=None, out=None):
+        """Device broken-L2 norm per species of U - V (or of U) over the
+        owned elements: sqrt(sum_e detJ_e sum_i W[e,s,i]^2), exact for the
+        orthonormal basis (the parity metric; reference ``l2_error``,
+        ``analysis.py:30-50``, for two fields on one space)."""
+        torch = _torch()
+        self._check_vec("U", U)
+        if V is not None:
+            self._check_vec("V", V)
+        if out is None:
+            out = torch.empty(self.space.n_species, dtype=torch.float64, device=self.device)
+        _native.check(self.lib.tdg_species_l2(
+            self._ctx, U.data_ptr(), None if V is None else V.data_ptr(), out.data_ptr(),
+            self._stream()), "tdg_species_l2")
+        return out
+
     def mgs(self, V, j: int, w, h):
         """One modified Gram-Schmidt sweep (GMRES Arnoldi step, reference
         ``timeint.py:162-170``) against rows V[0..j]: h[i] = w.V_i,

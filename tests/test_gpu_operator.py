@@ -582,3 +582,20 @@ def test_bench_spectral_radius_on_a_slab():
     assert op.n_rows > op.n_owned
     rho = bench.spectral_radius(op, U, 60)
     assert 0.8 * rho_g <= rho <= 1.05 * rho_g
+
+
+def test_species_l2_on_device_is_the_parity_metric():
+    """tdg_species_l2 == the broken-L2 per-species norm used for parity
+    (rel_l2_per_species) and the reference's l2_error for DG fields."""
+    space = DGSpace(unit_square(6, 4, jitter=0.1, seed=5), 2, 6)
+    rng = np.random.default_rng(2)
+    U = rng.standard_normal((space.mesh.n_elements, 6, space.nb))
+    V = U + 1e-3 * rng.standard_normal(U.shape)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    Ut, Vt = torch.from_numpy(U).cuda(), torch.from_numpy(V).cuda()
+    d = op.species_l2(Ut, Vt).cpu().numpy()
+    n = op.species_l2(Vt).cpu().numpy()
+    ref_d = np.sqrt(np.einsum("e,esi->s", space.detJ, (U - V) ** 2))
+    ref_n = np.sqrt(np.einsum("e,esi->s", space.detJ, V ** 2))
+    assert np.allclose(d, ref_d, rtol=1e-13) and np.allclose(n, ref_n, rtol=1e-13)
+    assert np.allclose(d / n, rel_l2_per_species(space, U, V), rtol=1e-12)
