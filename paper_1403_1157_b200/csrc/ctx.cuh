@@ -210,7 +210,16 @@ void launch_volume(tdg_ctx* ctx, const double* U, const double* U0, double* out,
       using T = TcVol<D, K, M>;
       const int64_t tasks = (p.ne + T::EW - 1) / T::EW;
       int64_t grid = (tasks + T::WARPS - 1) / T::WARPS;
-      const int64_t cap = int64_t(ctx->num_sms) * T::MINB;
+      // persistent grid: every CTA slot the registers / shared memory allow
+      static int resident = 0;
+      if (resident == 0) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_volume_tc<D, K, M>, 128,
+                                                          T::smem()) != cudaSuccess || nb < 1)
+          nb = T::MINB;
+        resident = nb;
+      }
+      const int64_t cap = int64_t(ctx->num_sms) * resident;
       grid = grid < cap ? grid : cap;
       k_volume_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.vtc, U, ctx->fc, U0, out,
                                                                    a, b, c, mode);
