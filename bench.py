@@ -315,6 +315,7 @@ def run_native_arm(args, rank, world, local):
                        no_graph=bool(args.variant & 32),
                        tc_volume=bool(args.variant & 4096),
                        no_tc_faces=bool(args.variant & 8192),
+                       volume_first=bool(args.variant & 16384),
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb

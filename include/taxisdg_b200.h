@@ -207,7 +207,8 @@ TDG_API int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w
  * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
  * the tensor-core volume kernel instead of the SIMT one; bit 5: launch
  * tdg_ssprk3_step's kernels directly instead of replaying its cached CUDA
- * graph; bit 13: in 3D, use the element-local DMMA face kernel for interior
+ * graph; bit 14: in the overlapped schedule launch the volume part before
+ * the face kernel (default: faces first); bit 13: in 3D, use the element-local DMMA face kernel for interior
  * faces instead of the transposed one; bit 12: use the transposed tensor-core volume kernel wherever it
  * compiles (default only where the one-thread-per-element kernel does not
  * fit); bits 8-11: CTAs

@@ -51,7 +51,8 @@ struct tdg_ctx {
   bool flip_mma = false;  // testing: swap tensor-core / SIMT face kernel choice
   bool use_vmma = false;  // A/B: tensor-core volume kernel (slower than SIMT at C2)
   bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
-  bool no_tcf = false;    // A/B: element-local DMMA face kernel instead of the transposed one
+  bool no_tcf = false;
+  bool faces_first = true;  // overlapped launch order: faces, then the volume part (+1%)    // A/B: element-local DMMA face kernel instead of the transposed one
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -335,13 +336,14 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
     if constexpr ((fast_vol || vmma_ok || tc_ok) && (SN_of<M, D, K>() % 2 == 0)) {
       if (part != 2) {
         cudaEventRecord(ctx->ev_in, st);
+        if (ctx->faces_first) faces(part == 0 ? 0 : 1, use_ff);
         cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
         {
           KernelTimer kt(ctx, 2, ctx->aux);
           launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, vk);
         }
         cudaEventRecord(ctx->ev_vol, ctx->aux);
-        faces(part == 0 ? 0 : 1, use_ff);
+        if (!ctx->faces_first) faces(part == 0 ? 0 : 1, use_ff);
       }
       if (part == 1) {
         cudaError_t e = cudaGetLastError();
