@@ -108,6 +108,8 @@ def test_variants_agree_at_size():
     d = op.apply_f(U)
     op.set_variant(mma_volume=True)
     e_ = op.apply_f(U)
+    op.set_variant(volume_first=True)
+    assert torch.allclose(op.apply_f(U), a, rtol=1e-12, atol=1e-12 * float(a.abs().max()))
     out = torch.empty_like(U)
     op.set_variant()
     op.rk_stage(U, U, out, 0.25, 0.5, 1e-3)      # overlapped (out != U)
