@@ -125,6 +125,12 @@ typedef struct tdg_desc {
   const int32_t* face_blocks;
   int64_t n_face_blocks;
   int64_t n_face_blocks_cut;
+  /* host-pipelined stepping: n_bands contiguous element bands (1 = none),
+   * band_ptr (HOST) = elements [n_bands+1] | interior-face offsets
+   * [2 n_bands+1] (faces internal to band k from [2k], straddling (k, k+1)
+   * from [2k+1]) | wall offsets [n_bands+1], tables.build_tables order */
+  int32_t n_bands;
+  const int64_t* band_ptr;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -154,6 +160,16 @@ TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double
  * result as tdg_rk_stage. */
 TDG_API int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out,
                               double a, double b, double c, double t, int part, void* stream);
+
+/* nsteps SSP-RK3 steps of a HOST state (pinned memory, undecomposed
+ * mesh): every step copies the state in and the result out, pipelined by
+ * element bands (the copy-in of band k overlaps the work of the bands
+ * already resident; the final stage is finished and copied out band by
+ * band; step n+1's copy-in of band k follows step n's copy-out of band
+ * k).  Bitwise the same result as copy-in, tdg_ssprk3_step, copy-out per
+ * step.  The public host-data entry point of the end-to-end measurement. */
+TDG_API int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, int64_t nsteps, double t,
+                                  double dt, void* stream);
 
 /* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U (a
  * second stage vector is allocated by the library on first use). */

@@ -38,6 +38,7 @@ class TdgDesc(ctypes.Structure):
         ("bf_elem", _p), ("bf_lf", _p), ("bf_code", _p), ("bf_geo", _p),
         ("face_mma", _p), ("vol_mma", _p), ("n_cut_faces", _i64), ("vol_tc", _p),
         ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64), ("n_face_blocks_cut", _i64),
+        ("n_bands", ctypes.c_int32), ("band_ptr", _p),
     ]
 
 
@@ -60,6 +61,7 @@ def load(path: str = LIB):
     lib.tdg_apply.argtypes = [_p, _p, _p, _d, ctypes.c_int, _p]
     lib.tdg_rk_stage.argtypes = [_p, _p, _p, _p, _d, _d, _d, _d, _p]
     lib.tdg_species_totals.argtypes = [_p, _p, _p, _p]
+    lib.tdg_ssprk3_steps_host.argtypes = [_p, _p, _i64, _d, _d, _p]
     lib.tdg_species_l2.argtypes = [_p, _p, _p, _p, _p]
     lib.tdg_mgs.argtypes = [_p, _p, _i64, ctypes.c_int, _p, _i64, _p, _p]
     lib.tdg_rk_stage_part.argtypes = [_p, _p, _p, _p, _d, _d, _d, _d, ctypes.c_int, _p]
@@ -74,7 +76,7 @@ def load(path: str = LIB):
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
     lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
-    for name in ("tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    for name in ("tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev"):

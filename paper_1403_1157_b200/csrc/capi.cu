@@ -142,6 +142,23 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     ctx->overlap = false;  // serial path still works
     cudaGetLastError();
   }
+  // element bands of the host-pipelined stepping (host array: elements
+  // [B+1] | interior-face offsets [2B+1] | wall offsets [B+1])
+  if (d.n_bands > 1 && d.band_ptr) {
+    const int nb = d.n_bands;
+    const int64_t* bp = d.band_ptr;
+    ctx->band_elem.assign(bp, bp + nb + 1);
+    ctx->band_face.assign(bp + nb + 1, bp + nb + 1 + 2 * nb + 1);
+    ctx->band_wall.assign(bp + 3 * nb + 2, bp + 4 * nb + 3);
+    const bool ok = ctx->band_elem.front() == 0 && ctx->band_elem.back() == d.n_elements &&
+                    ctx->band_face.front() == 0 && ctx->band_face.back() == d.n_int_faces &&
+                    ctx->band_wall.front() == 0 && ctx->band_wall.back() == d.n_bnd_faces;
+    if (!ok) {
+      tdg_destroy(ctx);
+      return fail(TDG_E_INVALID, "inconsistent band offsets");
+    }
+    ctx->n_bands = nb;
+  }
   *out = ctx;
   return TDG_OK;
 }
@@ -156,6 +173,13 @@ int tdg_destroy(tdg_ctx* ctx) {
   cudaFree(ctx->fc);
   cudaFree(ctx->part);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  cudaFree(ctx->hs_buf);
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
+  if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+  for (auto* v : {&ctx->ev_h2d, &ctx->ev_d2h, &ctx->ev_done, &ctx->ev_vol_b})
+    for (auto ev : *v) cudaEventDestroy(ev);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->gev_a) cudaEventDestroy(ctx->gev_a);
   if (ctx->gev_b) cudaEventDestroy(ctx->gev_b);
@@ -261,6 +285,15 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, 
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, int64_t nsteps, double t, double dt,
+                          void* stream) {
+  (void)t;
+  if (!ctx || !U_host) return fail(TDG_E_INVALID, "null argument");
+  if (nsteps < 0) return fail(TDG_E_INVALID, "negative step count");
+  if (ctx->d.n_ghost != 0) return fail(TDG_E_INVALID, "host stepping needs an undecomposed mesh");
+  return ctx->impl.host_steps(ctx, U_host, nsteps, dt, static_cast<cudaStream_t>(stream));
+}
 
 int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* result,
             void* stream) {

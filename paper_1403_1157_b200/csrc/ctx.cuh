@@ -26,6 +26,7 @@ struct Impl {
   int (*configure)(int nqv);
   int (*run)(tdg_ctx*, const double* U, const double* U0, double* out, double a, double b,
              double c, int mode, cudaStream_t st);
+  int (*host_steps)(tdg_ctx*, double* U_host, int64_t nsteps, double dt, cudaStream_t st);
   int max_nqv, max_nqf;
 };
 
@@ -52,7 +53,16 @@ struct tdg_ctx {
   bool use_vmma = false;  // A/B: tensor-core volume kernel (slower than SIMT at C2)
   bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
   bool no_tcf = false;
-  bool faces_first = true;  // overlapped launch order: faces, then the volume part (+1%)    // A/B: element-local DMMA face kernel instead of the transposed one
+  bool faces_first = true;
+  // host-pipelined stepping: element bands and the banded face order
+  // (tables.build_tables), device state / stage buffers, copy streams
+  int n_bands = 1;
+  std::vector<int64_t> band_elem, band_face, band_wall;
+  double* hs_buf = nullptr;  // [3][rows][S][nb]: U, stage 1, stage 2
+  size_t hs_n = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_d2h, ev_done, ev_vol_b;
+  cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;  // overlapped launch order: faces, then the volume part (+1%)    // A/B: element-local DMMA face kernel instead of the transposed one
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -203,9 +213,8 @@ void run_faces(tdg_ctx* ctx, const OpParams& p, const double* U, cudaStream_t st
 // fast volume kernels: vk 0 one thread per element, 1 tensor-core
 // (element-local GEMMs), 2 tensor-core transposed (elements x points)
 template <int D, int K, class M>
-void launch_volume(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a,
-                   double b, double c, int mode, cudaStream_t st, int vk) {
-  const OpParams& p = ctx->p;
+void launch_volume(tdg_ctx* ctx, const OpParams& p, const double* U, const double* U0, double* out,
+                   double a, double b, double c, int mode, cudaStream_t st, int vk) {
   if (vk == 2) {
     if constexpr (TcVol<D, K, M>::ok) {
       using T = TcVol<D, K, M>;
@@ -340,7 +349,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
         cudaStreamWaitEvent(ctx->aux, ctx->ev_in, 0);
         {
           KernelTimer kt(ctx, 2, ctx->aux);
-          launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode | 4, ctx->aux, vk);
+          launch_volume<D, K, M>(ctx, ctx->p, U, U0, out, a, b, c, mode | 4, ctx->aux, vk);
         }
         cudaEventRecord(ctx->ev_vol, ctx->aux);
         if (!ctx->faces_first) faces(part == 0 ? 0 : 1, use_ff);
@@ -355,7 +364,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
       const int64_t n2 = p.ne * (SN_of<M, D, K>() / 2);
       const int grid = int(n2 / 256 + 1 < 148 * 8 ? n2 / 256 + 1 : 148 * 8);
       k_fc_add<D, SN_of<M, D, K>(), Dims<D, K>::NEG><<<grid, 256, 0, st>>>(
-          ctx->fc, p.egeo, p.ne, out, c, mode);
+          ctx->fc, p.egeo, p.ne, out, c, mode, 0, p.ne);
     }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
@@ -370,7 +379,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   }
   if (p.ne > 0 && (use_vm || use_tc)) {
     KernelTimer kt(ctx, 2, st);
-    launch_volume<D, K, M>(ctx, U, U0, out, a, b, c, mode, st, vk);
+    launch_volume<D, K, M>(ctx, ctx->p, U, U0, out, a, b, c, mode, st, vk);
   } else if (p.ne > 0) {
     KernelTimer kt(ctx, 2, st);
     if (use_v4) {
@@ -396,9 +405,162 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "operator launch");
 }
 
+// Host-to-host SSP-RK3 steps with per-step host copies, pipelined by
+// element bands: step n's state is copied in band by band (each band's
+// volume part and the faces whose bands have arrived start at once), and
+// the final stage is finished and copied out band by band (the next step's
+// copy-in of band k follows this step's copy-out of band k).  Same
+// kernels, same per-face / per-element arithmetic and the same fixed-order
+// face-slot sums as the unbanded step: bitwise the same results.
+template <int D, int K, class M>
+int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t st) {
+  const OpParams& p = ctx->p;
+  constexpr bool fast_vol = FastVol<D, K, M>::ok, fast_face = FastFace<D, K, M>::ok;
+  constexpr int SN = SN_of<M, D, K>();
+  const int64_t rows = ctx->d.n_elements + ctx->d.n_ghost;
+  const size_t n = size_t(rows) * SN;
+  if (!ctx->hs_buf || ctx->hs_n < n) {
+    if (ctx->hs_buf) cudaFree(ctx->hs_buf);
+    ctx->hs_buf = nullptr;
+    ctx->hs_n = 0;
+    if (cudaMalloc(&ctx->hs_buf, 3 * n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TDG_E_CUDA, "cudaMalloc host-step buffers");
+    }
+    ctx->hs_n = n;
+  }
+  double* Ud = ctx->hs_buf;
+  double* W1 = Ud + n;
+  double* W2 = W1 + n;
+  const int nb = ctx->n_bands;
+  const bool banded = nb > 1 && ctx->d.n_ghost == 0 && ctx->overlap && fast_face && fast_vol &&
+                      p.nqf == Dims<D, K>::NQF && p.nqv == Dims<D, K>::NQV &&
+                      !ctx->force_generic && (SN % 2 == 0);
+  if (!banded) {  // plain per-step copies around the fused stages
+    for (int64_t it = 0; it < nsteps; ++it) {
+      cudaMemcpyAsync(Ud, Uh, n * sizeof(double), cudaMemcpyHostToDevice, st);
+      int rc = ctx->impl.run(ctx, Ud, nullptr, W1, 0.0, 1.0, dt, 2, st);
+      if (!rc) rc = ctx->impl.run(ctx, W1, Ud, W2, 0.75, 0.25, 0.25 * dt, 2, st);
+      if (!rc) rc = ctx->impl.run(ctx, W2, Ud, Ud, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, st);
+      if (rc) return rc;
+      cudaMemcpyAsync(Uh, Ud, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
+  }
+  if constexpr (fast_vol && fast_face && (SN % 2 == 0)) {
+    auto ev_new = [](std::vector<cudaEvent_t>& v, int k) {
+      while (int(v.size()) < k) {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        v.push_back(e);
+      }
+    };
+    if (!ctx->s_h2d) {
+      cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ctx->ev_s0, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming);
+    }
+    ev_new(ctx->ev_h2d, nb);
+    ev_new(ctx->ev_d2h, nb);
+    ev_new(ctx->ev_done, nb);
+    ev_new(ctx->ev_vol_b, nb);
+    const auto& be = ctx->band_elem;
+    const auto& bf = ctx->band_face;
+    const auto& bw = ctx->band_wall;
+    // faces of band k available once bands <= k are resident: the faces
+    // straddling (k-1, k), those internal to k, and band k's walls
+    auto faces_r1 = [&](int k, const double* Uin) {
+      OpParams pp = p;
+      const int64_t f0 = k > 0 ? bf[2 * k - 1] : 0, f1 = bf[2 * k + 1];
+      pp.ifel = p.ifel + 2 * f0;
+      pp.iflf = p.iflf + 2 * f0;
+      pp.ifcode = p.ifcode + f0;
+      pp.ifgeo = p.ifgeo + f0 * Dims<D, K>::NFG;
+      pp.nif = f1 - f0;
+      pp.bfel = p.bfel + bw[k];
+      pp.bflf = p.bflf + bw[k];
+      pp.bfcode = p.bfcode + bw[k];
+      pp.bfgeo = p.bfgeo + bw[k];
+      pp.nbf = bw[k + 1] - bw[k];
+      if (pp.nif + pp.nbf > 0) run_faces<D, K, M>(ctx, pp, Uin, st, true);
+    };
+    auto volume_band = [&](int k, const double* Uin, const double* U0, double* out, double a,
+                           double b, double c) {
+      OpParams pv = p;
+      const int64_t e0 = be[k];
+      pv.ne = be[k + 1] - e0;
+      pv.egeo = p.egeo + e0 * Dims<D, K>::NEG;
+      KernelTimer kt(ctx, 2, ctx->aux);
+      launch_volume<D, K, M>(ctx, pv, Uin + e0 * SN, U0 ? U0 + e0 * SN : nullptr, out + e0 * SN,
+                             a, b, c, 2 | 4, ctx->aux, 0);
+    };
+    auto fc_add = [&](int64_t e0, int64_t e1, double* out, double c, cudaStream_t s) {
+      KernelTimer kt(ctx, 3, s);
+      const int64_t n2 = (e1 - e0) * (SN / 2);
+      const int grid = int(n2 / 256 + 1 < 148 * 8 ? n2 / 256 + 1 : 148 * 8);
+      k_fc_add<D, SN, Dims<D, K>::NEG><<<grid, 256, 0, s>>>(ctx->fc, p.egeo, p.ne, out, c, 2, e0,
+                                                            e1);
+    };
+    for (int64_t it = 0; it < nsteps; ++it) {
+      // ---- stage 1: copy-in by band, overlapped with the band's work
+      cudaEventRecord(ctx->ev_s0, st);
+      cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_s0, 0);
+      for (int k = 0; k < nb; ++k) {
+        if (it > 0) cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_d2h[k], 0);
+        const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
+        cudaMemcpyAsync(Ud + o, Uh + o, m * sizeof(double), cudaMemcpyHostToDevice, ctx->s_h2d);
+        cudaEventRecord(ctx->ev_h2d[k], ctx->s_h2d);
+      }
+      for (int k = 0; k < nb; ++k) {
+        cudaStreamWaitEvent(ctx->aux, ctx->ev_h2d[k], 0);
+        volume_band(k, Ud, nullptr, W1, 0.0, 1.0, dt);
+        cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
+        faces_r1(k, Ud);
+      }
+      cudaEventRecord(ctx->ev_s1, ctx->aux);
+      cudaStreamWaitEvent(st, ctx->ev_s1, 0);
+      fc_add(0, p.ne, W1, dt, st);
+      // ---- stage 2: whole state resident
+      int rc = ctx->impl.run(ctx, W1, Ud, W2, 0.75, 0.25, 0.25 * dt, 2, st);
+      if (rc) return rc;
+      // ---- stage 3: finish and copy out band by band
+      const double c3 = (2.0 / 3.0) * dt;
+      cudaEventRecord(ctx->ev_s0, st);
+      cudaStreamWaitEvent(ctx->aux, ctx->ev_s0, 0);
+      for (int k = 0; k < nb; ++k) {
+        volume_band(k, W2, Ud, Ud, 1.0 / 3.0, 2.0 / 3.0, c3);
+        cudaEventRecord(ctx->ev_vol_b[k], ctx->aux);
+      }
+      auto finish = [&](int k) {  // all faces touching band k are done
+        cudaStreamWaitEvent(st, ctx->ev_vol_b[k], 0);
+        fc_add(be[k], be[k + 1], Ud, c3, st);
+        cudaEventRecord(ctx->ev_done[k], st);
+        cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[k], 0);
+        const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
+        cudaMemcpyAsync(Uh + o, Ud + o, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_d2h);
+        cudaEventRecord(ctx->ev_d2h[k], ctx->s_d2h);
+      };
+      for (int k = 0; k < nb; ++k) {
+        faces_r1(k, W2);
+        if (k > 0) finish(k - 1);
+      }
+      finish(nb - 1);
+    }
+    cudaEventRecord(ctx->ev_s1, ctx->s_d2h);
+    cudaStreamWaitEvent(st, ctx->ev_s1, 0);
+    cudaEventRecord(ctx->ev_s0, ctx->aux);
+    cudaStreamWaitEvent(st, ctx->ev_s0, 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
+}
+
 template <int D, int K, class M>
 Impl make_impl() {
-  return Impl{&configure<D, K, M>, &run<D, K, M>, Dims<D, K>::NQV, Dims<D, K>::NQF};
+  return Impl{&configure<D, K, M>, &run<D, K, M>, &host_steps<D, K, M>, Dims<D, K>::NQV,
+              Dims<D, K>::NQF};
 }
 
 template <class M>

@@ -633,13 +633,14 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
 template <int D, int SN, int NEG>
 __global__ void __launch_bounds__(256)
 k_fc_add(const double* __restrict__ FC, const double* __restrict__ egeo, int64_t ne,
-         double* __restrict__ out, double cc, int mode) {
+         double* __restrict__ out, double cc, int mode, int64_t e_begin, int64_t e_end) {
+  // elements [e_begin, e_end) of ne (slot stride ne)
   static_assert(SN % 2 == 0, "16-byte path");
   constexpr int H = SN / 2;
   const int64_t n2 = ne * H;
   const double2* f2 = reinterpret_cast<const double2*>(FC);
   double2* o2 = reinterpret_cast<double2*>(out);
-  for (int64_t idx = int64_t(blockIdx.x) * 256 + threadIdx.x; idx < n2;
+  for (int64_t idx = e_begin * H + int64_t(blockIdx.x) * 256 + threadIdx.x; idx < e_end * H;
        idx += int64_t(gridDim.x) * 256) {
     const int64_t e = idx / H;
     double sc = 1.0;

@@ -95,6 +95,8 @@ class DiscreteOperator:
             "face_Pw", "face_w", "elem_geo", "if_elems", "if_lf", "if_code",
             "if_geo", "bf_elem", "bf_lf", "bf_code", "bf_geo")})
         self._host = {
+            "band_ptr": np.ascontiguousarray(np.concatenate(
+                [t.band_elem_ptr, t.band_face_ptr, t.band_wall_ptr]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
             "lin_source": _checked_linear_source(model),
             "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
@@ -123,7 +125,8 @@ class DiscreteOperator:
             bf_geo=ptr(k["bf_geo"]), face_mma=ptr(k["face_mma"]),
             vol_mma=ptr(k["vol_mma"]), n_cut_faces=t.n_cut, vol_tc=ptr(k["vol_tc"]),
             face_tc=ptr(k["face_tc"]), face_blocks=ptr(k["face_blocks"]),
-            n_face_blocks=len(blocks), n_face_blocks_cut=n_cut_blocks)
+            n_face_blocks=len(blocks), n_face_blocks_cut=n_cut_blocks,
+            n_bands=t.n_bands, band_ptr=hptr(self._host["band_ptr"]))
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _native.check(self.lib.tdg_create(ctypes.byref(desc),
@@ -282,6 +285,22 @@ class DiscreteOperator:
             out.data_ptr(), float(a), float(b), float(c), float(t), int(part),
             self._stream()), "tdg_rk_stage_part")
         return out
+
+    def ssprk3_steps_host(self, U_host, nsteps: int, dt: float, t: float = 0.0):
+        """``nsteps`` SSP-RK3 steps of a pinned host state (CPU float64
+        tensor of the U shape), with the state copied in and the result
+        copied out every step, pipelined by element bands; returns the
+        (updated) host tensor.  Asynchronous on the current stream."""
+        torch = _torch()
+        shape = (self.n_rows, self.space.n_species, self.space.nb)
+        if not isinstance(U_host, torch.Tensor) or U_host.device.type != "cpu" \
+                or U_host.dtype != torch.float64 or tuple(U_host.shape) != shape \
+                or not U_host.is_contiguous() or not U_host.is_pinned():
+            raise ValueError(f"U_host must be a pinned, contiguous float64 CPU tensor {shape}")
+        _native.check(self.lib.tdg_ssprk3_steps_host(self._ctx, U_host.data_ptr(), int(nsteps),
+                                                     float(t), float(dt), self._stream()),
+                      "tdg_ssprk3_steps_host")
+        return U_host
 
     def ssprk3_step(self, U, work, dt: float, t: float = 0.0):
         self._check_vec("U", U, self.n_rows)

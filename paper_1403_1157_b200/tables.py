@@ -71,6 +71,15 @@ class OperatorTables:
     bf_code: np.ndarray
     bf_geo: np.ndarray
     n_cut: int = 0
+    # element bands for host-pipelined stepping (undecomposed meshes):
+    # band_elem_ptr[k] .. [k+1] are band k's elements; interior faces are
+    # ordered by (lowest band, straddles into the next band, signature):
+    # band_face_ptr[2k] = first face internal to band k, band_face_ptr[2k+1]
+    # = first face straddling (k, k+1); walls by band (band_wall_ptr)
+    n_bands: int = 1
+    band_elem_ptr: np.ndarray = None
+    band_face_ptr: np.ndarray = None
+    band_wall_ptr: np.ndarray = None
 
 
 def _face_tables(space: DGSpace, frule):
@@ -89,7 +98,7 @@ def _face_tables(space: DGSpace, frule):
 
 def build_tables(space: DGSpace, model, scheme: FluxScheme,
                  vol_degree=None, face_degree=None, n_owned=None,
-                 global_ids=None) -> OperatorTables:
+                 global_ids=None, bands: int = 4) -> OperatorTables:
     """Pack tables, element geometry and face lists.
 
     Slab-decomposed runs pass a local mesh whose first ``n_owned``
@@ -177,14 +186,38 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
     # faces touching a ghost row (SKIP_OUT) last, so a slab stage can run
     # the others while the ghost exchange is in flight
     cut = (code & CODE_SKIP_OUT) != 0
-    order = np.lexsort((code & 1023, cut))
-    code, geo, el, lfs = code[order], geo[order], el[order], lfs[order]
     n_cut = int(cut.sum())
+    # element bands (contiguous id ranges; host-pipelined stepping): faces
+    # of one band, then the faces straddling into the next band
+    n_own = n_owned
+    nbands = bands if (n_cut == 0 and n_own == mesh.n_elements
+                       and n_own >= 8192 * max(bands, 1)) else 1
+    ebnd = (np.arange(nbands + 1, dtype=np.int64) * n_own) // nbands
+    band_of = lambda e: np.searchsorted(ebnd, e, side="right") - 1
+    if nbands > 1:
+        e_o = np.where(el[:, 1] >= 0, el[:, 1], el[:, 0])
+        b_in, b_out = band_of(el[:, 0]), band_of(e_o)
+        lo, hi = np.minimum(b_in, b_out), np.maximum(b_in, b_out)
+        if np.any(hi - lo > 1):  # a face must not skip a band: no banding
+            nbands = 1
+    if nbands > 1:
+        key = 2 * lo + (hi > lo)
+        order = np.lexsort((code & 1023, key, cut))
+        key = key[order]
+    else:
+        order = np.lexsort((code & 1023, cut))
+    code, geo, el, lfs = code[order], geo[order], el[order], lfs[order]
 
     btag = mesh.face_tags[nbf].astype(np.int64)
-    border = np.lexsort((btag, tid[nbf, 0]))
-    nbf, btag = nbf[border], btag[border]
+    bband = band_of(fe[nbf, 0]) if nbands > 1 else np.zeros(len(nbf), np.int64)
+    border = np.lexsort((btag, tid[nbf, 0], bband))
+    nbf, btag, bband = nbf[border], btag[border], bband[border]
     bcode = tid[nbf, 0] | (btag << 11)
+    if nbands > 1:
+        band_face = np.searchsorted(key, np.arange(2 * nbands + 1), side="left")
+    else:
+        band_face = np.array([0, len(code), len(code)])
+    band_wall = np.searchsorted(bband, np.arange(nbands + 1), side="left")
 
     c64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
     i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
@@ -195,7 +228,10 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         face_w=c64(fr.weights), elem_geo=c64(egeo[:n_owned]),
         if_elems=i32(el), if_lf=i32(lfs), if_code=i32(code), if_geo=c64(geo),
         bf_elem=i32(fe[nbf, 0]), bf_lf=i32(fl[nbf, 0]),
-        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]), n_cut=n_cut)
+        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]), n_cut=n_cut,
+        n_bands=int(nbands), band_elem_ptr=ebnd.astype(np.int64),
+        band_face_ptr=np.asarray(band_face, dtype=np.int64),
+        band_wall_ptr=np.asarray(band_wall, dtype=np.int64))
 
 
 def _ceil(x, m):

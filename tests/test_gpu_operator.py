@@ -601,3 +601,26 @@ def test_species_l2_on_device_is_the_parity_metric():
     ref_n = np.sqrt(np.einsum("e,esi->s", space.detJ, V ** 2))
     assert np.allclose(d, ref_d, rtol=1e-13) and np.allclose(n, ref_n, rtol=1e-13)
     assert np.allclose(d / n, rel_l2_per_species(space, U, V), rtol=1e-12)
+
+
+@pytest.mark.parametrize("cells", [(128, 128), (16, 8)])
+def test_host_pipelined_steps_bitwise_equal_device_steps(cells):
+    """tdg_ssprk3_steps_host (per-step copy-in / copy-out pipelined by
+    element bands; 4 bands at 128x128, none at 16x8) == copy-in,
+    tdg_ssprk3_step, copy-out, bit for bit."""
+    space = DGSpace(unit_square(*cells, lengths=(1.0, 1.0)), 2, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    assert (op.tables.n_bands > 1) == (cells == (128, 128))
+    U0 = torch.from_numpy(initial_state(space, 9))
+    dt = 2e-5
+    Uh = U0.clone().pin_memory()
+    op.ssprk3_steps_host(Uh, 3, dt)
+    torch.cuda.synchronize()
+    Ud, W = U0.cuda(), torch.empty_like(U0).cuda()
+    for _ in range(3):
+        op.ssprk3_step(Ud, W, dt)
+    torch.cuda.synchronize()
+    assert torch.equal(Uh, Ud.cpu())
+    assert not torch.equal(Uh, U0)
+    with pytest.raises(ValueError):
+        op.ssprk3_steps_host(U0.clone(), 1, dt)        # not pinned
