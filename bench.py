@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--bands", type=int, default=4,
+                    help="element bands of the host-pipelined e2e stepping")
     ap.add_argument("--no-implicit", action="store_true",
                     help="skip the extra SDIRK3+JFNK figure of the explicit C2 run")
     ap.add_argument("--power-iters", type=int, default=200)
@@ -306,7 +308,8 @@ def run_native_arm(args, rank, world, local):
     log(f"problem built: {space.mesh.n_elements} elements")
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
-                          global_ids=None if slab is None else slab.global_ids)
+                          global_ids=None if slab is None else slab.global_ids,
+                          bands=args.bands)
     log("operator created")
     if args.variant:
         op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),

@@ -65,7 +65,7 @@ class DiscreteOperator:
     def __init__(self, space: DGSpace, model, scheme: FluxScheme,
                  nthreads: int = 1, npartitions: int | None = None,
                  vol_degree: int | None = None, face_degree: int | None = None,
-                 device=None, n_owned: int | None = None, global_ids=None):
+                 device=None, n_owned: int | None = None, global_ids=None, bands: int = 4):
         if model.n_species != space.n_species:
             raise ValueError(f"model has {model.n_species} species, space has "
                              f"{space.n_species}")
@@ -78,7 +78,7 @@ class DiscreteOperator:
         self.device = torch.device(device if device is not None else "cuda")
         self.lib = _native.load()
         t = build_tables(space, model, scheme, vol_degree, face_degree,
-                         n_owned=n_owned, global_ids=global_ids)
+                         n_owned=n_owned, global_ids=global_ids, bands=bands)
         self.tables = t
         self.n_owned = t.elem_geo.shape[0]
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
