@@ -206,6 +206,15 @@ def spectral_radius(op, U, iters):
     return rho
 
 
+def measured_hbm_gbs():
+    """Driver-measured HBM copy bandwidth (MEASURED_PEAKS.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def fp64_peak(op):
     """Measured DFMA throughput (TFLOP/s) of this GPU; the roofline
     denominator for the FP64-bound operator kernels."""
@@ -417,6 +426,13 @@ def run_native_arm(args, rank, world, local):
     peak = fp64_peak(op)
     if "fc_add" in per:  # streaming kernel: report its bandwidth instead
         per["fc_add"]["gbs"] = (t.dim + 3) * n_dofs * 8 / (per["fc_add"]["avg_ms"] * 1e-3) / 1e9
+        hbm = measured_hbm_gbs()
+        if hbm:
+            per["fc_add"]["hbm_peak_gbs"] = hbm
+            per["fc_add"]["hbm_frac"] = per["fc_add"]["gbs"] / hbm
+            per["fc_add"]["note"] = ("algorithmic bytes (d+1 slots + out read + out write) per "
+                                     "launch / time; MEASURED_PEAKS.json copy bandwidth; >1 means "
+                                     "part of the slots were still in L2")
     # the face kernel starts first and runs alone on the SMs it holds: its
     # span is its own duration; in the serial schedule take the longest
     dom = "faces" if ("faces" in per and "fc_add" in per) else \
