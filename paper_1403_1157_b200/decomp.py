@@ -105,10 +105,15 @@ def build_slab(cfg: Config, rank: int, nranks: int, cells=None,
 
 class HaloExchange:
     """Ghost-row exchange with the x-neighbours through torch.distributed
-    point-to-point ops (NCCL on GPUs, gloo on CPU).  ``start`` packs the
-    two boundary columns and posts the sends/receives; ``wait`` blocks
-    the caller's stream (NCCL) or thread (gloo) until the ghost rows of
-    U are filled."""
+    point-to-point ops.  ``start`` packs the two boundary columns and
+    posts the sends/receives; ``wait`` makes the caller's stream (NCCL) or
+    thread (gloo) wait until the ghost rows of U are filled.
+
+    With NCCL the device rows travel directly (GPU to GPU).  With gloo
+    (CPU tests, and several ranks sharing one GPU in the one-GPU slab
+    tests) device tensors are staged through host buffers: gloo cannot
+    address device memory, and no device kernel ever waits on another
+    rank -- the host does."""
 
     def __init__(self, slab: Slab, device=None):
         import torch
@@ -117,31 +122,43 @@ class HaloExchange:
         self.idx_l = torch.as_tensor(slab.send_left, device=device)
         self.idx_r = torch.as_tensor(slab.send_right, device=device)
         self._works = []
+        self._recv = []
+
+    def _staged(self, U):
+        import torch.distributed as dist
+        return U.is_cuda and dist.get_backend() == "gloo"
 
     def start(self, U):
-        import torch
         import torch.distributed as dist
         s = self.slab
         ops = []
         self._bufs = []
-        if s.rank > 0:
-            buf = U.index_select(0, self.idx_l)
+        self._recv = []
+        staged = self._staged(U)
+        for nb, idx, rsl in ((s.rank - 1, self.idx_l, s.recv_left),
+                             (s.rank + 1, self.idx_r, s.recv_right)):
+            if nb < 0 or nb >= s.nranks:
+                continue
+            buf = U.index_select(0, idx)
+            rv = U[rsl]
+            if staged:
+                buf = buf.cpu()
+                host_rv = rv.new_empty(rv.shape, device="cpu")
+                self._recv.append((rv, host_rv))
+                rv = host_rv
             self._bufs.append(buf)
-            ops.append(dist.P2POp(dist.isend, buf, s.rank - 1))
-            ops.append(dist.P2POp(dist.irecv, U[s.recv_left], s.rank - 1))
-        if s.rank < s.nranks - 1:
-            buf = U.index_select(0, self.idx_r)
-            self._bufs.append(buf)
-            ops.append(dist.P2POp(dist.isend, buf, s.rank + 1))
-            ops.append(dist.P2POp(dist.irecv, U[s.recv_right], s.rank + 1))
+            ops.append(dist.P2POp(dist.isend, buf, nb))
+            ops.append(dist.P2POp(dist.irecv, rv, nb))
         self._works = dist.batch_isend_irecv(ops) if ops else []
-        del torch
 
     def wait(self):
         for w in self._works:
             w.wait()
+        for dev_rows, host_rows in self._recv:
+            dev_rows.copy_(host_rows)
         self._works = []
         self._bufs = []
+        self._recv = []
 
     def exchange(self, U):
         self.start(U)

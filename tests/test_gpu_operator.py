@@ -624,3 +624,76 @@ def test_host_pipelined_steps_bitwise_equal_device_steps(cells):
     assert not torch.equal(Uh, U0)
     with pytest.raises(ValueError):
         op.ssprk3_steps_host(U0.clone(), 1, dt)        # not pinned
+
+
+def _slab_worker(rank, nranks, port, out):
+    import os
+    import torch.distributed as dist
+    from paper_1403_1157_b200.configs import CONFIGS
+    from paper_1403_1157_b200.decomp import HaloExchange, build_slab
+    from paper_1403_1157_b200.fields import bump_field
+    from paper_1403_1157_b200.stepping import SSPRK3
+    from paper_1403_1157_b200.timeint import integrate
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    try:
+        torch.cuda.set_device(0)
+        cfg = CONFIGS["c2"]
+        sl = build_slab(cfg, rank, nranks, cells=(24, 6))
+        space = DGSpace(sl.mesh, 2, 6)
+        fn = bump_field(2, 6, 3, np.zeros(2), np.asarray(cfg.lengths, float))
+        U0 = np.ascontiguousarray(space.project(fn).coeffs)
+        op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"),
+                 n_owned=sl.n_owned, global_ids=sl.global_ids)
+        halo = HaloExchange(sl, "cuda")
+        U = torch.from_numpy(U0).cuda()
+        U[sl.n_owned:] = float("nan")          # ghosts must come from the exchange
+        halo.exchange(U)
+        stepper = SSPRK3(op, halo)
+        for _ in range(2):
+            stepper.step(U, 1e-5)
+        Ui = torch.from_numpy(U0).cuda()
+        halo.exchange(Ui)
+        res = integrate(op, Ui, 0.0, 1.0, 5e-4, order=3, n_steps=1,
+                        newton_kwargs=dict(rtol=1e-10, atol=1e-13, gmres_rtol=1e-8), halo=halo)
+        torch.cuda.synchronize()
+        out[rank] = (sl.global_ids[:sl.n_owned], U[:sl.n_owned].cpu().numpy(),
+                     res.U[:sl.n_owned].cpu().numpy(), res.gmres_iterations)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_slab_run_on_one_gpu_matches_global():
+    """Two ranks (gloo, host-staged ghost exchange) sharing the GPU: the
+    slab SSP-RK3 path (split stage around the exchange) and the slab
+    SDIRK3+JFNK path (exchange inside G(V), all-reduced Krylov scalars)
+    equal the undecomposed device runs."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_1403_1157_b200.configs import CONFIGS, make_mesh
+    from paper_1403_1157_b200.fields import bump_field
+    from paper_1403_1157_b200.timeint import integrate
+    cfg = CONFIGS["c2"]
+    gspace = DGSpace(make_mesh(cfg, cells=(24, 6)), 2, 6)
+    fn = bump_field(2, 6, 3, np.zeros(2), np.asarray(cfg.lengths, float))
+    U0 = np.ascontiguousarray(gspace.project(fn).coeffs)
+    gop = _op(gspace, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
+    U, W = torch.from_numpy(U0).cuda(), torch.empty(U0.shape, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        gop.ssprk3_step(U, W, 1e-5)
+    ref_e = U.cpu().numpy()
+    ref_i = integrate(gop, torch.from_numpy(U0).cuda(), 0.0, 1.0, 5e-4, order=3, n_steps=1,
+                      newton_kwargs=dict(rtol=1e-10, atol=1e-13, gmres_rtol=1e-8))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_slab_worker, args=(2, port, out), nprocs=2, start_method="spawn")
+    for r in range(2):
+        gids, Ue, Ui, iters = out[r]
+        assert np.abs(Ue - ref_e[gids]).max() <= 1e-13 * np.abs(ref_e).max()
+        assert np.abs(Ui - ref_i.U.cpu().numpy()[gids]).max() <= 1e-9 * np.abs(ref_e).max()
+        assert iters == ref_i.gmres_iterations
