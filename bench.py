@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: testing only (host-staged exchange; ranks may share a GPU)")
     ap.add_argument("--bands", type=int, default=4,
                     help="element bands of the host-pipelined e2e stepping")
     ap.add_argument("--no-implicit", action="store_true",
@@ -306,11 +308,15 @@ def run_native_arm(args, rank, world, local):
     from paper_1403_1157_b200.operator import DiscreteOperator
     from paper_1403_1157_b200.roofline import apply_bytes, apply_flops, executed_flops
 
+    local = local % max(torch.cuda.device_count(), 1)  # testing: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or "RANK" in os.environ:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # testing only: host-staged exchange, several ranks per GPU
+            dist.init_process_group("gloo")
     dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
     cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
                                                          args.force_slab, dev)
@@ -573,11 +579,15 @@ def run_implicit(args, rank, world, local):
     import torch
     from paper_1403_1157_b200.operator import DiscreteOperator
     from paper_1403_1157_b200.timeint import integrate
+    local = local % max(torch.cuda.device_count(), 1)  # testing: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or "RANK" in os.environ:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # testing only: host-staged exchange, several ranks per GPU
+            dist.init_process_group("gloo")
     dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
     cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
                                                          args.force_slab, dev)
