@@ -81,3 +81,32 @@ def test_tiles_at_c2_size():
     st = tiles.stats()
     assert st["tiles"] == 512 and st["colors"] <= 6 and st["halo_fraction"] < 0.3
     assert tiles.max_rows < 400
+
+
+def test_element_bands_order_faces_for_host_pipelined_steps():
+    """tables.build_tables bands: contiguous element ranges; interior faces
+    ordered (lowest band, straddle, signature): faces [2k, 2k+1) lie in band
+    k, faces [2k+1, 2k+2) straddle (k, k+1); walls grouped by band; every
+    face exactly once; signatures sorted within each group."""
+    space = DGSpace(unit_square(128, 128), 1, 6)
+    t = build_tables(space, PlaqueModel(), FluxScheme("cdg2"), bands=4)
+    assert t.n_bands == 4
+    eb = t.band_elem_ptr
+    assert eb[0] == 0 and eb[-1] == space.mesh.n_elements and np.all(np.diff(eb) > 0)
+    band = lambda e: np.searchsorted(eb, e, side="right") - 1
+    fp = t.band_face_ptr
+    assert fp[0] == 0 and fp[-1] == len(t.if_code) and np.all(np.diff(fp) >= 0)
+    el = t.if_elems
+    for k in range(4):
+        a, b, c = fp[2 * k], fp[2 * k + 1], fp[2 * k + 2]
+        assert np.all(band(el[a:b, 0]) == k) and np.all(band(el[a:b, 1]) == k)
+        lo = np.minimum(band(el[b:c, 0]), band(el[b:c, 1]))
+        hi = np.maximum(band(el[b:c, 0]), band(el[b:c, 1]))
+        assert np.all(lo == k) and np.all(hi == k + 1)
+        for lo_, hi_ in ((a, b), (b, c)):
+            sig = t.if_code[lo_:hi_] & 1023
+            assert np.all(np.diff(sig) >= 0)
+        w0, w1 = t.band_wall_ptr[k], t.band_wall_ptr[k + 1]
+        assert np.all(band(t.bf_elem[w0:w1]) == k)
+    # small meshes and slab meshes are not banded
+    assert build_tables(DGSpace(unit_square(8), 1, 6), PlaqueModel(), FluxScheme("cdg2")).n_bands == 1
