@@ -451,6 +451,10 @@ def run_native_arm(args, rank, world, local):
         traffic = None
     step_flops = 3 * (fv + ff + fb)
     roof = {"bound": "fp64", "kernel": f"k_{dom}",
+            "bound_note": "fp64 workload (north_star: achieved FP64 throughput against the B200 "
+                          "FP64 peak); DFMA and DMMA share the 37 TFLOP/s FP64 datapath, so "
+                          "neither 'hbm' (<= 0.6 TB/s compulsory per step) nor the bf16 "
+                          "tensor peak bounds it",
             "achieved": per[dom]["algorithmic_tflops"], "peak": peak,
             "unit": "TFLOP/s", "frac": per[dom]["algorithmic_tflops"] / peak,
             "traffic": traffic,
