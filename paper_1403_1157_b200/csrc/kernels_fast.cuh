@@ -245,7 +245,7 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
     __syncwarp();
     const double* dpi = dph;
     const double* dpo = dph + F * NB;
-    double ui[F], uo[F], dU[F], gav[F];
+    double dU[F], gav[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) {
       double u = 0.0, v = 0.0, x = 0.0, y = 0.0;
@@ -267,10 +267,16 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
           y = x;
         }
       }
-      ui[q] = u;
-      uo[q] = v;
       dU[q] = u - v;
       gav[q] = 0.5 * (x + y);
+      // point values go straight to the species transpose (not kept)
+      if constexpr (M::kConv) {
+        if (lane_ok) {
+          xch[(0 * S + s) * F + q] = u;
+          xch[(1 * S + s) * F + q] = v;
+          xch[(2 * S + s) * F + q] = gav[q];
+        }
+      }
     }
     const double As = p.A[s];
     // coupled convective physics once per face point (smem transpose)
@@ -278,14 +284,6 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
 #pragma unroll
     for (int q = 0; q < F; ++q) conv[q] = 0.0;
     if constexpr (M::kConv) {
-      if (lane_ok) {
-#pragma unroll
-        for (int q = 0; q < F; ++q) {
-          xch[(0 * S + s) * F + q] = ui[q];
-          xch[(1 * S + s) * F + q] = uo[q];
-          xch[(2 * S + s) * F + q] = gav[q];
-        }
-      }
       __syncwarp();
       if (lane_ok) {
         for (int q = s; q < F; q += S) {
