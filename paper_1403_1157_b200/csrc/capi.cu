@@ -119,6 +119,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     cudaGetLastError();
   }
   int rc = impl.configure(d.nq_vol);
+  if (rc == TDG_OK) rc = impl.upload(p);
   if (rc != TDG_OK) {
     delete ctx;
     return rc;

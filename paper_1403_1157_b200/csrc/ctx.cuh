@@ -27,6 +27,7 @@ struct Impl {
   int (*run)(tdg_ctx*, const double* U, const double* U0, double* out, double a, double b,
              double c, int mode, cudaStream_t st);
   int (*host_steps)(tdg_ctx*, double* U_host, int64_t nsteps, double dt, cudaStream_t st);
+  int (*upload)(const OpParams& p);
   int max_nqv, max_nqf;
 };
 
@@ -557,10 +558,30 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
 }
 
+// constant-memory copies of the reference-element face tables used by the
+// register-resident face kernel (same for every mesh of one (d, k))
+template <int D, int K, class M>
+int upload_const(const OpParams& p) {
+  if constexpr (FastFace<D, K, M>::ok) {
+    if (p.nqf != Dims<D, K>::NQF) return TDG_OK;  // the fast kernel is not used
+    using CL = FaceConstLayout<D, K>;
+    cudaError_t e = cudaMemcpyToSymbol(c_face_tab<D, K>, p.fB, size_t(CL::OP) * sizeof(double), 0,
+                                       cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpyToSymbol(c_face_tab<D, K>, p.fPw, size_t(CL::OW - CL::OP) * sizeof(double),
+                             size_t(CL::OP) * sizeof(double), cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpyToSymbol(c_face_tab<D, K>, p.fw, size_t(CL::N - CL::OW) * sizeof(double),
+                             size_t(CL::OW) * sizeof(double), cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "face tables -> constant memory");
+  }
+  return TDG_OK;
+}
+
 template <int D, int K, class M>
 Impl make_impl() {
-  return Impl{&configure<D, K, M>, &run<D, K, M>, &host_steps<D, K, M>, Dims<D, K>::NQV,
-              Dims<D, K>::NQF};
+  return Impl{&configure<D, K, M>, &run<D, K, M>, &host_steps<D, K, M>, &upload_const<D, K, M>,
+              Dims<D, K>::NQV, Dims<D, K>::NQF};
 }
 
 template <class M>

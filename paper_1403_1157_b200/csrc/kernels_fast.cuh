@@ -45,6 +45,19 @@ struct FastFace {
   static constexpr int MINB = NB <= 6 ? 4 : 3;  // register budget: 128 / 168
 };
 
+// Per-signature trace tables B, lifting tables Pw and face weights of the
+// register-resident face kernel in constant memory: warp-uniform indexed
+// LDC reads go through the constant cache instead of the L1TEX data pipe,
+// which the kernel saturates (ncu: l1tex throughput ~90%).  Reference-element
+// data: identical for every mesh of one (d, k) at the default face rule.
+template <int D, int K>
+struct FaceConstLayout {
+  static constexpr int NT = Dims<D, K>::NT, F = Dims<D, K>::NQF, NB = Dims<D, K>::NB;
+  static constexpr int OB = 0, OP = NT * F * NB, OW = OP + NT * F * F, N = OW + F;
+};
+template <int D, int K>
+__constant__ double c_face_tab[FaceConstLayout<D, K>::N];
+
 template <int NB>
 __device__ __forceinline__ void load_row(const double* __restrict__ src, double* dst) {
   if constexpr (NB % 2 == 0) {
@@ -89,6 +102,12 @@ __device__ __forceinline__ void store_row(double* dst, const double* v) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) dst[i] = v[i];
   }
+}
+
+template <int D, int K, int NB>
+__device__ __forceinline__ void const_row(int off, double* dst) {
+#pragma unroll
+  for (int i = 0; i < NB; ++i) dst[i] = c_face_tab<D, K>[off + i];
 }
 
 template <int D, int NB>
@@ -214,6 +233,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
   }
   const double* Bi = tB + tin * F * NB;
   const double* Bo = tB + tout * F * NB;
+  using CL = FaceConstLayout<D, K>;
+  const int ciB = CL::OB + tin * F * NB, coB = CL::OB + tout * F * NB;
 
   double ri[NB], ro[NB];
 #pragma unroll
@@ -318,22 +339,22 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
       // -fac A rho with rho = -1/2 sfac / detJ (Pw dU)
       const double fac = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * As * wside * 0.5 * sfac;
       if (use_in) {
-        const double* Pw = tP + tin * F * F;
+        const int pw0 = CL::OP + tin * F * F;
 #pragma unroll
         for (int q = 0; q < F; ++q) {
           double a = 0.0;
 #pragma unroll
-          for (int pp = 0; pp < F; ++pp) a = fma(Pw[q * F + pp], dU[pp], a);
+          for (int pp = 0; pp < F; ++pp) a = fma(c_face_tab<D, K>[pw0 + q * F + pp], dU[pp], a);
           qv[q] = fma(fac * idi, a, qv[q]);
         }
       }
       if (use_out) {
-        const double* Pw = tP + tout * F * F;
+        const int pw0 = CL::OP + tout * F * F;
 #pragma unroll
         for (int q = 0; q < F; ++q) {
           double a = 0.0;
 #pragma unroll
-          for (int pp = 0; pp < F; ++pp) a = fma(Pw[q * F + pp], dU[pp], a);
+          for (int pp = 0; pp < F; ++pp) a = fma(c_face_tab<D, K>[pw0 + q * F + pp], dU[pp], a);
           qv[q] = fma(fac * ido, a, qv[q]);
         }
       }
@@ -341,7 +362,7 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
     // projection onto both sides' test functions
 #pragma unroll
     for (int q = 0; q < F; ++q) {
-      const double wq = tw[q] * sfac;
+      const double wq = c_face_tab<D, K>[CL::OW + q] * sfac;
       const double Y = wq * (As * gav[q] - (qv[q] + conv[q]));
       const double X = wq * 0.5 * p.adj * As * dU[q];
       double bi[NB], bo[NB], di[NB], dq[NB];
