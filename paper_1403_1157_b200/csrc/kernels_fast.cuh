@@ -104,6 +104,62 @@ __device__ __forceinline__ void store_row(double* dst, const double* v) {
   }
 }
 
+// 32-byte global accesses (sm_100 LDG/STG.256): a row of NB = 4m + 2
+// doubles starting at a 16-byte boundary is m 32-byte pieces plus one
+// 16-byte piece, in either order depending on its 32-byte alignment.  The
+// face kernel's lanes read / write such rows side by side, so fewer and
+// wider accesses cut the L1 wavefronts of its (saturated) data pipe.
+__device__ __forceinline__ void ld256(const double* p, double* d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
+}
+__device__ __forceinline__ void st256(double* p, const double* d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(d[0]), "d"(d[1]), "d"(d[2]),
+               "d"(d[3])
+               : "memory");
+}
+
+template <int NB>
+__device__ __forceinline__ void load_row_wide(const double* __restrict__ src, double* dst) {
+  if constexpr (NB % 4 == 2) {
+    constexpr int M = NB / 4;
+    const bool odd = (reinterpret_cast<uintptr_t>(src) & 16u) != 0;
+    const double* p32 = src + (odd ? 2 : 0);
+    const double* p16 = src + (odd ? 0 : 4 * M);
+    double w[4 * M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) ld256(p32 + 4 * k, w + 4 * k);
+    const double2 h = __ldg(reinterpret_cast<const double2*>(p16));
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const double ev = i < 4 * M ? w[i < 4 * M ? i : 0] : (i == 4 * M ? h.x : h.y);
+      const double od = i < 2 ? (i == 0 ? h.x : h.y) : w[i >= 2 ? i - 2 : 0];
+      dst[i] = odd ? od : ev;
+    }
+  } else {
+    load_row<NB>(src, dst);
+  }
+}
+
+template <int NB>
+__device__ __forceinline__ void store_row_wide(double* dst, const double* v) {
+  if constexpr (NB % 4 == 2) {
+    constexpr int M = NB / 4;
+    const bool odd = (reinterpret_cast<uintptr_t>(dst) & 16u) != 0;
+    double* p32 = dst + (odd ? 2 : 0);
+    double* p16 = dst + (odd ? 0 : 4 * M);
+    double w[4 * M];
+#pragma unroll
+    for (int i = 0; i < 4 * M; ++i) w[i] = odd ? v[i + 2] : v[i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) st256(p32 + 4 * k, w + 4 * k);
+    *reinterpret_cast<double2*>(p16) =
+        odd ? make_double2(v[0], v[1]) : make_double2(v[4 * M], v[4 * M + 1]);
+  } else {
+    store_row<NB>(dst, v);
+  }
+}
+
 template <int D, int K, int NB>
 __device__ __forceinline__ void const_row(int off, double* dst) {
 #pragma unroll
@@ -150,10 +206,10 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
     r.h = __ldg(g + 2 * D + 1);
     r.idi = __ldg(g + 2 * D + 2);
     r.ido = __ldg(g + 2 * D + 3);
-    load_row<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
+    load_row_wide<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
     // mirror faces (Dirichlet models only) have no outside element
     const int eo = (M::kMirror && r.eout < 0) ? r.ein : r.eout;
-    load_row<NB>(U + int64_t(eo) * SN + s * NB, r.co);
+    load_row_wide<NB>(U + int64_t(eo) * SN + s * NB, r.co);
     return;
   }
   const int64_t b = (gw - wi) * FPW + grp;
@@ -196,7 +252,7 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
   const bool lane_ok = grp < FPW;
   double* scratch = sm + T::TAB + (warp * FPW + (lane_ok ? grp : 0)) * T::PF;
   double* dph = scratch;                    // [2][F][NB]
-  double* xch = dph + 2 * F * NB;           // [3][S][F]
+  double* xch = dph + 2 * F * NB;           // [3][F][S]
   double* cvs = xch + 3 * S * F;            // [F][NCV]
 
   const int64_t wi = (p.nif + FPW - 1) / FPW;
@@ -293,9 +349,11 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
       // point values go straight to the species transpose (not kept)
       if constexpr (M::kConv) {
         if (lane_ok) {
-          xch[(0 * S + s) * F + q] = u;
-          xch[(1 * S + s) * F + q] = v;
-          xch[(2 * S + s) * F + q] = gav[q];
+          // [kind][q][species]: the S lanes of a face store consecutive
+          // doubles (conflict-free with the per-face scratch stride)
+          xch[(0 * F + q) * S + s] = u;
+          xch[(1 * F + q) * S + s] = v;
+          xch[(2 * F + q) * S + s] = gav[q];
         }
       }
     }
@@ -308,8 +366,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
       __syncwarp();
       if (lane_ok) {
         for (int q = s; q < F; q += S) {
-          const double* xq = xch + q;
-          auto fetch = [xq](int kind, int sp) { return xq[(kind * S + sp) * F]; };
+          const double* xq = xch + q * S;
+          auto fetch = [xq](int kind, int sp) { return xq[kind * F * S + sp]; };
           M::face_point(p.P, fetch, cvs + q * NCV);
         }
       }
@@ -391,9 +449,9 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
     }
   }
   if (active) {
-    store_row<NB>(FC + (int64_t(lfi) * p.ne + ein) * SN + s * NB, ri);
+    store_row_wide<NB>(FC + (int64_t(lfi) * p.ne + ein) * SN + s * NB, ri);
     if (two && !code_skip_out(code))
-      store_row<NB>(FC + (int64_t(lfo) * p.ne + eout) * SN + s * NB, ro);
+      store_row_wide<NB>(FC + (int64_t(lfo) * p.ne + eout) * SN + s * NB, ro);
   }
   __syncwarp();  // the warp's scratch is rewritten by the next group
   }
