@@ -39,7 +39,13 @@ struct FastFace {
   // per-face scratch: normal-derivative tables (2 sides), the species
   // transpose (u_in, u_out, avg d_n u at every point) and the coupled
   // per-point results (wave speed, flux normals)
-  static constexpr int PF = (2 * F * NB + 3 * S * F + F * NCV + 1) & ~1;
+  // species-transpose rows padded to an odd stride XS and the per-face
+  // scratch stride PF = 6 (mod 16) doubles: with 5-6 faces per warp the
+  // transposed stores and the per-point physics loads stay 2-way at most
+  // (bank-conflict search over the access patterns; ncu showed 6-way)
+  static constexpr int XS = S | 1;
+  static constexpr int PF0 = (2 * F * NB + 3 * XS * F + F * NCV + 1) & ~1;
+  static constexpr int PF = PF0 + ((6 - PF0 % 16) + 16) % 16;
   static constexpr size_t smem() { return size_t(TAB + WARPS * FPW * PF) * 8; }
   static constexpr bool ok = F <= 8 && S >= 3 && S <= 8 && NB <= 10 && smem() <= 100 * 1024;
   static constexpr int MINB = NB <= 6 ? 4 : 3;  // register budget: 128 / 168
@@ -252,8 +258,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
   const bool lane_ok = grp < FPW;
   double* scratch = sm + T::TAB + (warp * FPW + (lane_ok ? grp : 0)) * T::PF;
   double* dph = scratch;                    // [2][F][NB]
-  double* xch = dph + 2 * F * NB;           // [3][F][S]
-  double* cvs = xch + 3 * S * F;            // [F][NCV]
+  double* xch = dph + 2 * F * NB;           // [3][F][XS]
+  double* cvs = xch + 3 * T::XS * F;        // [F][NCV]
 
   const int64_t wi = (p.nif + FPW - 1) / FPW;
   // grid-stride over face groups: the tables above are staged once per CTA
@@ -351,9 +357,9 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
         if (lane_ok) {
           // [kind][q][species]: the S lanes of a face store consecutive
           // doubles (conflict-free with the per-face scratch stride)
-          xch[(0 * F + q) * S + s] = u;
-          xch[(1 * F + q) * S + s] = v;
-          xch[(2 * F + q) * S + s] = gav[q];
+          xch[(0 * F + q) * T::XS + s] = u;
+          xch[(1 * F + q) * T::XS + s] = v;
+          xch[(2 * F + q) * T::XS + s] = gav[q];
         }
       }
     }
@@ -366,8 +372,8 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
       __syncwarp();
       if (lane_ok) {
         for (int q = s; q < F; q += S) {
-          const double* xq = xch + q * S;
-          auto fetch = [xq](int kind, int sp) { return xq[kind * F * S + sp]; };
+          const double* xq = xch + q * T::XS;
+          auto fetch = [xq](int kind, int sp) { return xq[kind * F * T::XS + sp]; };
           M::face_point(p.P, fetch, cvs + q * NCV);
         }
       }
