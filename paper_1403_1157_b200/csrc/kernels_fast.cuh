@@ -203,15 +203,30 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
     r.lfi = lf.x;
     r.lfo = lf.y;
     const double* g = p.ifgeo + fc * NFG;
+    if constexpr (NFG == 8) {  // 2D: the 64-byte record in two 32-byte loads
+      double w[8];
+      ld256(g, w);
+      ld256(g + 4, w + 4);
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      r.jn[0][a] = __ldg(g + a);
-      r.jn[1][a] = __ldg(g + D + a);
+      for (int a = 0; a < D; ++a) {
+        r.jn[0][a] = w[a];
+        r.jn[1][a] = w[D + a];
+      }
+      r.sfac = w[2 * D];
+      r.h = w[2 * D + 1];
+      r.idi = w[2 * D + 2];
+      r.ido = w[2 * D + 3];
+    } else {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        r.jn[0][a] = __ldg(g + a);
+        r.jn[1][a] = __ldg(g + D + a);
+      }
+      r.sfac = __ldg(g + 2 * D);
+      r.h = __ldg(g + 2 * D + 1);
+      r.idi = __ldg(g + 2 * D + 2);
+      r.ido = __ldg(g + 2 * D + 3);
     }
-    r.sfac = __ldg(g + 2 * D);
-    r.h = __ldg(g + 2 * D + 1);
-    r.idi = __ldg(g + 2 * D + 2);
-    r.ido = __ldg(g + 2 * D + 3);
     load_row_wide<NB>(U + int64_t(r.ein) * SN + s * NB, r.ci);
     // mirror faces (Dirichlet models only) have no outside element
     const int eo = (M::kMirror && r.eout < 0) ? r.ein : r.eout;
