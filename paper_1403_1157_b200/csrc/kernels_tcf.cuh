@@ -39,7 +39,9 @@ struct TcFace {
   static constexpr int KT = (NB + 3) / 4, NBK = 4 * KT;
   static constexpr int NNT = (NB + 7) / 8, NBN = 8 * NNT;
   static constexpr int NCV = 1 + M::NFX;
-  // per-signature table offsets (doubles), see tables.tc_face_tables
+  // per-signature table offsets (doubles), see tables.tc_face_tables; every
+  // table is stored fragment-major ([k-step or point tile][...][lane]) so a
+  // warp's B-operand load is 32 consecutive doubles (2 L1 wavefronts)
   static constexpr int OBT = 0, OGT = OBT + NBK * QP, OBP = OGT + D * NBK * QP,
                        OGP = OBP + QP * NBN, OWB = OGP + D * QP * NBN, TS = OWB + QP * NBN;
   static constexpr int WARPS = 4;
@@ -134,8 +136,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
           const int kr = 4 * kt + t, qc = 8 * qt + g;
-          const double bi = __ldg(Ti + T::OBT + kr * QP + qc);
-          const double bo = __ldg(To + T::OBT + kr * QP + qc);
+          const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
+          const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
 #pragma unroll
           for (int k = 0; k < NV; ++k) {
             dmma(vi[k][0], vi[k][1], ci[k][kt], bi);
@@ -143,8 +145,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           }
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            const double gi = __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc);
-            const double go = __ldg(To + T::OGT + (a * NBK + kr) * QP + qc);
+            const double gi = __ldg(Ti + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane);
+            const double go = __ldg(To + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane);
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
               int kv = 0;
@@ -210,8 +212,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
             const int kr = 4 * kt + t, qc = 8 * qt + g;
-            dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + kr * QP + qc));
-            dmma(uo[0], uo[1], co[kt], __ldg(To + T::OBT + kr * QP + qc));
+            dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane));
+            dmma(uo[0], uo[1], co[kt], __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane));
           }
           double du[2];
 #pragma unroll
@@ -221,8 +223,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
             const int qr = 8 * qt + 2 * t + ks;
 #pragma unroll
             for (int nt = 0; nt < NNT; ++nt) {
-              dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + T::OWB + qr * NBN + 8 * nt + g));
-              dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + T::OWB + qr * NBN + 8 * nt + g));
+              dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + T::OWB + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
+              dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + T::OWB + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
             }
           }
         }
@@ -253,8 +255,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
           const int kr = 4 * kt + t, qc = 8 * qt + g;
-          const double bi = __ldg(Ti + T::OBT + kr * QP + qc);
-          const double bo = __ldg(To + T::OBT + kr * QP + qc);
+          const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
+          const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
           dmma(ui[0], ui[1], ci[kt], bi);
           dmma(uo[0], uo[1], co[kt], bo);
           if (lift) {
@@ -264,8 +266,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           }
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            dmma(dia[a][0], dia[a][1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + (a * NBK + kr) * QP + qc));
-            dmma(dqa[a][0], dqa[a][1], co[kt] * jn[1][a], __ldg(To + T::OGT + (a * NBK + kr) * QP + qc));
+            dmma(dia[a][0], dia[a][1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane));
+            dmma(dqa[a][0], dqa[a][1], co[kt] * jn[1][a], __ldg(To + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane));
           }
         }
         double di[2], dq[2], rho[2];
@@ -306,12 +308,12 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt) {
             const int nc = 8 * nt + g;
-            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + T::OBP + qr * NBN + nc));
-            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + qr * NBN + nc));
+            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
+            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-              dmma(rix[nt][0], rix[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (a * QP + qr) * NBN + nc));
-              dmma(rox[nt][0], rox[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (a * QP + qr) * NBN + nc));
+              dmma(rix[nt][0], rix[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane));
+              dmma(rox[nt][0], rox[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane));
             }
           }
         }

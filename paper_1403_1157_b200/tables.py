@@ -275,9 +275,31 @@ def _pi_cols(nb: int):
     return np.where(ok, pi, 0), ok
 
 
+_LANE = np.arange(32)
+_LG, _LT = _LANE >> 2, _LANE & 3       # m8n8k4 fragment coordinates g, t
+
+
+def _frag_kq(A):
+    """[4 KT][8 QT] table (B operand rows k = 4 kt + t, columns q = 8 qt + g)
+    -> fragment-major [KT][QT][32 lanes]."""
+    KT, QT = A.shape[0] // 4, A.shape[1] // 8
+    kt, qt = np.meshgrid(np.arange(KT), np.arange(QT), indexing="ij")
+    return A[4 * kt[..., None] + _LT, 8 * qt[..., None] + _LG]
+
+
+def _frag_qn(A):
+    """[8 QT][8 NNT] table (B operand rows q = 8 qt + 2 t + ks, columns
+    n = 8 nt + g) -> fragment-major [QT][2][NNT][32 lanes]."""
+    QT, NNT = A.shape[0] // 8, A.shape[1] // 8
+    qt, ks, nt = np.meshgrid(np.arange(QT), np.arange(2), np.arange(NNT), indexing="ij")
+    return A[8 * qt[..., None] + 2 * _LT + ks[..., None], 8 * nt[..., None] + _LG]
+
+
 def tc_face_tables(t: OperatorTables):
     """Per-signature operand tables of the transposed tensor-core face
-    kernel (csrc/kernels_tcf.cuh), concatenated per table id:
+    kernel (csrc/kernels_tcf.cuh), concatenated per table id, each stored
+    fragment-major (``_frag_kq`` / ``_frag_qn``: one warp-wide B-operand
+    load reads 32 consecutive doubles):
 
     BT  [NBK][QP]        B[q][k]                 traces u = c B^T, rho = m B^T
     GT  [d][NBK][QP]     G[q][k][a]              traces d_n u = sum_a (jn_a c) G_a^T
@@ -297,7 +319,11 @@ def tc_face_tables(t: OperatorTables):
         BP = np.zeros((QP, NBN)); BP[:F] = B[:, pic] * ok
         GP = np.zeros((d, QP, NBN)); GP[:, :F] = G.transpose(2, 0, 1)[:, :, pic] * ok
         WB = np.zeros((QP, NBN)); WB[:F] = (t.face_w[:, None] * B)[:, pic] * ok
-        parts.append(np.concatenate([x.ravel() for x in (BT, GT, BP, GP, WB)]))
+        parts.append(np.concatenate([_frag_kq(BT).ravel()]
+                                    + [_frag_kq(GT[a]).ravel() for a in range(d)]
+                                    + [_frag_qn(BP).ravel()]
+                                    + [_frag_qn(GP[a]).ravel() for a in range(d)]
+                                    + [_frag_qn(WB).ravel()]))
     stride = len(parts[0])
     return np.ascontiguousarray(np.concatenate(parts)), stride
 
