@@ -45,7 +45,8 @@ struct TcVol {
   static constexpr int KT = (NB + 3) / 4, NBK = 4 * KT;
   static constexpr int NNT = (NB + 7) / 8, NBN = 8 * NNT;
   static constexpr int NV = M::NVAL, NG = M::NGRAD, NF = M::NFLUX, NL = M::NNL;
-  // table offsets (doubles)
+  // table offsets (doubles); tables are fragment-major (tables.tc_volume_tables):
+  // a warp's B-operand load is 32 consecutive doubles
   static constexpr int OPHT = 0;                         // [NBK][QP]
   static constexpr int OGT = OPHT + NBK * QP;            // [D][NBK][QP]
   static constexpr int OPP = OGT + D * NBK * QP;         // [QP][NBN]
@@ -127,12 +128,12 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
           const int kr = 4 * kt + t, qc = 8 * qt + g;
-          const double bphi = tb[T::OPHT + kr * QP + qc];
+          const double bphi = tb[T::OPHT + (kt * QT + qt) * 32 + lane];
 #pragma unroll
           for (int k = 0; k < NV; ++k) dmma(v[k][0], v[k][1], cf[M::val_sp(k)][kt], bphi);
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            const double bg = tb[T::OGT + (a * NBK + kr) * QP + qc];
+            const double bg = tb[T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane];
 #pragma unroll
             for (int k = 0; k < NG; ++k) dmma(gr[k][a][0], gr[k][a][1], cf[M::grad_sp(k)][kt], bg);
           }
@@ -171,12 +172,12 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
             const int nc = 8 * nt + g;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-              const double bp = tb[T::OPG + (a * QP + qr) * NBN + nc];
+              const double bp = tb[T::OPG + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane];
 #pragma unroll
               for (int k = 0; k < NF; ++k) dmma(af[k][nt][0], af[k][nt][1], fr[k][a][ks], bp);
             }
             if constexpr (NL > 0) {
-              const double bq = tb[T::OPP + qr * NBN + nc];
+              const double bq = tb[T::OPP + ((qt * 2 + ks) * NNT + nt) * 32 + lane];
 #pragma unroll
               for (int k = 0; k < NL; ++k) dmma(al[k][nt][0], al[k][nt][1], nl[k][ks], bq);
             }
@@ -202,7 +203,7 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt)
             dmma(dif[nt][0], dif[nt][1], a,
-                 tb[T::OKS + (pq * NBK + 4 * kt + t) * NBN + 8 * nt + g]);
+                 tb[T::OKS + ((pq * KT + kt) * NNT + nt) * 32 + lane]);
         }
       const int fi = M::flux_index(s), li = M::nl_index(s);
       const double As = p.A[s];

@@ -295,6 +295,14 @@ def _frag_qn(A):
     return A[8 * qt[..., None] + 2 * _LT + ks[..., None], 8 * nt[..., None] + _LG]
 
 
+def _frag_kn(A):
+    """[4 KT][8 NNT] table (B operand rows k = 4 kt + t, columns n = 8 nt + g)
+    -> fragment-major [KT][NNT][32 lanes]."""
+    KT, NNT = A.shape[0] // 4, A.shape[1] // 8
+    kt, nt = np.meshgrid(np.arange(KT), np.arange(NNT), indexing="ij")
+    return A[4 * kt[..., None] + _LT, 8 * nt[..., None] + _LG]
+
+
 def tc_face_tables(t: OperatorTables):
     """Per-signature operand tables of the transposed tensor-core face
     kernel (csrc/kernels_tcf.cuh), concatenated per table id, each stored
@@ -371,7 +379,8 @@ def mma_volume_tables(t: OperatorTables) -> np.ndarray:
 
 def tc_volume_tables(t: OperatorTables) -> np.ndarray:
     """Operand tables of the transposed tensor-core volume kernel
-    (csrc/kernels_tc.cuh, k_volume_tc), concatenated:
+    (csrc/kernels_tc.cuh, k_volume_tc), concatenated, each stored
+    fragment-major (one warp-wide B-operand load = 32 consecutive doubles):
 
     PHT [NBK][QP]        Phi[q][k]                    B of the point values
     GT  [d][NBK][QP]     G[q][k][a]                   B of the reference gradients
@@ -393,7 +402,9 @@ def tc_volume_tables(t: OperatorTables) -> np.ndarray:
     PG = np.zeros((d, QP, NBN))
     PG[:, :Q] = (w[:, None, None] * t.vol_grad).transpose(2, 0, 1)[:, :, pic] * ok
     KS = np.zeros((nsym, NBK, NBN)); KS[:, :nb] = t.vol_stiff[:, :, pic] * ok
-    return np.ascontiguousarray(np.concatenate([x.ravel() for x in (PHT, GT, PP, PG, KS)]))
+    parts = ([_frag_kq(PHT)] + [_frag_kq(GT[a]) for a in range(d)] + [_frag_qn(PP)]
+             + [_frag_qn(PG[a]) for a in range(d)] + [_frag_kn(KS[q]) for q in range(nsym)])
+    return np.ascontiguousarray(np.concatenate([x.ravel() for x in parts]))
 
 
 def scheme_constants(space: DGSpace, scheme: FluxScheme):
