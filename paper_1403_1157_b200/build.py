@@ -18,9 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtaxisdg_b200.so")
 SOURCES = ["capi.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
            "inst_diffusion.cu"]
-HEADERS = ["common.cuh", "ctx.cuh", "kernels.cuh", "kernels_fast.cuh", "kernels_mma.cuh",
-           "models.cuh",
-           "vecops.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(128, FastFace<D, K, M>::MINB)
 k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, int64_t ngroups) {
   using T = FastFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW, NCV = T::NCV;
-  constexpr int NFG = Dims<D, K>::NFG;
+  [[maybe_unused]] constexpr int NFG = Dims<D, K>::NFG;
   extern __shared__ __align__(16) double sm[];
   double* tB = sm;
   double* tG = tB + T::TB;

@@ -150,9 +150,11 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
     const int e = side ? fr[2] : fr[1];
     cS[(side * NBK + k) * NCP + f * S + s] = ok ? __ldg(U + int64_t(e) * SN + sk) : 0.0;
   }
-  for (int idx = lane; idx < 2 * (NBK - NB) * NCP; idx += 32) {
-    const int side = idx / ((NBK - NB) * NCP), r = idx - side * (NBK - NB) * NCP;
-    cS[(side * NBK + NB) * NCP + r] = 0.0;
+  if constexpr (NBK > NB) {
+    for (int idx = lane; idx < 2 * (NBK - NB) * NCP; idx += 32) {
+      const int side = idx / ((NBK - NB) * NCP), r = idx - side * (NBK - NB) * NCP;
+      cS[(side * NBK + NB) * NCP + r] = 0.0;
+    }
   }
   if constexpr (NCP > NC) {
     for (int idx = lane; idx < 2 * NB * (NCP - NC); idx += 32) {

@@ -67,7 +67,7 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
             double cc, int mode) {
   using T = TcVol<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, NEG = T::NEG, NSYM = T::NSYM;
-  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NBK = T::NBK, NNT = T::NNT, NBN = T::NBN;
+  constexpr int QT = T::QT, KT = T::KT, NNT = T::NNT;
   constexpr int NV = T::NV, NG = T::NG, NF = T::NF, NL = T::NL;
   extern __shared__ __align__(16) double sm[];
   const double* tb = tabs;
@@ -127,7 +127,6 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
         }
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
-          const int kr = 4 * kt + t, qc = 8 * qt + g;
           const double bphi = tb[T::OPHT + (kt * QT + qt) * 32 + lane];
 #pragma unroll
           for (int k = 0; k < NV; ++k) dmma(v[k][0], v[k][1], cf[M::val_sp(k)][kt], bphi);
@@ -166,10 +165,8 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
         // projection: k-step ks takes the points of parity ks
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const int qr = 8 * qt + 2 * t + ks;
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt) {
-            const int nc = 8 * nt + g;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
               const double bp = tb[T::OPG + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane];

@@ -79,7 +79,7 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
   using T = TcFace<D, K, M>;
   using PH = TcfPhys<M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
-  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NBK = T::NBK, NNT = T::NNT, NBN = T::NBN;
+  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NNT = T::NNT;
   constexpr int NCV = T::NCV, TS = T::TS;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -135,7 +135,6 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
         }
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
-          const int kr = 4 * kt + t, qc = 8 * qt + g;
           const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
           const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
 #pragma unroll
@@ -211,8 +210,7 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0};
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
-            const int kr = 4 * kt + t, qc = 8 * qt + g;
-            dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane));
+              dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane));
             dmma(uo[0], uo[1], co[kt], __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane));
           }
           double du[2];
@@ -220,7 +218,6 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
           for (int j = 0; j < 2; ++j) du[j] = mirror ? 2.0 * (ui[j] - gs) : ui[j] - uo[j];
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
-            const int qr = 8 * qt + 2 * t + ks;
 #pragma unroll
             for (int nt = 0; nt < NNT; ++nt) {
               dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + T::OWB + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
@@ -254,7 +251,6 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
         for (int a = 0; a < D; ++a) dia[a][0] = dia[a][1] = dqa[a][0] = dqa[a][1] = 0.0;
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
-          const int kr = 4 * kt + t, qc = 8 * qt + g;
           const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
           const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
           dmma(ui[0], ui[1], ci[kt], bi);
@@ -304,10 +300,8 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
         }
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const int qr = 8 * qt + 2 * t + ks;
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt) {
-            const int nc = 8 * nt + g;
             dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
             dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
 #pragma unroll
