@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: testing only (host-staged exchange; ranks may share a GPU)")
-    ap.add_argument("--bands", type=int, default=4,
+    ap.add_argument("--bands", type=int, default=8,
                     help="element bands of the host-pipelined e2e stepping")
     ap.add_argument("--no-implicit", action="store_true",
                     help="skip the extra SDIRK3+JFNK figure of the explicit C2 run")
@@ -492,6 +492,7 @@ def run_native_arm(args, rank, world, local):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
+        t_enq = time.perf_counter()
         if host_api:
             op.ssprk3_steps_host(Uh, args.steps, dt)
         else:
@@ -500,6 +501,7 @@ def run_native_arm(args, rank, world, local):
                 stepper.step(Ud, dt)
                 Uh.copy_(Ud, non_blocking=True)
         b.record()
+        t_enq = time.perf_counter() - t_enq
         b.synchronize()
         ems = a.elapsed_time(b)
         if dist_on:
@@ -508,6 +510,7 @@ def run_native_arm(args, rank, world, local):
             ems = tt.item()
         e2e = {"value": total_dofs * 3 * args.steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": Uh.numel() * 8, "d2h_bytes_per_step": Uh.numel() * 8,
+               "ms_per_step": ems / args.steps, "host_issue_ms_per_step": t_enq * 1e3 / args.steps,
                "api": "DiscreteOperator.ssprk3_steps_host (tdg_ssprk3_steps_host): per-step "
                       "copy-in / copy-out pipelined by element bands" if host_api else
                       "copy-in, SSPRK3.step with the halo exchange, copy-out per step"}

@@ -177,6 +177,8 @@ int tdg_destroy(tdg_ctx* ctx) {
   cudaFree(ctx->hs_buf);
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  for (auto s : ctx->hs_st)
+    if (s) cudaStreamDestroy(s);
   if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
   if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
   for (auto* v : {&ctx->ev_h2d, &ctx->ev_d2h, &ctx->ev_done, &ctx->ev_vol_b})

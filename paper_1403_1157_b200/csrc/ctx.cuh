@@ -62,8 +62,9 @@ struct tdg_ctx {
   double* hs_buf = nullptr;  // [3][rows][S][nb]: U, stage 1, stage 2
   size_t hs_n = 0;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  std::vector<cudaEvent_t> ev_h2d, ev_d2h, ev_done, ev_vol_b;
-  cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;  // overlapped launch order: faces, then the volume part (+1%)    // A/B: element-local DMMA face kernel instead of the transposed one
+  cudaStream_t hs_st[6] = {};  // per stage: faces + slot sums, volume part
+  std::vector<cudaEvent_t> ev_h2d, ev_d2h, ev_done, ev_vol_b;  // done / vol: [stage][band]
+  cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
   // overlapped application: volume part on `aux` concurrent with the
   // face kernel on the caller's stream, then the face-slot sum
   bool overlap = true;
@@ -460,19 +461,28 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     if (!ctx->s_h2d) {
       cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking);
       cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
+      // later stages first: the chain to the copy-out (and so to the next
+      // copy-in) runs through stage 3, which must not queue behind the
+      // next step's stage-1 work
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      for (int s = 0; s < 6; ++s) {
+        const int pr = s < 2 ? lo : (s < 4 ? (lo + hi) / 2 : hi);
+        cudaStreamCreateWithPriority(&ctx->hs_st[s], cudaStreamNonBlocking, pr);
+      }
       cudaEventCreateWithFlags(&ctx->ev_s0, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming);
     }
     ev_new(ctx->ev_h2d, nb);
     ev_new(ctx->ev_d2h, nb);
-    ev_new(ctx->ev_done, nb);
-    ev_new(ctx->ev_vol_b, nb);
+    ev_new(ctx->ev_done, 3 * nb);
+    ev_new(ctx->ev_vol_b, 3 * nb);
     const auto& be = ctx->band_elem;
     const auto& bf = ctx->band_face;
     const auto& bw = ctx->band_wall;
-    // faces of band k available once bands <= k are resident: the faces
-    // straddling (k-1, k), those internal to k, and band k's walls
-    auto faces_r1 = [&](int k, const double* Uin) {
+    // faces of band k: those straddling (k-1, k), those internal to k and
+    // band k's walls; they read bands k-1 and k and write their slots
+    auto faces_band = [&](int k, const double* Uin, cudaStream_t s) {
       OpParams pp = p;
       const int64_t f0 = k > 0 ? bf[2 * k - 1] : 0, f1 = bf[2 * k + 1];
       pp.ifel = p.ifel + 2 * f0;
@@ -485,74 +495,81 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
       pp.bfcode = p.bfcode + bw[k];
       pp.bfgeo = p.bfgeo + bw[k];
       pp.nbf = bw[k + 1] - bw[k];
-      if (pp.nif + pp.nbf > 0) run_faces<D, K, M>(ctx, pp, Uin, st, true);
+      if (pp.nif + pp.nbf > 0) run_faces<D, K, M>(ctx, pp, Uin, s, true);
     };
     auto volume_band = [&](int k, const double* Uin, const double* U0, double* out, double a,
-                           double b, double c) {
+                           double b, double c, cudaStream_t s) {
       OpParams pv = p;
       const int64_t e0 = be[k];
       pv.ne = be[k + 1] - e0;
       pv.egeo = p.egeo + e0 * Dims<D, K>::NEG;
-      KernelTimer kt(ctx, 2, ctx->aux);
+      KernelTimer kt(ctx, 2, s);
       launch_volume<D, K, M>(ctx, pv, Uin + e0 * SN, U0 ? U0 + e0 * SN : nullptr, out + e0 * SN,
-                             a, b, c, 2 | 4, ctx->aux, 0);
+                             a, b, c, 2 | 4, s, 0);
     };
-    auto fc_add = [&](int64_t e0, int64_t e1, double* out, double c, cudaStream_t s) {
+    auto fc_add = [&](int k, double* out, double c, cudaStream_t s) {
       KernelTimer kt(ctx, 3, s);
-      const int64_t n2 = (e1 - e0) * (SN / 2);
+      const int64_t n2 = (be[k + 1] - be[k]) * (SN / 2);
       const int grid = int(n2 / 256 + 1 < 148 * 8 ? n2 / 256 + 1 : 148 * 8);
-      k_fc_add<D, SN, Dims<D, K>::NEG><<<grid, 256, 0, s>>>(ctx->fc, p.egeo, p.ne, out, c, 2, e0,
-                                                            e1);
+      k_fc_add<D, SN, Dims<D, K>::NEG><<<grid, 256, 0, s>>>(ctx->fc, p.egeo, p.ne, out, c, 2,
+                                                            be[k], be[k + 1]);
     };
+    // Wavefront over (stage, band).  Stage s of band k needs stage s-1 of
+    // bands k-1..k+1 (its faces read the neighbours); the copy-in of band k
+    // for step n+1 needs only the copy-out of band k of step n, so the copy
+    // engines stream continuously while the three stages trail behind.
+    // Every write-after-read on U / W1 / W2 / the slot buffer is ordered by
+    // these same edges (the readers of a band finish before the band's next
+    // slot sum, which precedes its copy-out, which precedes its next copy-in).
+    double* X[3] = {Ud, W1, W2};
+    double* Y[3] = {W1, W2, Ud};
+    const double* Z[3] = {nullptr, Ud, Ud};
+    const double ca[3] = {0.0, 0.75, 1.0 / 3.0}, cb[3] = {1.0, 0.25, 2.0 / 3.0};
+    const double cc[3] = {dt, 0.25 * dt, (2.0 / 3.0) * dt};
+    cudaEventRecord(ctx->ev_s0, st);
+    cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_s0, 0);
+    for (auto s : ctx->hs_st) cudaStreamWaitEvent(s, ctx->ev_s0, 0);
     for (int64_t it = 0; it < nsteps; ++it) {
-      // ---- stage 1: copy-in by band, overlapped with the band's work
-      cudaEventRecord(ctx->ev_s0, st);
-      cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_s0, 0);
       for (int k = 0; k < nb; ++k) {
         if (it > 0) cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_d2h[k], 0);
         const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
         cudaMemcpyAsync(Ud + o, Uh + o, m * sizeof(double), cudaMemcpyHostToDevice, ctx->s_h2d);
         cudaEventRecord(ctx->ev_h2d[k], ctx->s_h2d);
       }
-      for (int k = 0; k < nb; ++k) {
-        cudaStreamWaitEvent(ctx->aux, ctx->ev_h2d[k], 0);
-        volume_band(k, Ud, nullptr, W1, 0.0, 1.0, dt);
-        cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
-        faces_r1(k, Ud);
+      for (int s = 0; s < 3; ++s) {
+        cudaStream_t sf = ctx->hs_st[2 * s], sv = ctx->hs_st[2 * s + 1];
+        auto ready = [&](int k) { return s == 0 ? ctx->ev_h2d[k] : ctx->ev_done[(s - 1) * nb + k]; };
+        for (int k = 0; k < nb; ++k) {
+          cudaStreamWaitEvent(sv, ready(k), 0);
+          volume_band(k, X[s], Z[s], Y[s], ca[s], cb[s], cc[s], sv);
+          cudaEventRecord(ctx->ev_vol_b[s * nb + k], sv);
+        }
+        auto finish = [&](int k) {  // all faces touching band k are done
+          cudaStreamWaitEvent(sf, ctx->ev_vol_b[s * nb + k], 0);
+          fc_add(k, Y[s], cc[s], sf);
+          cudaEventRecord(ctx->ev_done[s * nb + k], sf);
+          if (s == 2) {
+            cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[s * nb + k], 0);
+            const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
+            cudaMemcpyAsync(Uh + o, Ud + o, m * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->s_d2h);
+            cudaEventRecord(ctx->ev_d2h[k], ctx->s_d2h);
+          }
+        };
+        for (int k = 0; k < nb; ++k) {
+          cudaStreamWaitEvent(sf, ready(k), 0);
+          faces_band(k, X[s], sf);
+          if (k > 0) finish(k - 1);
+        }
+        finish(nb - 1);
       }
-      cudaEventRecord(ctx->ev_s1, ctx->aux);
-      cudaStreamWaitEvent(st, ctx->ev_s1, 0);
-      fc_add(0, p.ne, W1, dt, st);
-      // ---- stage 2: whole state resident
-      int rc = ctx->impl.run(ctx, W1, Ud, W2, 0.75, 0.25, 0.25 * dt, 2, st);
-      if (rc) return rc;
-      // ---- stage 3: finish and copy out band by band
-      const double c3 = (2.0 / 3.0) * dt;
-      cudaEventRecord(ctx->ev_s0, st);
-      cudaStreamWaitEvent(ctx->aux, ctx->ev_s0, 0);
-      for (int k = 0; k < nb; ++k) {
-        volume_band(k, W2, Ud, Ud, 1.0 / 3.0, 2.0 / 3.0, c3);
-        cudaEventRecord(ctx->ev_vol_b[k], ctx->aux);
-      }
-      auto finish = [&](int k) {  // all faces touching band k are done
-        cudaStreamWaitEvent(st, ctx->ev_vol_b[k], 0);
-        fc_add(be[k], be[k + 1], Ud, c3, st);
-        cudaEventRecord(ctx->ev_done[k], st);
-        cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[k], 0);
-        const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
-        cudaMemcpyAsync(Uh + o, Ud + o, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_d2h);
-        cudaEventRecord(ctx->ev_d2h[k], ctx->s_d2h);
-      };
-      for (int k = 0; k < nb; ++k) {
-        faces_r1(k, W2);
-        if (k > 0) finish(k - 1);
-      }
-      finish(nb - 1);
     }
-    cudaEventRecord(ctx->ev_s1, ctx->s_d2h);
-    cudaStreamWaitEvent(st, ctx->ev_s1, 0);
-    cudaEventRecord(ctx->ev_s0, ctx->aux);
-    cudaStreamWaitEvent(st, ctx->ev_s0, 0);
+    // join: every stream's tail back onto the caller's stream
+    for (cudaStream_t s : {ctx->s_h2d, ctx->s_d2h, ctx->hs_st[0], ctx->hs_st[1], ctx->hs_st[2],
+                           ctx->hs_st[3], ctx->hs_st[4], ctx->hs_st[5]}) {
+      cudaEventRecord(ctx->ev_s1, s);
+      cudaStreamWaitEvent(st, ctx->ev_s1, 0);
+    }
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");

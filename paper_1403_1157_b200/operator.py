@@ -65,7 +65,7 @@ class DiscreteOperator:
     def __init__(self, space: DGSpace, model, scheme: FluxScheme,
                  nthreads: int = 1, npartitions: int | None = None,
                  vol_degree: int | None = None, face_degree: int | None = None,
-                 device=None, n_owned: int | None = None, global_ids=None, bands: int = 4):
+                 device=None, n_owned: int | None = None, global_ids=None, bands: int = 8):
         if model.n_species != space.n_species:
             raise ValueError(f"model has {model.n_species} species, space has "
                              f"{space.n_species}")

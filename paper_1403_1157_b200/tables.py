@@ -98,7 +98,7 @@ def _face_tables(space: DGSpace, frule):
 
 def build_tables(space: DGSpace, model, scheme: FluxScheme,
                  vol_degree=None, face_degree=None, n_owned=None,
-                 global_ids=None, bands: int = 4) -> OperatorTables:
+                 global_ids=None, bands: int = 8) -> OperatorTables:
     """Pack tables, element geometry and face lists.
 
     Slab-decomposed runs pass a local mesh whose first ``n_owned``
@@ -190,8 +190,8 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
     # element bands (contiguous id ranges; host-pipelined stepping): faces
     # of one band, then the faces straddling into the next band
     n_own = n_owned
-    nbands = bands if (n_cut == 0 and n_own == mesh.n_elements
-                       and n_own >= 8192 * max(bands, 1)) else 1
+    nbands = min(bands, n_own // 8192) if (n_cut == 0 and n_own == mesh.n_elements) else 1
+    nbands = max(nbands, 1)
     ebnd = (np.arange(nbands + 1, dtype=np.int64) * n_own) // nbands
     band_of = lambda e: np.searchsorted(ebnd, e, side="right") - 1
     if nbands > 1:
