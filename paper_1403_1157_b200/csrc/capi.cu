@@ -131,7 +131,8 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     delete ctx;
     return cuda_fail(e, "cudaMalloc face slots");
   }
-  e = cudaMalloc(&ctx->part, kRedBlocks * kMaxTotS * sizeof(double));
+  e = cudaMalloc(&ctx->part, kRedWorkBytes);
+  if (e == cudaSuccess) e = cudaMemset(ctx->part, 0, kRedWorkBytes);
   if (e != cudaSuccess) {
     cudaFree(ctx->fc);
     delete ctx;

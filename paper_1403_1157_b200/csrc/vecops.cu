@@ -3,9 +3,10 @@
 // and axpy updates on flat fp64 vectors).
 //
 // Reductions use a fixed grid (kRedBlocks CTAs, grid-stride loop in a
-// fixed order, warp-shuffle + shared-memory tree), then one CTA sums the
-// per-block partials in a fixed order: bitwise reproducible results, no
-// atomics.  HBM-bound: 16 B/element for dot, 8 B/element for norm.
+// fixed order, warp-shuffle + shared-memory tree), then the last CTA to
+// finish (one integer ticket) sums the per-block partials in a fixed
+// order: bitwise reproducible results, no floating-point atomics.
+// HBM-bound: 16 B/element for dot, 8 B/element for norm.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,10 +42,69 @@ __device__ __forceinline__ double block_sum(double v) {
 // Element order and per-thread accumulators depend only on n and the grid,
 // so a fused axpy+dot is bitwise an axpy followed by a dot.  Vectors must
 // be 16-byte aligned (torch allocations and rows of an even-length V).
-template <int MODE>
-__global__ void __launch_bounds__(kRedThreads) k_red_partial(
+// L2 eviction-priority hints for the MGS sweep: w and the current basis
+// vector (the next pass's v_prev) are marked evict-last, v_prev on its
+// last read evict-first, so w and V_i stay in the 126 MB L2 between passes
+// and each pass streams only V_i from HBM.
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld2_hint(const double2* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld2_nc_hint(const double2* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st2_hint(double2* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+}
+
+// The last CTA to finish (ticket) sums the per-block partials in a fixed
+// order (thread t: partials t, t+256, ...; then the block tree), so the
+// result does not depend on which CTA finishes last: one launch per
+// reduction, deterministic bits.
+__device__ __forceinline__ void finish_sum(double s, double* __restrict__ part, unsigned* ticket,
+                                           double* __restrict__ out, int sqrt_out) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < int(gridDim.x); i += kRedThreads) acc += __ldcg(part + i);
+  const double tot = block_sum(acc);
+  if (threadIdx.x == 0) {
+    *out = sqrt_out ? sqrt(tot) : tot;
+    *ticket = 0u;
+  }
+}
+
+template <int MODE, bool MGS>
+__global__ void __launch_bounds__(kRedThreads, kRedBlocks / 148) k_red_partial(
     const double* __restrict__ h_prev, const double* __restrict__ vprev, double* x,
-    const double* __restrict__ y, int64_t n, double* __restrict__ part) {
+    const double* __restrict__ y, int64_t n, double* __restrict__ part, unsigned* ticket,
+    double* __restrict__ out, int sqrt_out) {
   constexpr bool AXPY = MODE >= 2, SQ = MODE == 1 || MODE == 3;
   const double a = AXPY ? -1.0 * __ldg(h_prev) : 0.0;
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
@@ -53,42 +113,49 @@ __global__ void __launch_bounds__(kRedThreads) k_red_partial(
   double2* x2 = reinterpret_cast<double2*>(x);
   const double2* y2 = reinterpret_cast<const double2*>(y);
   const double2* p2 = reinterpret_cast<const double2*>(vprev);
+  const uint64_t keep = MGS ? l2_policy_last() : 0, drop = MGS ? l2_policy_first() : 0;
   auto step = [&](int64_t k, double& s0, double& s1) {
-    double2 xv = x2[k];
+    double2 xv = MGS ? ld2_hint(x2 + k, keep) : x2[k];
     if constexpr (AXPY) {
-      const double2 pv = __ldg(p2 + k);
+      const double2 pv = MGS ? ld2_nc_hint(p2 + k, drop) : __ldg(p2 + k);
       xv.x = fma(a, pv.x, xv.x);
       xv.y = fma(a, pv.y, xv.y);
-      x2[k] = xv;
+      if (MGS)
+        st2_hint(x2 + k, xv, keep);
+      else
+        x2[k] = xv;
     }
-    const double2 yv = SQ ? xv : __ldg(y2 + k);
+    const double2 yv = SQ ? xv : (MGS ? ld2_nc_hint(y2 + k, drop) : __ldg(y2 + k));
     s0 = fma(xv.x, yv.x, s0);
     s1 = fma(xv.y, yv.y, s1);
   };
-  int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
-  for (; k + stride < n2; k += 2 * stride) {
+  // pair m of this thread accumulates into (acc0, acc1) for even m and
+  // (acc2, acc3) for odd m; one pair per iteration with the two sets
+  // swapped after each keeps 8 CTAs/SM resident (32 registers).  The sets
+  // end up exchanged when the pair count is odd, which the final sum of
+  // the two sets does not see (a + b == b + a).
+  bool swapped = false;
+#pragma unroll 1
+  for (int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; k < n2; k += stride) {
     step(k, acc0, acc1);
-    step(k + stride, acc2, acc3);
+    const double t0 = acc0, t1 = acc1;
+    acc0 = acc2;
+    acc1 = acc3;
+    acc2 = t0;
+    acc3 = t1;
+    swapped = !swapped;
   }
-  if (k < n2) step(k, acc0, acc1);
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element -> even set
     double xv = x[n - 1];
     if constexpr (AXPY) {
       xv = fma(a, __ldg(vprev + n - 1), xv);
       x[n - 1] = xv;
     }
-    acc0 = fma(xv, SQ ? xv : __ldg(y + n - 1), acc0);
+    double& e0 = swapped ? acc2 : acc0;
+    e0 = fma(xv, SQ ? xv : __ldg(y + n - 1), e0);
   }
   const double s = block_sum((acc0 + acc1) + (acc2 + acc3));
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(kRedThreads) k_sum_final(const double* __restrict__ part, int np,
-                                                           double* __restrict__ out, int sqrt_out) {
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < np; i += kRedThreads) acc += part[i];
-  const double s = block_sum(acc);
-  if (threadIdx.x == 0) *out = sqrt_out ? sqrt(s) : s;
+  finish_sum(s, part, ticket, out, sqrt_out);
 }
 
 // species totals (fespace.py:170-174): int u_s = scale * sum_e detJ_e U[e,s,0].
@@ -202,26 +269,28 @@ cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part, double* out,
                        bool norm, cudaStream_t st) {
   double* xm = const_cast<double*>(x);
+  unsigned* ticket = red_ticket(part);
   if (norm)
-    k_red_partial<1><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, x, n, part);
+    k_red_partial<1, false><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, x, n, part,
+                                                                ticket, out, 1);
   else
-    k_red_partial<0><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, y, n, part);
-  k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, out, norm ? 1 : 0);
+    k_red_partial<0, false><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, y, n, part,
+                                                                ticket, out, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n, double* h,
                        double* part, cudaStream_t st) {
   // h[0] = w . V_0;  h[i] = (w -= h[i-1] V_{i-1}) . V_i;  h[j+1] = ||w -= h[j] V_j||
-  k_red_partial<0><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, w, V, n, part);
-  k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h, 0);
-  for (int i = 1; i <= j; ++i) {
-    k_red_partial<2><<<kRedBlocks, kRedThreads, 0, st>>>(h + i - 1, V + (i - 1) * ldv, w,
-                                                         V + i * ldv, n, part);
-    k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h + i, 0);
-  }
-  k_red_partial<3><<<kRedBlocks, kRedThreads, 0, st>>>(h + j, V + j * ldv, w, w, n, part);
-  k_sum_final<<<1, kRedThreads, 0, st>>>(part, kRedBlocks, h + j + 1, 1);
+  // (chaining the passes with programmatic dependent launch measured slower)
+  unsigned* ticket = red_ticket(part);
+  k_red_partial<0, true><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, w, V, n, part,
+                                                             ticket, h, 0);
+  for (int i = 1; i <= j; ++i)
+    k_red_partial<2, true><<<kRedBlocks, kRedThreads, 0, st>>>(
+        h + i - 1, V + (i - 1) * ldv, w, V + i * ldv, n, part, ticket, h + i, 0);
+  k_red_partial<3, true><<<kRedBlocks, kRedThreads, 0, st>>>(h + j, V + j * ldv, w, w, n, part,
+                                                             ticket, h + j + 1, 1);
   return cudaGetLastError();
 }
 

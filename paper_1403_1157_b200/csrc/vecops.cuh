@@ -5,6 +5,12 @@
 namespace tdg {
 constexpr int kRedBlocks = 1184;  // 8 CTAs per SM on 148 SMs; fixed => deterministic
 constexpr int kMaxTotS = 8;      // species of the totals reduction
+// reduction workspace: kRedBlocks*kMaxTotS partials, then the zeroed
+// ticket counter of the one-launch reductions
+constexpr size_t kRedWorkBytes = (size_t(kRedBlocks) * kMaxTotS + 2) * sizeof(double);
+inline unsigned* red_ticket(double* part) {
+  return reinterpret_cast<unsigned*>(part + size_t(kRedBlocks) * kMaxTotS);
+}
 cudaError_t launch_l2(const double* U, const double* V, const double* egeo, int64_t ne, int S,
                       int nb, int neg, double* part, double* out, cudaStream_t st);
 cudaError_t launch_totals(const double* U, const double* egeo, int64_t ne, int S, int nb, int neg,
