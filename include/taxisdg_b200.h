@@ -215,6 +215,22 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
 TDG_API int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w, int64_t n,
                     double* h, void* stream);
 
+/* GMRES basis vector (reference timeint.py:165,176: V[j+1] = w / hnext):
+ * v = w / hnext (host scalar) with ||v|| written to the DEVICE scalar
+ * norm_out in the same pass (same reduction tree as tdg_norm2, so bitwise
+ * its result); the next Jacobian-free product needs that norm. */
+TDG_API int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, double* v, int64_t n,
+                           double* norm_out, void* stream);
+
+/* Jacobian-free directional difference of newton_solve's jv (reference
+ * timeint.py:259-264): tdg_jv_shift computes eps = cnum / max(vnorm[0],
+ * 1e-300) on the device (cnum = sqrt(eps_mach)(1 + ||U||), vnorm a DEVICE
+ * scalar), writes it to eps_out and forms Up = U + eps v in one pass;
+ * tdg_jv_diff then forms r = (r - GU) / eps in place after r = G(Up). */
+TDG_API int tdg_jv_shift(const double* U, const double* v, const double* vnorm, double cnum,
+                         double* Up, double* eps_out, int64_t n, void* stream);
+TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t n, void* stream);
+
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
  * CTA-staged generic kernels; bit 1: use the four-lanes-per-element
  * volume kernel instead of the one-thread-per-element one; bit 2: run

@@ -70,6 +70,9 @@ def load(path: str = LIB):
     lib.tdg_norm2.argtypes = [_p, _p, _i64, _p, _p]
     lib.tdg_axpby.argtypes = [_d, _p, _d, _p, _i64, _p]
     lib.tdg_axpy_dev.argtypes = [_d, _p, _p, _p, _i64, _p]
+    lib.tdg_scale_norm.argtypes = [_p, _p, _d, _p, _i64, _p, _p]
+    lib.tdg_jv_shift.argtypes = [_p, _p, _p, _d, _p, _p, _i64, _p]
+    lib.tdg_jv_diff.argtypes = [_p, _p, _p, _i64, _p]
     lib.tdg_profile.argtypes = [_p, ctypes.c_int]
     lib.tdg_set_variant.argtypes = [_p, ctypes.c_int]
     lib.tdg_profile_read.argtypes = [_p, ctypes.POINTER(_d), ctypes.POINTER(_i64)]
@@ -79,7 +82,7 @@ def load(path: str = LIB):
     for name in ("tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
-                 "tdg_axpy_dev"):
+                 "tdg_axpy_dev", "tdg_scale_norm", "tdg_jv_shift", "tdg_jv_diff"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.tdg_version() != ABI_VERSION:
         raise ImportError("libtaxisdg_b200.so ABI version mismatch; rebuild")

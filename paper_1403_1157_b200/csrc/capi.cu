@@ -334,6 +334,30 @@ int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result, void* st
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "norm2");
 }
 
+int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, double* v, int64_t n,
+                   double* norm_out, void* stream) {
+  if (!ctx || !w || !v || !norm_out) return fail(TDG_E_INVALID, "null argument");
+  if (!aligned16(w) || !aligned16(v))
+    return fail(TDG_E_INVALID, "scale_norm operands must be 16-byte aligned");
+  cudaError_t e = launch_scale_norm(w, hnext, v, n, ctx->part, norm_out,
+                                    static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "scale_norm");
+}
+
+int tdg_jv_shift(const double* U, const double* v, const double* vnorm, double cnum, double* Up,
+                 double* eps_out, int64_t n, void* stream) {
+  if (!U || !v || !vnorm || !Up || !eps_out) return fail(TDG_E_INVALID, "null argument");
+  cudaError_t e = launch_jv_shift(U, v, vnorm, cnum, Up, eps_out, n,
+                                  static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "jv_shift");
+}
+
+int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t n, void* stream) {
+  if (!r || !GU || !eps) return fail(TDG_E_INVALID, "null argument");
+  cudaError_t e = launch_jv_diff(r, GU, eps, n, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "jv_diff");
+}
+
 int tdg_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream) {
   if (!x || !y) return fail(TDG_E_INVALID, "null argument");
   cudaError_t e = launch_axpby(a, x, b, y, n, static_cast<cudaStream_t>(stream));

@@ -104,8 +104,8 @@ template <int MODE, bool MGS>
 __global__ void __launch_bounds__(kRedThreads, kRedBlocks / 148) k_red_partial(
     const double* __restrict__ h_prev, const double* __restrict__ vprev, double* x,
     const double* __restrict__ y, int64_t n, double* __restrict__ part, unsigned* ticket,
-    double* __restrict__ out, int sqrt_out) {
-  constexpr bool AXPY = MODE >= 2, SQ = MODE == 1 || MODE == 3;
+    double* __restrict__ out, int sqrt_out, double sc) {
+  constexpr bool AXPY = MODE == 2 || MODE == 3, SQ = MODE == 1 || MODE == 3 || MODE == 4;
   const double a = AXPY ? -1.0 * __ldg(h_prev) : 0.0;
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
   const int64_t n2 = n >> 1;
@@ -115,7 +115,15 @@ __global__ void __launch_bounds__(kRedThreads, kRedBlocks / 148) k_red_partial(
   const double2* p2 = reinterpret_cast<const double2*>(vprev);
   const uint64_t keep = MGS ? l2_policy_last() : 0, drop = MGS ? l2_policy_first() : 0;
   auto step = [&](int64_t k, double& s0, double& s1) {
-    double2 xv = MGS ? ld2_hint(x2 + k, keep) : x2[k];
+    double2 xv;
+    if constexpr (MODE == 4) {  // x = y / sc (GMRES basis vector), then its norm
+      const double2 yv = __ldg(y2 + k);
+      xv.x = yv.x / sc;
+      xv.y = yv.y / sc;
+      x2[k] = xv;
+    } else {
+      xv = MGS ? ld2_hint(x2 + k, keep) : x2[k];
+    }
     if constexpr (AXPY) {
       const double2 pv = MGS ? ld2_nc_hint(p2 + k, drop) : __ldg(p2 + k);
       xv.x = fma(a, pv.x, xv.x);
@@ -147,6 +155,10 @@ __global__ void __launch_bounds__(kRedThreads, kRedBlocks / 148) k_red_partial(
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element -> even set
     double xv = x[n - 1];
+    if constexpr (MODE == 4) {
+      xv = __ldg(y + n - 1) / sc;
+      x[n - 1] = xv;
+    }
     if constexpr (AXPY) {
       xv = fma(a, __ldg(vprev + n - 1), xv);
       x[n - 1] = xv;
@@ -272,10 +284,10 @@ cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part
   unsigned* ticket = red_ticket(part);
   if (norm)
     k_red_partial<1, false><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, x, n, part,
-                                                                ticket, out, 1);
+                                                                ticket, out, 1, 0.0);
   else
     k_red_partial<0, false><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, xm, y, n, part,
-                                                                ticket, out, 0);
+                                                                ticket, out, 0, 0.0);
   return cudaGetLastError();
 }
 
@@ -285,12 +297,54 @@ cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n
   // (chaining the passes with programmatic dependent launch measured slower)
   unsigned* ticket = red_ticket(part);
   k_red_partial<0, true><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, w, V, n, part,
-                                                             ticket, h, 0);
+                                                             ticket, h, 0, 0.0);
   for (int i = 1; i <= j; ++i)
     k_red_partial<2, true><<<kRedBlocks, kRedThreads, 0, st>>>(
-        h + i - 1, V + (i - 1) * ldv, w, V + i * ldv, n, part, ticket, h + i, 0);
+        h + i - 1, V + (i - 1) * ldv, w, V + i * ldv, n, part, ticket, h + i, 0, 0.0);
   k_red_partial<3, true><<<kRedBlocks, kRedThreads, 0, st>>>(h + j, V + j * ldv, w, w, n, part,
-                                                             ticket, h + j + 1, 1);
+                                                             ticket, h + j + 1, 1, 0.0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_norm(const double* w, double hnext, double* v, int64_t n, double* part,
+                              double* norm_out, cudaStream_t st) {
+  k_red_partial<4, false><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, v, w, n, part,
+                                                              red_ticket(part), norm_out, 1, hnext);
+  return cudaGetLastError();
+}
+
+// Jacobian-free product pieces (reference timeint.py:259-264):
+// eps = sqrt(eps_mach)(1 + ||U||) / ||v|| with ||v|| a device scalar
+// (clamped at 1e-300: v = 0 then gives U + 0 and a zero quotient, the
+// reference's early return), Up = U + eps v in one pass; then
+// r = (r - GU) / eps in place.
+__global__ void k_jv_shift(const double* __restrict__ U, const double* __restrict__ v,
+                           const double* __restrict__ vnorm, double cnum, double* __restrict__ Up,
+                           double* __restrict__ eps_out, int64_t n) {
+  const double eps = cnum / fmax(__ldg(vnorm), 1e-300);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *eps_out = eps;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    Up[i] = fma(eps, v[i], U[i]);
+}
+
+__global__ void k_jv_diff(double* __restrict__ r, const double* __restrict__ GU,
+                          const double* __restrict__ eps, int64_t n) {
+  const double e = __ldg(eps);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    r[i] = (r[i] - GU[i]) / e;
+}
+
+cudaError_t launch_jv_shift(const double* U, const double* v, const double* vnorm, double cnum,
+                            double* Up, double* eps_out, int64_t n, cudaStream_t st) {
+  if (n > 0) k_jv_shift<<<grid_for(n, 256), 256, 0, st>>>(U, v, vnorm, cnum, Up, eps_out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_jv_diff(double* r, const double* GU, const double* eps, int64_t n,
+                           cudaStream_t st) {
+  if (n > 0) k_jv_diff<<<grid_for(n, 256), 256, 0, st>>>(r, GU, eps, n);
   return cudaGetLastError();
 }
 

@@ -350,6 +350,42 @@ class DiscreteOperator:
                                        n, h.data_ptr(), self._stream()), "tdg_mgs")
         return h
 
+    def scale_norm(self, w, hnext: float, v, norm_out):
+        """v = w / hnext (GMRES basis vector, reference ``timeint.py:165,176``)
+        and ||v|| into the device scalar ``norm_out``, one pass."""
+        w, v = w.reshape(-1), v.reshape(-1)
+        self._check_vec("w", w)
+        self._check_vec("v", v)
+        if w.numel() != v.numel():
+            raise ValueError("w and v differ in size")
+        _native.check(self.lib.tdg_scale_norm(self._ctx, w.data_ptr(), float(hnext), v.data_ptr(),
+                                              w.numel(), norm_out.data_ptr(), self._stream()),
+                      "tdg_scale_norm")
+        return v
+
+    def jv_shift(self, U, v, vnorm, cnum: float, Up, eps_out):
+        """eps = cnum / max(||v||, 1e-300) (device), Up = U + eps v
+        (reference ``timeint.py:259-264``)."""
+        n = U.numel()
+        for name, x in (("U", U), ("v", v), ("Up", Up)):
+            self._check_vec(name, x.reshape(-1))
+        if v.numel() != n or Up.numel() != n:
+            raise ValueError("jv_shift: size mismatch")
+        _native.check(self.lib.tdg_jv_shift(U.data_ptr(), v.data_ptr(), vnorm.data_ptr(),
+                                            float(cnum), Up.data_ptr(), eps_out.data_ptr(), n,
+                                            self._stream()), "tdg_jv_shift")
+        return Up
+
+    def jv_diff(self, r, GU, eps):
+        """r = (r - GU) / eps in place (device eps)."""
+        self._check_vec("r", r.reshape(-1))
+        self._check_vec("GU", GU.reshape(-1))
+        if r.numel() != GU.numel():
+            raise ValueError("jv_diff: size mismatch")
+        _native.check(self.lib.tdg_jv_diff(r.data_ptr(), GU.data_ptr(), eps.data_ptr(), r.numel(),
+                                           self._stream()), "tdg_jv_diff")
+        return r
+
     def dot(self, x, y, out=None):
         x, y = x.reshape(-1), y.reshape(-1)
         self._check_vec("x", x)

@@ -513,6 +513,39 @@ def test_fused_mgs_is_bitwise_the_dot_axpy_sequence():
         op.dot(x[1:], y[1:])
 
 
+@pytest.mark.parametrize("n", [100_002, 100_003])
+def test_fused_jfnk_vector_kernels_are_bitwise_the_unfused_sequence(n):
+    """tdg_scale_norm == (w / hnext, tdg_norm2); tdg_jv_shift + tdg_jv_diff
+    == the torch / tdg_axpy_dev sequence of newton_solve's jv (reference
+    timeint.py:165,176,259-264), bit for bit; v = 0 gives a zero product."""
+    import math
+    space = DGSpace(unit_square(8, 4), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    g = torch.Generator(device="cuda").manual_seed(11)
+    w = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    v, nrm = torch.empty_like(w), torch.zeros(1, dtype=torch.float64, device="cuda")
+    op.scale_norm(w, 3.7, v, nrm)
+    # true division, as numpy's w / hnext (torch divides by a Python
+    # scalar through its reciprocal)
+    assert torch.equal(v.cpu(), torch.from_numpy(w.cpu().numpy() / 3.7))
+    assert torch.equal(nrm, op.norm2(v, torch.zeros(1, dtype=torch.float64, device="cuda")))
+    U = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    r0 = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    GU = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    cnum = math.sqrt(2.0 ** -52) * (1.0 + 12.5)
+    for vv in (v, torch.zeros_like(v)):
+        vn = op.norm2(vv, torch.zeros(1, dtype=torch.float64, device="cuda"))
+        eps_ref = cnum / torch.clamp(vn, min=1e-300)
+        Up_ref = U.clone()
+        op.axpy_dev(1.0, eps_ref, vv, Up_ref)
+        d_ref = r0.clone().sub_(GU).div_(eps_ref)
+        eps, Up = torch.zeros(1, dtype=torch.float64, device="cuda"), torch.empty_like(U)
+        op.jv_shift(U, vv, vn, cnum, Up, eps)
+        d = op.jv_diff(r0.clone(), GU, eps)
+        assert torch.equal(eps, eps_ref) and torch.equal(Up, Up_ref) and torch.equal(d, d_ref)
+    assert torch.equal(Up, U) and not torch.any(op.jv_diff(U.clone(), U, eps))
+
+
 def _tiny_meshes():
     from paper_1403_1157_b200.mesh import Mesh
     one = Mesh([[0.0, 0.0], [1.0, 0.0], [0.2, 0.9]], [[0, 1, 2]],
