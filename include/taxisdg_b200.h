@@ -216,11 +216,13 @@ TDG_API int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w
                     double* h, void* stream);
 
 /* GMRES basis vector (reference timeint.py:165,176: V[j+1] = w / hnext):
- * v = w / hnext (host scalar) with ||v|| written to the DEVICE scalar
- * norm_out in the same pass (same reduction tree as tdg_norm2, so bitwise
- * its result); the next Jacobian-free product needs that norm. */
-TDG_API int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, double* v, int64_t n,
-                           double* norm_out, void* stream);
+ * v = w / hnext with ||v|| written to the DEVICE scalar norm_out in the
+ * same pass (same reduction tree as tdg_norm2, so bitwise its result); the
+ * next Jacobian-free product needs that norm.  The divisor is the host
+ * scalar hnext, or the DEVICE scalar hnext_dev[0] when hnext_dev is not
+ * null (the Arnoldi step can then run ahead of the host). */
+TDG_API int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, const double* hnext_dev,
+                           double* v, int64_t n, double* norm_out, void* stream);
 
 /* Jacobian-free directional difference of newton_solve's jv (reference
  * timeint.py:259-264): tdg_jv_shift computes eps = cnum / max(vnorm[0],

@@ -70,7 +70,7 @@ def load(path: str = LIB):
     lib.tdg_norm2.argtypes = [_p, _p, _i64, _p, _p]
     lib.tdg_axpby.argtypes = [_d, _p, _d, _p, _i64, _p]
     lib.tdg_axpy_dev.argtypes = [_d, _p, _p, _p, _i64, _p]
-    lib.tdg_scale_norm.argtypes = [_p, _p, _d, _p, _i64, _p, _p]
+    lib.tdg_scale_norm.argtypes = [_p, _p, _d, _p, _p, _i64, _p, _p]
     lib.tdg_jv_shift.argtypes = [_p, _p, _p, _d, _p, _p, _i64, _p]
     lib.tdg_jv_diff.argtypes = [_p, _p, _p, _i64, _p]
     lib.tdg_profile.argtypes = [_p, ctypes.c_int]

@@ -334,12 +334,12 @@ int tdg_norm2(tdg_ctx* ctx, const double* x, int64_t n, double* result, void* st
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "norm2");
 }
 
-int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, double* v, int64_t n,
-                   double* norm_out, void* stream) {
+int tdg_scale_norm(tdg_ctx* ctx, const double* w, double hnext, const double* hnext_dev,
+                   double* v, int64_t n, double* norm_out, void* stream) {
   if (!ctx || !w || !v || !norm_out) return fail(TDG_E_INVALID, "null argument");
   if (!aligned16(w) || !aligned16(v))
     return fail(TDG_E_INVALID, "scale_norm operands must be 16-byte aligned");
-  cudaError_t e = launch_scale_norm(w, hnext, v, n, ctx->part, norm_out,
+  cudaError_t e = launch_scale_norm(w, hnext, hnext_dev, v, n, ctx->part, norm_out,
                                     static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "scale_norm");
 }

@@ -350,17 +350,23 @@ class DiscreteOperator:
                                        n, h.data_ptr(), self._stream()), "tdg_mgs")
         return h
 
-    def scale_norm(self, w, hnext: float, v, norm_out):
+    def scale_norm(self, w, hnext, v, norm_out):
         """v = w / hnext (GMRES basis vector, reference ``timeint.py:165,176``)
-        and ||v|| into the device scalar ``norm_out``, one pass."""
+        and ||v|| into the device scalar ``norm_out``, one pass; ``hnext`` a
+        float or a one-element CUDA tensor (device divisor)."""
+        torch = _torch()
+        dev_div = isinstance(hnext, torch.Tensor)
+        if dev_div:
+            self._check_vec("hnext", hnext)
         w, v = w.reshape(-1), v.reshape(-1)
         self._check_vec("w", w)
         self._check_vec("v", v)
         if w.numel() != v.numel():
             raise ValueError("w and v differ in size")
-        _native.check(self.lib.tdg_scale_norm(self._ctx, w.data_ptr(), float(hnext), v.data_ptr(),
-                                              w.numel(), norm_out.data_ptr(), self._stream()),
-                      "tdg_scale_norm")
+        _native.check(self.lib.tdg_scale_norm(
+            self._ctx, w.data_ptr(), 0.0 if dev_div else float(hnext),
+            hnext.data_ptr() if dev_div else None, v.data_ptr(), w.numel(), norm_out.data_ptr(),
+            self._stream()), "tdg_scale_norm")
         return v
 
     def jv_shift(self, U, v, vnorm, cnum: float, Up, eps_out):

@@ -529,6 +529,9 @@ def test_fused_jfnk_vector_kernels_are_bitwise_the_unfused_sequence(n):
     # scalar through its reciprocal)
     assert torch.equal(v.cpu(), torch.from_numpy(w.cpu().numpy() / 3.7))
     assert torch.equal(nrm, op.norm2(v, torch.zeros(1, dtype=torch.float64, device="cuda")))
+    v2, nrm2 = torch.empty_like(w), torch.zeros(1, dtype=torch.float64, device="cuda")
+    op.scale_norm(w, torch.full((1,), 3.7, dtype=torch.float64, device="cuda"), v2, nrm2)
+    assert torch.equal(v2, v) and torch.equal(nrm2, nrm)            # device divisor
     U = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
     r0 = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
     GU = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
