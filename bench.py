@@ -157,14 +157,36 @@ def weak_config(cfg, world):
     return dataclasses.replace(cfg, cells=cells, lengths=lengths, description=desc)
 
 
-def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, device=None):
+def sample_config(cfg, max_dofs=5_000_000):
+    """The CPU baseline's bounded sample: an x-slab of the config with the
+    same cell size, order and physics, cut to about ``max_dofs`` DoFs (the
+    config itself when it is smaller)."""
+    import dataclasses
+    from paper_1403_1157_b200.basis import basis_size
+    per_cell = (2 if cfg.dim == 2 else 6) * 6 * basis_size(cfg.dim, cfg.order)
+    cells, lengths = list(cfg.cells), list(cfg.lengths)
+    for ax in range(cfg.dim - 1):       # shrink x first, then y (3D), same cell size
+        rest = int(np.prod(cells)) // cells[ax]
+        c = max(1, min(cells[ax], max_dofs // (per_cell * rest)))
+        lengths[ax] *= c / cells[ax]
+        cells[ax] = c
+    if tuple(cells) == tuple(cfg.cells):
+        return cfg
+    return dataclasses.replace(cfg, cells=tuple(cells), lengths=tuple(lengths))
+
+
+def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, device=None,
+                  cpu_sample=False):
     """(cfg, space, model, scheme, U0, slab); the slab is None at N=1
-    unless ``force_slab``."""
+    unless ``force_slab``; ``cpu_sample``: the CPU baseline's bounded
+    x-slab of the config (sample_config)."""
     from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
     from paper_1403_1157_b200.configs import CONFIGS, make_mesh
     from paper_1403_1157_b200.decomp import build_slab
     from paper_1403_1157_b200.fields import bump_field
     cfg = weak_config(CONFIGS[cfg_name], world)
+    if cpu_sample:
+        cfg = sample_config(cfg)
     slab = None
     if world == 1 and not force_slab:
         mesh = make_mesh(cfg)
@@ -244,7 +266,7 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
     """Time the CPU oracle port on the same config; returns (DoF-upd/s,
     sample description, n_dofs)."""
     from oracle import OracleOperator
-    cfg, space, model, scheme, U0, _ = build_problem(cfg_name, scheme_name)
+    cfg, space, model, scheme, U0, _ = build_problem(cfg_name, scheme_name, cpu_sample=True)
     op = OracleOperator(space, model, scheme, nthreads=nthreads)
     if dt is None:
         from paper_1403_1157_b200.configs import rho_constant
@@ -263,7 +285,7 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
     for _ in range(steps):
         U = step(U)
     el = time.perf_counter() - tic
-    return space.n_dofs * 3 * steps / el, el, space.n_dofs
+    return space.n_dofs * 3 * steps / el, el, cfg.cells, space.n_dofs
 
 
 # ---------------------------------------------------------------- arms
@@ -274,7 +296,13 @@ def run_reference_arm(args, rank):
     nthreads = os.cpu_count() or 1
     steps = max(1, args.steps)
     warm = max(0, min(args.warmup, 1))
-    val, el, ndofs = cpu_reference(args.config, args.scheme, steps, warm, nthreads)
+    val, el, cells, ndofs = cpu_reference(args.config, args.scheme, steps, warm, nthreads)
+    full = tuple(weak_config(__import__("paper_1403_1157_b200.configs", fromlist=["CONFIGS"])
+                             .CONFIGS[args.config], 1).cells)
+    where = ("one full " + args.config + "-sized mesh (= one rank's weak-scaling slab)"
+             if tuple(cells) == full else
+             "a " + "x".join(map(str, cells)) + "-cell x-slab of the " + args.config
+             + " mesh (same cells, order, physics; bounded CPU sample)")
     from paper_1403_1157_b200.configs import CONFIGS
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
@@ -287,8 +315,7 @@ def run_reference_arm(args, rank):
                    "n_dofs": ndofs},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthreads,
                          "kind": "port",
-                         "sample": f"{steps} SSP-RK3 steps of one full {args.config}-sized "
-                                   "mesh (= one rank's weak-scaling slab), numpy oracle "
+                         "sample": f"{steps} SSP-RK3 steps of {where}, numpy oracle "
                                    f"port of the reference (oracle/), {nthreads} threads"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -334,6 +361,7 @@ def run_native_arm(args, rank, world, local):
                        tc_volume=bool(args.variant & 4096),
                        no_tc_faces=bool(args.variant & 8192),
                        volume_first=bool(args.variant & 16384),
+                       face_rows_tc=bool(args.variant & 32768),
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb
@@ -543,9 +571,12 @@ def run_native_arm(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nthreads = os.cpu_count() or 1
-        val, el, _ = cpu_reference(args.config, args.scheme, 1, 0, nthreads, dt=dt)
+        val, el, cells, _ = cpu_reference(args.config, args.scheme, 1, 0, nthreads, dt=dt)
+        where = (f"the full {args.config} mesh" if tuple(cells) == tuple(cfg.cells) else
+                 "a " + "x".join(map(str, cells)) + f"-cell x-slab of the {args.config} mesh "
+                 "(same cells, order, physics; bounded CPU sample)")
         cpu = {"value": val, "unit": UNIT, "cores": nthreads, "kind": "port",
-               "sample": f"1 SSP-RK3 step (3 apply_f) of the full {args.config} mesh, "
+               "sample": f"1 SSP-RK3 step (3 apply_f) of {where}, "
                          f"numpy oracle port, {nthreads} threads, {el:.1f} s"}
 
     launches = sum(v["launches"] for v in per.values())

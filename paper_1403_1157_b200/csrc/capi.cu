@@ -389,8 +389,9 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
   ctx->force_tc = ((variant >> 12) & 1) != 0;
+  ctx->face_rows_tc = ((variant >> 15) & 1) != 0;  // bit 15: faces-as-rows TC face kernel (3D)
   ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)
-  ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first  // bit 12: transposed tensor-core volume everywhere
+  ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
   if (ctx->gexec) {  // kernel choice changed: re-capture
     cudaGraphExecDestroy(ctx->gexec);

@@ -55,6 +55,7 @@ struct tdg_ctx {
   bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
   bool no_tcf = false;
   bool faces_first = true;
+  bool face_rows_tc = false;  // 3D: faces-as-rows TC face kernel instead of species rows
   // host-pipelined stepping: element bands and the banded face order
   // (tables.build_tables), device state / stage buffers, copy streams
   int n_bands = 1;
@@ -104,6 +105,11 @@ int configure(int nqv) {
     e = cudaFuncSetAttribute(k_volume_mma<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(MmaVol<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure volume_mma");
+  }
+  if constexpr (TcsFace<D, K, M>::ok) {
+    e = cudaFuncSetAttribute(k_faces_tcs<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TcsFace<D, K, M>::smem()));
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcs");
   }
   if constexpr (TcFace<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_faces_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -280,12 +286,26 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
       const int64_t b1 = which == 1 ? nblk - ncb : nblk;
       if (b1 > b0) {
         KernelTimer kt(ctx, 0, st);
-        using T = TcFace<D, K, M>;
-        int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
-        const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 4;
-        grid = grid < cap ? grid : cap;
-        k_faces_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1, U,
-                                                                    ctx->fc);
+        bool done = false;
+        if constexpr (TcsFace<D, K, M>::ok) {
+          if (!ctx->face_rows_tc) {  // species rows, one face per warp (default)
+            using T = TcsFace<D, K, M>;
+            int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
+            const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 8;
+            grid = grid < cap ? grid : cap;
+            k_faces_tcs<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1,
+                                                                         U, ctx->fc);
+            done = true;
+          }
+        }
+        if (!done) {
+          using T = TcFace<D, K, M>;
+          int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
+          const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 4;
+          grid = grid < cap ? grid : cap;
+          k_faces_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1, U,
+                                                                      ctx->fc);
+        }
       }
       if (which != 2 && p.nbf > 0) {
         KernelTimer kt(ctx, 1, st);

@@ -327,4 +327,231 @@ k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restric
   }
 }
 
+// ---------------------------------------------------------------------
+// Interior faces on the FP64 tensor cores with the SPECIES as the M
+// dimension: a warp runs one face at a time (the faces of one block share
+// the trace-table signature), rows g = species, so everything per face --
+// Jinv n of both sides, the lifting weight, h -- is warp-uniform.  That
+// lets the normal derivatives fold into the B operand: the fragment of
+// dphi/dn = sum_a jn_a G_a is 3 FMAs per lane, replacing the D separate
+// DMMAs of the face-rows kernel above, and the coupled point physics reads
+// the traces of every species from one shared-memory transpose instead of
+// recomputing them (the face-rows kernel's pass A).  Same signature tables
+// (tables.tc_face_tables), same point-parity k-steps and mode permutation
+// pi(8nt + 2t + j) = 4(2nt + j) + t; with nb = 10, F = 35 (C4) a face takes
+// ~175 DMMAs instead of ~330.
+//
+//   pass 1 (point tiles qt): u_in, u_out, d_n u_in, d_n u_out for all
+//          species -> transpose xs[kind][q][s]; jumps -> modal lifting m
+//   physics: LLF wave speed / taxis flux normals once per point -> cv[q]
+//   pass 2 (point tiles qt): rho = m B, Y and X per (species, point),
+//          projection onto both sides' test functions (B and folded dphi/dn)
+template <int D, int K, class M>
+struct TcsFace {
+  using TF = TcFace<D, K, M>;
+  static constexpr int NB = TF::NB, S = M::S, SN = S * NB, F = TF::F, NFG = TF::NFG;
+  static constexpr int QP = TF::QP, QT = TF::QT, KT = TF::KT, NNT = TF::NNT, TS = TF::TS;
+  static constexpr int NCV = TF::NCV, XS = S | 1;
+  static constexpr int WARPS = 4;
+  static constexpr int PWS = 3 * QP * XS + QP * NCV + 1;  // per-warp scratch (doubles)
+  static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
+  static constexpr int MINB = 4;  // 128 registers (16 warps/SM): 3 -> 4 cut C4 faces 21.6 -> 18.6 ms; 5 spills
+  static constexpr bool ok = D == 3 && S <= 8 && !M::kMirror && TF::ok && smem() <= 96 * 1024;
+};
+
+template <int D, int K, class M>
+__global__ void __launch_bounds__(128, TcsFace<D, K, M>::MINB)
+k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
+            int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ FC) {
+  using T = TcsFace<D, K, M>;
+  using TF = TcFace<D, K, M>;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
+  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NNT = T::NNT, TS = T::TS;
+  constexpr int NCV = T::NCV, XS = T::XS;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const bool row = g < S;  // this lane's species row is real
+  const int sp = row ? g : 0;
+  double* xs = sm + warp * T::PWS;  // [3][QP][XS]: u_in, u_out, avg d_n u
+  double* cv = xs + 3 * QP * XS;    // [QP][NCV]
+  const double As = p.A[sp];
+
+  for (int64_t blk = blk0 + int64_t(blockIdx.x) * T::WARPS + warp; blk < blk1;
+       blk += int64_t(gridDim.x) * T::WARPS) {
+    const int2 bd = __ldg(reinterpret_cast<const int2*>(blocks) + blk);
+#pragma unroll 1
+    for (int fi = 0; fi < bd.y; ++fi) {
+      const int64_t f = int64_t(bd.x) + fi;
+      const int code = __ldg(p.ifcode + f);
+      const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
+      const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
+      const double* gg = p.ifgeo + f * NFG;
+      double jn[2][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        jn[0][a] = __ldg(gg + a);
+        jn[1][a] = __ldg(gg + D + a);
+      }
+      const double sfac = __ldg(gg + 2 * D), h = __ldg(gg + 2 * D + 1);
+      const double idi = __ldg(gg + 2 * D + 2), ido = __ldg(gg + 2 * D + 3);
+      const int sig = code & 1023;
+      const double* Ti = tabs + size_t(sig & 31) * TS;
+      const double* To = tabs + size_t((sig >> 5) & 31) * TS;
+      // A operands: this face's coefficients, row = species g, k = 4 kt + t
+      double ci[KT], co[KT];
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const bool in = row && 4 * kt + t < NB;
+        ci[kt] = in ? __ldg(U + int64_t(el.x) * SN + g * NB + 4 * kt + t) : 0.0;
+        co[kt] = in ? __ldg(U + int64_t(el.y) * SN + g * NB + 4 * kt + t) : 0.0;
+      }
+      const bool br2 = p.scheme == BR2;
+      const bool lift = p.scheme != IP && p.scheme != BO;
+      const bool use_in = lift && (br2 || code_minus_in(code));
+      const bool use_out = lift && (br2 || !code_minus_in(code));
+
+      // ---- pass 1: traces, transpose, jumps -> modal lifting -------------
+      double mi[NNT][2], mo[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) mi[nt][0] = mi[nt][1] = mo[nt][0] = mo[nt][1] = 0.0;
+#pragma unroll 1
+      for (int qt = 0; qt < QT; ++qt) {
+        double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0}, di[2] = {0.0, 0.0}, dq[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int ob = (kt * QT + qt) * 32 + lane;
+          dmma(ui[0], ui[1], ci[kt], __ldg(Ti + TF::OBT + ob));
+          dmma(uo[0], uo[1], co[kt], __ldg(To + TF::OBT + ob));
+          double gi = 0.0, go = 0.0;  // dphi/dn fragments (jn folded in)
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const int og = ((a * KT + kt) * QT + qt) * 32 + lane;
+            gi = fma(jn[0][a], __ldg(Ti + TF::OGT + og), gi);
+            go = fma(jn[1][a], __ldg(To + TF::OGT + og), go);
+          }
+          dmma(di[0], di[1], ci[kt], gi);
+          dmma(dq[0], dq[1], co[kt], go);
+        }
+        double du[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 8 * qt + 2 * t + j;
+          du[j] = ui[j] - uo[j];
+          if (row) {
+            xs[(0 * QP + q) * XS + g] = ui[j];
+            xs[(1 * QP + q) * XS + g] = uo[j];
+            xs[(2 * QP + q) * XS + g] = 0.5 * (di[j] + dq[j]);
+          }
+        }
+        if (lift) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < NNT; ++nt) {
+              const int ow = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
+              if (use_in) dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + TF::OWB + ow));
+              if (use_out) dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + TF::OWB + ow));
+            }
+        }
+      }
+      // lifting weights (operator.py:336-357): -fac A rho, rho = -1/2 sfac/detJ Pw dU
+      {
+        const double wside = br2 ? 0.5 : 1.0;
+        const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac * As;
+        const double ki = use_in ? fac0 * idi : 0.0, ko = use_out ? fac0 * ido : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            mi[nt][j] *= ki;
+            mo[nt][j] *= ko;
+          }
+      }
+      __syncwarp();
+      // ---- coupled point physics, once per face point ---------------------
+      if constexpr (M::kConv) {
+        for (int q = lane; q < F; q += 32) {
+          const double* xq = xs + q * XS;
+          auto fetch = [xq](int kind, int s2) { return xq[kind * QP * XS + s2]; };
+          M::face_point(p.P, fetch, cv + q * NCV);
+        }
+        __syncwarp();
+      }
+      // ---- pass 2: rho, flux, projection ---------------------------------
+      double ri[NNT][2], ro[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) ri[nt][0] = ri[nt][1] = ro[nt][0] = ro[nt][1] = 0.0;
+#pragma unroll 1
+      for (int qt = 0; qt < QT; ++qt) {
+        double rho[2] = {0.0, 0.0};
+        if (lift) {
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const int ob = (kt * QT + qt) * 32 + lane;
+            // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
+            if (use_in) dmma(rho[0], rho[1], mi[kt / 2][kt % 2], __ldg(Ti + TF::OBT + ob));
+            if (use_out) dmma(rho[0], rho[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
+          }
+        }
+        double Y[2], X[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 8 * qt + 2 * t + j;
+          const double du = xs[q * XS + sp] - xs[(QP + q) * XS + sp];
+          const double gav = xs[(2 * QP + q) * XS + sp];
+          double qv = rho[j];
+          if (p.scheme == IP) qv = p.eta / h * As * du;
+          if constexpr (M::kConv) {
+            if (q < F) {
+              double cnv = 0.5 * cv[q * NCV] * du;
+#pragma unroll
+              for (int k = 0; k < M::NFX; ++k)
+                if (g == k) cnv = fma(0.5, cv[q * NCV + 1 + k], cnv);
+              qv += cnv;
+            }
+          }
+          const double wq = (q < F && row) ? __ldg(p.fw + q) * sfac : 0.0;
+          Y[j] = wq * (As * gav - qv);
+          X[j] = wq * 0.5 * p.adj * As * du;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int nt = 0; nt < NNT; ++nt) {
+            const int ob = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
+            double gi = 0.0, go = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              const int og = (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane;
+              gi = fma(jn[0][a], __ldg(Ti + TF::OGP + og), gi);
+              go = fma(jn[1][a], __ldg(To + TF::OGP + og), go);
+            }
+            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + TF::OBP + ob));
+            dmma(ri[nt][0], ri[nt][1], X[ks], gi);
+            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + TF::OBP + ob));
+            dmma(ro[nt][0], ro[nt][1], X[ks], go);
+          }
+      }
+      // face-slot rows: lane entries (species g, basis 4 (2nt + j) + t)
+      const bool skip_out = code_skip_out(code);
+      if (row) {
+        double* fci = FC + (int64_t(lf.x) * p.ne + el.x) * SN + g * NB;
+        double* fco = FC + (int64_t(lf.y) * p.ne + el.y) * SN + g * NB;
+#pragma unroll
+        for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = 4 * (2 * nt + j) + t;
+            if (i < NB) {
+              fci[i] = ri[nt][j];
+              if (!skip_out) fco[i] = ro[nt][j];
+            }
+          }
+      }
+      __syncwarp();  // xs / cv are rewritten by the next face
+    }
+  }
+}
+
 }  // namespace tdg
