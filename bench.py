@@ -362,6 +362,7 @@ def run_native_arm(args, rank, world, local):
                        no_tc_faces=bool(args.variant & 8192),
                        volume_first=bool(args.variant & 16384),
                        face_rows_tc=bool(args.variant & 32768),
+                       one_copy_stream=bool(args.variant & 65536),
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb

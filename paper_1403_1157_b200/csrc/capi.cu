@@ -178,6 +178,8 @@ int tdg_destroy(tdg_ctx* ctx) {
   cudaFree(ctx->hs_buf);
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  if (ctx->s_h2d2) cudaStreamDestroy(ctx->s_h2d2);
+  if (ctx->s_d2h2) cudaStreamDestroy(ctx->s_d2h2);
   for (auto s : ctx->hs_st)
     if (s) cudaStreamDestroy(s);
   if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
@@ -389,7 +391,8 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->flip_mma = ((variant >> 3) & 1) != 0;
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
   ctx->force_tc = ((variant >> 12) & 1) != 0;
-  ctx->face_rows_tc = ((variant >> 15) & 1) != 0;  // bit 15: faces-as-rows TC face kernel (3D)
+  ctx->face_rows_tc = ((variant >> 15) & 1) != 0;
+  ctx->one_copy_stream = ((variant >> 16) & 1) != 0;  // bit 16: host steps on one copy stream per direction  // bit 15: faces-as-rows TC face kernel (3D)
   ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)
   ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3

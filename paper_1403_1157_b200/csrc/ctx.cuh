@@ -62,7 +62,8 @@ struct tdg_ctx {
   std::vector<int64_t> band_elem, band_face, band_wall;
   double* hs_buf = nullptr;  // [3][rows][S][nb]: U, stage 1, stage 2
   size_t hs_n = 0;
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_h2d2 = nullptr, s_d2h2 = nullptr;
+  bool one_copy_stream = false;  // A/B: all copy-ins (copy-outs) on one stream
   cudaStream_t hs_st[6] = {};  // per stage: faces + slot sums, volume part
   std::vector<cudaEvent_t> ev_h2d, ev_d2h, ev_done, ev_vol_b;  // done / vol: [stage][band]
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
@@ -481,6 +482,8 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     if (!ctx->s_h2d) {
       cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking);
       cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&ctx->s_h2d2, cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&ctx->s_d2h2, cudaStreamNonBlocking);
       // later stages first: the chain to the copy-out (and so to the next
       // copy-in) runs through stage 3, which must not queue behind the
       // next step's stage-1 work
@@ -547,14 +550,20 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     const double ca[3] = {0.0, 0.75, 1.0 / 3.0}, cb[3] = {1.0, 0.25, 2.0 / 3.0};
     const double cc[3] = {dt, 0.25 * dt, (2.0 / 3.0) * dt};
     cudaEventRecord(ctx->ev_s0, st);
+    // copies alternate between two streams per direction by band parity:
+    // one stream's copies run on one copy engine, which did not always
+    // reach the link rate (tools/pcie_probe.py: 33 vs 48 GB/s H2D)
+    auto cin = [&](int k) { return (k & 1) && !ctx->one_copy_stream ? ctx->s_h2d2 : ctx->s_h2d; };
+    auto cout = [&](int k) { return (k & 1) && !ctx->one_copy_stream ? ctx->s_d2h2 : ctx->s_d2h; };
     cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_s0, 0);
+    cudaStreamWaitEvent(ctx->s_h2d2, ctx->ev_s0, 0);
     for (auto s : ctx->hs_st) cudaStreamWaitEvent(s, ctx->ev_s0, 0);
     for (int64_t it = 0; it < nsteps; ++it) {
       for (int k = 0; k < nb; ++k) {
-        if (it > 0) cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_d2h[k], 0);
+        if (it > 0) cudaStreamWaitEvent(cin(k), ctx->ev_d2h[k], 0);
         const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
-        cudaMemcpyAsync(Ud + o, Uh + o, m * sizeof(double), cudaMemcpyHostToDevice, ctx->s_h2d);
-        cudaEventRecord(ctx->ev_h2d[k], ctx->s_h2d);
+        cudaMemcpyAsync(Ud + o, Uh + o, m * sizeof(double), cudaMemcpyHostToDevice, cin(k));
+        cudaEventRecord(ctx->ev_h2d[k], cin(k));
       }
       for (int s = 0; s < 3; ++s) {
         cudaStream_t sf = ctx->hs_st[2 * s], sv = ctx->hs_st[2 * s + 1];
@@ -569,11 +578,11 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
           fc_add(k, Y[s], cc[s], sf);
           cudaEventRecord(ctx->ev_done[s * nb + k], sf);
           if (s == 2) {
-            cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[s * nb + k], 0);
+            cudaStreamWaitEvent(cout(k), ctx->ev_done[s * nb + k], 0);
             const size_t o = size_t(be[k]) * SN, m = size_t(be[k + 1] - be[k]) * SN;
             cudaMemcpyAsync(Uh + o, Ud + o, m * sizeof(double), cudaMemcpyDeviceToHost,
-                            ctx->s_d2h);
-            cudaEventRecord(ctx->ev_d2h[k], ctx->s_d2h);
+                            cout(k));
+            cudaEventRecord(ctx->ev_d2h[k], cout(k));
           }
         };
         for (int k = 0; k < nb; ++k) {
@@ -585,7 +594,7 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
       }
     }
     // join: every stream's tail back onto the caller's stream
-    for (cudaStream_t s : {ctx->s_h2d, ctx->s_d2h, ctx->hs_st[0], ctx->hs_st[1], ctx->hs_st[2],
+    for (cudaStream_t s : {ctx->s_h2d, ctx->s_d2h, ctx->s_h2d2, ctx->s_d2h2, ctx->hs_st[0], ctx->hs_st[1], ctx->hs_st[2],
                            ctx->hs_st[3], ctx->hs_st[4], ctx->hs_st[5]}) {
       cudaEventRecord(ctx->ev_s1, s);
       cudaStreamWaitEvent(st, ctx->ev_s1, 0);

@@ -214,7 +214,7 @@ class DiscreteOperator:
                     mma_volume: bool = False, face_ctas_per_sm: int = 0,
                     no_graph: bool = False, tc_volume: bool = False,
                     no_tc_faces: bool = False, volume_first: bool = False,
-                    face_rows_tc: bool = False):
+                    face_rows_tc: bool = False, one_copy_stream: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
@@ -227,6 +227,7 @@ class DiscreteOperator:
             | (int(bool(mma_volume)) << 4) | (int(bool(no_graph)) << 5)
             | (int(bool(tc_volume)) << 12) | (int(bool(no_tc_faces)) << 13)
             | (int(bool(volume_first)) << 14) | (int(bool(face_rows_tc)) << 15)
+            | (int(bool(one_copy_stream)) << 16)
             | ((int(face_ctas_per_sm) & 15) << 8)),
             "tdg_set_variant")
 
