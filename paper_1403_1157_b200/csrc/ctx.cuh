@@ -456,9 +456,13 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
   double* W1 = Ud + n;
   double* W2 = W1 + n;
   const int nb = ctx->n_bands;
-  const bool banded = nb > 1 && ctx->d.n_ghost == 0 && ctx->overlap && fast_face && fast_vol &&
-                      p.nqf == Dims<D, K>::NQF && p.nqv == Dims<D, K>::NQV &&
-                      !ctx->force_generic && (SN % 2 == 0);
+  // volume part per band: the one-thread-per-element kernel, or the
+  // transposed tensor-core one where that does not fit (2D k = 3: C3)
+  constexpr bool tc_vol = TcVol<D, K, M>::ok;
+  const bool band_tc = tc_vol && p.vtc != nullptr && (ctx->force_tc || !fast_vol);
+  const bool banded = D == 2 && nb > 1 && ctx->d.n_ghost == 0 && ctx->overlap && fast_face &&
+                      (fast_vol || band_tc) && p.nqf == Dims<D, K>::NQF &&
+                      p.nqv == Dims<D, K>::NQV && !ctx->force_generic && (SN % 2 == 0);
   if (!banded) {  // plain per-step copies around the fused stages
     for (int64_t it = 0; it < nsteps; ++it) {
       cudaMemcpyAsync(Ud, Uh, n * sizeof(double), cudaMemcpyHostToDevice, st);
@@ -471,7 +475,7 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
   }
-  if constexpr (fast_vol && fast_face && (SN % 2 == 0)) {
+  if constexpr ((fast_vol || tc_vol) && fast_face && (SN % 2 == 0)) {
     auto ev_new = [](std::vector<cudaEvent_t>& v, int k) {
       while (int(v.size()) < k) {
         cudaEvent_t e;
@@ -528,7 +532,7 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
       pv.egeo = p.egeo + e0 * Dims<D, K>::NEG;
       KernelTimer kt(ctx, 2, s);
       launch_volume<D, K, M>(ctx, pv, Uin + e0 * SN, U0 ? U0 + e0 * SN : nullptr, out + e0 * SN,
-                             a, b, c, 2 | 4, s, 0);
+                             a, b, c, 2 | 4, s, band_tc ? 2 : 0);
     };
     auto fc_add = [&](int k, double* out, double c, cudaStream_t s) {
       KernelTimer kt(ctx, 3, s);

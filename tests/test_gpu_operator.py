@@ -639,13 +639,15 @@ def test_species_l2_on_device_is_the_parity_metric():
     assert np.allclose(d / n, rel_l2_per_species(space, U, V), rtol=1e-12)
 
 
-@pytest.mark.parametrize("cells,bands,expect", [((128, 128), 4, 4), ((16, 8), 4, 1),
-                                                ((256, 128), 8, 8), ((128, 128), 2, 2)])
-def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect):
+@pytest.mark.parametrize("cells,bands,expect,order", [((128, 128), 4, 4, 2), ((16, 8), 4, 1, 2),
+                                                      ((256, 128), 8, 8, 2), ((128, 128), 2, 2, 2),
+                                                      ((128, 128), 4, 4, 3)])
+def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect, order):
     """tdg_ssprk3_steps_host (per-step copy-in / copy-out, stage wavefront
-    over element bands; none at 16x8) == copy-in, tdg_ssprk3_step,
-    copy-out, bit for bit, over several pipelined steps."""
-    space = DGSpace(unit_square(*cells, lengths=(1.0, 1.0)), 2, 6)
+    over element bands; none at 16x8; p = 3 runs the tensor-core volume
+    kernel per band) == copy-in, tdg_ssprk3_step, copy-out, bit for bit,
+    over several pipelined steps."""
+    space = DGSpace(unit_square(*cells, lengths=(1.0, 1.0)), order, 6)
     op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"), bands=bands)
     assert op.tables.n_bands == expect
     U0 = torch.from_numpy(initial_state(space, 9))
