@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 1
+#define TDG_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -128,7 +128,9 @@ typedef struct tdg_desc {
   /* host-pipelined stepping: n_bands contiguous element bands (1 = none),
    * band_ptr (HOST) = elements [n_bands+1] | interior-face offsets
    * [2 n_bands+1] (faces internal to band k from [2k], straddling (k, k+1)
-   * from [2k+1]) | wall offsets [n_bands+1], tables.build_tables order */
+   * from [2k+1]) | wall offsets [n_bands+1] | face-block offsets
+   * [n_bands+1] (the blocks of band k's faces, which no block straddles),
+   * tables.build_tables / tc_face_blocks order */
   int32_t n_bands;
   const int64_t* band_ptr;
 } tdg_desc;

@@ -15,7 +15,7 @@ from .build import LIB
 __all__ = ["lib", "TdgDesc", "check", "TDG_OK", "load"]
 
 TDG_OK, TDG_E_INVALID, TDG_E_UNSUPPORTED, TDG_E_CUDA = 0, -1, -2, -3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double

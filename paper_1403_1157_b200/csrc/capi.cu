@@ -145,16 +145,19 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     cudaGetLastError();
   }
   // element bands of the host-pipelined stepping (host array: elements
-  // [B+1] | interior-face offsets [2B+1] | wall offsets [B+1])
+  // [B+1] | interior-face offsets [2B+1] | wall offsets [B+1] | face-block
+  // offsets [B+1])
   if (d.n_bands > 1 && d.band_ptr) {
     const int nb = d.n_bands;
     const int64_t* bp = d.band_ptr;
     ctx->band_elem.assign(bp, bp + nb + 1);
     ctx->band_face.assign(bp + nb + 1, bp + nb + 1 + 2 * nb + 1);
     ctx->band_wall.assign(bp + 3 * nb + 2, bp + 4 * nb + 3);
+    ctx->band_blk.assign(bp + 4 * nb + 3, bp + 5 * nb + 4);
     const bool ok = ctx->band_elem.front() == 0 && ctx->band_elem.back() == d.n_elements &&
                     ctx->band_face.front() == 0 && ctx->band_face.back() == d.n_int_faces &&
-                    ctx->band_wall.front() == 0 && ctx->band_wall.back() == d.n_bnd_faces;
+                    ctx->band_wall.front() == 0 && ctx->band_wall.back() == d.n_bnd_faces &&
+                    ctx->band_blk.front() == 0 && ctx->band_blk.back() == d.n_face_blocks;
     if (!ok) {
       tdg_destroy(ctx);
       return fail(TDG_E_INVALID, "inconsistent band offsets");

@@ -59,7 +59,7 @@ struct tdg_ctx {
   // host-pipelined stepping: element bands and the banded face order
   // (tables.build_tables), device state / stage buffers, copy streams
   int n_bands = 1;
-  std::vector<int64_t> band_elem, band_face, band_wall;
+  std::vector<int64_t> band_elem, band_face, band_wall, band_blk;
   double* hs_buf = nullptr;  // [3][rows][S][nb]: U, stage 1, stage 2
   size_t hs_n = 0;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_h2d2 = nullptr, s_d2h2 = nullptr;
@@ -262,6 +262,53 @@ void launch_volume(tdg_ctx* ctx, const OpParams& p, const double* U, const doubl
   }
 }
 
+// transposed tensor-core interior faces over face blocks [b0, b1) (3D;
+// species rows by default) and the walls [w0, w1) on the element-local
+// DMMA kernel
+template <int D, int K, class M>
+void run_faces_tc(tdg_ctx* ctx, const OpParams& p, const double* U, int64_t b0, int64_t b1,
+                  int64_t w0, int64_t w1, cudaStream_t st) {
+  if constexpr (TcFace<D, K, M>::ok && MmaFace<D, K, M>::ok) {
+    if (b1 > b0) {
+      KernelTimer kt(ctx, 0, st);
+      bool done = false;
+      if constexpr (TcsFace<D, K, M>::ok) {
+        if (!ctx->face_rows_tc) {  // species rows, one face per warp (default)
+          using T = TcsFace<D, K, M>;
+          int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
+          const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 8;
+          grid = grid < cap ? grid : cap;
+          k_faces_tcs<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1,
+                                                                       U, ctx->fc);
+          done = true;
+        }
+      }
+      if (!done) {
+        using T = TcFace<D, K, M>;
+        int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
+        const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 4;
+        grid = grid < cap ? grid : cap;
+        k_faces_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1, U,
+                                                                    ctx->fc);
+      }
+    }
+    if (w1 > w0) {
+      KernelTimer kt(ctx, 1, st);
+      using T = MmaFace<D, K, M>;
+      OpParams pw = p;
+      pw.nif = 0;
+      pw.bfel = p.bfel + w0;
+      pw.bflf = p.bflf + w0;
+      pw.bfcode = p.bfcode + w0;
+      pw.bfgeo = p.bfgeo + w0;
+      pw.nbf = w1 - w0;
+      const int64_t warps = (pw.nbf + T::NFW - 1) / T::NFW;
+      const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+      k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(pw, pw.fmma, U, ctx->fc);
+    }
+  }
+}
+
 template <int D, int K, class M>
 int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, double b,
         double c, int mode, cudaStream_t st) {
@@ -285,38 +332,7 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
       const int64_t nblk = ctx->d.n_face_blocks, ncb = ctx->d.n_face_blocks_cut;
       const int64_t b0 = which == 2 ? nblk - ncb : 0;
       const int64_t b1 = which == 1 ? nblk - ncb : nblk;
-      if (b1 > b0) {
-        KernelTimer kt(ctx, 0, st);
-        bool done = false;
-        if constexpr (TcsFace<D, K, M>::ok) {
-          if (!ctx->face_rows_tc) {  // species rows, one face per warp (default)
-            using T = TcsFace<D, K, M>;
-            int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
-            const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 8;
-            grid = grid < cap ? grid : cap;
-            k_faces_tcs<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1,
-                                                                         U, ctx->fc);
-            done = true;
-          }
-        }
-        if (!done) {
-          using T = TcFace<D, K, M>;
-          int64_t grid = (b1 - b0 + T::WARPS - 1) / T::WARPS;
-          const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 4;
-          grid = grid < cap ? grid : cap;
-          k_faces_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, b0, b1, U,
-                                                                      ctx->fc);
-        }
-      }
-      if (which != 2 && p.nbf > 0) {
-        KernelTimer kt(ctx, 1, st);
-        using T = MmaFace<D, K, M>;
-        OpParams pw = p;
-        pw.nif = 0;
-        const int64_t warps = (p.nbf + T::NFW - 1) / T::NFW;
-        const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
-        k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(pw, pw.fmma, U, ctx->fc);
-      }
+      run_faces_tc<D, K, M>(ctx, p, U, b0, b1, which != 2 ? 0 : p.nbf, p.nbf, st);
     }
   };
   auto faces = [&](int which, bool use_ff_) {
@@ -460,9 +476,16 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
   // transposed tensor-core one where that does not fit (2D k = 3: C3)
   constexpr bool tc_vol = TcVol<D, K, M>::ok;
   const bool band_tc = tc_vol && p.vtc != nullptr && (ctx->force_tc || !fast_vol);
-  const bool banded = D == 2 && nb > 1 && ctx->d.n_ghost == 0 && ctx->overlap && fast_face &&
-                      (fast_vol || band_tc) && p.nqf == Dims<D, K>::NQF &&
-                      p.nqv == Dims<D, K>::NQV && !ctx->force_generic && (SN % 2 == 0);
+  // faces per band: the register-resident kernel over face ranges (2D), or
+  // the transposed tensor-core kernel over the band's face blocks (3D)
+  constexpr bool tcf = TcFace<D, K, M>::ok && MmaFace<D, K, M>::ok;
+  const bool band_tcf = D == 3 && tcf && p.ftc != nullptr && p.fblk != nullptr &&
+                        p.fmma != nullptr && !ctx->no_tcf && !ctx->flip_mma &&
+                        int(ctx->band_blk.size()) == nb + 1;
+  const bool banded = nb > 1 && ctx->d.n_ghost == 0 && ctx->overlap &&
+                      (D == 2 ? fast_face : band_tcf) && (fast_vol || band_tc) &&
+                      p.nqf == Dims<D, K>::NQF && p.nqv == Dims<D, K>::NQV &&
+                      !ctx->force_generic && (SN % 2 == 0);
   if (!banded) {  // plain per-step copies around the fused stages
     for (int64_t it = 0; it < nsteps; ++it) {
       cudaMemcpyAsync(Ud, Uh, n * sizeof(double), cudaMemcpyHostToDevice, st);
@@ -475,7 +498,7 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
   }
-  if constexpr ((fast_vol || tc_vol) && fast_face && (SN % 2 == 0)) {
+  if constexpr ((fast_vol || tc_vol) && (fast_face || tcf) && (SN % 2 == 0)) {
     auto ev_new = [](std::vector<cudaEvent_t>& v, int k) {
       while (int(v.size()) < k) {
         cudaEvent_t e;
@@ -510,6 +533,11 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     // faces of band k: those straddling (k-1, k), those internal to k and
     // band k's walls; they read bands k-1 and k and write their slots
     auto faces_band = [&](int k, const double* Uin, cudaStream_t s) {
+      if (D == 3) {
+        run_faces_tc<D, K, M>(ctx, p, Uin, ctx->band_blk[k], ctx->band_blk[k + 1], bw[k],
+                              bw[k + 1], s);
+        return;
+      }
       OpParams pp = p;
       const int64_t f0 = k > 0 ? bf[2 * k - 1] : 0, f1 = bf[2 * k + 1];
       pp.ifel = p.ifel + 2 * f0;

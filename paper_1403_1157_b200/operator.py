@@ -83,8 +83,8 @@ class DiscreteOperator:
         self.n_owned = t.elem_geo.shape[0]
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
-        from .tables import (mma_face_tables, mma_volume_tables, tc_face_blocks,
-                             tc_face_tables, tc_volume_tables)
+        from .tables import (mma_face_tables, mma_volume_tables, tc_band_blocks,
+                             tc_face_blocks, tc_face_tables, tc_volume_tables)
         mma, self._mma_stride = mma_face_tables(t)
         blocks, n_cut_blocks = tc_face_blocks(t)
         self._keep = {"face_mma": dev(mma), "vol_mma": dev(mma_volume_tables(t)),
@@ -96,7 +96,8 @@ class DiscreteOperator:
             "if_geo", "bf_elem", "bf_lf", "bf_code", "bf_geo")})
         self._host = {
             "band_ptr": np.ascontiguousarray(np.concatenate(
-                [t.band_elem_ptr, t.band_face_ptr, t.band_wall_ptr]), dtype=np.int64),
+                [t.band_elem_ptr, t.band_face_ptr, t.band_wall_ptr,
+                 tc_band_blocks(t, blocks)]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
             "lin_source": _checked_linear_source(model),
             "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}

@@ -339,12 +339,16 @@ def tc_face_tables(t: OperatorTables):
 def tc_face_blocks(t: OperatorTables, block: int = 8):
     """Blocks of up to ``block`` consecutive interior faces with one trace-
     table signature each (the M dimension of the transposed face kernel),
-    never straddling the non-cut / cut boundary.  Returns (int32 [nblk][2]
-    = (first face, count), number of blocks of cut faces at the end)."""
+    never straddling the non-cut / cut boundary nor a band segment
+    (``band_face_ptr``).  Returns (int32 [nblk][2] = (first face, count),
+    number of blocks of cut faces at the end)."""
     nif = len(t.if_code)
     if nif == 0:
         return np.zeros((0, 2), np.int32), 0
     sig = (t.if_code.astype(np.int64) & 1023) + (np.arange(nif) >= nif - t.n_cut) * 1024
+    if t.n_bands > 1:
+        seg = np.searchsorted(t.band_face_ptr, np.arange(nif), side="right")
+        sig = sig + seg * 2048
     brk = np.flatnonzero(np.diff(sig)) + 1
     starts = np.concatenate([[0], brk])
     lens = np.diff(np.concatenate([starts, [nif]]))
@@ -356,6 +360,16 @@ def tc_face_blocks(t: OperatorTables, block: int = 8):
     blocks = np.ascontiguousarray(np.stack([first, cnt], axis=1), dtype=np.int32)
     n_cut_blocks = int((first >= nif - t.n_cut).sum()) if t.n_cut else 0
     return blocks, n_cut_blocks
+
+
+def tc_band_blocks(t: OperatorTables, blocks: np.ndarray) -> np.ndarray:
+    """Block offsets [n_bands+1] of the bands' faces (the faces straddling
+    (k-1, k) and those internal to k, i.e. faces from band_face_ptr[2k-1])
+    in the tc_face_blocks list."""
+    B = t.n_bands
+    start = np.array([0] + [int(t.band_face_ptr[2 * k - 1]) for k in range(1, B)]
+                     + [len(t.if_code)], dtype=np.int64)
+    return np.searchsorted(blocks[:, 0].astype(np.int64), start, side="left").astype(np.int64)
 
 
 def mma_volume_tables(t: OperatorTables) -> np.ndarray:
