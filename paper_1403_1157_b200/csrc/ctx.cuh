@@ -378,7 +378,8 @@ int run(tdg_ctx* ctx, const double* U, const double* U0, double* out, double a, 
   const bool use_tc = tc_ok && !use_vm && p.vtc != nullptr && p.nqv == Dims<D, K>::NQV &&
                       !ctx->force_generic && (ctx->force_tc || !use_fv);
   const int vk = use_vm ? 1 : (use_tc ? 2 : 0);
-  const bool overlap = (use_fv || use_vm || use_tc) && use_ff && ctx->overlap && ctx->aux &&
+  const bool overlap = (use_fv || use_vm || use_tc) && (use_ff || use_tcf) && ctx->overlap &&
+                       ctx->aux &&
                        out != U && p.ne > 0 && (SN_of<M, D, K>() % 2 == 0);
   if (overlap) {
     if constexpr ((fast_vol || vmma_ok || tc_ok) && (SN_of<M, D, K>() % 2 == 0)) {
