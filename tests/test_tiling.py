@@ -110,3 +110,55 @@ def test_element_bands_order_faces_for_host_pipelined_steps():
         assert np.all(band(t.bf_elem[w0:w1]) == k)
     # small meshes and slab meshes are not banded
     assert build_tables(DGSpace(unit_square(8), 1, 6), PlaqueModel(), FluxScheme("cdg2")).n_bands == 1
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_face_blocks_respect_band_segments(dim):
+    """tc_face_blocks never straddles a band segment (nor a signature), and
+    tc_band_blocks gives each band exactly the blocks of its faces (those
+    straddling (k-1, k) and those internal to k): the 3D host-pipelined
+    steps launch the transposed face kernel per band over these blocks."""
+    from paper_1403_1157_b200.tables import tc_band_blocks, tc_face_blocks
+    mesh = unit_square(128, 128) if dim == 2 else unit_cube(16)
+    t = build_tables(DGSpace(mesh, 1, 6), PlaqueModel(), FluxScheme("cdg2"), bands=3)
+    assert t.n_bands == 3
+    blocks, ncut = tc_face_blocks(t)
+    assert ncut == 0
+    first, cnt = blocks[:, 0].astype(np.int64), blocks[:, 1].astype(np.int64)
+    assert first[0] == 0 and np.array_equal(first[1:], first[:-1] + cnt[:-1])
+    assert first[-1] + cnt[-1] == len(t.if_code) and np.all((cnt >= 1) & (cnt <= 8))
+    seg = np.searchsorted(t.band_face_ptr, np.arange(len(t.if_code)), side="right")
+    sig = t.if_code & 1023
+    for f0, c in zip(first, cnt):
+        assert len(set(seg[f0:f0 + c])) == 1 and len(set(sig[f0:f0 + c])) == 1
+    bb = tc_band_blocks(t, blocks)
+    assert bb[0] == 0 and bb[-1] == len(blocks) and np.all(np.diff(bb) >= 0)
+    for k in range(3):
+        f_lo = 0 if k == 0 else t.band_face_ptr[2 * k - 1]
+        f_hi = t.band_face_ptr[2 * k + 1] if k < 2 else len(t.if_code)
+        assert first[bb[k]] == f_lo
+        last = bb[k + 1] - 1
+        assert first[last] + cnt[last] == f_hi
+
+
+def test_cpu_baseline_sample_is_a_bounded_slab_of_the_config():
+    """bench.sample_config: the CPU baseline of large configs is an x-slab
+    (then y-slab in 3D) with the config's cell size, order and physics,
+    at most ~5M DoFs; small configs are timed whole."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1403_1157_b200.basis import basis_size
+    from paper_1403_1157_b200.configs import CONFIGS
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        cfg = bench.weak_config(CONFIGS[name], 1)
+        smp = bench.sample_config(cfg)
+        per = (2 if cfg.dim == 2 else 6) * 6 * basis_size(cfg.dim, cfg.order)
+        dofs = int(np.prod(smp.cells)) * per
+        if name in ("c1", "c2"):
+            assert smp == cfg
+        else:
+            assert dofs <= 5_000_000 and smp.order == cfg.order and smp.dim == cfg.dim
+        for a in range(cfg.dim):    # same cell size
+            assert smp.lengths[a] / smp.cells[a] == pytest.approx(cfg.lengths[a] / cfg.cells[a])
