@@ -353,7 +353,9 @@ def run_native_arm(args, rank, world, local):
                           global_ids=None if slab is None else slab.global_ids,
                           bands=args.bands)
     log("operator created")
-    if args.variant:
+    if args.variant >> 17:  # bits beyond set_variant's keywords: raw
+        op.lib.tdg_set_variant(op._ctx, int(args.variant))
+    elif args.variant:
         op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),
                        serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
                        mma_volume=bool(args.variant & 16),

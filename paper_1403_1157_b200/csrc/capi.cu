@@ -395,7 +395,8 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
   ctx->force_tc = ((variant >> 12) & 1) != 0;
   ctx->face_rows_tc = ((variant >> 15) & 1) != 0;
-  ctx->one_copy_stream = ((variant >> 16) & 1) != 0;  // bit 16: host steps on one copy stream per direction  // bit 15: faces-as-rows TC face kernel (3D)
+  ctx->one_copy_stream = ((variant >> 16) & 1) != 0;
+  ctx->walls_first = ((variant >> 17) & 1) != 0;  // bit 17: 3D wall faces before interior  // bit 16: host steps on one copy stream per direction  // bit 15: faces-as-rows TC face kernel (3D)
   ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)
   ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3

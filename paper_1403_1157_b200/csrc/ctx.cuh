@@ -55,7 +55,8 @@ struct tdg_ctx {
   bool force_tc = false;  // testing: transposed tensor-core volume kernel everywhere
   bool no_tcf = false;
   bool faces_first = true;
-  bool face_rows_tc = false;  // 3D: faces-as-rows TC face kernel instead of species rows
+  bool face_rows_tc = false;
+  bool walls_first = false;   // 3D: wall faces before the interior tensor-core faces  // 3D: faces-as-rows TC face kernel instead of species rows
   // host-pipelined stepping: element bands and the banded face order
   // (tables.build_tables), device state / stage buffers, copy streams
   int n_bands = 1;
@@ -269,6 +270,22 @@ template <int D, int K, class M>
 void run_faces_tc(tdg_ctx* ctx, const OpParams& p, const double* U, int64_t b0, int64_t b1,
                   int64_t w0, int64_t w1, cudaStream_t st) {
   if constexpr (TcFace<D, K, M>::ok && MmaFace<D, K, M>::ok) {
+    auto walls = [&]() {
+      if (w1 <= w0) return;
+      KernelTimer kt(ctx, 1, st);
+      using T = MmaFace<D, K, M>;
+      OpParams pw = p;
+      pw.nif = 0;
+      pw.bfel = p.bfel + w0;
+      pw.bflf = p.bflf + w0;
+      pw.bfcode = p.bfcode + w0;
+      pw.bfgeo = p.bfgeo + w0;
+      pw.nbf = w1 - w0;
+      const int64_t warps = (pw.nbf + T::NFW - 1) / T::NFW;
+      const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
+      k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(pw, pw.fmma, U, ctx->fc);
+    };
+    if (ctx->walls_first) walls();
     if (b1 > b0) {
       KernelTimer kt(ctx, 0, st);
       bool done = false;
@@ -292,20 +309,7 @@ void run_faces_tc(tdg_ctx* ctx, const OpParams& p, const double* U, int64_t b0, 
                                                                     ctx->fc);
       }
     }
-    if (w1 > w0) {
-      KernelTimer kt(ctx, 1, st);
-      using T = MmaFace<D, K, M>;
-      OpParams pw = p;
-      pw.nif = 0;
-      pw.bfel = p.bfel + w0;
-      pw.bflf = p.bflf + w0;
-      pw.bfcode = p.bfcode + w0;
-      pw.bfgeo = p.bfgeo + w0;
-      pw.nbf = w1 - w0;
-      const int64_t warps = (pw.nbf + T::NFW - 1) / T::NFW;
-      const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
-      k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(pw, pw.fmma, U, ctx->fc);
-    }
+    if (!ctx->walls_first) walls();
   }
 }
 
