@@ -352,9 +352,9 @@ struct TcsFace {
   static constexpr int NB = TF::NB, S = M::S, SN = S * NB, F = TF::F, NFG = TF::NFG;
   static constexpr int QP = TF::QP, QT = TF::QT, KT = TF::KT, NNT = TF::NNT, TS = TF::TS;
   static constexpr int NCV = TF::NCV, XS = S | 1;
-  // the last mode tile holds at most 2 modes (nb = 10: modes 8, 9 at
-  // t = 0, 1): both sides' projections share one DMMA pair there
-  static constexpr bool MERGE = NNT >= 2 && NB - 8 * (NNT - 1) <= 2;
+  // the last mode tile holds at most 4 modes (nb = 10: 2, nb = 20: 4),
+  // all in its even columns: both sides' projections share one DMMA pair
+  static constexpr bool MERGE = NNT >= 2 && NB - 8 * (NNT - 1) <= 4;
   static constexpr int WARPS = 4;
   static constexpr int PWS = 3 * QP * XS + QP * NCV + 1;  // per-warp scratch (doubles)
   static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
@@ -523,12 +523,13 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt) {
             if (T::MERGE && nt == NNT - 1) {
-              // merged tail tile: B columns 0-3 carry the in-side modes,
-              // columns 4-7 the out-side ones (normal-layout lane - 16,
-              // sign of Y folded in), so one DMMA pair serves both sides
-              const bool oc = g >= 4;
+              // merged tail tile: the even B columns (C j = 0) carry the
+              // in-side modes, the odd ones (j = 1, modes past nb) the
+              // out-side ones (normal-layout lane - 4, sign of Y folded
+              // in), so one DMMA pair serves both sides
+              const bool oc = (g & 1) != 0;
               const double* Tx = oc ? To : Ti;
-              const int ln = oc ? lane - 16 : lane;
+              const int ln = oc ? lane - 4 : lane;
               const int ob = ((qt * 2 + ks) * NNT + nt) * 32 + ln;
               double gx = 0.0;
 #pragma unroll
@@ -564,12 +565,13 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
         for (int nt = 0; nt < NNT; ++nt)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            if (T::MERGE && nt == NNT - 1) {  // in-side modes at t < 2, out-side at t >= 2
-              if (j == 0) {
-                if (t < 2)
-                  fci[8 * nt + t] = ri[nt][0];
+            if (T::MERGE && nt == NNT - 1) {  // j = 0: in-side mode, j = 1: out-side
+              const int i = 8 * nt + t;
+              if (i < NB) {
+                if (j == 0)
+                  fci[i] = ri[nt][0];
                 else if (!skip_out)
-                  fco[8 * nt + t - 2] = ri[nt][0];
+                  fco[i] = ri[nt][1];
               }
               continue;
             }
