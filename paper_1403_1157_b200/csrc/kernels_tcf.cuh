@@ -358,7 +358,8 @@ struct TcsFace {
   static constexpr int WARPS = 4;
   static constexpr int PWS = 3 * QP * XS + QP * NCV + 1;  // per-warp scratch (doubles)
   static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
-  static constexpr int MINB = 4;  // 128 registers (16 warps/SM): 3 -> 4 cut C4 faces 21.6 -> 18.6 ms; 5 spills
+  // 128 registers (16 warps/SM): 3 -> 4 cut C4 faces 21.6 -> 18.6 ms; 5 spills
+  static constexpr int MINB = K >= 3 ? 3 : 4;
   static constexpr bool ok = D == 3 && S <= 8 && !M::kMirror && TF::ok && smem() <= 96 * 1024;
 };
 
