@@ -665,7 +665,7 @@ def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect, o
         op.ssprk3_steps_host(U0.clone(), 1, dt)        # not pinned
 
 
-@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("k", [1, 2, 3])
 def test_host_pipelined_steps_3d_bitwise_equal_device_steps(k):
     """3D host-pipelined steps (tensor-core faces over each band's face
     blocks, tensor-core volume per band, then the face-slot sum) ==
