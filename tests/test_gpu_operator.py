@@ -571,7 +571,7 @@ def test_tiny_meshes_match_oracle(mesh_name, order, scheme):
     model = PlaqueModel(PlaqueParams(**AMPLIFIED))
     U = initial_state(space, 11)
     ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
-    for variant in ({}, {"generic": True}, {"serial": True}):
+    for variant in ({}, {"generic": True}, {"serial": True}, {"face_rows_tc": True}):
         op = _op(space, model, FluxScheme(scheme))
         op.set_variant(**variant)
         got = op.apply_f(U)
