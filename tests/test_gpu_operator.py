@@ -597,6 +597,26 @@ def test_heat_3d_tensor_core_kernels_match_oracle(scheme, dirichlet, order):
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), variant
 
 
+@pytest.mark.parametrize("order,cells", [(2, 6), (3, 4)])
+@pytest.mark.parametrize("scheme", ["cdg2", "br2"])
+def test_3d_face_blocks_at_size_match_oracle(order, cells, scheme):
+    """The species-rows tensor-core face kernel over many face blocks of
+    mixed signatures (all ten Kuhn-cube signatures, blocks cut at 8 faces
+    and at signature changes) and the merged tail mode tile, against the
+    oracle (reference operator.py:253-288) and the faces-as-rows kernel."""
+    from paper_1403_1157_b200.mesh import unit_cube
+    space = DGSpace(unit_cube(cells), order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    U = initial_state(space, 17)
+    ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
+    op = _op(space, model, FluxScheme(scheme))
+    got = op.apply_f(U)
+    assert rel_l2_per_species(space, got, ref).max() <= 1e-12
+    op.set_variant(face_rows_tc=True)
+    other = op.apply_f(U)
+    assert rel_l2_per_species(space, got, other).max() <= 1e-13
+
+
 def test_bench_spectral_radius_on_a_slab():
     """bench.spectral_radius on a slab operator (ghost rows present) runs and
     matches the undecomposed estimate (dt selection at N > 1)."""
