@@ -353,9 +353,7 @@ def run_native_arm(args, rank, world, local):
                           global_ids=None if slab is None else slab.global_ids,
                           bands=args.bands)
     log("operator created")
-    if args.variant >> 17:  # bits beyond set_variant's keywords: raw
-        op.lib.tdg_set_variant(op._ctx, int(args.variant))
-    elif args.variant:
+    if args.variant:
         op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),
                        serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
                        mma_volume=bool(args.variant & 16),
@@ -365,6 +363,7 @@ def run_native_arm(args, rank, world, local):
                        volume_first=bool(args.variant & 16384),
                        face_rows_tc=bool(args.variant & 32768),
                        one_copy_stream=bool(args.variant & 65536),
+                       walls_first=bool(args.variant & 131072),
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb

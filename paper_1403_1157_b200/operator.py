@@ -215,20 +215,24 @@ class DiscreteOperator:
                     mma_volume: bool = False, face_ctas_per_sm: int = 0,
                     no_graph: bool = False, tc_volume: bool = False,
                     no_tc_faces: bool = False, volume_first: bool = False,
-                    face_rows_tc: bool = False, one_copy_stream: bool = False):
+                    face_rows_tc: bool = False, one_copy_stream: bool = False,
+                    walls_first: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
         volume part with the face kernel; ``face_ctas_per_sm`` caps the
-        grid of the grid-stride face kernel (0 default, 15 uncapped).
-        Defaults: fastest."""
+        grid of the grid-stride face kernel (0 default, 15 uncapped);
+        ``face_rows_tc`` the faces-as-rows 3D tensor-core face kernel;
+        ``one_copy_stream`` one copy stream per direction in
+        ``ssprk3_steps_host``; ``walls_first`` 3D wall faces before the
+        interior ones.  Defaults: fastest."""
         _native.check(self.lib.tdg_set_variant(
             self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
             | (int(bool(serial)) << 2) | (int(bool(flip_mma)) << 3)
             | (int(bool(mma_volume)) << 4) | (int(bool(no_graph)) << 5)
             | (int(bool(tc_volume)) << 12) | (int(bool(no_tc_faces)) << 13)
             | (int(bool(volume_first)) << 14) | (int(bool(face_rows_tc)) << 15)
-            | (int(bool(one_copy_stream)) << 16)
+            | (int(bool(one_copy_stream)) << 16) | (int(bool(walls_first)) << 17)
             | ((int(face_ctas_per_sm) & 15) << 8)),
             "tdg_set_variant")
 
