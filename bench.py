@@ -364,6 +364,7 @@ def run_native_arm(args, rank, world, local):
                        face_rows_tc=bool(args.variant & 32768),
                        one_copy_stream=bool(args.variant & 65536),
                        walls_first=bool(args.variant & 131072),
+                       copy_streams=(args.variant >> 18) & 7,
                        face_ctas_per_sm=(args.variant >> 8) & 15)
     t = op.tables
     d, nb = t.dim, t.nb

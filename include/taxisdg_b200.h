@@ -247,7 +247,9 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
  * the face kernel (default: faces first); bit 13: in 3D, use the element-local DMMA face kernel for interior
  * faces instead of the transposed one; bit 15: in 3D, use the faces-as-rows
  * transposed face kernel instead of the species-as-rows one; bit 16:
- * tdg_ssprk3_steps_host with one copy stream per direction; bit 12: use the transposed tensor-core volume kernel wherever it
+ * tdg_ssprk3_steps_host with one copy stream per direction; bits 18-20:
+ * that many copy streams per direction (0: default); bit 17: 3D wall
+ * faces before the interior ones; bit 12: use the transposed tensor-core volume kernel wherever it
  * compiles (default only where the one-thread-per-element kernel does not
  * fit); bits 8-11: CTAs
  * per SM of the register-resident face kernel's grid-stride grid (0 =

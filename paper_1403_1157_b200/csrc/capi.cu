@@ -179,10 +179,10 @@ int tdg_destroy(tdg_ctx* ctx) {
   cudaFree(ctx->part);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   cudaFree(ctx->hs_buf);
-  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
-  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
-  if (ctx->s_h2d2) cudaStreamDestroy(ctx->s_h2d2);
-  if (ctx->s_d2h2) cudaStreamDestroy(ctx->s_d2h2);
+  for (int i = 0; i < tdg_ctx::kCopyStreams; ++i) {
+    if (ctx->s_in[i]) cudaStreamDestroy(ctx->s_in[i]);
+    if (ctx->s_out[i]) cudaStreamDestroy(ctx->s_out[i]);
+  }
   for (auto s : ctx->hs_st)
     if (s) cudaStreamDestroy(s);
   if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
@@ -395,7 +395,10 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->use_vmma = ((variant >> 4) & 1) != 0;
   ctx->force_tc = ((variant >> 12) & 1) != 0;
   ctx->face_rows_tc = ((variant >> 15) & 1) != 0;
-  ctx->one_copy_stream = ((variant >> 16) & 1) != 0;
+  // bit 16: host steps on one copy stream per direction; bits 18-20: that
+  // many copy streams per direction (0: the default 2)
+  const int ncs = (variant >> 18) & 7;
+  ctx->copy_streams = ((variant >> 16) & 1) ? 1 : (ncs ? ncs : 2);
   ctx->walls_first = ((variant >> 17) & 1) != 0;  // bit 17: 3D wall faces before interior  // bit 16: host steps on one copy stream per direction  // bit 15: faces-as-rows TC face kernel (3D)
   ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)
   ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first

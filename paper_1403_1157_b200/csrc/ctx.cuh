@@ -63,8 +63,12 @@ struct tdg_ctx {
   std::vector<int64_t> band_elem, band_face, band_wall, band_blk;
   double* hs_buf = nullptr;  // [3][rows][S][nb]: U, stage 1, stage 2
   size_t hs_n = 0;
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_h2d2 = nullptr, s_d2h2 = nullptr;
-  bool one_copy_stream = false;  // A/B: all copy-ins (copy-outs) on one stream
+  // copy streams per direction: band k's copy-in / copy-out on stream
+  // k mod copy_streams, so a band waiting for its previous copy-out does
+  // not hold back the next bands' copies (head-of-line blocking)
+  static constexpr int kCopyStreams = 8;
+  cudaStream_t s_in[kCopyStreams] = {}, s_out[kCopyStreams] = {};
+  int copy_streams = 2;
   cudaStream_t hs_st[6] = {};  // per stage: faces + slot sums, volume part
   std::vector<cudaEvent_t> ev_h2d, ev_d2h, ev_done, ev_vol_b;  // done / vol: [stage][band]
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
@@ -511,11 +515,11 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
         v.push_back(e);
       }
     };
-    if (!ctx->s_h2d) {
-      cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking);
-      cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
-      cudaStreamCreateWithFlags(&ctx->s_h2d2, cudaStreamNonBlocking);
-      cudaStreamCreateWithFlags(&ctx->s_d2h2, cudaStreamNonBlocking);
+    if (!ctx->s_in[0]) {
+      for (int i = 0; i < tdg_ctx::kCopyStreams; ++i) {
+        cudaStreamCreateWithFlags(&ctx->s_in[i], cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&ctx->s_out[i], cudaStreamNonBlocking);
+      }
       // later stages first: the chain to the copy-out (and so to the next
       // copy-in) runs through stage 3, which must not queue behind the
       // next step's stage-1 work
@@ -587,13 +591,12 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
     const double ca[3] = {0.0, 0.75, 1.0 / 3.0}, cb[3] = {1.0, 0.25, 2.0 / 3.0};
     const double cc[3] = {dt, 0.25 * dt, (2.0 / 3.0) * dt};
     cudaEventRecord(ctx->ev_s0, st);
-    // copies alternate between two streams per direction by band parity:
-    // one stream's copies run on one copy engine, which did not always
-    // reach the link rate (tools/pcie_probe.py: 33 vs 48 GB/s H2D)
-    auto cin = [&](int k) { return (k & 1) && !ctx->one_copy_stream ? ctx->s_h2d2 : ctx->s_h2d; };
-    auto cout = [&](int k) { return (k & 1) && !ctx->one_copy_stream ? ctx->s_d2h2 : ctx->s_d2h; };
-    cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_s0, 0);
-    cudaStreamWaitEvent(ctx->s_h2d2, ctx->ev_s0, 0);
+    const int ncs = ctx->copy_streams < 1 ? 1
+                    : (ctx->copy_streams > tdg_ctx::kCopyStreams ? tdg_ctx::kCopyStreams
+                                                                 : ctx->copy_streams);
+    auto cin = [&](int k) { return ctx->s_in[k % ncs]; };
+    auto cout = [&](int k) { return ctx->s_out[k % ncs]; };
+    for (int i = 0; i < ncs; ++i) cudaStreamWaitEvent(ctx->s_in[i], ctx->ev_s0, 0);
     for (auto s : ctx->hs_st) cudaStreamWaitEvent(s, ctx->ev_s0, 0);
     for (int64_t it = 0; it < nsteps; ++it) {
       for (int k = 0; k < nb; ++k) {
@@ -631,11 +634,15 @@ int host_steps(tdg_ctx* ctx, double* Uh, int64_t nsteps, double dt, cudaStream_t
       }
     }
     // join: every stream's tail back onto the caller's stream
-    for (cudaStream_t s : {ctx->s_h2d, ctx->s_d2h, ctx->s_h2d2, ctx->s_d2h2, ctx->hs_st[0], ctx->hs_st[1], ctx->hs_st[2],
-                           ctx->hs_st[3], ctx->hs_st[4], ctx->hs_st[5]}) {
+    auto join = [&](cudaStream_t s) {
       cudaEventRecord(ctx->ev_s1, s);
       cudaStreamWaitEvent(st, ctx->ev_s1, 0);
+    };
+    for (int i = 0; i < ncs; ++i) {
+      join(ctx->s_in[i]);
+      join(ctx->s_out[i]);
     }
+    for (cudaStream_t s : ctx->hs_st) join(s);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");

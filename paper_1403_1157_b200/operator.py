@@ -216,7 +216,7 @@ class DiscreteOperator:
                     no_graph: bool = False, tc_volume: bool = False,
                     no_tc_faces: bool = False, volume_first: bool = False,
                     face_rows_tc: bool = False, one_copy_stream: bool = False,
-                    walls_first: bool = False):
+                    walls_first: bool = False, copy_streams: int = 0):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
         volume kernel; ``serial`` disables the two-stream overlap of the
@@ -224,7 +224,8 @@ class DiscreteOperator:
         grid of the grid-stride face kernel (0 default, 15 uncapped);
         ``face_rows_tc`` the faces-as-rows 3D tensor-core face kernel;
         ``one_copy_stream`` one copy stream per direction in
-        ``ssprk3_steps_host``; ``walls_first`` 3D wall faces before the
+        ``ssprk3_steps_host`` (``copy_streams``: that many, 0 = default);
+        ``walls_first`` 3D wall faces before the
         interior ones.  Defaults: fastest."""
         _native.check(self.lib.tdg_set_variant(
             self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
@@ -233,6 +234,7 @@ class DiscreteOperator:
             | (int(bool(tc_volume)) << 12) | (int(bool(no_tc_faces)) << 13)
             | (int(bool(volume_first)) << 14) | (int(bool(face_rows_tc)) << 15)
             | (int(bool(one_copy_stream)) << 16) | (int(bool(walls_first)) << 17)
+            | ((int(copy_streams) & 7) << 18)
             | ((int(face_ctas_per_sm) & 15) << 8)),
             "tdg_set_variant")
 
