@@ -683,6 +683,10 @@ def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect, o
     assert not torch.equal(Uh, U0)
     with pytest.raises(ValueError):
         op.ssprk3_steps_host(U0.clone(), 1, dt)        # not pinned
+    Z = U0.clone().pin_memory()
+    op.ssprk3_steps_host(Z, 0, dt)                     # zero steps: untouched
+    torch.cuda.synchronize()
+    assert torch.equal(Z, U0)
 
 
 @pytest.mark.parametrize("k", [1, 2, 3])
