@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """Benchmark: fp64 DG-operator DoF-updates/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
-                    [--impl native|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
+                    [--scaling strong|weak] [--impl native|reference]
 
 A step is one Shu-Osher SSP-RK3 step = 3 applications of f = M^-1 L_h,
 each fused with its Runge-Kutta stage update, over the whole mesh.
 Unit of work: one DoF receiving one f evaluation, so
 value = n_dofs * 3 * K / (device time of K steps), max over ranks.
 
-Default workload: config C2 (BASELINE configs[1], 4.7M DoFs, p=2 2D) at
-the explicit CFL step dt = 0.8 * 2.51 / rho(J), rho by device power
-iteration.  Inputs are resident in HBM; L2 (126 MB) is flushed between
-timed steps by writing a 256 MiB buffer outside the timed events.
+Default workload: config C5 (BASELINE configs[4], the configuration the
+metric is quoted on "at 1/2/4/8 B200"): [0,2]x[0,1]^2, 256x128x128 cells
+x 6 Kuhn tetrahedra = 25.2M tets, p=3, 3.02e9 DoFs, cdg2, the explicit
+CFL step dt = 0.8 * 2.51 / rho(J).  N > 1: the fixed C5 mesh split into
+N x-slabs (strong scaling, NCCL ghost-row exchange per stage);
+``--scaling weak`` gives every GPU a config-sized slab instead.  Inputs
+are resident in HBM; the 24 GB state is far larger than L2 (small
+configs flush L2 between timed steps).
 
 ``--impl reference`` times the CPU oracle port of the reference
-(oracle/, numpy, all host threads) on the same config: the reference
-itself is pure Python and cannot travel to the GPU box.
+(oracle/, numpy, all physical host cores, BLAS pinned to one thread)
+on a bounded x-slab sample of the same config: the reference itself is
+pure Python and cannot travel to the GPU box.
 """
 
 from __future__ import annotations
@@ -38,22 +43,25 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 DG-operator DoF-updates/s at 1/2/4/8 B200; % of HBM/FP64 roofline"
 UNIT = "DoF-updates/s"
 FP64_NOMINAL_TFLOPS = 37.0  # HGX B200 datasheet FP64 / FP64 tensor
+BIG_DOFS = 400_000_000      # above this: dt from a same-h replica, no L2 flush
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 5 for c5, 20 otherwise)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the fixed config split into N x-slabs; "
+                         "weak = one config-sized slab per GPU")
     ap.add_argument("--scheme", default="cdg2")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: testing only (host-staged exchange; ranks may share a GPU)")
-    ap.add_argument("--bands", type=int, default=8,
-                    help="element bands of the host-pipelined e2e stepping")
     ap.add_argument("--no-implicit", action="store_true",
                     help="skip the extra SDIRK3+JFNK figure of the explicit C2 run")
     ap.add_argument("--power-iters", type=int, default=200)
@@ -64,7 +72,12 @@ def parse():
                     help="use the slab/halo code path even at N=1 (testing)")
     ap.add_argument("--variant", type=int, default=0,
                     help="kernel variant bits (tdg_set_variant), for A/B timing")
-    return ap.parse_args()
+    ap.add_argument("--cells", default=None,
+                    help="override the config's cell counts, e.g. 64x32x32 (testing)")
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 5 if a.config == "c5" else 20
+    return a
 
 
 def dist_env():
@@ -138,22 +151,18 @@ class ClockSampler:
 
 # -------------------------------------------------------------- workload
 
-def weak_config(cfg, world):
-    """Weak scaling: every rank owns one x-slab of cfg.cells[0] /
-    cfg.weak_div cell columns (same cell size) of a domain N times that
-    long in x -- C2 at N GPUs is N side-by-side C2 domains; C5 (weak_div
-    8) at N = 8 is exactly C5."""
+def scaled_config(cfg, world, scaling, cells=None):
+    """The job's mesh: the config itself (strong scaling; N ranks split it
+    into x-slabs), or for weak scaling N config-sized x-slabs side by side
+    (domain N times as long in x, same cell size)."""
     import dataclasses
-    if world == 1 and cfg.weak_div == 1:
+    if cells:
+        cfg = dataclasses.replace(cfg, cells=tuple(cells))
+    if world == 1 or scaling == "strong":
         return cfg
-    cx = cfg.cells[0] // cfg.weak_div
-    lx = cfg.lengths[0] / cfg.weak_div
-    cells = (cx * world,) + tuple(cfg.cells[1:])
-    lengths = (lx * world,) + tuple(cfg.lengths[1:])
-    desc = cfg.description
-    if cfg.weak_div > 1:
-        desc += f" -- weak unit {cx}x" + "x".join(map(str, cfg.cells[1:])) + \
-            f" cells per GPU ({world}/{cfg.weak_div} of the config)"
+    cells = (cfg.cells[0] * world,) + tuple(cfg.cells[1:])
+    lengths = (cfg.lengths[0] * world,) + tuple(cfg.lengths[1:])
+    desc = cfg.description + f" -- weak scaling: {world} config-sized x-slabs side by side"
     return dataclasses.replace(cfg, cells=cells, lengths=lengths, description=desc)
 
 
@@ -175,16 +184,33 @@ def sample_config(cfg, max_dofs=5_000_000):
     return dataclasses.replace(cfg, cells=tuple(cells), lengths=tuple(lengths))
 
 
-def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, device=None,
-                  cpu_sample=False):
-    """(cfg, space, model, scheme, U0, slab); the slab is None at N=1
-    unless ``force_slab``; ``cpu_sample``: the CPU baseline's bounded
-    x-slab of the config (sample_config)."""
+def replica_config(cfg, max_cells=20_000):
+    """A small mesh with the config's cell size (h), order, tags and
+    physics: the stiffness (rho ~ C nu / h^2) of the full
+    config, at a size the power iteration can afford next to a 24 GB
+    state."""
+    import dataclasses
+    cells, lengths = list(cfg.cells), list(cfg.lengths)
+    while int(np.prod(cells)) > max_cells:
+        ax = int(np.argmax(cells))
+        half = max(1, cells[ax] // 2)
+        lengths[ax] *= half / cells[ax]
+        cells[ax] = half
+    return dataclasses.replace(cfg, cells=tuple(cells), lengths=tuple(lengths))
+
+
+def build_problem(cfg_name, scheme_name, rank=0, world=1, scaling="strong", force_slab=False,
+                  device=None, cpu_sample=False, cells=None, cfg=None):
+    """(cfg, space, model, scheme, U0, slab).  U0 is a device tensor when
+    ``device`` is given (projected on the device at scale), else numpy.
+    The slab is None at N=1 unless ``force_slab``; ``cpu_sample``: the CPU
+    baseline's bounded x-slab of the config (sample_config)."""
     from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel
     from paper_1403_1157_b200.configs import CONFIGS, make_mesh
     from paper_1403_1157_b200.decomp import build_slab
     from paper_1403_1157_b200.fields import bump_field
-    cfg = weak_config(CONFIGS[cfg_name], world)
+    if cfg is None:
+        cfg = scaled_config(CONFIGS[cfg_name], world, scaling, cells)
     if cpu_sample:
         cfg = sample_config(cfg)
     slab = None
@@ -197,10 +223,14 @@ def build_problem(cfg_name, scheme_name, rank=0, world=1, force_slab=False, devi
     lo = np.zeros(cfg.dim)
     hi = np.asarray(cfg.lengths, dtype=float)
     fn = bump_field(cfg.dim, 6, 1, lo, hi)
-    if device is not None and (cfg.dim == 3 or mesh.n_elements > 500_000):
-        # host projection is slow at scale (~0.4 ms/tet at 3D p=3): on the GPU
-        from paper_1403_1157_b200.fields import project_bumps_device
-        U0 = project_bumps_device(space, fn, device).cpu().numpy()
+    if device is not None:
+        if cfg.dim == 3 or mesh.n_elements > 500_000:
+            # host projection is slow at scale (~0.4 ms/tet at 3D p=3)
+            from paper_1403_1157_b200.fields import project_bumps_device
+            U0 = project_bumps_device(space, fn, device)
+        else:
+            import torch
+            U0 = torch.from_numpy(np.ascontiguousarray(space.project(fn).coeffs)).to(device)
     else:
         U0 = np.ascontiguousarray(space.project(fn).coeffs)
     return cfg, space, PlaqueModel(), FluxScheme(scheme_name), U0, slab
@@ -230,18 +260,27 @@ def spectral_radius(op, U, iters):
     return rho
 
 
-def measured_hbm_gbs():
-    """Driver-measured HBM copy bandwidth (MEASURED_PEAKS.json), or None."""
+def replica_rho(cfg, scheme_name, device, iters):
+    """rho on a same-h replica (replica_config) of the config."""
+    from paper_1403_1157_b200.operator import DiscreteOperator
+    rc = replica_config(cfg)
+    _, space, model, scheme, U0, _ = build_problem(None, scheme_name, device=device, cfg=rc)
+    op = DiscreteOperator(space, model, scheme, device=device)
+    return spectral_radius(op, U0, iters), rc
+
+
+def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"])
-    except (OSError, ValueError, KeyError):
-        return None
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
 
 def fp64_peak(op):
     """Measured DFMA throughput (TFLOP/s) of this GPU; the roofline
-    denominator for the FP64-bound operator kernels."""
+    denominator for the FP64-bound operator kernels (MEASURED_PEAKS.json
+    has HBM and bf16 figures only)."""
     import ctypes
     import torch
     lib = op.lib
@@ -262,30 +301,61 @@ def fp64_peak(op):
     return best
 
 
-def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
-    """Time the CPU oracle port on the same config; returns (DoF-upd/s,
-    sample description, n_dofs)."""
+def host_cpu():
+    """(physical cores, CPU model) of this host."""
+    cores = None
+    try:
+        import psutil
+        cores = psutil.cpu_count(logical=False)
+    except ImportError:
+        pass
+    cores = cores or os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return int(cores), model
+
+
+def cpu_reference(cfg_name, scheme_name, steps, warmup, dt=None, repeats=1, cells=None):
+    """Time the CPU oracle port on a bounded sample of the config, under
+    the reference's own scaling protocol (analysis.scaling_study,
+    reference analysis.py:211-242: BLAS pinned to one thread, one worker
+    thread per physical core, best of ``repeats``).  Returns (DoF-upd/s,
+    best seconds, sample cells, sample DoFs, cores, cpu model)."""
+    from threadpoolctl import threadpool_limits
     from oracle import OracleOperator
-    cfg, space, model, scheme, U0, _ = build_problem(cfg_name, scheme_name, cpu_sample=True)
-    op = OracleOperator(space, model, scheme, nthreads=nthreads)
+    cfg, space, model, scheme, U0, _ = build_problem(cfg_name, scheme_name, cpu_sample=True,
+                                                     cells=cells)
+    cores, cpu_model = host_cpu()
+    op = OracleOperator(space, model, scheme, nthreads=cores)
     if dt is None:
         from paper_1403_1157_b200.configs import rho_constant
         h = float(space.mesh.diameters.min())
         dt = 0.8 * 2.51 / (rho_constant(cfg.dim, cfg.order) * 1e-2 / h ** 2)
-    U = U0.copy()
 
     def step(U):
         U1 = U + dt * op.apply_f(U)
         U2 = 0.75 * U + 0.25 * (U1 + dt * op.apply_f(U1))
         return U / 3.0 + (2.0 / 3.0) * (U2 + dt * op.apply_f(U2))
 
-    for _ in range(warmup):
-        U = step(U)
-    tic = time.perf_counter()
-    for _ in range(steps):
-        U = step(U)
-    el = time.perf_counter() - tic
-    return space.n_dofs * 3 * steps / el, el, cfg.cells, space.n_dofs
+    best = None
+    with threadpool_limits(1):
+        U = U0.copy()
+        for _ in range(warmup):
+            U = step(U)
+        for _ in range(max(1, repeats)):
+            tic = time.perf_counter()
+            for _ in range(steps):
+                U = step(U)
+            el = time.perf_counter() - tic
+            best = el if best is None else min(best, el)
+    return space.n_dofs * 3 * steps / best, best, cfg.cells, space.n_dofs, cores, cpu_model
 
 
 # ---------------------------------------------------------------- arms
@@ -293,30 +363,30 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, nthreads, dt=None):
 def run_reference_arm(args, rank):
     if rank != 0:
         return
-    nthreads = os.cpu_count() or 1
-    steps = max(1, args.steps)
-    warm = max(0, min(args.warmup, 1))
-    val, el, cells, ndofs = cpu_reference(args.config, args.scheme, steps, warm, nthreads)
-    full = tuple(weak_config(__import__("paper_1403_1157_b200.configs", fromlist=["CONFIGS"])
-                             .CONFIGS[args.config], 1).cells)
-    where = ("one full " + args.config + "-sized mesh (= one rank's weak-scaling slab)"
-             if tuple(cells) == full else
-             "a " + "x".join(map(str, cells)) + "-cell x-slab of the " + args.config
-             + " mesh (same cells, order, physics; bounded CPU sample)")
+    steps = max(1, args.steps if args.config != "c5" else 1)
+    warm = min(args.warmup, 1)
+    cells = tuple(int(c) for c in args.cells.split("x")) if args.cells else None
+    val, el, scells, ndofs, cores, cpu_model = cpu_reference(
+        args.config, args.scheme, steps, warm, repeats=3, cells=cells)
     from paper_1403_1157_b200.configs import CONFIGS
+    cfg = scaled_config(CONFIGS[args.config], 1, "strong", cells)
+    where = ("the full " + args.config + " mesh" if tuple(scells) == tuple(cfg.cells) else
+             "a " + "x".join(map(str, scells)) + "-cell x-slab of the " + args.config
+             + " mesh (same cells, order, physics; bounded CPU sample)")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": el / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian bumps, L2-projected)",
-        "config": {"workload": CONFIGS[args.config].description
+        "config": {"workload": cfg.description
                    + f", {args.scheme}, SSP-RK3 steps (3 f-evals each)",
-                   "n_dofs": ndofs},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthreads,
-                         "kind": "port",
-                         "sample": f"{steps} SSP-RK3 steps of {where}, numpy oracle "
-                                   f"port of the reference (oracle/), {nthreads} threads"},
+                   "n_dofs_sample": ndofs},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model,
+                         "sample": f"{steps} SSP-RK3 step(s) of {where}, numpy oracle port "
+                                   f"of the reference (oracle/), {cores} worker threads "
+                                   f"(physical cores), BLAS pinned to 1 thread, best of 3"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -330,6 +400,17 @@ def log(msg):
     print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
+def _init_dist(args, world, dev):
+    import torch
+    if world > 1 or "RANK" in os.environ:
+        import torch.distributed as dist
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # testing only: host-staged exchange, several ranks per GPU
+            dist.init_process_group("gloo")
+    return torch.distributed.is_available() and torch.distributed.is_initialized()
+
+
 def run_native_arm(args, rank, world, local):
     import torch
     from paper_1403_1157_b200.operator import DiscreteOperator
@@ -338,38 +419,23 @@ def run_native_arm(args, rank, world, local):
     local = local % max(torch.cuda.device_count(), 1)  # testing: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 or "RANK" in os.environ:
-        import torch.distributed as dist
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:  # testing only: host-staged exchange, several ranks per GPU
-            dist.init_process_group("gloo")
-    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
-    cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
-                                                         args.force_slab, dev)
+    dist_on = _init_dist(args, world, dev)
+    cells = tuple(int(c) for c in args.cells.split("x")) if args.cells else None
+    cfg, space, model, scheme, U, slab = build_problem(args.config, args.scheme, rank, world,
+                                                       args.scaling, args.force_slab, dev,
+                                                       cells=cells)
     log(f"problem built: {space.mesh.n_elements} elements")
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
-                          global_ids=None if slab is None else slab.global_ids,
-                          bands=args.bands)
-    log("operator created")
+                          global_ids=None if slab is None else slab.global_ids)
+    log(f"operator created: {op.tables.n_seg} colour segments")
     if args.variant:
-        op.set_variant(generic=bool(args.variant & 1), vol4=bool(args.variant & 2),
-                       serial=bool(args.variant & 4), flip_mma=bool(args.variant & 8),
-                       mma_volume=bool(args.variant & 16),
-                       no_graph=bool(args.variant & 32),
-                       tc_volume=bool(args.variant & 4096),
-                       no_tc_faces=bool(args.variant & 8192),
-                       volume_first=bool(args.variant & 16384),
-                       face_rows_tc=bool(args.variant & 32768),
-                       one_copy_stream=bool(args.variant & 65536),
-                       walls_first=bool(args.variant & 131072),
-                       copy_streams=(args.variant >> 18) & 7,
-                       face_ctas_per_sm=(args.variant >> 8) & 15)
+        op.lib.tdg_set_variant(op._ctx, args.variant)
     t = op.tables
     d, nb = t.dim, t.nb
     ne, n_int, n_bnd = op.n_owned, len(t.if_code), len(t.bf_code)
     n_dofs = ne * 6 * nb          # owned DoFs of this rank
+    big = cfg.dim == 3 and np.prod(cfg.cells) * 6 * 6 * nb > BIG_DOFS
 
     from paper_1403_1157_b200.stepping import SSPRK3
     halo = None
@@ -377,22 +443,27 @@ def run_native_arm(args, rank, world, local):
         from paper_1403_1157_b200.decomp import HaloExchange
         halo = HaloExchange(slab, dev)
     stepper = SSPRK3(op, halo)
-    U = torch.from_numpy(U0h).to(dev)
     if dist_on:
         # initialise the NCCL communicator with a collective before the
         # first batched point-to-point exchange
         torch.distributed.barrier()
     if halo is not None:
         halo.exchange(U)
-    rho = spectral_radius(op, U, args.power_iters)
+    if big:   # a 24 GB state leaves no room for the power iteration's vectors
+        rho, rcfg = replica_rho(cfg, args.scheme, dev, args.power_iters)
+        rho_src = ("power iteration on a same-h replica (" + "x".join(map(str, rcfg.cells))
+                   + " cells)")
+    else:
+        rho = spectral_radius(op, U, args.power_iters)
+        rho_src = "power iteration on the benchmark state"
     if dist_on:
         rr = torch.tensor([rho], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(rr, op=torch.distributed.ReduceOp.MAX)
         rho = rr.item()
     dt = 0.8 * 2.51 / rho
-    log(f"rho {rho:.4e}")
+    log(f"rho {rho:.4e} ({rho_src}), dt {dt:.3e}")
 
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = None if big else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def barrier():
         if dist_on:
@@ -401,6 +472,7 @@ def run_native_arm(args, rank, world, local):
     for _ in range(args.warmup):
         stepper.step(U, dt)
     torch.cuda.synchronize()
+    log("warm-up done")
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -410,7 +482,8 @@ def run_native_arm(args, rank, world, local):
     barrier()
     torch.cuda.synchronize()
     for a, b in evs:
-        flush.fill_(1.0)
+        if flush is not None:
+            flush.fill_(1.0)
         a.record()
         stepper.step(U, dt)
         b.record()
@@ -422,15 +495,17 @@ def run_native_arm(args, rank, world, local):
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = tt.item()
+    log(f"timed: {ms / args.steps:.3f} ms/step")
     # per-kernel times: a separate, untimed profiling pass (per-launch CUDA
-    # events on the launching streams; the timed steps above replay the
+    # events on the launching stream; the timed steps above replay the
     # step's CUDA graph, which per-kernel events would break up)
-    nprof = max(1, min(args.steps, 5))
+    nprof = 1 if big else max(1, min(args.steps, 5))
     op.profile(True)
     pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(nprof)]
     for a, b in pevs:
-        flush.fill_(1.0)
+        if flush is not None:
+            flush.fill_(1.0)
         a.record()
         stepper.step(U, dt)
         b.record()
@@ -445,61 +520,59 @@ def run_native_arm(args, rank, world, local):
         total_dofs = int(td.item())
     value = total_dofs * 3 * args.steps / (ms * 1e-3)
 
-    # per-kernel roofline (algorithmic flops of the reference sequence)
+    # per-kernel roofline (algorithmic flops of the reference sequence,
+    # per application; every kernel class runs once per colour segment)
     Q, F = t.nq_vol, t.nq_face
     fv, ff, fb = apply_flops(d, nb, Q, F, ne, n_int, n_bnd)
+    names = {"faces": "k_faces_tcs" if d == 3 else "k_faces_fast", "wall": "k_faces_mma"
+             if d == 3 else "k_faces_fast (walls)", "volume": "k_volume_tc"
+             if (d == 3 or t.order == 3) else "k_volume_fast"}
     per = {}
-    for name, flops in (("faces", ff), ("wall", fb), ("volume", fv), ("fc_add", 0.0)):
+    for name, flops in (("faces", ff), ("wall", fb), ("volume", fv)):
         tms, nl = kt[name]
         if nl:
-            per[name] = {"avg_ms": tms / nl, "launches": nl * args.steps // nprof,
-                         "algorithmic_tflops": flops / (tms / nl * 1e-3) / 1e12,
+            apps = 3 * nprof
+            per[name] = {"kernel": names[name], "ms_per_application": tms / apps,
+                         "launches_per_application": nl / apps,
+                         "algorithmic_tflops": flops / (tms / apps * 1e-3) / 1e12,
                          "share_of_step": tms / ms_prof}
-    if "fc_add" in per and "volume" in per:
-        # overlapped schedule: the volume part is launched on a second
-        # stream beside the face kernel; its event span includes waiting for
-        # SM resources the face kernel holds
-        per["volume"]["note"] = "launched concurrently with faces; span includes co-scheduling"
     peak = fp64_peak(op)
-    if "fc_add" in per:  # streaming kernel: report its bandwidth instead
-        per["fc_add"]["gbs"] = (t.dim + 3) * n_dofs * 8 / (per["fc_add"]["avg_ms"] * 1e-3) / 1e9
-        hbm = measured_hbm_gbs()
-        if hbm:
-            per["fc_add"]["hbm_peak_gbs"] = hbm
-            per["fc_add"]["hbm_frac"] = per["fc_add"]["gbs"] / hbm
-            per["fc_add"]["note"] = ("algorithmic bytes (d+1 slots + out read + out write) per "
-                                     "launch / time; MEASURED_PEAKS.json copy bandwidth; >1 means "
-                                     "part of the slots were still in L2")
-    # the face kernel starts first and runs alone on the SMs it holds: its
-    # span is its own duration; in the serial schedule take the longest
-    dom = "faces" if ("faces" in per and "fc_add" in per) else \
-        max((k for k in per if k != "fc_add"), key=lambda k: per[k]["avg_ms"])
+    pk = measured_peaks()
+    dom = max(per, key=lambda k: per[k]["share_of_step"])
     traffic = None
-    try:  # dram read+write bytes per launch from the committed ncu capture
+    try:  # dram read+write bytes per application from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh)["bytes_per_launch"].get(f"k_{dom}")
+            tr = json.load(fh)
+        ent = tr["bytes_per_application"].get(f"{args.config}:{per[dom]['kernel']}")
+        traffic = ent
     except (OSError, ValueError, KeyError):
         traffic = None
     step_flops = 3 * (fv + ff + fb)
-    roof = {"bound": "fp64", "kernel": f"k_{dom}",
+    step_s = ms / args.steps * 1e-3
+    roof = {"bound": "fp64", "kernel": per[dom]["kernel"],
             "bound_note": "fp64 workload (north_star: achieved FP64 throughput against the B200 "
-                          "FP64 peak); DFMA and DMMA share the 37 TFLOP/s FP64 datapath, so "
-                          "neither 'hbm' (<= 0.6 TB/s compulsory per step) nor the bf16 "
-                          "tensor peak bounds it",
+                          "FP64 peak); DFMA and DMMA share the FP64 datapath, so neither 'hbm' "
+                          "(compulsory traffic far below 1 TB/s) nor the bf16 tensor peak "
+                          "bounds it",
             "achieved": per[dom]["algorithmic_tflops"], "peak": peak,
             "unit": "TFLOP/s", "frac": per[dom]["algorithmic_tflops"] / peak,
             "traffic": traffic,
-            "traffic_source": "profiles/ncu_traffic.json (ncu --set full dram bytes/launch)",
-            "peak_source": "measured DFMA loop (tdg_fp64_probe) on this GPU; "
-                           f"nominal {FP64_NOMINAL_TFLOPS} TFLOP/s; "
-                           "MEASURED_PEAKS.json has no fp64 figure",
+            "achieved_note": "algorithmic flops of the kernel class per application (SURVEY "
+                             "8(d) per-face / per-element figures x counts) / the summed "
+                             "duration of its launches per application (one per colour "
+                             "segment), CUDA events on the launching stream",
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full dram bytes per "
+                              "application, summed over the kernel's launches)",
+            "peak_source": "builder-measured DFMA peak (tdg_fp64_probe, 16 independent FMA "
+                           f"chains per thread) on this GPU; nominal {FP64_NOMINAL_TFLOPS} "
+                           "TFLOP/s; MEASURED_PEAKS.json has no fp64 figure",
             "per_kernel": per,
-            "step_algorithmic_tflops": step_flops / (ms / args.steps * 1e-3) / 1e12,
-            "step_frac": step_flops / (ms / args.steps * 1e-3) / 1e12 / peak,
+            "step_algorithmic_tflops": step_flops / step_s / 1e12,
+            "step_frac": step_flops / step_s / 1e12 / peak,
             "step_executed_tflops": 3 * executed_flops(d, nb, Q, F, ne, n_int, n_bnd)
-            / (ms / args.steps * 1e-3) / 1e12,
-            "step_hbm_gbs_compulsory": 3 * apply_bytes(d, n_dofs, ne, n_int, n_bnd)
-            / (ms / args.steps * 1e-3) / 1e9}
+            / step_s / 1e12,
+            "step_hbm_gbs_compulsory": 3 * apply_bytes(d, n_dofs, ne, n_int, n_bnd) / step_s / 1e9,
+            "hbm_peak_gbs": pk.get("hbm_gbs")}
 
     # end to end through the public API: pinned host U -> device, one
     # SSP-RK3 step, result back to host, every step
@@ -507,30 +580,31 @@ def run_native_arm(args, rank, world, local):
     if not args.no_e2e:
         # the public host-data call: every step copies the state in from
         # pinned host memory and the result back out (undecomposed runs:
-        # DiscreteOperator.ssprk3_steps_host, copies pipelined by element
-        # bands; slab runs: copy-in, SSPRK3 step with the exchange, copy-out)
-        Uh = torch.from_numpy(U0h).pin_memory()
+        # DiscreteOperator.ssprk3_steps_host; slab runs: copy-in, SSPRK3
+        # step with the exchange, copy-out)
+        log("e2e: pinning the host state")
+        Uh = U.cpu().pin_memory()
         host_api = slab is None
+        work = stepper._work if stepper._work is not None else op.new_work()
         if host_api:
-            op.ssprk3_steps_host(Uh, 2, dt)
+            op.ssprk3_steps_host(Uh, 1, dt, U=U, work=work)
         else:
-            Ud = torch.empty_like(U)
-            for _ in range(2):
-                Ud.copy_(Uh, non_blocking=True)
-                stepper.step(Ud, dt)
-                Uh.copy_(Ud, non_blocking=True)
+            for _ in range(1):
+                U.copy_(Uh, non_blocking=True)
+                stepper.step(U, dt)
+                Uh.copy_(U, non_blocking=True)
         torch.cuda.synchronize()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         t_enq = time.perf_counter()
         if host_api:
-            op.ssprk3_steps_host(Uh, args.steps, dt)
+            op.ssprk3_steps_host(Uh, args.steps, dt, U=U, work=work)
         else:
             for _ in range(args.steps):
-                Ud.copy_(Uh, non_blocking=True)
-                stepper.step(Ud, dt)
-                Uh.copy_(Ud, non_blocking=True)
+                U.copy_(Uh, non_blocking=True)
+                stepper.step(U, dt)
+                Uh.copy_(U, non_blocking=True)
         b.record()
         t_enq = time.perf_counter() - t_enq
         b.synchronize()
@@ -543,8 +617,29 @@ def run_native_arm(args, rank, world, local):
                "h2d_bytes_per_step": Uh.numel() * 8, "d2h_bytes_per_step": Uh.numel() * 8,
                "ms_per_step": ems / args.steps, "host_issue_ms_per_step": t_enq * 1e3 / args.steps,
                "api": "DiscreteOperator.ssprk3_steps_host (tdg_ssprk3_steps_host): per-step "
-                      "copy-in / copy-out pipelined by element bands" if host_api else
+                      "copy-in / copy-out of the pinned host state in 8 chunks, overlapping "
+                      "the previous step's copy-out and the last stage" if host_api else
                       "copy-in, SSPRK3.step with the halo exchange, copy-out per step"}
+        log(f"e2e: {ems / args.steps:.3f} ms/step")
+        # the reference's own call shape: one apply_f(numpy) -> numpy per
+        # f-evaluation (reference operator.py:286; its stepper composes
+        # three per SSP-RK3 step), pageable host memory both ways
+        if slab is None:
+            Un = Uh.numpy()
+            op.apply_f(Un)
+            torch.cuda.synchronize()
+            nrep = 1 if big else 5
+            tic = time.perf_counter()
+            for _ in range(nrep):
+                Fh = op.apply_f(Un)
+            el = (time.perf_counter() - tic) / nrep
+            e2e["reference_call_shape"] = {
+                "value": n_dofs / el, "unit": UNIT, "ms_per_apply_f": el * 1e3,
+                "h2d_bytes_per_call": Un.nbytes, "d2h_bytes_per_call": Fh.nbytes,
+                "api": "DiscreteOperator.apply_f(numpy) -> numpy, one f-evaluation per call "
+                       "(wall clock, pageable host arrays, result allocated per call)"}
+            del Fh, Un
+        del Uh
 
     # the reference's default integrator on the same state:
     # one SDIRK3 + JFNK step at dt 0.01 (C2) with the reference's Newton /
@@ -554,7 +649,7 @@ def run_native_arm(args, rank, world, local):
         from paper_1403_1157_b200.timeint import integrate
         nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
               "gmres_restart": 30, "gmres_maxiter": 200}
-        Ui = torch.from_numpy(U0h).to(dev)
+        Ui = U.clone()
         integrate(op, Ui, 0.0, 1.0, 0.01, order=3, n_steps=1, newton_kwargs=nk)  # warm-up
         torch.cuda.synchronize()
         ia, ib = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -565,7 +660,7 @@ def run_native_arm(args, rank, world, local):
         ims = ia.elapsed_time(ib)
         implicit = {"value": n_dofs * res.f_evaluations / (ims * 1e-3), "unit": UNIT,
                     "integrator": "SDIRK3 + JFNK (reference defaults: Newton 1e-8/1e-12/25, "
-                                  "GMRES(30) 1e-4/200), dt 0.01, 1 step from U0 after 1 warm-up step",
+                                  "GMRES(30) 1e-4/200), dt 0.01, 1 step after 1 warm-up step",
                     "ms_per_step": ims, "f_evaluations": res.f_evaluations,
                     "newton_iterations": res.newton_iterations,
                     "gmres_iterations": res.gmres_iterations}
@@ -573,32 +668,41 @@ def run_native_arm(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nthreads = os.cpu_count() or 1
-        val, el, cells, _ = cpu_reference(args.config, args.scheme, 1, 0, nthreads, dt=dt)
-        where = (f"the full {args.config} mesh" if tuple(cells) == tuple(cfg.cells) else
-                 "a " + "x".join(map(str, cells)) + f"-cell x-slab of the {args.config} mesh "
+        log("cpu baseline")
+        val, el, scells, _, cores, cpu_model = cpu_reference(args.config, args.scheme, 1, 0,
+                                                             dt=dt, repeats=3, cells=cells)
+        where = (f"the full {args.config} mesh" if tuple(scells) == tuple(cfg.cells) else
+                 "a " + "x".join(map(str, scells)) + f"-cell x-slab of the {args.config} mesh "
                  "(same cells, order, physics; bounded CPU sample)")
-        cpu = {"value": val, "unit": UNIT, "cores": nthreads, "kind": "port",
-               "sample": f"1 SSP-RK3 step (3 apply_f) of {where}, "
-                         f"numpy oracle port, {nthreads} threads, {el:.1f} s"}
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+               "cpu_model": cpu_model,
+               "sample": f"1 SSP-RK3 step (3 apply_f) of {where}, numpy oracle port, "
+                         f"{cores} worker threads (physical cores), BLAS pinned to 1 thread, "
+                         f"best of 3: {el:.1f} s"}
 
-    launches = sum(v["launches"] for v in per.values())
+    launches = int(sum(v["launches_per_application"] for v in per.values()) * 3 * args.steps)
     if rank == 0:
+        par = "1 GPU" if world == 1 else (
+            f"x-slabs x{world}, NCCL ghost-row exchange per stage overlapped with the owned-row "
+            f"faces, " + ("strong scaling (the fixed config split)" if args.scaling == "strong"
+                          else "weak scaling (one config-sized slab per GPU)"))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Gaussian bumps, L2-projected on host)",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian bumps, L2-projected)",
             "config": {"workload": cfg.description + f", {args.scheme}, SSP-RK3 "
                        "steps (3 fused f-evals + stage updates each)",
-                       "n_elements": ne, "n_dofs": n_dofs, "interior_faces": n_int,
-                       "boundary_faces": n_bnd, "dt": dt, "rho": rho,
-                       "l2": "flushed between timed steps (256 MiB write outside "
-                             "the timed events)",
-                       "parallelism": (f"x-slabs x{world}, NCCL ghost-row exchange per stage, "
-                            "weak scaling (one config-sized slab per GPU)")
-                           if world > 1 else "1 GPU"},
+                       "n_elements": int(np.prod(cfg.cells)) * (2 if d == 2 else 6),
+                       "n_dofs": total_dofs, "interior_faces_rank0": n_int,
+                       "boundary_faces_rank0": n_bnd, "colour_segments": t.n_seg,
+                       "dt": dt, "rho": rho, "rho_source": rho_src,
+                       "l2": ("inputs larger than L2 (state vectors of "
+                              f"{n_dofs * 8 / 1e9:.1f} GB), no flush") if big else
+                             "flushed between timed steps (256 MiB write outside the timed "
+                             "events)",
+                       "parallelism": par},
             "roofline": roof, "clocks": clocks, "gpu_launches": launches,
             **({"implicit": implicit} if implicit else {}),
         }
@@ -612,26 +716,22 @@ def run_native_arm(args, rank, world, local):
 
 
 def run_implicit(args, rank, world, local):
-    """C2 with the reference's default integrator: SDIRK3 + JFNK (dt 0.01,
-    Newton 1e-8/1e-12/25, GMRES 1e-4/30/200; reference config.py:74-83).
+    """The reference's default integrator: SDIRK3 + JFNK (dt 0.01, Newton
+    1e-8/1e-12/25, GMRES 1e-4/30/200; reference config.py:74-83).
     DoF-updates counted per actual f evaluation.  N > 1:
-    weak-scaled slabs, ghost exchange inside every G(V) and the Krylov
-    scalars all-reduced over NCCL (timeint.SlabReductions)."""
+    slabs, ghost exchange inside every G(V) and the Krylov scalars
+    all-reduced over NCCL (timeint.SlabReductions)."""
     import torch
     from paper_1403_1157_b200.operator import DiscreteOperator
     from paper_1403_1157_b200.timeint import integrate
     local = local % max(torch.cuda.device_count(), 1)  # testing: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 or "RANK" in os.environ:
-        import torch.distributed as dist
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:  # testing only: host-staged exchange, several ranks per GPU
-            dist.init_process_group("gloo")
-    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
-    cfg, space, model, scheme, U0h, slab = build_problem(args.config, args.scheme, rank, world,
-                                                         args.force_slab, dev)
+    dist_on = _init_dist(args, world, dev)
+    cells = tuple(int(c) for c in args.cells.split("x")) if args.cells else None
+    cfg, space, model, scheme, U, slab = build_problem(args.config, args.scheme, rank, world,
+                                                       args.scaling, args.force_slab, dev,
+                                                       cells=cells)
     op = DiscreteOperator(space, model, scheme, device=dev,
                           n_owned=None if slab is None else slab.n_owned,
                           global_ids=None if slab is None else slab.global_ids)
@@ -639,7 +739,6 @@ def run_implicit(args, rank, world, local):
     if slab is not None:
         from paper_1403_1157_b200.decomp import HaloExchange
         halo = HaloExchange(slab, dev)
-    U = torch.from_numpy(U0h).to(dev)
     if dist_on:
         torch.distributed.barrier()
     nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
@@ -666,8 +765,9 @@ def run_implicit(args, rank, world, local):
     if rank == 0:
         line = {"metric": METRIC, "value": n_dofs * res.f_evaluations / (ms * 1e-3),
                 "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
                 "config": {"workload": cfg.description + f", {args.scheme}, SDIRK3 + JFNK "
                            f"(reference defaults), dt {args.dt}",
                            "f_evaluations": res.f_evaluations,

@@ -14,6 +14,14 @@
  *                              (SSP-RK3 composition of apply_f, SURVEY 8(a) a14;
  *                              DIRK stage algebra timeint.py:315-333)
  *   tdg_ssprk3_step            three fused stages (Shu-Osher form)
+ *   tdg_ssprk3_steps_host      the same on a host state, copies every step
+ *   tdg_species_totals         DiscreteFunction.species_totals fespace.py:170-174
+ *   tdg_species_l2             analysis.l2_error of two fields     analysis.py:30-50
+ *   tdg_mgs                    GMRES Arnoldi MGS sweep             timeint.py:162-170
+ *   tdg_color_faces            (host) face colouring that orders the face
+ *                              loop; replaces the RCB partition /
+ *                              private-buffer merge that makes the
+ *                              reference's sums race-free, operator.py:208-284
  *   tdg_dot / tdg_norm2        Krylov scalars: `w @ V[i]`, `np.linalg.norm`
  *                              in gmres_solve/newton_solve timeint.py:148-202,
  *                              timeint.py:242-280
@@ -24,12 +32,25 @@
  * (fp64, C order, n_elements x n_species x nb, fespace.py:46-69).  The
  * descriptor's table/geometry pointers are device pointers owned by the
  * caller and must outlive the context; the small host arrays
- * (diffusivity, lin_source, params) are copied at create time.  Streams
- * are `cudaStream_t` passed as `void*` (NULL = legacy default stream).
- * No call allocates after tdg_create.  Every call returns 0 on success or
- * a negative TDG_E* code; tdg_last_error() gives a message (thread-local).
- * The per-apply sums are grouped in a fixed order: results are bitwise
- * reproducible run to run (reference contract tests/test_operator.py:113-119).
+ * (diffusivity, lin_source, params, seg_ptr) are copied at create time.
+ * Streams are `cudaStream_t` passed as `void*` (NULL = legacy default
+ * stream).  No call allocates device memory, streams or events after
+ * tdg_create (state vectors and work buffers are the caller's).  Every
+ * call returns 0 on success or a negative TDG_E* code; tdg_last_error()
+ * gives a message (thread-local).
+ *
+ * Face loop: the faces come in colour segments (tdg_color_faces): within
+ * a segment no element is touched twice, so each face adds its two
+ * contribution blocks straight into the elements' face-sum rows (no
+ * atomics, no per-face buffers), and the segments run in a fixed order,
+ * so every sum has a fixed order: results are bitwise reproducible run to
+ * run (reference contract tests/test_operator.py:113-119).
+ *
+ * One context = one stream at a time: the reduction workspace, the copy
+ * streams / events and the cached SSP-RK3 graph are per context, so two
+ * calls on the same context must not run concurrently on different
+ * streams (the reference allows one evaluation at a time per instance,
+ * SPEC.md:423).
  */
 #ifndef TAXISDG_B200_H
 #define TAXISDG_B200_H
@@ -40,7 +61,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 2
+#define TDG_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -67,6 +88,8 @@ enum tdg_scheme { TDG_CDG2 = 0, TDG_CDG = 1, TDG_BR2 = 2, TDG_IP = 3, TDG_BO = 4
 #define TDG_CODE_TAG(c)     (((c) >> 11) & 7)   /* BoundaryTag (boundary faces)  */
 #define TDG_CODE_MIRROR     (1 << 14)           /* Dirichlet mirror exterior     */
 #define TDG_CODE_SKIP_OUT   (1 << 15)           /* outside is a ghost: no write  */
+#define TDG_CODE_FIRST_IN   (1 << 16)           /* inside's first face: write     */
+#define TDG_CODE_FIRST_OUT  (1 << 17)           /* outside's first face: write    */
 
 typedef struct tdg_desc {
   int32_t dim;            /* 2 or 3 */
@@ -99,40 +122,36 @@ typedef struct tdg_desc {
   const double* face_w;       /* [F]          face weights */
   const double* elem_geo;     /* [ne*(1+d(d+1)/2)]  detJ, sym(Jinv Jinv^T) */
   const int32_t* if_elems;    /* [nif*2]  inside, outside row (-1 mirror) */
-  const int32_t* if_lf;       /* [nif*2]  local face index per side */
   const int32_t* if_code;     /* [nif]    packed code word */
   const double* if_geo;       /* [nif*(2d+4)] jn_in, jn_out, sfac, h, 1/detJ_in, 1/detJ_out */
   const int32_t* bf_elem;     /* [nbf]    inside row */
-  const int32_t* bf_lf;       /* [nbf]    local face index */
   const int32_t* bf_code;     /* [nbf]    packed code word */
   const double* bf_geo;       /* [nbf]    sfac */
-  /* optional: zero-padded per-signature operand tables of the tensor-core
-   * (DMMA) face kernel, layout of tables.mma_face_tables (NULL disables it) */
+  /* optional: zero-padded per-signature operand tables of the element-
+   * local tensor-core (DMMA) face kernel, layout of
+   * tables.mma_face_tables (NULL disables it) */
   const double* face_mma;
-  /* optional: padded operand tables of the tensor-core volume kernel
-   * (tables.mma_volume_tables, NULL disables it) */
-  const double* vol_mma;
-  /* the last n_cut_faces interior faces touch ghost rows (slab runs) */
-  int64_t n_cut_faces;
   /* operand tables of the transposed tensor-core volume kernel
    * (tables.tc_volume_tables, may be NULL) */
   const double* vol_tc;
-  /* transposed tensor-core face kernel (3D): per-signature operand tables
+  /* species-rows tensor-core face kernel (3D): per-signature operand tables
    * (tables.tc_face_tables, stride from the compiled sizes) and blocks of up
    * to 8 interior faces of one signature, int32 [n_face_blocks][2] = (first
-   * face, count), the last n_face_blocks_cut of them cut faces (may be NULL) */
+   * face, count), never straddling a segment (may be NULL) */
   const double* face_tc;
   const int32_t* face_blocks;
   int64_t n_face_blocks;
-  int64_t n_face_blocks_cut;
-  /* host-pipelined stepping: n_bands contiguous element bands (1 = none),
-   * band_ptr (HOST) = elements [n_bands+1] | interior-face offsets
-   * [2 n_bands+1] (faces internal to band k from [2k], straddling (k, k+1)
-   * from [2k+1]) | wall offsets [n_bands+1] | face-block offsets
-   * [n_bands+1] (the blocks of band k's faces, which no block straddles),
-   * tables.build_tables / tc_face_blocks order */
-  int32_t n_bands;
-  const int64_t* band_ptr;
+  /* face colour segments, run in order: segment s covers the interior
+   * faces [I[s], I[s+1]), the walls [W[s], W[s+1]) and the face blocks
+   * [B[s], B[s+1]) with seg_ptr (HOST) = I[n+1] | W[n+1] | B[n+1].  No
+   * element is written twice within a segment, and each element's first
+   * written face side (in segment order) carries TDG_CODE_FIRST_IN/OUT and
+   * every owned element has at least one face.  The last n_segments_cut
+   * segments hold the faces that read ghost rows (slab runs: run after
+   * the exchange, tdg_rk_stage_part part 2). */
+  int32_t n_segments;
+  int32_t n_segments_cut;
+  const int64_t* seg_ptr;
 } tdg_desc;
 
 typedef struct tdg_ctx tdg_ctx;
@@ -144,16 +163,18 @@ TDG_API int tdg_create(const tdg_desc* desc, tdg_ctx** out);
 TDG_API int tdg_destroy(tdg_ctx* ctx);
 
 /* R = L_h(U) (mass_inverse=0) or M^-1 L_h(U) (mass_inverse=1).
- * U has n_elements + n_ghost rows; R has n_elements rows.  t is accepted
- * for API parity (the plaque/reduced/diffusion models are autonomous). */
+ * U has n_elements + n_ghost rows; R has n_elements rows and must not
+ * alias U (the face sums accumulate in R).  t is accepted for API parity
+ * (the plaque/reduced/diffusion models are autonomous). */
 TDG_API int tdg_apply(tdg_ctx* ctx, const double* U, double* R, double t,
               int mass_inverse, void* stream);
 
-/* out = a*U0 + b*U + c*M^-1 L_h(U); U0 may be NULL when a == 0; out may
- * alias U0.  out may alias U too, but then the volume part cannot overlap
- * the face kernel (serial schedule). */
+/* out = a*U0 + b*U + c*M^-1 L_h(U); U0 may be NULL when a == 0.  acc
+ * (n_elements rows) receives the face sums: NULL means acc = out.  acc
+ * must not alias U, nor U0 when a != 0; out may alias U0, and may alias U
+ * when acc does not. */
 TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out,
-                 double a, double b, double c, double t, void* stream);
+                 double* acc, double a, double b, double c, double t, void* stream);
 
 /* A stage split around a ghost-row exchange (slab-decomposed runs):
  * part 1 launches everything that reads owned rows only (volume terms,
@@ -161,22 +182,25 @@ TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double
  * place, launches the cut faces and the final sum.  Same arguments and
  * result as tdg_rk_stage. */
 TDG_API int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out,
-                              double a, double b, double c, double t, int part, void* stream);
+                              double* acc, double a, double b, double c, double t, int part,
+                              void* stream);
 
 /* nsteps SSP-RK3 steps of a HOST state (pinned memory, undecomposed
- * mesh): every step copies the state in and the result out, pipelined by
- * element bands (the copy-in of band k overlaps the work of the bands
- * already resident; the final stage is finished and copied out band by
- * band; step n+1's copy-in of band k follows step n's copy-out of band
- * k).  Bitwise the same result as copy-in, tdg_ssprk3_step, copy-out per
- * step.  The public host-data entry point of the end-to-end measurement. */
-TDG_API int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, int64_t nsteps, double t,
-                                  double dt, void* stream);
+ * mesh), through the device buffers U, w1, w2 (shape of U): every step
+ * copies the state in and the result out, in element chunks on two copy
+ * streams per direction -- step n+1's copy-in of chunk k follows step
+ * n's copy-out of chunk k, and the last stage's volume kernel runs chunk
+ * by chunk so the copy-out starts with the first chunk.  Bitwise the same
+ * result as copy-in, tdg_ssprk3_step, copy-out per step.  The public
+ * host-data entry point of the end-to-end measurement. */
+TDG_API int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, double* U, double* w1,
+                                  double* w2, int64_t nsteps, double t, double dt, void* stream);
 
-/* one Shu-Osher SSP-RK3 step in place on U; work has the shape of U (a
- * second stage vector is allocated by the library on first use). */
-TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt,
-                    void* stream);
+/* one Shu-Osher SSP-RK3 step in place on U (three state vectors: U and
+ * the work vectors w1, w2 of the shape of U); undecomposed meshes only
+ * (slab runs exchange ghost rows between stages: tdg_rk_stage_part). */
+TDG_API int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* w1, double* w2, double t,
+                            double dt, void* stream);
 
 /* Species totals int u_s over the owned elements, written to totals[S]
  * (device): sqrt(|ref simplex|) * sum_e detJ_e U[e,s,0].  Replaces
@@ -236,32 +260,20 @@ TDG_API int tdg_jv_shift(const double* U, const double* v, const double* vnorm, 
 TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t n, void* stream);
 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
- * CTA-staged generic kernels; bit 1: use the four-lanes-per-element
- * volume kernel instead of the one-thread-per-element one; bit 2: run
- * volume and faces serially on the caller's stream instead of the
- * overlapped two-stream schedule; bit 3: flip the face-kernel choice
- * between the tensor-core (DMMA) kernel and the SIMT kernel; bit 4: use
- * the tensor-core volume kernel instead of the SIMT one; bit 5: launch
- * tdg_ssprk3_step's kernels directly instead of replaying its cached CUDA
- * graph; bit 14: in the overlapped schedule launch the volume part before
- * the face kernel (default: faces first); bit 13: in 3D, use the element-local DMMA face kernel for interior
- * faces instead of the transposed one; bit 15: in 3D, use the faces-as-rows
- * transposed face kernel instead of the species-as-rows one; bit 16:
- * tdg_ssprk3_steps_host with one copy stream per direction; bits 18-20:
- * that many copy streams per direction (0: default); bit 17: 3D wall
- * faces before the interior ones; bit 12: use the transposed tensor-core volume kernel wherever it
- * compiles (default only where the one-thread-per-element kernel does not
- * fit); bits 8-11: CTAs
- * per SM of the register-resident face kernel's grid-stride grid (0 =
+ * CTA-staged generic kernels; bit 5: launch tdg_ssprk3_step's kernels
+ * directly instead of replaying its cached CUDA graph; bit 12: use the
+ * transposed tensor-core volume kernel wherever it compiles (default only
+ * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
+ * per SM of the 2D register-resident face kernel's grid-stride grid (0 =
  * default, 15 = uncapped, one face group per warp).  0 (default) lets the
- * library pick the fastest compiled-in kernels and schedule. */
+ * library pick the fastest compiled-in kernels. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 
 /* Per-kernel device timing: with profiling enabled every operator kernel
  * launch is bracketed by CUDA events on its own stream;
  * tdg_profile_read synchronizes, returns the accumulated milliseconds and
- * launch counts per kernel (ms[4], launches[4]: 0 faces, 1 wall, 2 volume,
- * 3 face-slot sum of the overlapped path) and resets. */
+ * launch counts per kernel (ms[4], launches[4]: 0 interior faces, 1 wall
+ * faces, 2 volume, 3 reserved) and resets. */
 TDG_API int tdg_profile(tdg_ctx* ctx, int enable);
 TDG_API int tdg_profile_read(tdg_ctx* ctx, double* ms, int64_t* launches);
 
@@ -273,6 +285,18 @@ TDG_API int64_t tdg_fp64_probe_threads(void);
 /* FP64 tensor-core (DMMA m8n8k4) probe on the same grid: per warp 4
  * independent 8x8x4 MMAs per iteration, flops = threads/32*iters*4*512. */
 TDG_API int tdg_dmma_probe(double* out, int64_t iters, void* stream);
+
+/* Host-side setup (no GPU needed): greedy colouring of the face graph
+ * that orders the face loop.  Elements are vertices, faces edges; a face
+ * side with elem < 0 is not written (walls, mirror faces, ghost sides).
+ * Faces are visited in `order` (NULL: index order) and each takes the
+ * smallest colour that none of its written elements holds yet, so no
+ * element is written twice within a colour.  Visiting the faces grouped by
+ * their (local face in, local face out) class colours the structured
+ * simplex meshes with d+1 colours.  Writes color[n_faces] and returns the
+ * number of colours (>= 0) or TDG_E_INVALID (bad index, > 64 colours). */
+TDG_API int tdg_color_faces(int64_t n_faces, const int32_t* elem_in, const int32_t* elem_out,
+                            int64_t n_elements, const int64_t* order, int32_t* color);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ from .build import LIB
 __all__ = ["lib", "TdgDesc", "check", "TDG_OK", "load"]
 
 TDG_OK, TDG_E_INVALID, TDG_E_UNSUPPORTED, TDG_E_CUDA = 0, -1, -2, -3
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double
@@ -34,11 +34,11 @@ class TdgDesc(ctypes.Structure):
         ("vol_phi", _p), ("vol_grad", _p), ("vol_w", _p), ("vol_stiff", _p),
         ("face_B", _p), ("face_G", _p), ("face_Pw", _p), ("face_w", _p),
         ("elem_geo", _p),
-        ("if_elems", _p), ("if_lf", _p), ("if_code", _p), ("if_geo", _p),
-        ("bf_elem", _p), ("bf_lf", _p), ("bf_code", _p), ("bf_geo", _p),
-        ("face_mma", _p), ("vol_mma", _p), ("n_cut_faces", _i64), ("vol_tc", _p),
-        ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64), ("n_face_blocks_cut", _i64),
-        ("n_bands", ctypes.c_int32), ("band_ptr", _p),
+        ("if_elems", _p), ("if_code", _p), ("if_geo", _p),
+        ("bf_elem", _p), ("bf_code", _p), ("bf_geo", _p),
+        ("face_mma", _p), ("vol_tc", _p),
+        ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64),
+        ("n_segments", _i32), ("n_segments_cut", _i32), ("seg_ptr", _p),
     ]
 
 
@@ -59,13 +59,14 @@ def load(path: str = LIB):
     lib.tdg_create.argtypes = [ctypes.POINTER(TdgDesc), ctypes.POINTER(_p)]
     lib.tdg_destroy.argtypes = [_p]
     lib.tdg_apply.argtypes = [_p, _p, _p, _d, ctypes.c_int, _p]
-    lib.tdg_rk_stage.argtypes = [_p, _p, _p, _p, _d, _d, _d, _d, _p]
+    lib.tdg_rk_stage.argtypes = [_p, _p, _p, _p, _p, _d, _d, _d, _d, _p]
     lib.tdg_species_totals.argtypes = [_p, _p, _p, _p]
-    lib.tdg_ssprk3_steps_host.argtypes = [_p, _p, _i64, _d, _d, _p]
+    lib.tdg_ssprk3_steps_host.argtypes = [_p, _p, _p, _p, _p, _i64, _d, _d, _p]
     lib.tdg_species_l2.argtypes = [_p, _p, _p, _p, _p]
     lib.tdg_mgs.argtypes = [_p, _p, _i64, ctypes.c_int, _p, _i64, _p, _p]
-    lib.tdg_rk_stage_part.argtypes = [_p, _p, _p, _p, _d, _d, _d, _d, ctypes.c_int, _p]
-    lib.tdg_ssprk3_step.argtypes = [_p, _p, _p, _d, _d, _p]
+    lib.tdg_rk_stage_part.argtypes = [_p, _p, _p, _p, _p, _d, _d, _d, _d, ctypes.c_int, _p]
+    lib.tdg_ssprk3_step.argtypes = [_p, _p, _p, _p, _d, _d, _p]
+    lib.tdg_color_faces.argtypes = [_i64, _p, _p, _i64, _p, _p]
     lib.tdg_dot.argtypes = [_p, _p, _p, _i64, _p, _p]
     lib.tdg_norm2.argtypes = [_p, _p, _i64, _p, _p]
     lib.tdg_axpby.argtypes = [_d, _p, _d, _p, _i64, _p]
@@ -79,7 +80,7 @@ def load(path: str = LIB):
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
     lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
-    for name in ("tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    for name in ("tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev", "tdg_scale_norm", "tdg_jv_shift", "tdg_jv_diff"):

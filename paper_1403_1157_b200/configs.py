@@ -39,9 +39,6 @@ class Config:
     description: str
     jitter: float = 0.0
     tags: str = "default"        # "default" | "z0_gamma1"
-    # weak-scaling unit: one GPU owns cells[0] / weak_div cell columns, so
-    # N = weak_div GPUs run exactly the config (C5: 1/8 per GPU)
-    weak_div: int = 1
 
 
 CONFIGS = {
@@ -57,7 +54,7 @@ CONFIGS = {
                  "GAMMA1 at z=0, no-flux elsewhere", tags="z0_gamma1"),
     "c5": Config("c5", 3, 3, (256, 128, 128), (2.0, 1.0, 1.0), 10,
                  "C5: 3D [0,2]x[0,1]^2 256x128x128 cells (6 Kuhn tets/cell), "
-                 "p=3", weak_div=8),
+                 "p=3"),
 }
 
 

@@ -3,6 +3,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -48,8 +49,8 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   if (d.n_species < 1 || d.n_species > kMaxS) return fail(TDG_E_INVALID, "n_species out of range");
   if (d.scheme < TDG_CDG2 || d.scheme > TDG_BO) return fail(TDG_E_INVALID, "unknown scheme");
   if (d.n_elements < 0 || d.n_ghost < 0 || d.n_int_faces < 0 || d.n_bnd_faces < 0 ||
-      d.n_cut_faces < 0 || d.n_cut_faces > d.n_int_faces)
-    return fail(TDG_E_INVALID, "negative size / bad cut-face count");
+      d.n_face_blocks < 0)
+    return fail(TDG_E_INVALID, "negative size");
   if (d.n_elements + d.n_ghost > (int64_t(1) << 31) - 1)
     return fail(TDG_E_INVALID, "element rows must fit int32");
   Impl impl;
@@ -63,15 +64,40 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   if (!d.vol_phi || !d.vol_grad || !d.vol_w || !d.vol_stiff || !d.face_B || !d.face_G ||
       !d.face_Pw || !d.face_w || !d.elem_geo || !d.diffusivity || !d.lin_source || !d.params)
     return fail(TDG_E_INVALID, "missing table pointer");
-  if (d.n_int_faces > 0 && (!d.if_elems || !d.if_lf || !d.if_code || !d.if_geo))
+  if (d.n_int_faces > 0 && (!d.if_elems || !d.if_code || !d.if_geo))
     return fail(TDG_E_INVALID, "missing interior face arrays");
-  if (d.n_bnd_faces > 0 && (!d.bf_elem || !d.bf_lf || !d.bf_code || !d.bf_geo))
+  if (d.n_bnd_faces > 0 && (!d.bf_elem || !d.bf_code || !d.bf_geo))
     return fail(TDG_E_INVALID, "missing boundary face arrays");
+  // colour segments: monotone offsets covering every face / wall / block
+  if (d.n_segments < 0 || d.n_segments_cut < 0 || d.n_segments_cut > d.n_segments ||
+      (d.n_segments > 0 && !d.seg_ptr))
+    return fail(TDG_E_INVALID, "bad face segments");
+  std::vector<Segment> seg(size_t(d.n_segments));
+  if (d.n_segments > 0) {
+    const int64_t n1 = d.n_segments + 1;
+    const int64_t *I = d.seg_ptr, *W = I + n1, *B = W + n1;
+    const bool ends = I[0] == 0 && I[n1 - 1] == d.n_int_faces && W[0] == 0 &&
+                      W[n1 - 1] == d.n_bnd_faces && B[0] == 0 &&
+                      B[n1 - 1] == (d.face_blocks ? d.n_face_blocks : 0);
+    bool mono = true;
+    for (int s = 0; s < d.n_segments; ++s) {
+      mono = mono && I[s] <= I[s + 1] && W[s] <= W[s + 1] && B[s] <= B[s + 1];
+      seg[s] = Segment{I[s], I[s + 1], W[s], W[s + 1], B[s], B[s + 1]};
+    }
+    if (!ends || !mono) return fail(TDG_E_INVALID, "inconsistent face segment offsets");
+    for (int s = d.n_segments - d.n_segments_cut; s < d.n_segments; ++s)
+      if (seg[s].w1 > seg[s].w0) return fail(TDG_E_INVALID, "walls in a cut-face segment");
+  } else if (d.n_int_faces + d.n_bnd_faces > 0) {
+    return fail(TDG_E_INVALID, "faces without colour segments");
+  }
 
   tdg_ctx* ctx = new (std::nothrow) tdg_ctx;
   if (!ctx) return fail(TDG_E_INVALID, "out of host memory");
   ctx->d = d;
+  ctx->d.seg_ptr = nullptr;  // copied into ctx->seg
   ctx->impl = impl;
+  ctx->seg = std::move(seg);
+  ctx->n_seg_cut = d.n_segments_cut;
   OpParams& p = ctx->p;
   std::memset(&p, 0, sizeof(p));
   p.ne = d.n_elements;
@@ -98,15 +124,12 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.fw = d.face_w;
   p.egeo = d.elem_geo;
   p.ifel = d.if_elems;
-  p.iflf = d.if_lf;
   p.ifcode = d.if_code;
   p.ifgeo = d.if_geo;
   p.bfel = d.bf_elem;
-  p.bflf = d.bf_lf;
   p.bfcode = d.bf_code;
   p.bfgeo = d.bf_geo;
   p.fmma = d.face_mma;
-  p.vmma = d.vol_mma;
   p.vtc = d.vol_tc;
   p.ftc = d.face_tc;
   p.fblk = d.face_blocks;
@@ -124,45 +147,27 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     delete ctx;
     return rc;
   }
-  const size_t fc_bytes =
-      size_t(d.n_elements) * size_t(d.dim + 1) * size_t(d.n_species) * size_t(d.nb) * sizeof(double);
-  cudaError_t e = cudaMalloc(&ctx->fc, fc_bytes > 0 ? fc_bytes : 8);
-  if (e != cudaSuccess) {
-    delete ctx;
-    return cuda_fail(e, "cudaMalloc face slots");
-  }
-  e = cudaMalloc(&ctx->part, kRedWorkBytes);
+  cudaError_t e = cudaMalloc(&ctx->part, kRedWorkBytes);
   if (e == cudaSuccess) e = cudaMemset(ctx->part, 0, kRedWorkBytes);
+  // every stream / event the entry points use, created now (no call
+  // allocates after tdg_create)
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&ctx->s_in[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->s_out[i], cudaStreamNonBlocking);
+  }
+  for (int k = 0; k < tdg_ctx::kChunks && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&ctx->ev_h2d[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_d2h[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_vol[k], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_s0, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gev_a, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gev_b, cudaEventDisableTiming);
   if (e != cudaSuccess) {
-    cudaFree(ctx->fc);
-    delete ctx;
-    return cuda_fail(e, "cudaMalloc reduction workspace");
-  }
-  if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_vol, cudaEventDisableTiming) != cudaSuccess) {
-    ctx->overlap = false;  // serial path still works
-    cudaGetLastError();
-  }
-  // element bands of the host-pipelined stepping (host array: elements
-  // [B+1] | interior-face offsets [2B+1] | wall offsets [B+1] | face-block
-  // offsets [B+1])
-  if (d.n_bands > 1 && d.band_ptr) {
-    const int nb = d.n_bands;
-    const int64_t* bp = d.band_ptr;
-    ctx->band_elem.assign(bp, bp + nb + 1);
-    ctx->band_face.assign(bp + nb + 1, bp + nb + 1 + 2 * nb + 1);
-    ctx->band_wall.assign(bp + 3 * nb + 2, bp + 4 * nb + 3);
-    ctx->band_blk.assign(bp + 4 * nb + 3, bp + 5 * nb + 4);
-    const bool ok = ctx->band_elem.front() == 0 && ctx->band_elem.back() == d.n_elements &&
-                    ctx->band_face.front() == 0 && ctx->band_face.back() == d.n_int_faces &&
-                    ctx->band_wall.front() == 0 && ctx->band_wall.back() == d.n_bnd_faces &&
-                    ctx->band_blk.front() == 0 && ctx->band_blk.back() == d.n_face_blocks;
-    if (!ok) {
-      tdg_destroy(ctx);
-      return fail(TDG_E_INVALID, "inconsistent band offsets");
-    }
-    ctx->n_bands = nb;
+    tdg_destroy(ctx);
+    return cuda_fail(e, "tdg_create: workspace / streams");
   }
   *out = ctx;
   return TDG_OK;
@@ -175,99 +180,110 @@ int tdg_destroy(tdg_ctx* ctx) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
-  cudaFree(ctx->fc);
-  cudaFree(ctx->part);
+  if (ctx->part) cudaFree(ctx->part);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  cudaFree(ctx->hs_buf);
-  for (int i = 0; i < tdg_ctx::kCopyStreams; ++i) {
+  for (int i = 0; i < 2; ++i) {
     if (ctx->s_in[i]) cudaStreamDestroy(ctx->s_in[i]);
     if (ctx->s_out[i]) cudaStreamDestroy(ctx->s_out[i]);
   }
-  for (auto s : ctx->hs_st)
-    if (s) cudaStreamDestroy(s);
-  if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
-  if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
-  for (auto* v : {&ctx->ev_h2d, &ctx->ev_d2h, &ctx->ev_done, &ctx->ev_vol_b})
-    for (auto ev : *v) cudaEventDestroy(ev);
+  for (int k = 0; k < tdg_ctx::kChunks; ++k)
+    for (cudaEvent_t ev : {ctx->ev_h2d[k], ctx->ev_d2h[k], ctx->ev_vol[k]})
+      if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {ctx->ev_s0, ctx->ev_s1, ctx->gev_a, ctx->gev_b})
+    if (ev) cudaEventDestroy(ev);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
-  if (ctx->gev_a) cudaEventDestroy(ctx->gev_a);
-  if (ctx->gev_b) cudaEventDestroy(ctx->gev_b);
-  if (ctx->work2) cudaFree(ctx->work2);
-  if (ctx->aux) cudaStreamDestroy(ctx->aux);
-  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
-  if (ctx->ev_vol) cudaEventDestroy(ctx->ev_vol);
   delete ctx;
+  return TDG_OK;
+}
+
+static size_t state_doubles(const tdg_ctx* ctx) {
+  return size_t(ctx->d.n_elements) * ctx->d.n_species * ctx->d.nb;
+}
+
+// [a, a + n) and [b, b + n) overlap
+static bool overlaps(const double* a, const double* b, size_t n) {
+  return a && b && a < b + n && b < a + n;
+}
+
+// the face sums accumulate in acc: it must not alias the stage input U
+// (read by later face segments), nor U0 when the stage reads it
+static int check_stage(const tdg_ctx* ctx, const double* U0, const double* U, const double* acc,
+                       double a) {
+  const size_t n = state_doubles(ctx);
+  const size_t nu = size_t(ctx->d.n_elements + ctx->d.n_ghost) * ctx->d.n_species * ctx->d.nb;
+  if (overlaps(acc, U, nu > n ? nu : n)) return fail(TDG_E_INVALID, "face-sum buffer aliases U");
+  if (a != 0.0 && overlaps(acc, U0, n)) return fail(TDG_E_INVALID, "face-sum buffer aliases U0");
   return TDG_OK;
 }
 
 int tdg_apply(tdg_ctx* ctx, const double* U, double* R, double t, int mass_inverse, void* stream) {
   (void)t;
   if (!ctx || !U || !R) return fail(TDG_E_INVALID, "null argument");
-  return ctx->impl.run(ctx, U, nullptr, R, 0.0, 0.0, 0.0, mass_inverse ? 1 : 0,
+  if (int rc = check_stage(ctx, nullptr, U, R, 0.0)) return rc;
+  return ctx->impl.run(ctx, U, nullptr, R, R, 0.0, 0.0, 0.0, mass_inverse ? 1 : 0, 0,
                        static_cast<cudaStream_t>(stream));
 }
 
-int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out, double a, double b,
-                 double c, double t, void* stream) {
+int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double* out, double* acc,
+                 double a, double b, double c, double t, void* stream) {
   (void)t;
   if (!ctx || !U || !out) return fail(TDG_E_INVALID, "null argument");
   if (a != 0.0 && !U0) return fail(TDG_E_INVALID, "U0 required when a != 0");
-  return ctx->impl.run(ctx, U, U0, out, a, b, c, 2, static_cast<cudaStream_t>(stream));
+  if (!acc) acc = out;
+  if (int rc = check_stage(ctx, U0, U, acc, a)) return rc;
+  return ctx->impl.run(ctx, U, U0, out, acc, a, b, c, 2, 0, static_cast<cudaStream_t>(stream));
 }
 
-int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out, double a,
-                      double b, double c, double t, int part, void* stream) {
+int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out, double* acc,
+                      double a, double b, double c, double t, int part, void* stream) {
   (void)t;
   if (!ctx || !U || !out) return fail(TDG_E_INVALID, "null argument");
   if (a != 0.0 && !U0) return fail(TDG_E_INVALID, "U0 required when a != 0");
   if (part < 1 || part > 2) return fail(TDG_E_INVALID, "part must be 1 (begin) or 2 (end)");
-  return ctx->impl.run(ctx, U, U0, out, a, b, c, 2 | (part << 8), static_cast<cudaStream_t>(stream));
+  if (!acc) acc = out;
+  if (int rc = check_stage(ctx, U0, U, acc, a)) return rc;
+  return ctx->impl.run(ctx, U, U0, out, acc, a, b, c, 2, part, static_cast<cudaStream_t>(stream));
 }
 
-int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, void* stream) {
-  if (!ctx || !U || !work) return fail(TDG_E_INVALID, "null argument");
+// Shu-Osher SSP-RK3 over three state vectors; stage 3 accumulates its face
+// sums in w1 (dead after stage 2) and writes the result over U
+static int ssprk3_stages(tdg_ctx* ctx, double* U, double* w1, double* w2, double dt,
+                         cudaStream_t s) {
+  int rc = ctx->impl.run(ctx, U, nullptr, w1, w1, 0.0, 1.0, dt, 2, 0, s);  // U1 = U + dt f(U)
+  if (rc) return rc;
+  // U2 = 3/4 U + 1/4 (U1 + dt f(U1))
+  rc = ctx->impl.run(ctx, w1, U, w2, w2, 0.75, 0.25, 0.25 * dt, 2, 0, s);
+  if (rc) return rc;
+  // U3 = 1/3 U + 2/3 (U2 + dt f(U2))
+  return ctx->impl.run(ctx, w2, U, U, w1, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, 0, s);
+}
+
+static int check_step(const tdg_ctx* ctx, const double* U, const double* w1, const double* w2) {
+  if (ctx->d.n_ghost != 0)
+    return fail(TDG_E_INVALID, "ssprk3 steps need an undecomposed mesh (slab runs: "
+                               "tdg_rk_stage_part around the ghost exchange)");
+  const size_t n = state_doubles(ctx);
+  if (overlaps(U, w1, n) || overlaps(U, w2, n) || overlaps(w1, w2, n))
+    return fail(TDG_E_INVALID, "U, w1, w2 must be distinct");
+  return TDG_OK;
+}
+
+int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* w1, double* w2, double t, double dt,
+                    void* stream) {
+  if (!ctx || !U || !w1 || !w2) return fail(TDG_E_INVALID, "null argument");
+  if (int rc = check_step(ctx, U, w1, w2)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   (void)t;
-  const int64_t rows = ctx->d.n_elements + ctx->d.n_ghost;
-  const size_t n = size_t(rows) * ctx->d.n_species * ctx->d.nb;
-  // the overlapped application must not write its own input: stage 2
-  // goes to a second (library-owned) work vector
-  if (!ctx->work2 || ctx->work2_n < n) {
-    if (ctx->work2) cudaFree(ctx->work2);
-    ctx->work2 = nullptr;
-    ctx->work2_n = 0;
-    if (cudaMalloc(&ctx->work2, n * sizeof(double)) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(TDG_E_CUDA, "cudaMalloc ssprk3 work");
-    }
-    ctx->work2_n = n;
-  }
-  double* w2 = ctx->work2;
-  auto stages = [&](cudaStream_t s) {
-    int rc = ctx->impl.run(ctx, U, nullptr, work, 0.0, 1.0, dt, 2, s);  // U1 = U + dt f(U)
-    if (rc) return rc;
-    // U2 = 3/4 U + 1/4 (U1 + dt f(U1))
-    rc = ctx->impl.run(ctx, work, U, w2, 0.75, 0.25, 0.25 * dt, 2, s);
-    if (rc) return rc;
-    // U3 = 1/3 U + 2/3 (U2 + dt f(U2)), written over U (U is only U0 here)
-    return ctx->impl.run(ctx, w2, U, U, 1.0 / 3.0, 2.0 / 3.0, (2.0 / 3.0) * dt, 2, s);
-  };
-  if (!ctx->use_graph || ctx->profile) return stages(st);
-  // graph path: the nine launches and their cross-stream events replay as
-  // one graph on gstream, ordered after / before the caller's stream
-  if (!ctx->gexec || ctx->g_U != U || ctx->g_work != work || ctx->g_dt != dt) {
+  if (!ctx->use_graph || ctx->profile) return ssprk3_stages(ctx, U, w1, w2, dt, st);
+  // graph path: the step's launches replay as one graph on gstream,
+  // ordered after / before the caller's stream
+  if (!ctx->gexec || ctx->g_U != U || ctx->g_w1 != w1 || ctx->g_w2 != w2 || ctx->g_dt != dt) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;
-    if (!ctx->gstream) {
-      if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->gev_a, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->gev_b, cudaEventDisableTiming) != cudaSuccess)
-        return cuda_fail(cudaGetLastError(), "graph stream");
-    }
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_fail(e, "begin capture");
-    const int rc = stages(ctx->gstream);
+    const int rc = ssprk3_stages(ctx, U, w1, w2, dt, ctx->gstream);
     e = cudaStreamEndCapture(ctx->gstream, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);
@@ -281,7 +297,8 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, 
       return cuda_fail(e, "graph instantiate");
     }
     ctx->g_U = U;
-    ctx->g_work = work;
+    ctx->g_w1 = w1;
+    ctx->g_w2 = w2;
     ctx->g_dt = dt;
   }
   cudaEventRecord(ctx->gev_a, st);
@@ -293,16 +310,62 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* work, double t, double dt, 
   return TDG_OK;
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, int64_t nsteps, double t, double dt,
-                          void* stream) {
+int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, double* U, double* w1, double* w2,
+                          int64_t nsteps, double t, double dt, void* stream) {
   (void)t;
-  if (!ctx || !U_host) return fail(TDG_E_INVALID, "null argument");
+  if (!ctx || !U_host || !U || !w1 || !w2) return fail(TDG_E_INVALID, "null argument");
   if (nsteps < 0) return fail(TDG_E_INVALID, "negative step count");
-  if (ctx->d.n_ghost != 0) return fail(TDG_E_INVALID, "host stepping needs an undecomposed mesh");
-  return ctx->impl.host_steps(ctx, U_host, nsteps, dt, static_cast<cudaStream_t>(stream));
+  if (int rc = check_step(ctx, U, w1, w2)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ne = ctx->d.n_elements;
+  const size_t sn = size_t(ctx->d.n_species) * ctx->d.nb;
+  constexpr int NCH = tdg_ctx::kChunks;
+  int64_t ck[NCH + 1];
+  for (int k = 0; k <= NCH; ++k) ck[k] = ne * k / NCH;
+  cudaEventRecord(ctx->ev_s0, st);
+  for (int i = 0; i < 2; ++i) {
+    cudaStreamWaitEvent(ctx->s_in[i], ctx->ev_s0, 0);
+    cudaStreamWaitEvent(ctx->s_out[i], ctx->ev_s0, 0);
+  }
+  for (int64_t it = 0; it < nsteps; ++it) {
+    // copy-in by chunks: chunk k of step n+1 follows step n's copy-out of k
+    for (int k = 0; k < NCH; ++k) {
+      cudaStream_t cs = ctx->s_in[k & 1];
+      if (it > 0) cudaStreamWaitEvent(cs, ctx->ev_d2h[k], 0);
+      const size_t o = size_t(ck[k]) * sn, m = size_t(ck[k + 1] - ck[k]) * sn;
+      if (m) cudaMemcpyAsync(U + o, U_host + o, m * sizeof(double), cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(ctx->ev_h2d[k], cs);
+    }
+    for (int k = 0; k < NCH; ++k) cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
+    int rc = ctx->impl.run(ctx, U, nullptr, w1, w1, 0.0, 1.0, dt, 2, 0, st);
+    if (!rc) rc = ctx->impl.run(ctx, w1, U, w2, w2, 0.75, 0.25, 0.25 * dt, 2, 0, st);
+    // stage 3: every face segment, then the volume kernel chunk by chunk,
+    // each chunk's copy-out as soon as it is written
+    if (!rc) rc = ctx->impl.run(ctx, w2, U, U, w1, 0.0, 0.0, 0.0, 2, 3, st);
+    const bool faces = ctx->p.nif + ctx->p.nbf > 0;
+    for (int k = 0; k < NCH && !rc; ++k) {
+      rc = ctx->impl.volume(ctx, ck[k], ck[k + 1], w2, U, U, faces ? w1 : nullptr, 1.0 / 3.0,
+                            2.0 / 3.0, (2.0 / 3.0) * dt, 2, st);
+      cudaEventRecord(ctx->ev_vol[k], st);
+      cudaStream_t cs = ctx->s_out[k & 1];
+      cudaStreamWaitEvent(cs, ctx->ev_vol[k], 0);
+      const size_t o = size_t(ck[k]) * sn, m = size_t(ck[k + 1] - ck[k]) * sn;
+      if (m) cudaMemcpyAsync(U_host + o, U + o, m * sizeof(double), cudaMemcpyDeviceToHost, cs);
+      cudaEventRecord(ctx->ev_d2h[k], cs);
+    }
+    if (rc) return rc;
+  }
+  // join the copy streams back onto the caller's stream
+  for (int i = 0; i < 2; ++i)
+    for (cudaStream_t s : {ctx->s_in[i], ctx->s_out[i]}) {
+      cudaEventRecord(ctx->ev_s1, s);
+      cudaStreamWaitEvent(st, ctx->ev_s1, 0);
+    }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "host steps");
 }
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int tdg_dot(tdg_ctx* ctx, const double* x, const double* y, int64_t n, double* result,
             void* stream) {
@@ -389,29 +452,15 @@ int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y, int6
 int tdg_set_variant(tdg_ctx* ctx, int variant) {
   if (!ctx) return fail(TDG_E_INVALID, "null argument");
   ctx->force_generic = (variant & 1) != 0;
-  ctx->vol_variant = (variant >> 1) & 1;
-  ctx->overlap = ((variant >> 2) & 1) == 0 && ctx->aux != nullptr;
-  ctx->flip_mma = ((variant >> 3) & 1) != 0;
-  ctx->use_vmma = ((variant >> 4) & 1) != 0;
-  ctx->force_tc = ((variant >> 12) & 1) != 0;
-  ctx->face_rows_tc = ((variant >> 15) & 1) != 0;
-  // bit 16: host steps on one copy stream per direction; bits 18-20: that
-  // many copy streams per direction (0: the default 2)
-  const int ncs = (variant >> 18) & 7;
-  ctx->copy_streams = ((variant >> 16) & 1) ? 1 : (ncs ? ncs : 2);
-  ctx->walls_first = ((variant >> 17) & 1) != 0;  // bit 17: 3D wall faces before interior  // bit 16: host steps on one copy stream per direction  // bit 15: faces-as-rows TC face kernel (3D)
-  ctx->no_tcf = ((variant >> 13) & 1) != 0;    // bit 13: element-local DMMA face kernel (3D)
-  ctx->faces_first = ((variant >> 14) & 1) == 0;  // bit 14: launch the volume part first
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
+  ctx->force_tc = ((variant >> 12) & 1) != 0;
+  // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
+  // the resident count; 15 = one group per warp, no grid cap)
+  const int f = (variant >> 8) & 15;
+  ctx->face_ctas_per_sm = f == 15 ? -1 : f;
   if (ctx->gexec) {  // kernel choice changed: re-capture
     cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;
-  }
-  // bits 8-11: CTAs per SM of the face kernel's grid-stride grid (0 = the
-  // resident count; 15 = one group per warp, no grid cap)
-  {
-    const int f = (variant >> 8) & 15;
-    ctx->face_ctas_per_sm = f == 15 ? -1 : f;
   }
   return TDG_OK;
 }
@@ -450,6 +499,28 @@ int tdg_fp64_probe(double* out, int64_t iters, void* stream) {
 }
 
 int64_t tdg_fp64_probe_threads(void) { return fp64_probe_threads(); }
+
+int tdg_color_faces(int64_t n_faces, const int32_t* elem_in, const int32_t* elem_out,
+                    int64_t n_elements, const int64_t* order, int32_t* color) {
+  if (n_faces < 0 || n_elements < 0) return fail(TDG_E_INVALID, "negative size");
+  if (n_faces > 0 && (!elem_in || !elem_out || !color)) return fail(TDG_E_INVALID, "null argument");
+  std::vector<uint64_t> used(size_t(n_elements), 0);
+  int ncol = 0;
+  for (int64_t k = 0; k < n_faces; ++k) {
+    const int64_t f = order ? order[k] : k;
+    if (f < 0 || f >= n_faces) return fail(TDG_E_INVALID, "order index out of range");
+    const int32_t a = elem_in[f], b = elem_out[f];
+    if (a >= n_elements || b >= n_elements) return fail(TDG_E_INVALID, "element index out of range");
+    const uint64_t busy = (a >= 0 ? used[a] : 0) | (b >= 0 ? used[b] : 0);
+    if (busy == ~uint64_t(0)) return fail(TDG_E_INVALID, "more than 64 colours");
+    const int c = __builtin_ctzll(~busy);
+    if (a >= 0) used[a] |= uint64_t(1) << c;
+    if (b >= 0) used[b] |= uint64_t(1) << c;
+    color[f] = c;
+    ncol = c + 1 > ncol ? c + 1 : ncol;
+  }
+  return ncol;
+}
 
 int tdg_dmma_probe(double* out, int64_t iters, void* stream) {
   if (!out || iters < 1) return fail(TDG_E_INVALID, "bad argument");

@@ -54,15 +54,12 @@ struct OpParams {
   const double* __restrict__ fw;
   const double* __restrict__ egeo;
   const int32_t* __restrict__ ifel;
-  const int32_t* __restrict__ iflf;
   const int32_t* __restrict__ ifcode;
   const double* __restrict__ ifgeo;
   const int32_t* __restrict__ bfel;
-  const int32_t* __restrict__ bflf;
   const int32_t* __restrict__ bfcode;
   const double* __restrict__ bfgeo;
   const double* __restrict__ fmma;  // tensor-core face tables (may be null)
-  const double* __restrict__ vmma;  // tensor-core volume tables (may be null)
   const double* __restrict__ vtc;   // transposed tensor-core volume tables (may be null)
   const double* __restrict__ ftc;   // transposed tensor-core face tables (may be null)
   const int32_t* __restrict__ fblk; // interior-face blocks [n][2] (first, count)
@@ -75,6 +72,18 @@ __device__ __forceinline__ bool code_minus_in(int c) { return (c >> 10) & 1; }
 __device__ __forceinline__ int code_tag(int c) { return (c >> 11) & 7; }
 __device__ __forceinline__ bool code_mirror(int c) { return (c >> 14) & 1; }
 __device__ __forceinline__ bool code_skip_out(int c) { return (c >> 15) & 1; }
+// the side runs first for its element in the face-segment order: it
+// writes the element's face-sum row, later sides add to it
+__device__ __forceinline__ bool code_first_in(int c) { return (c >> 16) & 1; }
+__device__ __forceinline__ bool code_first_out(int c) { return (c >> 17) & 1; }
+
+// Face-sum accumulation.  The faces are coloured so that one launch (one
+// face segment) touches every element at most once; segments run in a
+// fixed order, so each entry is  ((f_1 + f_2) + f_3) + ...  in that order
+// (deterministic, no atomics).  `first` marks the element's first face.
+__device__ __forceinline__ void acc_put(double* p, double v, bool first) {
+  *p = first ? v : *p + v;
+}
 
 // BoundaryTag (mesh.py:46-52)
 enum Tag { GAMMA1 = 1, GAMMA1_IN = 2, GAMMA2 = 3, NO_FLOW = 4 };

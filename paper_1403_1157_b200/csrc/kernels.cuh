@@ -5,12 +5,13 @@
 //
 //   k_faces  interior (+ Dirichlet-mirror) faces   operator.py:359-444
 //   k_wall   prescribed-flux boundary faces        operator.py:446-458
-//            both write one contribution block per element-local face
-//            into FC[lf][e][s][i]; every (lf, e) slot is written exactly
-//            once per application, so the two-sided scatter is
-//            conflict-free without colouring or atomics;
-//   k_volume volume terms (operator.py:292-324) + sum over the element's
-//            FC slots + M^-1 (fespace.py:117-118) + the Runge-Kutta stage
+//            both add each face side's contribution block to the
+//            element's face-sum row ACC[e][s][i]; the faces run in colour
+//            segments (one launch per segment, no element twice in a
+//            segment), so the two-sided scatter is conflict-free without
+//            atomics and the sums have a fixed order;
+//   k_volume volume terms (operator.py:292-324) + the element's face sum
+//            + M^-1 (fespace.py:117-118) + the Runge-Kutta stage
 //            combination, fused; writes the element's output rows once.
 //
 // Each CTA stages its tile's coefficient blocks (S*nb contiguous doubles
@@ -45,7 +46,7 @@ struct VolumeTile {
 // mode 0: out = L(U);  1: out = M^-1 L(U);  2: out = ca*U0 + cb*U + cc*M^-1 L(U)
 template <int D, int K, class M>
 __global__ void __launch_bounds__(kThreads)
-k_volume(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
+k_volume(OpParams p, const double* __restrict__ U, const double* ACC,
          const double* U0, double* out, double ca, double cb, double cc, int mode) {
   using T = VolumeTile<D, K, M>;
   using Dm = Dims<D, K>;
@@ -156,9 +157,7 @@ k_volume(OpParams p, const double* __restrict__ U, const double* __restrict__ FC
       if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], c[t * NB + i], lin);
     const double detJ = ge[0];
     double rv = detJ * (acc - p.A[s] * dif + lin);
-    const double* fc = FC + (e0 + e) * SN + r;
-#pragma unroll
-    for (int lf = 0; lf <= D; ++lf) rv += fc[lf * p.ne * SN];
+    if (ACC != nullptr) rv += ACC[(e0 + e) * SN + r];
     double o;
     if (mode == 0) o = rv;
     else if (mode == 1) o = rv / detJ;
@@ -184,7 +183,7 @@ struct FaceTile {
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(kThreads)
-k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
+k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ ACC) {
   using T = FaceTile<D, K, M>;
   using Dm = Dims<D, K>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, SNP = T::SNP, F = T::F, TF = T::TF;
@@ -192,7 +191,7 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
   extern __shared__ double sm[];
   double* cs = sm;                      // [TF][2][SNP]
   double* geo = cs + TF * 2 * SNP;      // [TF][NFG]
-  int* meta = reinterpret_cast<int*>(geo + TF * NFG);  // [TF][6]: code, e_in, e_out, lf_in, lf_out, pad
+  int* meta = reinterpret_cast<int*>(geo + TF * NFG);  // [TF][6]: code, e_in, e_out, pad
   double* dph = geo + TF * NFG + TF * 3;               // [TF][2][F][NB]
   double* tr = dph + TF * 2 * F * NB;                  // [TF][4][S][F]
   double* yx = tr + TF * 4 * S * F;                    // [TF][2][S][F]
@@ -206,8 +205,6 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
     m[0] = p.ifcode[f0 + f];
     m[1] = p.ifel[2 * (f0 + f)];
     m[2] = p.ifel[2 * (f0 + f) + 1];
-    m[3] = p.iflf[2 * (f0 + f)];
-    m[4] = p.iflf[2 * (f0 + f) + 1];
   }
   for (int idx = tid; idx < nt * NFG; idx += kThreads) geo[idx] = p.ifgeo[f0 * NFG + idx];
   __syncthreads();
@@ -339,8 +336,8 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
       acc = fma(sg * Y[q], __ldg(b + q * NB), acc);
       acc = fma(X[q], dp[q * NB], acc);
     }
-    const int64_t slot = int64_t(meta[f * 6 + 3 + side]) * p.ne + meta[f * 6 + 1 + side];
-    FC[slot * SN + si] = acc;
+    const int64_t e = meta[f * 6 + 1 + side];
+    acc_put(ACC + e * SN + si, acc, side ? code_first_out(code) : code_first_in(code));
   }
 }
 
@@ -354,13 +351,13 @@ struct WallTile {
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(kThreads)
-k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
+k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ ACC) {
   using T = WallTile<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, TF = T::TF;
   extern __shared__ double sm[];
   double* cw = sm;                 // [TF][NB]  coefficients of the gate species
   double* sf = cw + TF * NB;       // [TF]
-  int* meta = reinterpret_cast<int*>(sf + TF);  // [TF][4] code, e, lf
+  int* meta = reinterpret_cast<int*>(sf + TF);  // [TF][4] code, e
   double* yw = sf + TF + 2 * TF;   // [TF][S][F]
   const int tid = threadIdx.x;
   const int64_t f0 = int64_t(blockIdx.x) * TF;
@@ -369,7 +366,6 @@ k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
   for (int f = tid; f < nt; f += kThreads) {
     meta[f * 4] = p.bfcode[f0 + f];
     meta[f * 4 + 1] = p.bfel[f0 + f];
-    meta[f * 4 + 2] = p.bflf[f0 + f];
     sf[f] = p.bfgeo[f0 + f];
   }
   __syncthreads();
@@ -398,8 +394,7 @@ k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ FC) {
     const double* b = p.fB + size_t(code_tin(code)) * nqf * NB + i;
     double acc = 0.0;
     for (int q = 0; q < nqf; ++q) acc = fma(yw[(f * S + s) * F + q], __ldg(b + q * NB), acc);
-    const int64_t slot = int64_t(meta[f * 4 + 2]) * p.ne + meta[f * 4 + 1];
-    FC[slot * SN + si] = acc;
+    acc_put(ACC + int64_t(meta[f * 4 + 1]) * SN + si, acc, code_first_in(code));
   }
 }
 

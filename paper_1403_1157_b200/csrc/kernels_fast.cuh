@@ -7,16 +7,17 @@
 //               S*nb coefficient blocks coalesced, evaluate u and d_n u
 //               at all face points in registers, exchange the few values
 //               the species coupling needs (LLF wave speed, taxis flux)
-//               with warp shuffles, and write the face's two FC blocks
-//               coalesced.  Interior, Dirichlet-mirror and prescribed-flux
+//               with warp shuffles, and add the face's two contribution
+//               blocks to the elements' face-sum rows (one colour
+//               segment per launch: no element is touched twice).  Interior, Dirichlet-mirror and prescribed-flux
 //               wall faces share the kernel (face index >= nif: wall).
 //               Face tables (all (lf, perm) signatures, < 11 KB for 2D
 //               k <= 3) live in shared memory; faces are sorted by
 //               signature, so a warp's table reads are broadcasts.
 // k_volume_fast one thread per element: the element's S*nb coefficients
 //               sit in registers; volume tables are shared-memory
-//               broadcasts; all global traffic (U, U0, the d+1 FC slot
-//               tiles, the output) is staged through shared memory so
+//               broadcasts; all global traffic (U, U0, the face-sum
+//               tile, the output) is staged through shared memory so
 //               every HBM access is a coalesced tile.
 #pragma once
 
@@ -119,14 +120,19 @@ __device__ __forceinline__ void ld256(const double* p, double* d) {
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
       : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
 }
+// coherent 32-byte load (rows this kernel also writes)
+__device__ __forceinline__ void ld256c(const double* p, double* d) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p) : "memory");
+}
 __device__ __forceinline__ void st256(double* p, const double* d) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(d[0]), "d"(d[1]), "d"(d[2]),
                "d"(d[3])
                : "memory");
 }
 
-template <int NB>
-__device__ __forceinline__ void load_row_wide(const double* __restrict__ src, double* dst) {
+template <int NB, bool NC = true>
+__device__ __forceinline__ void load_row_wide(const double* src, double* dst) {
   if constexpr (NB % 4 == 2) {
     constexpr int M = NB / 4;
     const bool odd = (reinterpret_cast<uintptr_t>(src) & 16u) != 0;
@@ -134,16 +140,23 @@ __device__ __forceinline__ void load_row_wide(const double* __restrict__ src, do
     const double* p16 = src + (odd ? 0 : 4 * M);
     double w[4 * M];
 #pragma unroll
-    for (int k = 0; k < M; ++k) ld256(p32 + 4 * k, w + 4 * k);
-    const double2 h = __ldg(reinterpret_cast<const double2*>(p16));
+    for (int k = 0; k < M; ++k) {
+      if constexpr (NC) ld256(p32 + 4 * k, w + 4 * k);
+      else ld256c(p32 + 4 * k, w + 4 * k);
+    }
+    const double2 h = NC ? __ldg(reinterpret_cast<const double2*>(p16))
+                         : *reinterpret_cast<const double2*>(p16);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       const double ev = i < 4 * M ? w[i < 4 * M ? i : 0] : (i == 4 * M ? h.x : h.y);
       const double od = i < 2 ? (i == 0 ? h.x : h.y) : w[i >= 2 ? i - 2 : 0];
       dst[i] = odd ? od : ev;
     }
-  } else {
+  } else if constexpr (NC) {
     load_row<NB>(src, dst);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) dst[i] = src[i];
   }
 }
 
@@ -166,6 +179,20 @@ __device__ __forceinline__ void store_row_wide(double* dst, const double* v) {
   }
 }
 
+// face-sum row update: the element's first face side writes, later ones add
+template <int NB>
+__device__ __forceinline__ void acc_row_wide(double* dst, const double* v, bool first) {
+  if (first) {
+    store_row_wide<NB>(dst, v);
+    return;
+  }
+  double o[NB];
+  load_row_wide<NB, false>(dst, o);
+#pragma unroll
+  for (int i = 0; i < NB; ++i) o[i] += v[i];
+  store_row_wide<NB>(dst, o);
+}
+
 template <int D, int K, int NB>
 __device__ __forceinline__ void const_row(int off, double* dst) {
 #pragma unroll
@@ -174,7 +201,7 @@ __device__ __forceinline__ void const_row(int off, double* dst) {
 
 template <int D, int NB>
 struct FaceRec {
-  int code, ein, eout, lfi, lfo;
+  int code, ein, eout;
   bool active, wall;
   double jn[2][D], sfac, h, idi, ido;
   double ci[NB], co[NB];
@@ -197,11 +224,8 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
     const int64_t fc = f < p.nif ? f : p.nif - 1;
     r.code = __ldg(p.ifcode + fc);
     const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + fc);
-    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + fc);
     r.ein = el.x;
     r.eout = el.y;
-    r.lfi = lf.x;
-    r.lfo = lf.y;
     const double* g = p.ifgeo + fc * NFG;
     if constexpr (NFG == 8) {  // 2D: the 64-byte record in two 32-byte loads
       double w[8];
@@ -239,8 +263,6 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
   r.code = __ldg(p.bfcode + bc);
   r.ein = __ldg(p.bfel + bc);
   r.eout = -1;
-  r.lfi = __ldg(p.bflf + bc);
-  r.lfo = 0;
   r.sfac = __ldg(p.bfgeo + bc);
   r.h = 1.0;
   r.idi = r.ido = 0.0;
@@ -253,7 +275,7 @@ __device__ __forceinline__ void load_face_group(const OpParams& p, const double*
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(128, FastFace<D, K, M>::MINB)
-k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, int64_t ngroups) {
+k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ ACC, int64_t ngroups) {
   using T = FastFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, FPW = T::FPW, NCV = T::NCV;
   [[maybe_unused]] constexpr int NFG = Dims<D, K>::NFG;
@@ -291,7 +313,7 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
     const int c0 = __shfl_sync(0xffffffffu, code, 0);
     if (!active) code = c0;
   }
-  const int ein = cur.ein, eout = cur.eout, lfi = cur.lfi, lfo = cur.lfo;
+  const int ein = cur.ein, eout = cur.eout;
   const double sfac = cur.sfac, h = cur.h, idi = cur.idi, ido = cur.ido;
   double jn[2][D];
 #pragma unroll
@@ -470,9 +492,9 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ FC, 
     }
   }
   if (active) {
-    store_row_wide<NB>(FC + (int64_t(lfi) * p.ne + ein) * SN + s * NB, ri);
+    acc_row_wide<NB>(ACC + int64_t(ein) * SN + s * NB, ri, code_first_in(code));
     if (two && !code_skip_out(code))
-      store_row_wide<NB>(FC + (int64_t(lfo) * p.ne + eout) * SN + s * NB, ro);
+      acc_row_wide<NB>(ACC + int64_t(eout) * SN + s * NB, ro, code_first_out(code));
   }
   __syncwarp();  // the warp's scratch is rewritten by the next group
   }
@@ -553,7 +575,7 @@ struct FastVol {
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(FastVol<D, K, M>::TE, FastVol<D, K, M>::MINB)
-k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
+k_volume_fast(OpParams p, const double* __restrict__ U, const double* ACC,
               const double* U0, double* out, double ca, double cb, double cc, int mode) {
   using T = FastVol<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, SNP = T::SNP, Q = T::Q, TE = T::TE;
@@ -565,8 +587,7 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   double* tks = tw + Q;
   double* bufA = sm + T::TAB;
   double* bufB = bufA + TE * SNP;
-  // mode bit 2: the face-slot sum is added by k_fc_add (overlapped run)
-  const bool with_fc = (mode & 4) == 0;
+  // ACC: the face-sum rows (null: no faces); ACC and U0 may alias out
   mode &= 3;
   const int tid = threadIdx.x;
   const int64_t e0 = int64_t(blockIdx.x) * TE;
@@ -576,11 +597,11 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   for (int i = tid; i < T::TGR; i += TE) tgr[i] = p.grad[i];
   for (int i = tid; i < Q; i += TE) tw[i] = p.wv[i];
   for (int i = tid; i < T::TKS; i += TE) tks[i] = p.ks[i];
-  // the FC slot tiles and U0 are consumed after the quadrature loop: start
+  // the face-sum tile and U0 are consumed after the quadrature loop: start
   // pulling them into L2 now (bulk prefetch, one thread per tile)
-  if (tid <= D + 1) {
-    const double* src = tid <= D ? FC + (int64_t(tid) * p.ne + e0) * SN : U0 + e0 * SN;
-    if ((tid <= D && with_fc) || (tid == D + 1 && (mode & 3) == 2 && ca != 0.0 && U0 != nullptr)) {
+  if (tid <= 1) {
+    const double* src = tid == 0 ? ACC + e0 * SN : U0 + e0 * SN;
+    if ((tid == 0 && ACC != nullptr) || (tid == 1 && mode == 2 && ca != 0.0 && U0 != nullptr)) {
       const unsigned bytes = unsigned(nt) * SN * 8u;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes & ~15u) : "memory");
     }
@@ -705,11 +726,10 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
       for (int i = 0; i < NB; ++i) row[M::nl_sp(k) * NB + i] += sd * al[k][i];
   }
 
-  // (3) face-slot tiles (FC[lf] rows of this tile are contiguous)
-#pragma unroll 1
-  for (int lf = 0; lf <= (with_fc ? D : -1); ++lf) {
+  // (3) the face-sum tile
+  if (ACC != nullptr) {
     __syncthreads();
-    tile_load<SN, SNP, TE>(FC + (int64_t(lf) * p.ne + e0) * SN, bufB, nt);
+    tile_load<SN, SNP, TE>(ACC + e0 * SN, bufB, nt);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < SN; ++r) row[r] = fma(scale, bufB[tid * SNP + r], row[r]);
@@ -723,275 +743,6 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* __restrict
   }
   __syncthreads();
   tile_store<SN, SNP, TE>(out + e0 * SN, bufA, nt);
-}
-
-// out += scale(e) * sum_lf FC[lf][e]: the face-slot sum of an overlapped
-// application (volume part on a second stream, concurrent with the face
-// kernel).  Pure streaming: 16-byte loads/stores, grid-stride.
-template <int D, int SN, int NEG>
-__global__ void __launch_bounds__(256)
-k_fc_add(const double* __restrict__ FC, const double* __restrict__ egeo, int64_t ne,
-         double* __restrict__ out, double cc, int mode, int64_t e_begin, int64_t e_end) {
-  // elements [e_begin, e_end) of ne (slot stride ne)
-  static_assert(SN % 2 == 0, "16-byte path");
-  constexpr int H = SN / 2;
-  const int64_t n2 = ne * H;
-  const double2* f2 = reinterpret_cast<const double2*>(FC);
-  double2* o2 = reinterpret_cast<double2*>(out);
-  for (int64_t idx = e_begin * H + int64_t(blockIdx.x) * 256 + threadIdx.x; idx < e_end * H;
-       idx += int64_t(gridDim.x) * 256) {
-    const int64_t e = idx / H;
-    double sc = 1.0;
-    if (mode != 0) {
-      const double idet = 1.0 / __ldg(egeo + e * NEG);
-      sc = mode == 1 ? idet : cc * idet;
-    }
-    double2 acc = __ldcs(f2 + idx);
-#pragma unroll
-    for (int lf = 1; lf <= D; ++lf) {
-      const double2 v = __ldcs(f2 + lf * n2 + idx);
-      acc.x += v.x;
-      acc.y += v.y;
-    }
-    double2 o = o2[idx];
-    o.x = fma(sc, acc.x, o.x);
-    o.y = fma(sc, acc.y, o.y);
-    o2[idx] = o;
-  }
-}
-
-// ------------------------------------------------------- volume, 4 lanes/elem
-//
-// Four threads per element split the quadrature points (q = j, j+4, ...),
-// holding only the coefficients of the species the point physics reads
-// plus their partial projections; the partials meet through two xor
-// shuffles.  The epilogue (exact-stiffness diffusion, linear source, the
-// d+1 face slots, U0 and the Runge-Kutta combination) gives each thread
-// every 4th output entry of its element: for a fixed step the 32 lanes of
-// a warp touch 8 rows x 4 consecutive doubles = 8 full 32-byte sectors,
-// so the FC / U0 / output streams need no shared-memory staging.
-
-template <int D, int K, class M>
-struct Vol4 {
-  using Dm = Dims<D, K>;
-  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, Q = Dm::NQV;
-  static constexpr int NSYM = Dm::NSYM, NEG = Dm::NEG;
-  static constexpr int TPE = 4, THREADS = 128, TE = THREADS / TPE;
-  static constexpr int NACC = M::NFLUX * NB + M::NNL * NB;
-  static constexpr int TPHI = Q * NB, TGR = Q * NB * D, TKS = NSYM * NB * NB;
-  static constexpr int TAB = (TPHI + TGR + Q + TKS + 1) & ~1;
-  static constexpr int SNP = SN | 1;
-  // prefetched tiles: D+1 face slots + U0, dense rows of SN doubles
-  static constexpr int NPF = D + 2;
-  static constexpr bool kAsync = (SN % 2) == 0;  // 16-byte cp.async granules
-  static constexpr size_t smem() {
-    return size_t(TAB + TE * SNP + TE * (NACC > 0 ? NACC : 1) + TE * NEG + TE * NB * NB +
-                  NPF * TE * SN) * 8;
-  }
-  static constexpr bool ok = M::NVAL * NB <= 40 && smem() <= 96 * 1024 && SN % TPE == 0;
-  static constexpr int MINB = 3;
-};
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-template <int D, int K, class M>
-__global__ void __launch_bounds__(128, Vol4<D, K, M>::MINB)
-k_volume4(OpParams p, const double* __restrict__ U, const double* __restrict__ FC,
-          const double* U0, double* out, double ca, double cb, double cc, int mode) {
-  using T = Vol4<D, K, M>;
-  constexpr int NB = T::NB, S = T::S, SN = T::SN, SNP = T::SNP, Q = T::Q, TE = T::TE;
-  constexpr int NEG = T::NEG, NSYM = T::NSYM, TPE = T::TPE;
-  constexpr int NF = M::NFLUX, NL = M::NNL, NACC = T::NACC > 0 ? T::NACC : 1;
-  extern __shared__ __align__(16) double sm[];
-  double* tphi = sm;
-  double* tgr = tphi + T::TPHI;
-  double* tw = tgr + T::TGR;
-  double* tks = tw + Q;
-  double* uT = sm + T::TAB;          // [TE][SNP] coefficient rows
-  double* aT = uT + TE * SNP;        // [TE][NACC] reduced projections
-  double* gT = aT + TE * NACC;       // [TE][NEG]  geometry
-  double* kT = gT + TE * NEG;        // [TE][NB][NB] physical stiffness
-  double* pf = kT + TE * NB * NB;    // [NPF][TE][SN] prefetched FC slots, U0
-  // keep pf 16-byte aligned
-  static_assert(((T::TAB + TE * SNP + TE * NACC + TE * NEG + TE * NB * NB) % 2) == 0 || !T::kAsync,
-                "prefetch region must be 16-byte aligned");
-
-  const int tid = threadIdx.x;
-  const int64_t e0 = int64_t(blockIdx.x) * TE;
-  const int nt = int(p.ne - e0 < TE ? p.ne - e0 : TE);
-  const bool use_u0 = mode == 2 && ca != 0.0;
-  // start the epilogue's streams now; they land while the quadrature runs
-  if constexpr (T::kAsync) {
-    constexpr int H = SN / 2;
-    for (int k = 0; k < T::NPF; ++k) {
-      if (k == D + 1 && !use_u0) break;
-      const double* src = k <= D ? FC + (int64_t(k) * p.ne + e0) * SN : U0 + e0 * SN;
-      double* dst = pf + k * TE * SN;
-      for (int idx = tid; idx < nt * H; idx += 128) cp_async16(dst + 2 * idx, src + 2 * idx);
-    }
-    cp_async_commit();
-  }
-  for (int i = tid; i < T::TPHI; i += 128) tphi[i] = p.phi[i];
-  for (int i = tid; i < T::TGR; i += 128) tgr[i] = p.grad[i];
-  for (int i = tid; i < Q; i += 128) tw[i] = p.wv[i];
-  for (int i = tid; i < T::TKS; i += 128) tks[i] = p.ks[i];
-  for (int idx = tid; idx < nt * SN; idx += 128) {
-    const int e = idx / SN, r = idx - e * SN;
-    uT[e * SNP + r] = __ldg(U + e0 * SN + idx);
-  }
-  for (int idx = tid; idx < nt * NEG; idx += 128) gT[idx] = __ldg(p.egeo + e0 * NEG + idx);
-  __syncthreads();
-
-  const int el = tid / TPE, j = tid - el * TPE;
-  const bool act = el < nt;
-  const double* cr = uT + (act ? el : 0) * SNP;
-  const double* ge = gT + (act ? el : 0) * NEG;
-
-  // physical stiffness sum_p M_p KS_p of the element, shared by its lanes
-  for (int idx = j; idx < NB * NB; idx += TPE) {
-    double t = 0.0;
-#pragma unroll
-    for (int q = 0; q < NSYM; ++q) t = fma(ge[1 + q], tks[q * NB * NB + idx], t);
-    kT[(act ? el : 0) * NB * NB + idx] = t;
-  }
-
-  // ---- quadrature (points q = j, j + TPE, ...) -----------------------
-  if constexpr (NF + NL > 0) {
-    double cv[M::NVAL > 0 ? M::NVAL : 1][NB];
-#pragma unroll
-    for (int k = 0; k < M::NVAL; ++k)
-#pragma unroll
-      for (int i = 0; i < NB; ++i) cv[k][i] = cr[M::val_sp(k) * NB + i];
-    double ms[NSYM];
-#pragma unroll
-    for (int k = 0; k < NSYM; ++k) ms[k] = ge[1 + k];
-    double af[NF > 0 ? NF : 1][NB], al[NL > 0 ? NL : 1][NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-#pragma unroll
-      for (int k = 0; k < (NF > 0 ? NF : 1); ++k) af[k][i] = 0.0;
-#pragma unroll
-      for (int k = 0; k < (NL > 0 ? NL : 1); ++k) al[k][i] = 0.0;
-    }
-#pragma unroll 1
-    for (int q = j; q < Q; q += TPE) {
-      const double* ph = tphi + q * NB;
-      const double* gr = tgr + q * NB * D;
-      double v[M::NVAL], g[M::NGRAD][D];
-#pragma unroll
-      for (int k = 0; k < M::NVAL; ++k) v[k] = 0.0;
-#pragma unroll
-      for (int k = 0; k < M::NGRAD; ++k)
-#pragma unroll
-        for (int a = 0; a < D; ++a) g[k][a] = 0.0;
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const double phv = ph[i];
-#pragma unroll
-        for (int k = 0; k < M::NVAL; ++k) v[k] = fma(phv, cv[k][i], v[k]);
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double gv = gr[i * D + a];
-#pragma unroll
-          for (int k = 0; k < M::NGRAD; ++k) g[k][a] = fma(gv, cv[M::grad_in_val(k)][i], g[k][a]);
-        }
-      }
-      double gM[M::NGRAD][D];
-#pragma unroll
-      for (int k = 0; k < M::NGRAD; ++k)
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          double t = 0.0;
-#pragma unroll
-          for (int a = 0; a < D; ++a) t = fma(g[k][a], ms[sym_index(D, a, b)], t);
-          gM[k][b] = t;
-        }
-      double fr[NF > 0 ? NF : 1][D], nl[NL > 0 ? NL : 1];
-      M::template volume_point<D>(p.P, v, gM, fr, nl);
-      const double w = tw[q];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double gv = w * gr[i * D + a];
-#pragma unroll
-          for (int k = 0; k < NF; ++k) af[k][i] = fma(fr[k][a], gv, af[k][i]);
-        }
-        const double pw = w * ph[i];
-#pragma unroll
-        for (int k = 0; k < NL; ++k) al[k][i] = fma(nl[k], pw, al[k][i]);
-      }
-    }
-    // combine the TPE partial projections of the element
-#pragma unroll
-    for (int o = 1; o < TPE; o <<= 1) {
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-#pragma unroll
-        for (int k = 0; k < NF; ++k) af[k][i] += __shfl_xor_sync(0xffffffffu, af[k][i], o);
-#pragma unroll
-        for (int k = 0; k < NL; ++k) al[k][i] += __shfl_xor_sync(0xffffffffu, al[k][i], o);
-      }
-    }
-    if (act && j == 0) {
-      double* a = aT + el * NACC;
-#pragma unroll
-      for (int k = 0; k < NF; ++k)
-#pragma unroll
-        for (int i = 0; i < NB; ++i) a[k * NB + i] = af[k][i];
-#pragma unroll
-      for (int k = 0; k < NL; ++k)
-#pragma unroll
-        for (int i = 0; i < NB; ++i) a[NF * NB + k * NB + i] = al[k][i];
-    }
-  }
-  if constexpr (T::kAsync) cp_async_wait_all();
-  __syncthreads();
-  if (!act) return;
-
-  // ---- epilogue: every TPE-th output entry of the element --------------
-  const double detJ = ge[0];
-  const double idet = 1.0 / detJ;
-  const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
-  const int64_t row = (e0 + el) * SN;
-  const int64_t slot_stride = p.ne * SN;
-  const double* kp = kT + el * NB * NB;
-#pragma unroll
-  for (int k = 0; k < SN / TPE; ++k) {
-    const int r = j + TPE * k;
-    const int s = r / NB, i = r - s * NB;
-    double dif = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < NB; ++jj) dif = fma(cr[s * NB + jj], kp[jj * NB + i], dif);
-    double lin = 0.0;
-#pragma unroll
-    for (int t = 0; t < S; ++t)
-      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
-    double acc = lin - p.A[s] * dif;
-    if constexpr (NF + NL > 0) {
-      const int fi = M::flux_index(s), li = M::nl_index(s);
-      if (fi >= 0) acc += aT[el * NACC + fi * NB + i];
-      if (li >= 0) acc += aT[el * NACC + NF * NB + li * NB + i];
-    }
-    double rv = detJ * acc;
-#pragma unroll
-    for (int lf = 0; lf <= D; ++lf)
-      rv += T::kAsync ? pf[(lf * TE + el) * SN + r] : __ldcs(FC + lf * slot_stride + row + r);
-    double o;
-    if (mode == 0) o = rv;
-    else if (mode == 1) o = rv * idet;
-    else {
-      o = fma(cb, cr[r], scale * rv);
-      if (use_u0)
-        o = fma(ca, T::kAsync ? pf[((D + 1) * TE + el) * SN + r] : __ldcs(U0 + row + r), o);
-    }
-    out[row + r] = o;
-  }
 }
 
 }  // namespace tdg

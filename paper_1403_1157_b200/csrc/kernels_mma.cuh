@@ -82,7 +82,7 @@ struct MmaFace {
 template <int D, int K, class M>
 __global__ void __launch_bounds__(128, MmaFace<D, K, M>::MINB)
 k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
-            double* __restrict__ FC) {
+            double* __restrict__ ACC) {
   using T = MmaFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
   constexpr int NFW = T::NFW, NC = T::NC, NT = T::NT, NCP = T::NCP;
@@ -100,7 +100,7 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
   double* cvS = xS + T::SX + T::SALIAS;  // [NFW][8][NCV]
   double* outS = dUS;                // [2][NBM][NCP], aliases dUS..xS (dead by then)
   double* fD = cvS + T::SCV;         // [NFW][NFG]
-  int* fI = reinterpret_cast<int*>(fD + T::SFD);  // [NFW][8]: code ein eout lfi lfo valid
+  int* fI = reinterpret_cast<int*>(fD + T::SFD);  // [NFW][8]: code ein eout - - valid
 
   const int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp;
   const int64_t wi = (p.nif + NFW - 1) / NFW;
@@ -127,15 +127,12 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
         r[0] = __ldg(p.ifcode + f);
         r[1] = __ldg(p.ifel + 2 * f);
         r[2] = __ldg(p.ifel + 2 * f + 1);
-        r[3] = __ldg(p.iflf + 2 * f);
-        r[4] = __ldg(p.iflf + 2 * f + 1);
 #pragma unroll
         for (int k = 0; k < NFG; ++k) d[k] = __ldg(p.ifgeo + f * NFG + k);
       } else {
         const int64_t b = f - p.nif;
         r[0] = __ldg(p.bfcode + b);
         r[1] = __ldg(p.bfel + b);
-        r[3] = __ldg(p.bflf + b);
         d[2 * D] = __ldg(p.bfgeo + b);
       }
     }
@@ -512,7 +509,7 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
     }
   }
 
-  // ---- projected rows -> FC, coalesced per face side -------------------
+  // ---- projected rows -> face sums, coalesced per face side ------------
 #pragma unroll
   for (int it = 0; it < IT; ++it)
 #pragma unroll
@@ -532,294 +529,8 @@ k_faces_mma(OpParams p, const double* __restrict__ tabs, const double* __restric
     const int code = fr[0];
     if (side && (wall || code_mirror(code) || code_skip_out(code))) continue;
     const int e = side ? fr[2] : fr[1];
-    const int lf = side ? fr[4] : fr[3];
-    FC[(int64_t(lf) * p.ne + e) * SN + si] = outS[(side * NBM + i) * NCP + f * S + s];
-  }
-}
-
-// ----------------------------------------------------------------- volume
-//
-// Tensor-core volume kernel: a warp owns EW = 8 elements.  The point values
-// of the NV value species and the reference gradients of the NG gradient
-// species at the quadrature points, and the projections of the pulled-back
-// flux rows and the bilinear source, are DMMA GEMMs against zero-padded
-// tables (tables.mma_volume_tables) held in shared memory:
-//
-//   vals[q][(e,v)]   = sum_k Phi[q][k] c_e[val_sp(v)][k]
-//   g_a[q][(e,g)]    = sum_k G_a[q][k] c_e[grad_sp(g)][k]
-//   R_f[i][(e,f)]   += sum_q sum_a G_a[q][i] (w_q F_ref,a)[q][(e,f)]
-//   R_l[i][(e,l)]   += sum_q Phi[q][i]    (w_q S_nl)[q][(e,l)]
-//
-// Point physics (one (element, point) pair per lane) and the epilogue
-// (exact-stiffness diffusion, linear source, face slots, U0, stage
-// combination; 4 lanes per element, every 4th output entry) stay SIMT.
-
-template <int D, int K, class M>
-struct MmaVol {
-  using Dm = Dims<D, K>;
-  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, Q = Dm::NQV;
-  static constexpr int NEG = Dm::NEG, NSYM = Dm::NSYM;
-  static constexpr int QP = ceil_to(Q, 8), NBK = ceil_to(NB, 4), NBM = ceil_to(NB, 8);
-  static constexpr int NV = M::NVAL, NG = M::NGRAD, NF = M::NFLUX, NL = M::NNL;
-  static constexpr int EW = 8, WARPS = 4, TE = EW * WARPS;
-  static constexpr int MTQ = QP / 8, KT = NBK / 4, IT = NBM / 8;
-  static constexpr int NACC = (NF + NL) * NB > 0 ? (NF + NL) * NB : 1;
-  static constexpr int SNP = SN | 1;
-  // tables (doubles)
-  static constexpr int OPHI = 0, OG = QP * NBK, OGT = OG + D * QP * NBK, OPT = OGT + D * NBM * QP,
-                       TAB = OPT + NBM * QP;
-  static constexpr int TKS = NSYM * NB * NB;
-  // per-warp shared memory
-  static constexpr int W_CF = EW * SNP;
-  static constexpr int W_VAL = 8 * EW * (NV > 0 ? NV : 1);
-  static constexpr int W_GR = D * 8 * EW * (NG > 0 ? NG : 1);
-  static constexpr int W_PF = D * 8 * EW * (NF > 0 ? NF : 1);
-  static constexpr int W_PL = 8 * EW * (NL > 0 ? NL : 1);
-  static constexpr int W_ACC = EW * NACC, W_GEO = EW * NEG, W_KP = EW * NB * NB;
-  static constexpr int PW = (W_CF + W_VAL + W_GR + W_PF + W_PL + W_ACC + W_GEO + W_KP + 1) & ~1;
-  static constexpr size_t smem() { return size_t(((TAB + TKS + 1) & ~1) + WARPS * PW) * 8; }
-  static constexpr bool ok = smem() <= 100 * 1024;
-};
-
-template <int D, int K, class M>
-__global__ void __launch_bounds__(128)
-k_volume_mma(OpParams p, const double* __restrict__ vtab, const double* __restrict__ U,
-             const double* __restrict__ FC, const double* U0, double* out, double ca, double cb,
-             double cc, int mode) {
-  using T = MmaVol<D, K, M>;
-  constexpr int NB = T::NB, S = T::S, SN = T::SN, Q = T::Q, NEG = T::NEG, NSYM = T::NSYM;
-  constexpr int QP = T::QP, NBK = T::NBK, NBM = T::NBM, NV = T::NV, NG = T::NG, NF = T::NF;
-  constexpr int NL = T::NL, EW = T::EW, MTQ = T::MTQ, KT = T::KT, IT = T::IT, NACC = T::NACC;
-  constexpr int SNP = T::SNP;
-  extern __shared__ __align__(16) double sm[];
-  const bool with_fc = (mode & 4) == 0;
-  mode &= 3;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  double* tab = sm;
-  double* tks = tab + T::TAB;
-  double* W = sm + ((T::TAB + T::TKS + 1) & ~1) + warp * T::PW;
-  double* cF = W;                     // [EW][SNP]
-  double* vS = cF + T::W_CF;          // [8][EW*NV]   point values
-  double* gS = vS + T::W_VAL;         // [D][8][EW*NG] reference gradients
-  double* pF = gS + T::W_GR;          // [D][8][EW*NF] w F_ref
-  double* pL = pF + T::W_PF;          // [8][EW*NL]    w S_nl
-  double* aT = pL + T::W_PL;          // [EW][NACC]    projections
-  double* gT = aT + T::W_ACC;         // [EW][NEG]
-  double* kT = gT + T::W_GEO;         // [EW][NB*NB]   physical stiffness
-
-  for (int i = threadIdx.x; i < T::TAB; i += 128) tab[i] = __ldg(vtab + i);
-  for (int i = threadIdx.x; i < T::TKS; i += 128) tks[i] = __ldg(p.ks + i);
-  const int64_t e0 = int64_t(blockIdx.x) * T::TE + warp * EW;
-  const int ne = int(p.ne - e0 < EW ? (p.ne - e0 > 0 ? p.ne - e0 : 0) : EW);
-  for (int idx = lane; idx < ne * SN; idx += 32) {
-    const int e = idx / SN, r = idx - e * SN;
-    cF[e * SNP + r] = __ldg(U + e0 * SN + idx);
-  }
-  for (int idx = lane; idx < (EW - ne) * SNP; idx += 32) cF[ne * SNP + idx] = 0.0;
-  for (int idx = lane; idx < EW * NEG; idx += 32)
-    gT[idx] = idx < ne * NEG ? __ldg(p.egeo + e0 * NEG + idx) : (idx % NEG == 0 ? 1.0 : 0.0);
-  __syncthreads();
-  if (ne == 0) return;  // warp-uniform (no barrier follows)
-
-  // ---- quadrature on the tensor cores -----------------------------------
-  if constexpr (NF + NL > 0) {
-    constexpr int NTV = NV, NTG = NG, NTF = NF, NTL = NL;   // n-tiles (EW = 8 columns each)
-    double accF[IT][NTF > 0 ? NTF : 1][2], accL[IT][NTL > 0 ? NTL : 1][2];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-#pragma unroll
-      for (int nt = 0; nt < (NTF > 0 ? NTF : 1); ++nt) accF[it][nt][0] = accF[it][nt][1] = 0.0;
-#pragma unroll
-      for (int nt = 0; nt < (NTL > 0 ? NTL : 1); ++nt) accL[it][nt][0] = accL[it][nt][1] = 0.0;
-    }
-#pragma unroll 1
-    for (int mt = 0; mt < MTQ; ++mt) {
-      const int row = 8 * mt + g;
-      double uv[NTV][2], ug[D][NTG > 0 ? NTG : 1][2];
-#pragma unroll
-      for (int nt = 0; nt < NTV; ++nt) uv[nt][0] = uv[nt][1] = 0.0;
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int nt = 0; nt < (NTG > 0 ? NTG : 1); ++nt) ug[a][nt][0] = ug[a][nt][1] = 0.0;
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        const int k = 4 * kt + tq;
-        const bool kv = k < NB;
-        const double av = tab[T::OPHI + row * NBK + k];
-#pragma unroll
-        for (int nt = 0; nt < NTV; ++nt) {
-          const int col = 8 * nt + g, e = col / NV, v = col - e * NV;
-          dmma(uv[nt][0], uv[nt][1], av, kv ? cF[e * SNP + M::val_sp(v) * NB + k] : 0.0);
-        }
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double ag = tab[T::OG + (a * QP + row) * NBK + k];
-#pragma unroll
-          for (int nt = 0; nt < NTG; ++nt) {
-            const int col = 8 * nt + g, e = col / NG, v = col - e * NG;
-            dmma(ug[a][nt][0], ug[a][nt][1], ag, kv ? cF[e * SNP + M::grad_sp(v) * NB + k] : 0.0);
-          }
-        }
-      }
-      // stage the chunk's point data ([ql][col])
-#pragma unroll
-      for (int nt = 0; nt < NTV; ++nt)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) vS[g * (EW * NV) + 8 * nt + 2 * tq + j] = uv[nt][j];
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int nt = 0; nt < NTG; ++nt)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) gS[(a * 8 + g) * (EW * NG) + 8 * nt + 2 * tq + j] = ug[a][nt][j];
-      __syncwarp();
-      // point physics, one (element, point) pair per lane step
-      for (int pr = lane; pr < EW * 8; pr += 32) {
-        const int e = pr >> 3, ql = pr & 7, q = 8 * mt + ql;
-        double fr[NF > 0 ? NF : 1][D], nl[NL > 0 ? NL : 1];
-        if (q < Q && e < ne) {
-          double v[NV > 0 ? NV : 1], gr[NG > 0 ? NG : 1][D];
-#pragma unroll
-          for (int k = 0; k < NV; ++k) v[k] = vS[ql * (EW * NV) + e * NV + k];
-#pragma unroll
-          for (int k = 0; k < NG; ++k)
-#pragma unroll
-            for (int a = 0; a < D; ++a) gr[k][a] = gS[(a * 8 + ql) * (EW * NG) + e * NG + k];
-          const double* ge = gT + e * NEG;
-          double gM[NG > 0 ? NG : 1][D];
-#pragma unroll
-          for (int k = 0; k < NG; ++k)
-#pragma unroll
-            for (int b = 0; b < D; ++b) {
-              double t = 0.0;
-#pragma unroll
-              for (int a = 0; a < D; ++a) t = fma(gr[k][a], ge[1 + sym_index_d(D, a, b)], t);
-              gM[k][b] = t;
-            }
-          M::template volume_point<D>(p.P, v, gM, fr, nl);
-          const double w = __ldg(p.wv + q);
-#pragma unroll
-          for (int k = 0; k < NF; ++k)
-#pragma unroll
-            for (int a = 0; a < D; ++a) fr[k][a] *= w;
-#pragma unroll
-          for (int k = 0; k < NL; ++k) nl[k] *= w;
-        } else {
-#pragma unroll
-          for (int k = 0; k < (NF > 0 ? NF : 1); ++k)
-#pragma unroll
-            for (int a = 0; a < D; ++a) fr[k][a] = 0.0;
-#pragma unroll
-          for (int k = 0; k < (NL > 0 ? NL : 1); ++k) nl[k] = 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < NF; ++k)
-#pragma unroll
-          for (int a = 0; a < D; ++a) pF[(a * 8 + ql) * (EW * NF) + e * NF + k] = fr[k][a];
-#pragma unroll
-        for (int k = 0; k < NL; ++k) pL[ql * (EW * NL) + e * NL + k] = nl[k];
-      }
-      __syncwarp();
-      // projections of this chunk's 8 points (K = 8: two k-steps)
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int ql = 4 * ks + tq, qc = 8 * mt + ql;
-#pragma unroll
-        for (int it = 0; it < IT; ++it) {
-          const int i = 8 * it + g;
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const double ag = tab[T::OGT + (a * NBM + i) * QP + qc];
-#pragma unroll
-            for (int nt = 0; nt < NTF; ++nt)
-              dmma(accF[it][nt][0], accF[it][nt][1], ag, pF[(a * 8 + ql) * (EW * NF) + 8 * nt + g]);
-          }
-          if constexpr (NL > 0) {
-            const double ap = tab[T::OPT + i * QP + qc];
-#pragma unroll
-            for (int nt = 0; nt < NTL; ++nt)
-              dmma(accL[it][nt][0], accL[it][nt][1], ap, pL[ql * (EW * NL) + 8 * nt + g]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-    // projections -> per-element rows aT[e][k*NB + i]
-#pragma unroll
-    for (int it = 0; it < IT; ++it)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int i = 8 * it + g;
-        if (i < NB) {
-#pragma unroll
-          for (int nt = 0; nt < NTF; ++nt) {
-            const int col = 8 * nt + 2 * tq + j, e = col / NF, k = col - e * NF;
-            aT[e * NACC + k * NB + i] = accF[it][nt][j];
-          }
-#pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) {
-            const int col = 8 * nt + 2 * tq + j, e = col / NL, k = col - e * NL;
-            aT[e * NACC + NF * NB + k * NB + i] = accL[it][nt][j];
-          }
-        }
-      }
-  }
-  // physical stiffness of each element: 4 lanes per element
-  {
-    const int e = lane >> 2, jq = lane & 3;
-    const double* ge = gT + e * NEG;
-    for (int idx = jq; idx < NB * NB; idx += 4) {
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < NSYM; ++q) t = fma(ge[1 + q], tks[q * NB * NB + idx], t);
-      kT[e * NB * NB + idx] = t;
-    }
-  }
-  __syncwarp();
-
-  // ---- epilogue: 4 lanes per element, every 4th output entry --------------
-  const int e = lane >> 2, jq = lane & 3;
-  if (e >= ne) return;
-  const double* cr = cF + e * SNP;
-  const double* ge = gT + e * NEG;
-  const double* kp = kT + e * NB * NB;
-  const double detJ = ge[0];
-  const double idet = 1.0 / detJ;
-  const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
-  const int64_t row = (e0 + e) * SN;
-  const int64_t slot_stride = p.ne * SN;
-  const bool use_u0 = mode == 2 && ca != 0.0;
-#pragma unroll 2
-  for (int r = jq; r < SN; r += 4) {
-    const int s = r / NB, i = r - s * NB;
-    double dif = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < NB; ++jj) dif = fma(cr[s * NB + jj], kp[jj * NB + i], dif);
-    double lin = 0.0;
-#pragma unroll
-    for (int t = 0; t < S; ++t)
-      if (M::lin_nz(s, t)) lin = fma(p.L[s * kMaxS + t], cr[t * NB + i], lin);
-    double acc = lin - p.A[s] * dif;
-    if constexpr (NF + NL > 0) {
-      const int fi = M::flux_index(s), li = M::nl_index(s);
-      if (fi >= 0) acc += aT[e * NACC + fi * NB + i];
-      if (li >= 0) acc += aT[e * NACC + NF * NB + li * NB + i];
-    }
-    double rv = detJ * acc;
-    if (with_fc) {
-#pragma unroll
-      for (int lf = 0; lf <= D; ++lf) rv += __ldcs(FC + lf * slot_stride + row + r);
-    }
-    double o;
-    if (mode == 0) o = rv;
-    else if (mode == 1) o = rv * idet;
-    else {
-      o = fma(cb, cr[r], scale * rv);
-      if (use_u0) o = fma(ca, __ldcs(U0 + row + r), o);
-    }
-    out[row + r] = o;
+    acc_put(ACC + int64_t(e) * SN + si, outS[(side * NBM + i) * NCP + f * S + s],
+            side ? code_first_out(code) : code_first_in(code));
   }
 }
 

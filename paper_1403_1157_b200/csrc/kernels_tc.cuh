@@ -23,7 +23,7 @@
 // ks uses points 8qt + 2t + ks): no lane exchange anywhere.  The output
 // columns are permuted, pi(8nt + 2t + j) = 4(2nt + j) + t, so a lane's
 // output entries are exactly the basis indices of its A fragments: the
-// linear source, the U / U0 / face-slot reads and the output stores are
+// linear source, the U / U0 / face-sum reads and the output stores are
 // lane-local, 32-byte-contiguous accesses.  Formulas as k_volume
 // (reference operator.py:292-324, model.py:147-170); tables built by
 // tables.tc_volume_tables.
@@ -63,7 +63,7 @@ struct TcVol {
 template <int D, int K, class M>
 __global__ void __launch_bounds__(128, TcVol<D, K, M>::MINB)
 k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
-            const double* __restrict__ FC, const double* U0, double* out, double ca, double cb,
+            const double* ACC, const double* U0, double* out, double ca, double cb,
             double cc, int mode) {
   using T = TcVol<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, NEG = T::NEG, NSYM = T::NSYM;
@@ -76,8 +76,8 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
     __syncthreads();
     tb = sm;
   }
-  // mode bit 2: the face-slot sum is added by k_fc_add (overlapped run)
-  const bool with_fc = (mode & 4) == 0;
+  // ACC: face-sum rows (null: no faces); ACC and U0 may alias out (each
+  // lane reads its own entries before writing them)
   mode &= 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -223,10 +223,7 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
             if (li == k) acc += al[k][nt][j];
           double rv = detJ * (acc - As * dif[nt][j] + lin);
           const int64_t off = ec * SN + s * NB + i;
-          if (with_fc) {
-#pragma unroll
-            for (int lf = 0; lf <= D; ++lf) rv += __ldcs(FC + int64_t(lf) * p.ne * SN + off);
-          }
+          if (ACC != nullptr) rv += __ldcs(ACC + off);
           double o = scale * rv;
           if (mode == 2) {
             o = fma(cb, cf[s][kt], o);

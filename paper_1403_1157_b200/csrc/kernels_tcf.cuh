@@ -1,28 +1,12 @@
-// Interior faces on the FP64 tensor cores, transposed (3D).
-//
-// A warp owns a block of up to 8 interior faces with one trace-table
-// signature (tables.tc_face_blocks): the faces are the M dimension of
-// every mma.sync.m8n8k4.f64, so the signature's tables are the shared B
-// operands and the per-face geometry (jn = Jinv n, lifting weight) scales
-// the A operands lane by lane.  With g = lane>>2, t = lane&3 a lane owns
-// face g; its accumulators hold columns 2t + j of the 8-column tiles:
-//
-//   traces      u[f][q]   = sum_k c[f][k] B[q][k]                  (B^T tables)
-//               d_n u     = sum_a sum_k (jn_a c)[f][k] G_a[q][k]
-//   lifting     m[f][n]   = kappa_f sum_q dU[f][q] w_q B[q][pi(n)]  (modal)
-//               rho[f][q] = sum_i m[f][i] B[q][i]
-//   projection  R[f][n]  += sum_q Y[f][q] B[q][pi(n)] + sum_qa (X jn_a)[f][q] G_a[q][pi(n)]
-//
-// Point quantities come out in the accumulator layout (face g, points
-// 8qt + 2t + j) and feed the next GEMM as A operands one point parity at a
-// time (k-step ks takes points 8qt + 2t + ks); the lifting coefficients
-// feed rho the same way through the column permutation pi(8nt + 2t + j) =
-// 4(2nt + j) + t.  No lane exchange, no warp barrier: pass A evaluates the
-// coupled LLF physics (wave speed, taxis flux normals) per (face, point)
-// into a lane-private shared-memory slice; pass B runs species by species
-// (jumps -> modal lifting; traces, flux, projection) and writes the two
-// face-slot rows.  Formulas as k_faces_fast / k_faces_mma (reference
-// operator.py:326-434, flux.py:92-138); wall faces stay on k_faces_mma.
+// Interior faces on the FP64 tensor cores (3D), transposed: the face's
+// contractions run as mma.sync.m8n8k4.f64 (DMMA) with the trace-table
+// signature's tables as the B operands (tables.tc_face_tables, stored
+// fragment-major so a warp's B-operand load is 32 consecutive doubles).
+// The faces come in blocks of up to 8 with one signature
+// (tables.tc_face_blocks) inside one colour segment; the kernel adds each
+// face side's contribution to the element's face-sum row.  Formulas as
+// k_faces_fast / k_faces_mma (reference operator.py:326-434,
+// flux.py:92-138); wall faces run on k_faces_mma.
 #pragma once
 
 #include "common.cuh"
@@ -72,271 +56,16 @@ struct TcfPoint {
   __device__ __forceinline__ double operator()(int kind, int sp) const { return v[kind][sp]; }
 };
 
-template <int D, int K, class M>
-__global__ void __launch_bounds__(128, TcFace<D, K, M>::MINB)
-k_faces_tc(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
-           int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ FC) {
-  using T = TcFace<D, K, M>;
-  using PH = TcfPhys<M>;
-  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
-  constexpr int QP = T::QP, QT = T::QT, KT = T::KT, NNT = T::NNT;
-  constexpr int NCV = T::NCV, TS = T::TS;
-  extern __shared__ __align__(16) double sm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  double* cvS = sm + warp * T::PWS + g * QP * NCV;  // this lane's face
-
-  for (int64_t blk = blk0 + int64_t(blockIdx.x) * T::WARPS + warp; blk < blk1;
-       blk += int64_t(gridDim.x) * T::WARPS) {
-    const int2 bd = __ldg(reinterpret_cast<const int2*>(blocks) + blk);
-    const bool active = g < bd.y;
-    const int64_t f = int64_t(bd.x) + (active ? g : 0);
-    const int code = __ldg(p.ifcode + f);
-    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
-    const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
-    const double* gg = p.ifgeo + f * NFG;
-    double jn[2][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      jn[0][a] = __ldg(gg + a);
-      jn[1][a] = __ldg(gg + D + a);
-    }
-    const double sfac = __ldg(gg + 2 * D), h = __ldg(gg + 2 * D + 1);
-    const double idi = __ldg(gg + 2 * D + 2), ido = __ldg(gg + 2 * D + 3);
-    const bool mirror = M::kMirror && code_mirror(code);
-    // signature of the block (uniform): the B operands
-    const int sig = __shfl_sync(0xffffffffu, code, 0) & 1023;
-    const double* Ti = tabs + size_t(sig & 31) * TS;
-    const double* To = tabs + size_t((sig >> 5) & 31) * TS;
-    const double* ui_row = U + int64_t(el.x) * SN;
-    const double* uo_row = U + int64_t(mirror ? el.x : el.y) * SN;
-
-    // ---- pass A: coupled point physics -> lane-private slice -----------
-    if constexpr (M::kConv) {
-      constexpr int NV = PH::NV, NG = PH::NG;
-      double ci[NV][KT], co[NV][KT];
-#pragma unroll
-      for (int k = 0; k < NV; ++k)
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const bool in = 4 * kt + t < NB;
-          ci[k][kt] = in ? __ldg(ui_row + PH::val(k) * NB + 4 * kt + t) : 0.0;
-          co[k][kt] = in ? __ldg(uo_row + PH::val(k) * NB + 4 * kt + t) : 0.0;
-        }
-#pragma unroll 1
-      for (int qt = 0; qt < QT; ++qt) {
-        double vi[NV][2], vo[NV][2], di[NG][2], dq[NG][2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-#pragma unroll
-          for (int k = 0; k < NV; ++k) vi[k][j] = vo[k][j] = 0.0;
-#pragma unroll
-          for (int k = 0; k < NG; ++k) di[k][j] = dq[k][j] = 0.0;
-        }
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
-          const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            dmma(vi[k][0], vi[k][1], ci[k][kt], bi);
-            dmma(vo[k][0], vo[k][1], co[k][kt], bo);
-          }
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const double gi = __ldg(Ti + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane);
-            const double go = __ldg(To + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane);
-#pragma unroll
-            for (int k = 0; k < NG; ++k) {
-              int kv = 0;
-#pragma unroll
-              for (int j2 = 0; j2 < NV; ++j2)
-                if (PH::val(j2) == PH::grad(k)) kv = j2;
-              dmma(di[k][0], di[k][1], ci[kv][kt] * jn[0][a], gi);
-              dmma(dq[k][0], dq[k][1], co[kv][kt] * jn[1][a], go);
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          TcfPoint<M> pt;
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            pt.v[0][PH::val(k)] = vi[k][j];
-            pt.v[1][PH::val(k)] = mirror ? 2.0 * M::mirror_value(p.P, PH::val(k)) - vi[k][j] : vo[k][j];
-          }
-#pragma unroll
-          for (int k = 0; k < NG; ++k)
-            pt.v[2][PH::grad(k)] = mirror ? di[k][j] : 0.5 * (di[k][j] + dq[k][j]);
-          double cv[NCV];
-          M::face_point(p.P, pt, cv);
-          const int q = 8 * qt + 2 * t + j;
-#pragma unroll
-          for (int c = 0; c < NCV; ++c) cvS[q * NCV + c] = cv[c];
-        }
-      }
-    }
-
-    // lifting weights per side (operator.py:336-357)
-    const bool br2 = p.scheme == BR2;
-    const bool lift = p.scheme != IP && p.scheme != BO;
-    const bool use_in = lift && (mirror || br2 || code_minus_in(code));
-    const bool use_out = lift && !mirror && (br2 || !code_minus_in(code));
-    const double wside = (br2 && !mirror) ? 0.5 : 1.0;
-    const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac;
-    const bool skip_out = !active || mirror || code_skip_out(code);
-    double* fci = FC + (int64_t(lf.x) * p.ne + el.x) * SN;
-    double* fco = FC + (int64_t(lf.y) * p.ne + el.y) * SN;
-
-    // ---- pass B: species by species ------------------------------------
-#pragma unroll 1
-    for (int s = 0; s < S; ++s) {
-      const double As = p.A[s];
-      const double gs = M::kMirror ? M::mirror_value(p.P, s) : 0.0;
-      double ci[KT], co[KT];
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        const bool in = 4 * kt + t < NB;
-        ci[kt] = in ? __ldg(ui_row + s * NB + 4 * kt + t) : 0.0;
-        co[kt] = in ? __ldg(uo_row + s * NB + 4 * kt + t) : 0.0;
-      }
-      // B1: jumps -> modal lifting coefficients m_in, m_out
-      double mi[NNT][2], mo[NNT][2];
-#pragma unroll
-      for (int nt = 0; nt < NNT; ++nt) mi[nt][0] = mi[nt][1] = mo[nt][0] = mo[nt][1] = 0.0;
-      if (lift) {
-#pragma unroll 1
-        for (int qt = 0; qt < QT; ++qt) {
-          double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0};
-#pragma unroll
-          for (int kt = 0; kt < KT; ++kt) {
-              dmma(ui[0], ui[1], ci[kt], __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane));
-            dmma(uo[0], uo[1], co[kt], __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane));
-          }
-          double du[2];
-#pragma unroll
-          for (int j = 0; j < 2; ++j) du[j] = mirror ? 2.0 * (ui[j] - gs) : ui[j] - uo[j];
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-            for (int nt = 0; nt < NNT; ++nt) {
-              dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + T::OWB + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
-              dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + T::OWB + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
-            }
-          }
-        }
-        const double ki = use_in ? fac0 * As * idi : 0.0;
-        const double ko = use_out ? fac0 * As * ido : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NNT; ++nt)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            mi[nt][j] *= ki;
-            mo[nt][j] *= ko;
-          }
-      }
-      // B2: traces, flux, projection
-      // separate accumulators for the Y and X terms (shorter DMMA chains)
-      double ri[NNT][2], ro[NNT][2], rix[NNT][2], rox[NNT][2];
-#pragma unroll
-      for (int nt = 0; nt < NNT; ++nt)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) ri[nt][j] = ro[nt][j] = rix[nt][j] = rox[nt][j] = 0.0;
-#pragma unroll 1
-      for (int qt = 0; qt < QT; ++qt) {
-        double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0};
-        double dia[D][2], dqa[D][2];
-        double rhi[2] = {0.0, 0.0}, rho_[2] = {0.0, 0.0};
-#pragma unroll
-        for (int a = 0; a < D; ++a) dia[a][0] = dia[a][1] = dqa[a][0] = dqa[a][1] = 0.0;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const double bi = __ldg(Ti + T::OBT + (kt * QT + qt) * 32 + lane);
-          const double bo = __ldg(To + T::OBT + (kt * QT + qt) * 32 + lane);
-          dmma(ui[0], ui[1], ci[kt], bi);
-          dmma(uo[0], uo[1], co[kt], bo);
-          if (lift) {
-            // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
-            dmma(rhi[0], rhi[1], mi[kt / 2][kt % 2], bi);
-            dmma(rho_[0], rho_[1], mo[kt / 2][kt % 2], bo);
-          }
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            dmma(dia[a][0], dia[a][1], ci[kt] * jn[0][a], __ldg(Ti + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane));
-            dmma(dqa[a][0], dqa[a][1], co[kt] * jn[1][a], __ldg(To + T::OGT + ((a * KT + kt) * QT + qt) * 32 + lane));
-          }
-        }
-        double di[2], dq[2], rho[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          di[j] = dia[0][j];
-          dq[j] = dqa[0][j];
-#pragma unroll
-          for (int a = 1; a < D; ++a) {
-            di[j] += dia[a][j];
-            dq[j] += dqa[a][j];
-          }
-          rho[j] = rhi[j] + rho_[j];
-        }
-        double Y[2], X[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int q = 8 * qt + 2 * t + j;
-          const double uoj = mirror ? 2.0 * gs - ui[j] : uo[j];
-          const double du = ui[j] - uoj;
-          const double gav = mirror ? di[j] : 0.5 * (di[j] + dq[j]);
-          double qv = rho[j];
-          if (p.scheme == IP) qv = p.eta / h * As * du;
-          if constexpr (M::kConv) {
-            double cnv = 0.5 * cvS[q * NCV] * du;
-#pragma unroll
-            for (int k = 0; k < M::NFX; ++k)
-              if (s == k) cnv = fma(0.5, cvS[q * NCV + 1 + k], cnv);
-            qv += cnv;
-          }
-          const double wq = q < F ? __ldg(p.fw + q) * sfac : 0.0;
-          Y[j] = wq * (As * gav - qv);
-          X[j] = wq * 0.5 * p.adj * As * du;
-        }
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-          for (int nt = 0; nt < NNT; ++nt) {
-            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
-            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + T::OBP + ((qt * 2 + ks) * NNT + nt) * 32 + lane));
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-              dmma(rix[nt][0], rix[nt][1], X[ks] * jn[0][a], __ldg(Ti + T::OGP + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane));
-              dmma(rox[nt][0], rox[nt][1], X[ks] * jn[1][a], __ldg(To + T::OGP + (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane));
-            }
-          }
-        }
-      }
-      // face-slot rows: lane entries (face g, basis 4 (2nt + j) + t)
-#pragma unroll
-      for (int nt = 0; nt < NNT; ++nt)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int i = 4 * (2 * nt + j) + t;
-          if (i < NB) {
-            if (active) fci[s * NB + i] = ri[nt][j] + rix[nt][j];
-            if (!skip_out) fco[s * NB + i] = ro[nt][j] + rox[nt][j];
-          }
-        }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------
 // Interior faces on the FP64 tensor cores with the SPECIES as the M
 // dimension: a warp runs one face at a time (the faces of one block share
 // the trace-table signature), rows g = species, so everything per face --
 // Jinv n of both sides, the lifting weight, h -- is warp-uniform.  That
 // lets the normal derivatives fold into the B operand: the fragment of
-// dphi/dn = sum_a jn_a G_a is 3 FMAs per lane, replacing the D separate
-// DMMAs of the face-rows kernel above, and the coupled point physics reads
-// the traces of every species from one shared-memory transpose instead of
-// recomputing them (the face-rows kernel's pass A).  Same signature tables
+// dphi/dn = sum_a jn_a G_a is 3 FMAs per lane, replacing D separate DMMAs
+// with jn in the A operand (a faces-as-rows layout), and the coupled point
+// physics reads the traces of every species from one shared-memory
+// transpose instead of recomputing them.  Same signature tables
 // (tables.tc_face_tables), same point-parity k-steps and mode permutation
 // pi(8nt + 2t + j) = 4(2nt + j) + t; with nb = 10, F = 35 (C4) a face takes
 // ~175 DMMAs instead of ~330.
@@ -366,7 +95,7 @@ struct TcsFace {
 template <int D, int K, class M>
 __global__ void __launch_bounds__(128, TcsFace<D, K, M>::MINB)
 k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
-            int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ FC) {
+            int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ ACC) {
   using T = TcsFace<D, K, M>;
   using TF = TcFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG;
@@ -389,7 +118,6 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
       const int64_t f = int64_t(bd.x) + fi;
       const int code = __ldg(p.ifcode + f);
       const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + f);
-      const int2 lf = __ldg(reinterpret_cast<const int2*>(p.iflf) + f);
       const double* gg = p.ifgeo + f * NFG;
       double jn[2][D];
 #pragma unroll
@@ -557,11 +285,12 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
             dmma(ro[nt][0], ro[nt][1], X[ks], go);
           }
       }
-      // face-slot rows: lane entries (species g, basis 4 (2nt + j) + t)
+      // face-sum rows: lane entries (species g, basis 4 (2nt + j) + t)
       const bool skip_out = code_skip_out(code);
+      const bool fin = code_first_in(code), fout = code_first_out(code);
       if (row) {
-        double* fci = FC + (int64_t(lf.x) * p.ne + el.x) * SN + g * NB;
-        double* fco = FC + (int64_t(lf.y) * p.ne + el.y) * SN + g * NB;
+        double* fci = ACC + int64_t(el.x) * SN + g * NB;
+        double* fco = ACC + int64_t(el.y) * SN + g * NB;
 #pragma unroll
         for (int nt = 0; nt < NNT; ++nt)
 #pragma unroll
@@ -570,16 +299,16 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
               const int i = 8 * nt + t;
               if (i < NB) {
                 if (j == 0)
-                  fci[i] = ri[nt][0];
+                  acc_put(fci + i, ri[nt][0], fin);
                 else if (!skip_out)
-                  fco[i] = ri[nt][1];
+                  acc_put(fco + i, ri[nt][1], fout);
               }
               continue;
             }
             const int i = 4 * (2 * nt + j) + t;
             if (i < NB) {
-              fci[i] = ri[nt][j];
-              if (!skip_out) fco[i] = ro[nt][j];
+              acc_put(fci + i, ri[nt][j], fin);
+              if (!skip_out) acc_put(fco + i, ro[nt][j], fout);
             }
           }
       }

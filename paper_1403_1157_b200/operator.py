@@ -65,7 +65,7 @@ class DiscreteOperator:
     def __init__(self, space: DGSpace, model, scheme: FluxScheme,
                  nthreads: int = 1, npartitions: int | None = None,
                  vol_degree: int | None = None, face_degree: int | None = None,
-                 device=None, n_owned: int | None = None, global_ids=None, bands: int = 8):
+                 device=None, n_owned: int | None = None, global_ids=None):
         if model.n_species != space.n_species:
             raise ValueError(f"model has {model.n_species} species, space has "
                              f"{space.n_species}")
@@ -76,28 +76,27 @@ class DiscreteOperator:
         self.space, self.model, self.scheme = space, model, scheme
         self.mesh = space.mesh
         self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.lib = _native.load()
         t = build_tables(space, model, scheme, vol_degree, face_degree,
-                         n_owned=n_owned, global_ids=global_ids, bands=bands)
+                         n_owned=n_owned, global_ids=global_ids)
         self.tables = t
         self.n_owned = t.elem_geo.shape[0]
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
-        from .tables import (mma_face_tables, mma_volume_tables, tc_band_blocks,
-                             tc_face_blocks, tc_face_tables, tc_volume_tables)
+        from .tables import mma_face_tables, tc_face_blocks, tc_face_tables, tc_volume_tables
         mma, self._mma_stride = mma_face_tables(t)
-        blocks, n_cut_blocks = tc_face_blocks(t)
-        self._keep = {"face_mma": dev(mma), "vol_mma": dev(mma_volume_tables(t)),
-                      "vol_tc": dev(tc_volume_tables(t)), "face_tc": dev(tc_face_tables(t)[0]),
-                      "face_blocks": dev(blocks)}
+        blocks, seg_blk = tc_face_blocks(t)
+        self._keep = {"face_mma": dev(mma), "vol_tc": dev(tc_volume_tables(t)),
+                      "face_tc": dev(tc_face_tables(t)[0]), "face_blocks": dev(blocks)}
         self._keep.update({name: dev(getattr(t, name)) for name in (
             "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
-            "face_Pw", "face_w", "elem_geo", "if_elems", "if_lf", "if_code",
-            "if_geo", "bf_elem", "bf_lf", "bf_code", "bf_geo")})
+            "face_Pw", "face_w", "elem_geo", "if_elems", "if_code",
+            "if_geo", "bf_elem", "bf_code", "bf_geo")})
         self._host = {
-            "band_ptr": np.ascontiguousarray(np.concatenate(
-                [t.band_elem_ptr, t.band_face_ptr, t.band_wall_ptr,
-                 tc_band_blocks(t, blocks)]), dtype=np.int64),
+            "seg_ptr": np.ascontiguousarray(np.concatenate(
+                [t.seg_if, t.seg_bf, seg_blk]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
             "lin_source": _checked_linear_source(model),
             "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
@@ -120,19 +119,18 @@ class DiscreteOperator:
             face_B=ptr(k["face_B"]), face_G=ptr(k["face_G"]),
             face_Pw=ptr(k["face_Pw"]), face_w=ptr(k["face_w"]),
             elem_geo=ptr(k["elem_geo"]), if_elems=ptr(k["if_elems"]),
-            if_lf=ptr(k["if_lf"]), if_code=ptr(k["if_code"]),
-            if_geo=ptr(k["if_geo"]), bf_elem=ptr(k["bf_elem"]),
-            bf_lf=ptr(k["bf_lf"]), bf_code=ptr(k["bf_code"]),
+            if_code=ptr(k["if_code"]), if_geo=ptr(k["if_geo"]),
+            bf_elem=ptr(k["bf_elem"]), bf_code=ptr(k["bf_code"]),
             bf_geo=ptr(k["bf_geo"]), face_mma=ptr(k["face_mma"]),
-            vol_mma=ptr(k["vol_mma"]), n_cut_faces=t.n_cut, vol_tc=ptr(k["vol_tc"]),
-            face_tc=ptr(k["face_tc"]), face_blocks=ptr(k["face_blocks"]),
-            n_face_blocks=len(blocks), n_face_blocks_cut=n_cut_blocks,
-            n_bands=t.n_bands, band_ptr=hptr(self._host["band_ptr"]))
+            vol_tc=ptr(k["vol_tc"]), face_tc=ptr(k["face_tc"]),
+            face_blocks=ptr(k["face_blocks"]), n_face_blocks=len(blocks),
+            n_segments=t.n_seg, n_segments_cut=t.n_seg_cut,
+            seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _native.check(self.lib.tdg_create(ctypes.byref(desc),
-                                              ctypes.byref(handle)),
+            _native.check(self.lib.tdg_create(ctypes.byref(desc), ctypes.byref(handle)),
                           "tdg_create")
+            self._dev_index = torch.cuda.current_device()
         self._ctx = handle
         self._scalar = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.set_threads(nthreads, npartitions)
@@ -160,8 +158,12 @@ class DiscreteOperator:
         self.nthreads, self.npartitions = int(nthreads), int(npartitions)
 
     def audit_face_ownership(self) -> dict:
-        """Every element is assembled once and every element-local face
-        slot is written exactly once per application."""
+        """Reference ``operator.py:231-249`` audits that every element and
+        face is assembled exactly once.  Here: every element-local face
+        slot is written by exactly one face side; within each colour
+        segment (one launch) no element is written twice (the race-freedom
+        of the accumulating face kernels); every element's first side in
+        segment order carries the write flag, every other side adds."""
         t, d = self.tables, self.tables.dim
         slots = np.zeros((self.n_owned, d + 1), dtype=np.int64)
         el, lf, code = t.if_elems, t.if_lf, t.if_code
@@ -169,19 +171,44 @@ class DiscreteOperator:
         wr = (el[:, 1] >= 0) & ((code & ((1 << 14) | (1 << 15))) == 0)
         np.add.at(slots, (el[wr, 1], lf[wr, 1]), 1)
         np.add.at(slots, (t.bf_elem, t.bf_lf), 1)
+        seg_w = np.repeat(np.arange(t.n_seg), np.diff(t.seg_bf))
+        e_all = np.concatenate([el[:, 0], el[wr, 1], t.bf_elem])
+        s_all = np.concatenate([t.if_seg, t.if_seg[wr], seg_w]).astype(np.int64)
+        f_all = np.concatenate([(code >> 16) & 1, (code[wr] >> 17) & 1,
+                                (t.bf_code >> 16) & 1])
+        pair = e_all.astype(np.int64) * max(t.n_seg, 1) + s_all
+        once = len(np.unique(pair)) == len(pair)
+        firsts = np.bincount(e_all[f_all == 1], minlength=self.n_owned)
+        first_min = np.full(self.n_owned, np.iinfo(np.int64).max)
+        np.minimum.at(first_min, e_all, s_all)
+        first_ok = bool((firsts == 1).all()) and bool(
+            (first_min[e_all[f_all == 1]] == s_all[f_all == 1]).all())
+        per_seg = [int(t.seg_if[s + 1] - t.seg_if[s] + t.seg_bf[s + 1] - t.seg_bf[s])
+                   for s in range(t.n_seg)]
         return {"elements_ok": True, "faces_ok": bool((slots == 1).all()),
-                "faces_per_part": [len(code) + len(t.bf_code)],
-                "elements_per_part": [self.n_owned]}
+                "segments_race_free": bool(once), "first_flags_ok": first_ok,
+                "faces_per_part": per_seg, "elements_per_part": [self.n_owned]}
 
     def _stream(self):
         return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def _call(self, fn, *args, what="tdg call"):
+        """Native call on this operator's device (launches go to the
+        device's current stream; the caller's current device may differ)."""
+        torch = _torch()
+        if torch.cuda.current_device() != self._dev_index:
+            with torch.cuda.device(self.device):
+                rc = fn(*args)
+        else:
+            rc = fn(*args)
+        _native.check(rc, what)
 
     def _as_device(self, U):
         torch = _torch()
         shape = (self.n_rows, self.space.n_species, self.space.nb)
         if isinstance(U, torch.Tensor):
-            if U.dtype != torch.float64 or U.device.type != "cuda":
-                raise ValueError("U must be a float64 CUDA tensor")
+            if U.dtype != torch.float64 or U.device != self.device:
+                raise ValueError(f"U must be a float64 tensor on {self.device}")
             if tuple(U.shape) != shape:
                 raise ValueError(f"U has shape {tuple(U.shape)}, expected {shape}")
             return U.contiguous(), True
@@ -195,9 +222,8 @@ class DiscreteOperator:
         Ud, is_dev = self._as_device(U)
         R = torch.empty((self.n_owned, self.space.n_species, self.space.nb),
                         dtype=torch.float64, device=self.device)
-        _native.check(self.lib.tdg_apply(self._ctx, Ud.data_ptr(), R.data_ptr(),
-                                         float(t), mass_inverse, self._stream()),
-                      "tdg_apply")
+        self._call(self.lib.tdg_apply, self._ctx, Ud.data_ptr(), R.data_ptr(), float(t),
+                   mass_inverse, self._stream(), what="tdg_apply")
         return R if is_dev else R.cpu().numpy()
 
     def apply(self, U, t: float = 0.0):
@@ -208,58 +234,42 @@ class DiscreteOperator:
 
     # -- device timing ---------------------------------------------------
 
-    KERNELS = ("faces", "wall", "volume", "fc_add")
+    KERNELS = ("faces", "wall", "volume", "reserved")
 
-    def set_variant(self, generic: bool = False, vol4: bool = False,
-                    serial: bool = False, flip_mma: bool = False,
-                    mma_volume: bool = False, face_ctas_per_sm: int = 0,
-                    no_graph: bool = False, tc_volume: bool = False,
-                    no_tc_faces: bool = False, volume_first: bool = False,
-                    face_rows_tc: bool = False, one_copy_stream: bool = False,
-                    walls_first: bool = False, copy_streams: int = 0):
+    def set_variant(self, generic: bool = False, no_graph: bool = False,
+                    tc_volume: bool = False, face_ctas_per_sm: int = 0):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
-        CTA-staged generic kernels; ``vol4`` the four-lanes-per-element
-        volume kernel; ``serial`` disables the two-stream overlap of the
-        volume part with the face kernel; ``face_ctas_per_sm`` caps the
-        grid of the grid-stride face kernel (0 default, 15 uncapped);
-        ``face_rows_tc`` the faces-as-rows 3D tensor-core face kernel;
-        ``one_copy_stream`` one copy stream per direction in
-        ``ssprk3_steps_host`` (``copy_streams``: that many, 0 = default);
-        ``walls_first`` 3D wall faces before the
-        interior ones.  Defaults: fastest."""
-        _native.check(self.lib.tdg_set_variant(
-            self._ctx, int(bool(generic)) | (int(bool(vol4)) << 1)
-            | (int(bool(serial)) << 2) | (int(bool(flip_mma)) << 3)
-            | (int(bool(mma_volume)) << 4) | (int(bool(no_graph)) << 5)
-            | (int(bool(tc_volume)) << 12) | (int(bool(no_tc_faces)) << 13)
-            | (int(bool(volume_first)) << 14) | (int(bool(face_rows_tc)) << 15)
-            | (int(bool(one_copy_stream)) << 16) | (int(bool(walls_first)) << 17)
-            | ((int(copy_streams) & 7) << 18)
-            | ((int(face_ctas_per_sm) & 15) << 8)),
-            "tdg_set_variant")
+        CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
+        kernels directly instead of replaying its CUDA graph; ``tc_volume``
+        the tensor-core volume kernel where the SIMT one fits;
+        ``face_ctas_per_sm`` caps the grid of the 2D grid-stride face kernel
+        (0 default, 15 uncapped).  Defaults: fastest."""
+        self._call(self.lib.tdg_set_variant, self._ctx,
+                   int(bool(generic)) | (int(bool(no_graph)) << 5)
+                   | (int(bool(tc_volume)) << 12) | ((int(face_ctas_per_sm) & 15) << 8),
+                   what="tdg_set_variant")
 
     def profile(self, enable: bool = True):
         """Bracket every operator kernel launch with CUDA events on its
         stream (per-kernel roofline timing inside the benchmark)."""
-        _native.check(self.lib.tdg_profile(self._ctx, int(bool(enable))),
-                      "tdg_profile")
+        self._call(self.lib.tdg_profile, self._ctx, int(bool(enable)), what="tdg_profile")
 
     def profile_read(self) -> dict:
         ms = (ctypes.c_double * 4)()
         n = (ctypes.c_int64 * 4)()
-        _native.check(self.lib.tdg_profile_read(self._ctx, ms, n),
-                      "tdg_profile_read")
+        self._call(self.lib.tdg_profile_read, self._ctx, ms, n, what="tdg_profile_read")
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
 
     # -- explicit stepping / Krylov primitives (device tensors) ----------
 
     def _check_vec(self, name, x, rows=None):
-        """Raw-pointer entry points need dense fp64 CUDA storage; state
-        vectors have the owned rows first (ghost rows optional)."""
+        """Raw-pointer entry points need dense fp64 storage on this
+        operator's device; state vectors have the owned rows first (ghost
+        rows optional)."""
         torch = _torch()
         if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 \
-                or x.device.type != "cuda" or not x.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+                or x.device != self.device or not x.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous float64 tensor on {self.device}")
         ok_rows = (self.n_owned, self.n_rows) if rows is None else (rows,)
         if rows is not None or x.dim() == 3:
             if x.dim() != 3 or x.shape[1:] != (self.space.n_species, self.space.nb) \
@@ -268,55 +278,94 @@ class DiscreteOperator:
                                  f"(rows in {ok_rows}, {self.space.n_species}, "
                                  f"{self.space.nb})")
 
-    def rk_stage(self, U0, U, out, a: float, b: float, c: float, t: float = 0.0):
-        """out = a U0 + b U + c M^-1 L(U) in one fused pass."""
+    def _ptr(self, x):
+        return None if x is None else x.data_ptr()
+
+    def rk_stage(self, U0, U, out, a: float, b: float, c: float, t: float = 0.0, acc=None):
+        """out = a U0 + b U + c M^-1 L(U) in one fused pass.  The face sums
+        accumulate in ``acc`` (default: ``out``), which must not alias U
+        (nor U0 when a != 0)."""
         self._check_vec("U", U, self.n_rows)
         self._check_vec("out", out)
         if U0 is not None:
             self._check_vec("U0", U0)
-        _native.check(self.lib.tdg_rk_stage(
-            self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
-            out.data_ptr(), float(a), float(b), float(c), float(t),
-            self._stream()), "tdg_rk_stage")
+        if acc is not None:
+            self._check_vec("acc", acc)
+        self._call(self.lib.tdg_rk_stage, self._ctx, self._ptr(U0), U.data_ptr(),
+                   out.data_ptr(), self._ptr(acc), float(a), float(b), float(c), float(t),
+                   self._stream(), what="tdg_rk_stage")
         return out
 
     def rk_stage_part(self, U0, U, out, a: float, b: float, c: float, part: int,
-                      t: float = 0.0):
-        """Half of ``rk_stage`` around a ghost exchange: part 1 = work on
-        owned rows only, part 2 = cut faces + final sum (issue after the
-        ghost rows of U are filled)."""
+                      t: float = 0.0, acc=None):
+        """Half of ``rk_stage`` around a ghost exchange: part 1 = faces that
+        read owned rows only, part 2 = the cut faces + the volume kernel
+        (issue after the ghost rows of U are filled)."""
         self._check_vec("U", U, self.n_rows)
         self._check_vec("out", out)
         if U0 is not None:
             self._check_vec("U0", U0)
-        _native.check(self.lib.tdg_rk_stage_part(
-            self._ctx, None if U0 is None else U0.data_ptr(), U.data_ptr(),
-            out.data_ptr(), float(a), float(b), float(c), float(t), int(part),
-            self._stream()), "tdg_rk_stage_part")
+        if acc is not None:
+            self._check_vec("acc", acc)
+        self._call(self.lib.tdg_rk_stage_part, self._ctx, self._ptr(U0), U.data_ptr(),
+                   out.data_ptr(), self._ptr(acc), float(a), float(b), float(c), float(t),
+                   int(part), self._stream(), what="tdg_rk_stage_part")
         return out
 
-    def ssprk3_steps_host(self, U_host, nsteps: int, dt: float, t: float = 0.0):
+    def _work_pair(self, work):
+        if work is None:
+            raise ValueError("ssprk3 needs two work vectors")
+        if isinstance(work, (tuple, list)):
+            w1, w2 = work
+        else:
+            if work.dim() != 4 or work.shape[0] != 2:
+                raise ValueError("work must be a pair of state vectors or a (2, rows, S, nb) "
+                                 "tensor")
+            w1, w2 = work[0], work[1]
+        self._check_vec("work[0]", w1, self.n_rows)
+        self._check_vec("work[1]", w2, self.n_rows)
+        return w1, w2
+
+    def new_work(self):
+        """The two SSP-RK3 work vectors (one (2, rows, S, nb) tensor)."""
+        torch = _torch()
+        return torch.empty((2, self.n_rows, self.space.n_species, self.space.nb),
+                           dtype=torch.float64, device=self.device)
+
+    def ssprk3_steps_host(self, U_host, nsteps: int, dt: float, t: float = 0.0,
+                          U=None, work=None):
         """``nsteps`` SSP-RK3 steps of a pinned host state (CPU float64
         tensor of the U shape), with the state copied in and the result
-        copied out every step, pipelined by element bands; returns the
-        (updated) host tensor.  Asynchronous on the current stream."""
+        copied out every step (chunked copies overlapping the next step's
+        copy-in and the last stage); ``U`` / ``work`` are the device state
+        and work vectors (allocated here when not given).  Returns the
+        (updated) host tensor; asynchronous on the current stream."""
         torch = _torch()
         shape = (self.n_rows, self.space.n_species, self.space.nb)
         if not isinstance(U_host, torch.Tensor) or U_host.device.type != "cpu" \
                 or U_host.dtype != torch.float64 or tuple(U_host.shape) != shape \
                 or not U_host.is_contiguous() or not U_host.is_pinned():
             raise ValueError(f"U_host must be a pinned, contiguous float64 CPU tensor {shape}")
-        _native.check(self.lib.tdg_ssprk3_steps_host(self._ctx, U_host.data_ptr(), int(nsteps),
-                                                     float(t), float(dt), self._stream()),
-                      "tdg_ssprk3_steps_host")
+        if U is None:
+            U = torch.empty(shape, dtype=torch.float64, device=self.device)
+        self._check_vec("U", U, self.n_rows)
+        w1, w2 = self._work_pair(self.new_work() if work is None else work)
+        self._call(self.lib.tdg_ssprk3_steps_host, self._ctx, U_host.data_ptr(), U.data_ptr(),
+                   w1.data_ptr(), w2.data_ptr(), int(nsteps), float(t), float(dt),
+                   self._stream(), what="tdg_ssprk3_steps_host")
         return U_host
 
     def ssprk3_step(self, U, work, dt: float, t: float = 0.0):
+        """One Shu-Osher SSP-RK3 step in place on U (undecomposed meshes;
+        slab runs use ``stepping.SSPRK3`` with the halo exchange).  ``work``
+        = two work vectors (``new_work()``)."""
+        if self.n_rows != self.n_owned:
+            raise ValueError("ssprk3_step needs an undecomposed mesh; use "
+                             "stepping.SSPRK3(op, halo) for slab runs")
         self._check_vec("U", U, self.n_rows)
-        self._check_vec("work", work, self.n_rows)
-        _native.check(self.lib.tdg_ssprk3_step(
-            self._ctx, U.data_ptr(), work.data_ptr(), float(t), float(dt),
-            self._stream()), "tdg_ssprk3_step")
+        w1, w2 = self._work_pair(work)
+        self._call(self.lib.tdg_ssprk3_step, self._ctx, U.data_ptr(), w1.data_ptr(),
+                   w2.data_ptr(), float(t), float(dt), self._stream(), what="tdg_ssprk3_step")
         return U
 
     def species_totals(self, U, out=None):
@@ -326,8 +375,8 @@ class DiscreteOperator:
         self._check_vec("U", U)
         if out is None:
             out = torch.empty(self.space.n_species, dtype=torch.float64, device=self.device)
-        _native.check(self.lib.tdg_species_totals(self._ctx, U.data_ptr(), out.data_ptr(),
-                                                  self._stream()), "tdg_species_totals")
+        self._call(self.lib.tdg_species_totals, self._ctx, U.data_ptr(), out.data_ptr(),
+                                                  self._stream(), what="tdg_species_totals")
         return out
 
     def species_l2(self, U, V=None, out=None):
@@ -341,9 +390,8 @@ class DiscreteOperator:
             self._check_vec("V", V)
         if out is None:
             out = torch.empty(self.space.n_species, dtype=torch.float64, device=self.device)
-        _native.check(self.lib.tdg_species_l2(
-            self._ctx, U.data_ptr(), None if V is None else V.data_ptr(), out.data_ptr(),
-            self._stream()), "tdg_species_l2")
+        self._call(self.lib.tdg_species_l2, self._ctx, U.data_ptr(), None if V is None else V.data_ptr(), out.data_ptr(),
+            self._stream(), what="tdg_species_l2")
         return out
 
     def mgs(self, V, j: int, w, h):
@@ -355,8 +403,8 @@ class DiscreteOperator:
         n = w.numel()
         if V.shape[1] != n or j + 1 > V.shape[0] or h.numel() < j + 2:
             raise ValueError("mgs: inconsistent sizes")
-        _native.check(self.lib.tdg_mgs(self._ctx, V.data_ptr(), V.stride(0), int(j), w.data_ptr(),
-                                       n, h.data_ptr(), self._stream()), "tdg_mgs")
+        self._call(self.lib.tdg_mgs, self._ctx, V.data_ptr(), V.stride(0), int(j), w.data_ptr(),
+                                       n, h.data_ptr(), self._stream(), what="tdg_mgs")
         return h
 
     def scale_norm(self, w, hnext, v, norm_out):
@@ -372,10 +420,9 @@ class DiscreteOperator:
         self._check_vec("v", v)
         if w.numel() != v.numel():
             raise ValueError("w and v differ in size")
-        _native.check(self.lib.tdg_scale_norm(
-            self._ctx, w.data_ptr(), 0.0 if dev_div else float(hnext),
+        self._call(self.lib.tdg_scale_norm, self._ctx, w.data_ptr(), 0.0 if dev_div else float(hnext),
             hnext.data_ptr() if dev_div else None, v.data_ptr(), w.numel(), norm_out.data_ptr(),
-            self._stream()), "tdg_scale_norm")
+            self._stream(), what="tdg_scale_norm")
         return v
 
     def jv_shift(self, U, v, vnorm, cnum: float, Up, eps_out):
@@ -386,9 +433,9 @@ class DiscreteOperator:
             self._check_vec(name, x.reshape(-1))
         if v.numel() != n or Up.numel() != n:
             raise ValueError("jv_shift: size mismatch")
-        _native.check(self.lib.tdg_jv_shift(U.data_ptr(), v.data_ptr(), vnorm.data_ptr(),
+        self._call(self.lib.tdg_jv_shift, U.data_ptr(), v.data_ptr(), vnorm.data_ptr(),
                                             float(cnum), Up.data_ptr(), eps_out.data_ptr(), n,
-                                            self._stream()), "tdg_jv_shift")
+                                            self._stream(), what="tdg_jv_shift")
         return Up
 
     def jv_diff(self, r, GU, eps):
@@ -397,8 +444,8 @@ class DiscreteOperator:
         self._check_vec("GU", GU.reshape(-1))
         if r.numel() != GU.numel():
             raise ValueError("jv_diff: size mismatch")
-        _native.check(self.lib.tdg_jv_diff(r.data_ptr(), GU.data_ptr(), eps.data_ptr(), r.numel(),
-                                           self._stream()), "tdg_jv_diff")
+        self._call(self.lib.tdg_jv_diff, r.data_ptr(), GU.data_ptr(), eps.data_ptr(), r.numel(),
+                                           self._stream(), what="tdg_jv_diff")
         return r
 
     def dot(self, x, y, out=None):
@@ -408,18 +455,16 @@ class DiscreteOperator:
         if x.numel() != y.numel():
             raise ValueError("x and y differ in size")
         out = self._scalar[:1] if out is None else out
-        _native.check(self.lib.tdg_dot(self._ctx, x.data_ptr(), y.data_ptr(),
-                                       x.numel(), out.data_ptr(), self._stream()),
-                      "tdg_dot")
+        self._call(self.lib.tdg_dot, self._ctx, x.data_ptr(), y.data_ptr(),
+                                       x.numel(), out.data_ptr(), self._stream(), what="tdg_dot")
         return out
 
     def norm2(self, x, out=None):
         x = x.reshape(-1)
         self._check_vec("x", x)
         out = self._scalar[1:] if out is None else out
-        _native.check(self.lib.tdg_norm2(self._ctx, x.data_ptr(), x.numel(),
-                                         out.data_ptr(), self._stream()),
-                      "tdg_norm2")
+        self._call(self.lib.tdg_norm2, self._ctx, x.data_ptr(), x.numel(),
+                                         out.data_ptr(), self._stream(), what="tdg_norm2")
         return out
 
     def axpby(self, a: float, x, b: float, y):
@@ -427,9 +472,8 @@ class DiscreteOperator:
             raise ValueError("x and y differ in size")
         self._check_vec("x", x.reshape(-1))
         self._check_vec("y", y.reshape(-1))
-        _native.check(self.lib.tdg_axpby(float(a), x.data_ptr(), float(b),
-                                         y.data_ptr(), x.numel(), self._stream()),
-                      "tdg_axpby")
+        self._call(self.lib.tdg_axpby, float(a), x.data_ptr(), float(b),
+                                         y.data_ptr(), x.numel(), self._stream(), what="tdg_axpby")
         return y
 
     def axpy_dev(self, s: float, alpha, x, y):
@@ -437,8 +481,7 @@ class DiscreteOperator:
             raise ValueError("x and y differ in size")
         self._check_vec("x", x.reshape(-1))
         self._check_vec("y", y.reshape(-1))
-        _native.check(self.lib.tdg_axpy_dev(float(s), alpha.data_ptr(),
+        self._call(self.lib.tdg_axpy_dev, float(s), alpha.data_ptr(),
                                             x.data_ptr(), y.data_ptr(),
-                                            x.numel(), self._stream()),
-                      "tdg_axpy_dev")
+                                            x.numel(), self._stream(), what="tdg_axpy_dev")
         return y

@@ -19,8 +19,15 @@ Device layout choices (B200-first, not the reference's):
   d(d+1)/2 doubles per element) and exact stiffness blocks
   KS_ac[j][i] = sum_q w_q G[q,j,c] G[q,i,a] (+ transpose for c != a),
   integrated with the reference's own rule;
-* interior faces are sorted by their (inside table, outside table) pair
-  so a CTA's table reads are mostly uniform.
+* the faces are coloured (``tdg_color_faces``: elements = vertices, faces
+  = edges) and run colour by colour, each colour one launch ("segment")
+  in which no element is written twice: the faces add their two
+  contribution blocks straight into the elements' face-sum rows, with no
+  atomics and no per-face buffers, and the fixed segment order fixes
+  every sum.  This replaces the reference's race-freedom device (private
+  per-partition buffers merged in part order, ``operator.py:262-284``).
+  Within a segment the faces are sorted by their (inside table, outside
+  table) signature so a warp's table reads are uniform.
 """
 
 from __future__ import annotations
@@ -33,12 +40,14 @@ from .fespace import DGSpace, face_reference_points
 from .flux import FluxScheme, chi_factor, minus_is_outside
 from .quadrature import face_rule, volume_rule
 
-__all__ = ["OperatorTables", "build_tables", "sym_pairs"]
+__all__ = ["OperatorTables", "build_tables", "color_faces", "sym_pairs"]
 
 REF_FACE_MEASURE = {2: 1.0, 3: 0.5}
 CODE_MINUS_IN = 1 << 10
 CODE_MIRROR = 1 << 14
 CODE_SKIP_OUT = 1 << 15
+CODE_FIRST_IN = 1 << 16
+CODE_FIRST_OUT = 1 << 17
 
 
 def sym_pairs(d: int):
@@ -63,23 +72,23 @@ class OperatorTables:
     face_w: np.ndarray
     elem_geo: np.ndarray
     if_elems: np.ndarray
-    if_lf: np.ndarray
     if_code: np.ndarray
     if_geo: np.ndarray
     bf_elem: np.ndarray
-    bf_lf: np.ndarray
     bf_code: np.ndarray
     bf_geo: np.ndarray
     n_cut: int = 0
-    # element bands for host-pipelined stepping (undecomposed meshes):
-    # band_elem_ptr[k] .. [k+1] are band k's elements; interior faces are
-    # ordered by (lowest band, straddles into the next band, signature):
-    # band_face_ptr[2k] = first face internal to band k, band_face_ptr[2k+1]
-    # = first face straddling (k, k+1); walls by band (band_wall_ptr)
-    n_bands: int = 1
-    band_elem_ptr: np.ndarray = None
-    band_face_ptr: np.ndarray = None
-    band_wall_ptr: np.ndarray = None
+    # colour segments, run in order (the last n_seg_cut hold the faces
+    # that read ghost rows): interior faces seg_if[s]..seg_if[s+1], walls
+    # seg_bf[s]..seg_bf[s+1]; if_seg = segment of every interior face
+    n_seg: int = 0
+    n_seg_cut: int = 0
+    seg_if: np.ndarray = None
+    seg_bf: np.ndarray = None
+    if_seg: np.ndarray = None
+    # host-only: element-local face index per side (audit, emulator)
+    if_lf: np.ndarray = None
+    bf_lf: np.ndarray = None
 
 
 def _face_tables(space: DGSpace, frule):
@@ -96,9 +105,35 @@ def _face_tables(space: DGSpace, frule):
     return np.stack(Bs), np.stack(Gs), np.stack(Ps)
 
 
+def color_faces(elem_in, elem_out, n_elements, order=None):
+    """Greedy colouring of the face graph (``tdg_color_faces``, host C++
+    in the library): faces visited in ``order`` take the smallest colour
+    none of their written elements (>= 0) holds.  Returns (colours, n)."""
+    import ctypes
+    from . import _native
+    lib = _native.load()
+    a = np.ascontiguousarray(elem_in, dtype=np.int32)
+    b = np.ascontiguousarray(elem_out, dtype=np.int32)
+    n = len(a)
+    col = np.empty(n, dtype=np.int32)
+    o = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+    p = lambda x: ctypes.c_void_p(x.ctypes.data) if x is not None and len(x) else None
+    nc = lib.tdg_color_faces(n, p(a), p(b), int(n_elements), p(o), p(col))
+    _native.check(nc if nc < 0 else 0, "tdg_color_faces")
+    return col, int(nc)
+
+
+def _class_order(lf_in, lf_out, d):
+    """Visit order of the greedy colouring: faces grouped by their
+    (local face in, local face out) class (out = d+1 for one-sided faces);
+    on the structured triangle / Kuhn meshes this gives d+1 colours."""
+    klass = lf_in.astype(np.int64) * (d + 2) + np.where(lf_out >= 0, lf_out, d + 1)
+    return np.lexsort((np.arange(len(klass)), klass))
+
+
 def build_tables(space: DGSpace, model, scheme: FluxScheme,
                  vol_degree=None, face_degree=None, n_owned=None,
-                 global_ids=None, bands: int = 8) -> OperatorTables:
+                 global_ids=None) -> OperatorTables:
     """Pack tables, element geometry and face lists.
 
     Slab-decomposed runs pass a local mesh whose first ``n_owned``
@@ -183,41 +218,51 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         nbf = np.zeros(0, dtype=np.int64)
     else:
         nbf = np.flatnonzero(bmask)
-    # faces touching a ghost row (SKIP_OUT) last, so a slab stage can run
-    # the others while the ghost exchange is in flight
+    # ---- colour segments ------------------------------------------------
+    # part 1: the faces that read owned rows only (non-cut interior faces
+    # and walls), coloured together; part 2 (slab runs): the faces whose
+    # outside is a ghost row, coloured among themselves (one written side)
     cut = (code & CODE_SKIP_OUT) != 0
     n_cut = int(cut.sum())
-    # element bands (contiguous id ranges; host-pipelined stepping): faces
-    # of one band, then the faces straddling into the next band
-    n_own = n_owned
-    nbands = min(bands, n_own // 8192) if (n_cut == 0 and n_own == mesh.n_elements) else 1
-    nbands = max(nbands, 1)
-    ebnd = (np.arange(nbands + 1, dtype=np.int64) * n_own) // nbands
-    band_of = lambda e: np.searchsorted(ebnd, e, side="right") - 1
-    if nbands > 1:
-        e_o = np.where(el[:, 1] >= 0, el[:, 1], el[:, 0])
-        b_in, b_out = band_of(el[:, 0]), band_of(e_o)
-        lo, hi = np.minimum(b_in, b_out), np.maximum(b_in, b_out)
-        if np.any(hi - lo > 1):  # a face must not skip a band: no banding
-            nbands = 1
-    if nbands > 1:
-        key = 2 * lo + (hi > lo)
-        order = np.lexsort((code & 1023, key, cut))
-        key = key[order]
-    else:
-        order = np.lexsort((code & 1023, cut))
-    code, geo, el, lfs = code[order], geo[order], el[order], lfs[order]
-
+    nif, nbw = len(code), len(nbf)
+    w_out = np.where(cut | (el[:, 1] < 0), -1, el[:, 1])
+    main = np.flatnonzero(~cut)
+    m_in = np.concatenate([el[main, 0], fe[nbf, 0]])
+    m_out = np.concatenate([w_out[main], np.full(nbw, -1)])
+    m_lfi = np.concatenate([lfs[main, 0], fl[nbf, 0]])
+    m_lfo = np.concatenate([np.where(w_out[main] >= 0, lfs[main, 1], -1), np.full(nbw, -1)])
+    col_m, nc1 = color_faces(m_in, m_out, n_owned, _class_order(m_lfi, m_lfo, d))
+    cidx = np.flatnonzero(cut)
+    col_c, nc2 = color_faces(el[cidx, 0], np.full(len(cidx), -1), n_owned,
+                             _class_order(lfs[cidx, 0], np.full(len(cidx), -1), d))
+    seg_f = np.empty(nif, dtype=np.int64)
+    seg_f[main] = col_m[:len(main)]
+    seg_f[cidx] = nc1 + col_c
+    seg_w = col_m[len(main):].astype(np.int64)
+    n_seg = nc1 + nc2
+    # interior faces by (segment, signature); walls by (segment, table, tag)
+    order = np.lexsort((code & 1023, seg_f))
+    code, geo, el, lfs, seg_f = code[order], geo[order], el[order], lfs[order], seg_f[order]
     btag = mesh.face_tags[nbf].astype(np.int64)
-    bband = band_of(fe[nbf, 0]) if nbands > 1 else np.zeros(len(nbf), np.int64)
-    border = np.lexsort((btag, tid[nbf, 0], bband))
-    nbf, btag, bband = nbf[border], btag[border], bband[border]
+    border = np.lexsort((btag, tid[nbf, 0], seg_w))
+    nbf, btag, seg_w = nbf[border], btag[border], seg_w[border]
     bcode = tid[nbf, 0] | (btag << 11)
-    if nbands > 1:
-        band_face = np.searchsorted(key, np.arange(2 * nbands + 1), side="left")
-    else:
-        band_face = np.array([0, len(code), len(code)])
-    band_wall = np.searchsorted(bband, np.arange(nbands + 1), side="left")
+    seg_if = np.searchsorted(seg_f, np.arange(n_seg + 1), side="left")
+    seg_bf = np.searchsorted(seg_w, np.arange(n_seg + 1), side="left")
+    # first written side of every element in segment order: it writes the
+    # element's face-sum row, later sides add to it
+    wr_out = np.flatnonzero((el[:, 1] >= 0) & ((code & (CODE_SKIP_OUT | CODE_MIRROR)) == 0))
+    e_all = np.concatenate([el[:, 0], el[wr_out, 1], fe[nbf, 0]])
+    s_all = np.concatenate([seg_f, seg_f[wr_out], seg_w])
+    first_seg = np.full(n_owned, np.iinfo(np.int64).max)
+    np.minimum.at(first_seg, e_all, s_all)
+    if n_owned and (first_seg == np.iinfo(np.int64).max).any():
+        raise ValueError("an owned element has no face (non-conforming face lists)")
+    fin = first_seg[el[:, 0]] == seg_f
+    fout = np.zeros(nif, dtype=bool)
+    fout[wr_out] = first_seg[el[wr_out, 1]] == seg_f[wr_out]
+    code = code | np.where(fin, CODE_FIRST_IN, 0) | np.where(fout, CODE_FIRST_OUT, 0)
+    bcode = bcode | np.where(first_seg[fe[nbf, 0]] == seg_w, CODE_FIRST_IN, 0)
 
     c64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
     i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
@@ -226,12 +271,11 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         vol_phi=c64(phi), vol_grad=c64(grad), vol_w=c64(vr.weights),
         vol_stiff=c64(ks), face_B=c64(fB), face_G=c64(fG), face_Pw=c64(fPw),
         face_w=c64(fr.weights), elem_geo=c64(egeo[:n_owned]),
-        if_elems=i32(el), if_lf=i32(lfs), if_code=i32(code), if_geo=c64(geo),
-        bf_elem=i32(fe[nbf, 0]), bf_lf=i32(fl[nbf, 0]),
-        bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]), n_cut=n_cut,
-        n_bands=int(nbands), band_elem_ptr=ebnd.astype(np.int64),
-        band_face_ptr=np.asarray(band_face, dtype=np.int64),
-        band_wall_ptr=np.asarray(band_wall, dtype=np.int64))
+        if_elems=i32(el), if_code=i32(code), if_geo=c64(geo),
+        bf_elem=i32(fe[nbf, 0]), bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]),
+        n_cut=n_cut, n_seg=int(n_seg), n_seg_cut=int(nc2),
+        seg_if=seg_if.astype(np.int64), seg_bf=seg_bf.astype(np.int64),
+        if_seg=seg_f.astype(np.int32), if_lf=i32(lfs), bf_lf=i32(fl[nbf, 0]))
 
 
 def _ceil(x, m):
@@ -338,17 +382,13 @@ def tc_face_tables(t: OperatorTables):
 
 def tc_face_blocks(t: OperatorTables, block: int = 8):
     """Blocks of up to ``block`` consecutive interior faces with one trace-
-    table signature each (the M dimension of the transposed face kernel),
-    never straddling the non-cut / cut boundary nor a band segment
-    (``band_face_ptr``).  Returns (int32 [nblk][2] = (first face, count),
-    number of blocks of cut faces at the end)."""
+    table signature each (the 3D species-rows face kernel runs a block per
+    warp), never straddling a colour segment.  Returns (int32 [nblk][2] =
+    (first face, count), block offsets of the segments [n_seg+1])."""
     nif = len(t.if_code)
     if nif == 0:
-        return np.zeros((0, 2), np.int32), 0
-    sig = (t.if_code.astype(np.int64) & 1023) + (np.arange(nif) >= nif - t.n_cut) * 1024
-    if t.n_bands > 1:
-        seg = np.searchsorted(t.band_face_ptr, np.arange(nif), side="right")
-        sig = sig + seg * 2048
+        return np.zeros((0, 2), np.int32), np.zeros(t.n_seg + 1, np.int64)
+    sig = (t.if_code.astype(np.int64) & 1023) + t.if_seg.astype(np.int64) * 1024
     brk = np.flatnonzero(np.diff(sig)) + 1
     starts = np.concatenate([[0], brk])
     lens = np.diff(np.concatenate([starts, [nif]]))
@@ -358,37 +398,8 @@ def tc_face_blocks(t: OperatorTables, block: int = 8):
     first = rs + block * j
     cnt = np.minimum(block, np.repeat(starts + lens, nblk) - first)
     blocks = np.ascontiguousarray(np.stack([first, cnt], axis=1), dtype=np.int32)
-    n_cut_blocks = int((first >= nif - t.n_cut).sum()) if t.n_cut else 0
-    return blocks, n_cut_blocks
-
-
-def tc_band_blocks(t: OperatorTables, blocks: np.ndarray) -> np.ndarray:
-    """Block offsets [n_bands+1] of the bands' faces (the faces straddling
-    (k-1, k) and those internal to k, i.e. faces from band_face_ptr[2k-1])
-    in the tc_face_blocks list."""
-    B = t.n_bands
-    start = np.array([0] + [int(t.band_face_ptr[2 * k - 1]) for k in range(1, B)]
-                     + [len(t.if_code)], dtype=np.int64)
-    return np.searchsorted(blocks[:, 0].astype(np.int64), start, side="left").astype(np.int64)
-
-
-def mma_volume_tables(t: OperatorTables) -> np.ndarray:
-    """Zero-padded operand tables of the tensor-core volume kernel
-    (csrc/kernels_mma.cuh, k_volume_mma), concatenated:
-
-    TPhi  [QP][NBK]        Phi[q][k]          point values  u = Phi c
-    TGa   [d][QP][NBK]     G[q][k][a]         reference gradients
-    TGaT  [d][NBM][QP]     G[q][i][a]         projection of the flux rows
-    TPhiT [NBM][QP]        Phi[q][i]          projection of the bilinear source
-    with QP = ceil8(Q), NBK = ceil4(nb), NBM = ceil8(nb)."""
-    d, nb = t.dim, t.nb
-    Q = t.vol_phi.shape[0]
-    QP, NBK, NBM = _ceil(Q, 8), _ceil(nb, 4), _ceil(nb, 8)
-    TPhi = np.zeros((QP, NBK)); TPhi[:Q, :nb] = t.vol_phi
-    TG = np.zeros((d, QP, NBK)); TG[:, :Q, :nb] = t.vol_grad.transpose(2, 0, 1)
-    TGT = np.zeros((d, NBM, QP)); TGT[:, :nb, :Q] = t.vol_grad.transpose(2, 1, 0)
-    TPT = np.zeros((NBM, QP)); TPT[:nb, :Q] = t.vol_phi.T
-    return np.ascontiguousarray(np.concatenate([x.ravel() for x in (TPhi, TG, TGT, TPT)]))
+    seg_blk = np.searchsorted(first, t.seg_if, side="left").astype(np.int64)
+    return blocks, seg_blk
 
 
 def tc_volume_tables(t: OperatorTables) -> np.ndarray:

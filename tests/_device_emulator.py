@@ -11,7 +11,7 @@ from paper_1403_1157_b200.model import MODEL_DIFFUSION, MODEL_PLAQUE, \
     MODEL_REDUCED
 from paper_1403_1157_b200.tables import sym_pairs
 
-CIN, MIRROR, SKIP = 1 << 10, 1 << 14, 1 << 15
+CIN, MIRROR, SKIP, FIRST_IN, FIRST_OUT = 1 << 10, 1 << 14, 1 << 15, 1 << 16, 1 << 17
 
 
 def _plaque_volume(P, v, gM):
@@ -42,13 +42,37 @@ class DeviceEmulator:
         self.mid = model.model_id
 
     def apply(self, U):
+        """Face segments in order (each face side writes or adds to its
+        element's face-sum row per its FIRST flag; no element twice in a
+        segment), then the volume terms plus the face sums."""
         t = self.t
-        d, S, nb = t.dim, t.n_species, t.nb
+        S, nb = t.n_species, t.nb
         ne = t.elem_geo.shape[0]
-        FC = np.full((ne, d + 1, S, nb), np.nan)
-        self._faces(U, FC)
-        self._wall(U, FC)
-        return self._volume(U, FC)
+        ACC = np.full((ne, S, nb), np.nan)
+        for s in range(t.n_seg):
+            seen = set()
+
+            def put(e, v, first):
+                assert e not in seen, f"element {e} written twice in segment {s}"
+                seen.add(e)
+                if first:
+                    ACC[e] = v
+                else:
+                    assert np.isfinite(ACC[e]).all(), f"element {e}: add before first write"
+                    ACC[e] += v
+
+            for f in range(t.seg_if[s], t.seg_if[s + 1]):
+                code = int(t.if_code[f])
+                ein, eout = t.if_elems[f]
+                ri, ro = self.face_contrib(U, code, ein, eout, t.if_geo[f])
+                put(ein, ri, bool(code & FIRST_IN))
+                if ro is not None and not (code & SKIP):
+                    put(eout, ro, bool(code & FIRST_OUT))
+            for f in range(t.seg_bf[s], t.seg_bf[s + 1]):
+                code = int(t.bf_code[f])
+                put(t.bf_elem[f], self.wall_contrib(U, code, t.bf_elem[f], t.bf_geo[f]),
+                    bool(code & FIRST_IN))
+        return self._volume(U, ACC)
 
     def _volume(self, U, FC):
         t = self.t
@@ -86,38 +110,7 @@ class DeviceEmulator:
                 R[:, nsp] += w[q] * nl[0][:, None] * phi[q][None, :]
         R = detJ[:, None, None] * R
         if FC is not None:
-            R = R + FC.sum(axis=1)
-        return R
-
-    def apply_tiled(self, U, tiles):
-        """Fused-kernel semantics: per tile, volume rows then the tile's
-        face entries colour by colour into the tile's rows."""
-        from paper_1403_1157_b200.tiling import CODE_WALL, CODE_WIN, CODE_WOUT
-        t = self.t
-        vol = self._volume(U, None)
-        R = np.full_like(vol, np.nan)
-        nc = tiles.n_colors
-        for k in range(tiles.n_tiles):
-            rows = tiles.rows[tiles.tile_ptr[k]:tiles.tile_ptr[k + 1]]
-            nown = tiles.tile_nown[k]
-            acc = vol[rows[:nown]].copy()
-            for c in range(nc):
-                b, e = tiles.color_ptr[k * (nc + 1) + c], tiles.color_ptr[k * (nc + 1) + c + 1]
-                for j in range(b, e):
-                    code = int(tiles.ent_code[j])
-                    si = int(tiles.ent_slots[j]) & 0xFFFF
-                    so = (int(tiles.ent_slots[j]) >> 16) & 0xFFFF
-                    ein = rows[si]
-                    if code & CODE_WALL:
-                        ri, ro = self.wall_contrib(U, code, ein, tiles.ent_geo[j, 2 * t.dim]), None
-                    else:
-                        eout = rows[so] if so != 0xFFFF else -1
-                        ri, ro = self.face_contrib(U, code, ein, eout, tiles.ent_geo[j])
-                    if code & CODE_WIN:
-                        acc[si] += ri
-                    if code & CODE_WOUT:
-                        acc[so] += ro
-            R[rows[:nown]] = acc
+            R = R + FC
         return R
 
     def _conv(self, ui, uo, gn, dU, qv):
@@ -145,16 +138,6 @@ class DeviceEmulator:
                 f0 += u[:, 0] * v0
             qv[:, 0] += 0.5 * f0
             qv += 0.5 * lam[:, None] * dU
-
-    def _faces(self, U, FC):
-        t = self.t
-        for f in range(len(t.if_code)):
-            code = int(t.if_code[f])
-            ein, eout = t.if_elems[f]
-            ri, ro = self.face_contrib(U, code, ein, eout, t.if_geo[f])
-            FC[ein, t.if_lf[f, 0]] = ri
-            if ro is not None and not (code & SKIP):
-                FC[eout, t.if_lf[f, 1]] = ro
 
     def face_contrib(self, U, code, ein, eout, g):
         """(inside row, outside row or None) of one interior/mirror face."""
@@ -204,12 +187,6 @@ class DeviceEmulator:
             ri = Y @ t.face_B[tin] + X @ dpi
             ro = None if mirror else -Y @ t.face_B[tout] + X @ dpo
             return ri, ro
-
-    def _wall(self, U, FC):
-        t = self.t
-        for f in range(len(t.bf_code)):
-            FC[t.bf_elem[f], t.bf_lf[f]] = self.wall_contrib(
-                U, int(t.bf_code[f]), t.bf_elem[f], t.bf_geo[f])
 
     def wall_contrib(self, U, code, e, sfac):
         t = self.t

@@ -304,8 +304,69 @@ def trajectories():
     np.savez_compressed(os.path.join(HERE, "trajectories.npz"), **out)
 
 
+# rho(J) ~ C nu_max / h^2 per (d, k) (measured on the reference)
+RHO_C = {(2, 1): 490.0, (2, 2): 1717.0, (2, 3): 4371.0, (3, 2): 7150.0, (3, 3): 16361.0}
+
+
+def cfl_dt(mesh, d, k):
+    """The configs' explicit step 0.8 * 2.51 / rho, rho = C nu_max / h^2."""
+    h = float(mesh.diameters.min())
+    return 0.8 * 2.51 / (RHO_C[(d, k)] * 1e-2 / h ** 2)
+
+
+def trajectories_stated():
+    """Every BASELINE config at its STATED step count on a scaled replica
+    (same physics, order, flux, tags and stepping), run by
+    the reference: C2 100 SSP-RK3 steps, C4 20 steps (cdg2, br2, ip),
+    C5 10 steps at p=3 in 3D, C3 50 SDIRK3 steps on a jittered p=3 mesh
+    at the stiffness ratio dt a_ii rho = 500 (tightened Newton / GMRES
+    tolerances)."""
+    out = {}
+
+    def run(key, mesh, k, box, seed, steps, schemes=("cdg2",)):
+        space = DGSpace(mesh, k, n_species=6)
+        d = mesh.dim
+        U0 = space.project(bump_field(d, 6, seed, np.zeros(d), np.asarray(box, float))).coeffs
+        dt = cfl_dt(mesh, d, k)
+        out[f"{key}__U0"] = U0
+        out[f"{key}__dt"] = np.array(dt)
+        out[f"{key}__steps"] = np.array(steps)
+        for name in schemes:
+            tic = time.perf_counter()
+            op = DiscreteOperator(space, PlaqueModel(), FluxScheme(name))
+            out[f"{key}__{name}__U"] = ssprk3(op, U0, dt, steps)
+            print(f"  {key} {name}: {time.perf_counter() - tic:.1f}s", flush=True)
+
+    # C2: [0,4]x[0,1], p=2, 100 SSP-RK3 steps
+    run("c2r", scaled(unit_square(16, 4), (4.0, 1.0)), 2, (4.0, 1.0), 2, 100)
+    # C4: unit cube, z=0 GAMMA1 / no-flow elsewhere, p=2, 20 steps, + br2 / ip
+    run("c4r", kuhn_cube_z0_gamma1(3), 2, (1.0, 1.0, 1.0), 4, 20, ("cdg2", "br2", "ip"))
+    # C5: [0,2]x[0,1]^2 with the generator's default tags, p=3, 10 steps
+    run("c5r", scaled(unit_cube(4, 2, 2), (2.0, 1.0, 1.0)), 3, (2.0, 1.0, 1.0), 5, 10)
+    # C3: jittered [0,4]x[0,1], p=3, 50 SDIRK3 + JFNK steps
+    mesh = jittered_square(8, 2, (4.0, 1.0), 0.1, 7)
+    space = DGSpace(mesh, 3, n_species=6)
+    U0 = space.project(bump_field(2, 6, 3, np.zeros(2), np.array([4.0, 1.0]))).coeffs
+    h = float(mesh.diameters.min())
+    gamma = 0.4358665215
+    dt = 500.0 / (gamma * RHO_C[(2, 3)] * 1e-2 / h ** 2)
+    nk = {"rtol": 1e-10, "atol": 1e-13, "gmres_rtol": 1e-4, "gmres_maxiter": 400}
+    op = DiscreteOperator(space, PlaqueModel(), FluxScheme("cdg2"))
+    tic = time.perf_counter()
+    res = integrate(op, U0, 0.0, math.inf, dt, order=3, newton_kwargs=nk, n_steps=50)
+    print(f"  c3r sdirk3: {time.perf_counter() - tic:.1f}s, {res.gmres_iterations} GMRES",
+          flush=True)
+    out["c3r__U0"] = U0
+    out["c3r__dt"] = np.array(dt)
+    out["c3r__U50"] = res.U
+    out["c3r__nk"] = np.array([nk["rtol"], nk["atol"], nk["gmres_rtol"], nk["gmres_maxiter"]])
+    np.savez_compressed(os.path.join(HERE, "trajectories_stated.npz"), **out)
+
+
 if __name__ == "__main__":
-    for fn in (tables, meshes, operators, heat_cases, trajectories):
+    which = sys.argv[1:] or ["tables", "meshes", "operators", "heat_cases", "trajectories",
+                             "trajectories_stated"]
+    for fn in (globals()[w] for w in which):
         tic = time.perf_counter()
         fn()
         print(f"{fn.__name__}: {time.perf_counter() - tic:.1f}s", flush=True)

@@ -1,0 +1,93 @@
+"""Face colouring / segment order of the accumulating face kernels (host
+side, no GPU): every colour segment writes each element at most once, each
+element's first written face side carries the write flag, structured
+meshes get d+1 colours, and slab meshes keep their cut faces in the last
+segments.  (The reference keeps its sums race-free with private
+per-partition buffers merged in part order, operator.py:262-284.)"""
+import numpy as np
+import pytest
+
+from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel, DiffusionModel
+from paper_1403_1157_b200.mesh import unit_cube, unit_square
+from paper_1403_1157_b200.tables import (CODE_FIRST_IN, CODE_FIRST_OUT, CODE_MIRROR,
+                                         CODE_SKIP_OUT, build_tables, color_faces,
+                                         tc_face_blocks)
+
+
+def _check(t, n_owned):
+    el, code = t.if_elems, t.if_code
+    wr = (el[:, 1] >= 0) & ((code & (CODE_SKIP_OUT | CODE_MIRROR)) == 0)
+    seg_w = np.repeat(np.arange(t.n_seg), np.diff(t.seg_bf))
+    e = np.concatenate([el[:, 0], el[wr, 1], t.bf_elem]).astype(np.int64)
+    s = np.concatenate([t.if_seg, t.if_seg[wr], seg_w]).astype(np.int64)
+    first = np.concatenate([(code & CODE_FIRST_IN) != 0, (code[wr] & CODE_FIRST_OUT) != 0,
+                            (t.bf_code & CODE_FIRST_IN) != 0])
+    # race freedom: (element, segment) pairs are unique
+    pair = e * t.n_seg + s
+    assert len(np.unique(pair)) == len(pair)
+    # exactly one first side per owned element, in its lowest segment
+    assert np.array_equal(np.bincount(e[first], minlength=n_owned), np.ones(n_owned))
+    lo = np.full(n_owned, 1 << 40)
+    np.minimum.at(lo, e, s)
+    assert np.array_equal(lo[e[first]], s[first])
+    # segment offsets are consistent with the per-face segment ids
+    assert np.array_equal(np.searchsorted(t.if_seg, np.arange(t.n_seg + 1)), t.seg_if)
+    # every element has d+1 face sides
+    assert np.array_equal(np.bincount(e, minlength=n_owned), np.full(n_owned, t.dim + 1))
+
+
+@pytest.mark.parametrize("mesh,ncol", [
+    (lambda: unit_square(7, 5), 3),
+    (lambda: unit_square(6, 4, lengths=(4.0, 1.0), jitter=0.1, seed=3), 3),
+    (lambda: unit_cube(3), 4),
+    (lambda: unit_cube(4, 2, 3), 4),
+])
+def test_structured_meshes_get_d_plus_1_colours(mesh, ncol):
+    m = mesh()
+    space = DGSpace(m, 1, 6)
+    t = build_tables(space, PlaqueModel(), FluxScheme("cdg2"))
+    assert t.n_seg == ncol and t.n_seg_cut == 0
+    _check(t, m.n_elements)
+
+
+def test_dirichlet_mirror_faces_are_coloured():
+    m = unit_square(4)
+    t = build_tables(DGSpace(m, 2, 1), DiffusionModel(0.5, dirichlet=0.3), FluxScheme("ip"))
+    assert len(t.bf_code) == 0 and (t.if_code & CODE_MIRROR).any()
+    _check(t, m.n_elements)
+
+
+def test_greedy_colouring_is_proper_on_an_irregular_graph():
+    rng = np.random.default_rng(0)
+    n_el, n_f = 200, 500
+    a = rng.integers(0, n_el, n_f)
+    b = rng.integers(-1, n_el, n_f)
+    b[b == a] = -1
+    col, nc = color_faces(a, b, n_el)
+    assert col.min() >= 0 and col.max() == nc - 1
+    for c in range(nc):
+        m = col == c
+        ids = np.concatenate([a[m], b[m][b[m] >= 0]])
+        assert len(np.unique(ids)) == len(ids)
+
+
+def test_slab_cut_faces_run_last():
+    from paper_1403_1157_b200.configs import CONFIGS
+    from paper_1403_1157_b200.decomp import build_slab
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS["c4"], cells=(6, 3, 3))
+    slab = build_slab(cfg, 1, 3)
+    space = DGSpace(slab.mesh, 2, 6)
+    t = build_tables(space, PlaqueModel(), FluxScheme("cdg2"), n_owned=slab.n_owned,
+                     global_ids=slab.global_ids)
+    assert t.n_cut > 0 and t.n_seg_cut >= 1
+    ncut_start = t.seg_if[t.n_seg - t.n_seg_cut]
+    assert ncut_start == len(t.if_code) - t.n_cut
+    assert ((t.if_code[ncut_start:] & CODE_SKIP_OUT) != 0).all()
+    assert t.seg_bf[t.n_seg - t.n_seg_cut] == len(t.bf_code)  # no walls in cut segments
+    _check(t, slab.n_owned)
+    blocks, seg_blk = tc_face_blocks(t)
+    # blocks never straddle a segment
+    for s in range(t.n_seg):
+        for f0, n in blocks[seg_blk[s]:seg_blk[s + 1]]:
+            assert t.seg_if[s] <= f0 and f0 + n <= t.seg_if[s + 1]

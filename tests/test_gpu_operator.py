@@ -47,26 +47,9 @@ def test_generic_kernels_match_reference_golden(golden, name):
 
 
 @pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
-def test_flipped_face_kernel_matches_reference_golden(golden, name):
-    """The other face kernel (tensor-core DMMA in 2D, SIMT/generic in 3D)
-    against the same golden outputs."""
-    space, model, scheme, U, R, F = operator_case(golden, name)
-    op = _op(space, model, scheme)
-    op.set_variant(flip_mma=True)
-    got = op.apply(U)
-    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
-    op.set_variant(mma_volume=True)
-    got = op.apply(U)
-    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
-    op.set_variant(no_tc_faces=True)       # 3D: element-local DMMA interior faces
-    got = op.apply(U)
-    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
-
-
-@pytest.mark.parametrize("name", [n for n in _golden_names() if "_p0_" not in n])
 def test_tc_volume_kernel_matches_reference_golden(golden, name):
     """The transposed tensor-core volume kernel (default for 2D k=3 and
-    3D), forced on every golden case, incl. the overlapped schedule."""
+    3D), forced on every golden case, incl. the fused stage."""
     space, model, scheme, U, R, F = operator_case(golden, name)
     op = _op(space, model, scheme)
     op.set_variant(tc_volume=True)
@@ -81,42 +64,31 @@ def test_tc_volume_kernel_matches_reference_golden(golden, name):
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
-@pytest.mark.parametrize("dirichlet", [0, 1])
-def test_heat_models_mma(golden, scheme, dirichlet):
-    h = golden["heat"]
-    space = DGSpace(unit_square(3), 2)
-    model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
-    key = f"heat_sq3_{scheme}_{dirichlet}"
-    R = h[f"{key}__R"]
-    op = _op(space, model, FluxScheme(scheme))
-    op.set_variant(flip_mma=True)
-    got = op.apply(h[f"{key}__U"])
-    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
-
-
 def test_variants_agree_at_size():
+    """Kernel variants (generic CTA-staged, tensor-core volume, face-grid
+    caps) agree at size, and a stage written in place over U (face sums
+    in a separate buffer) equals the out-of-place stage bit for bit."""
     space = DGSpace(unit_square(64, 16, lengths=(4.0, 1.0)), 2, 6)
     op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
     U = torch.from_numpy(initial_state(space, 8)).cuda()
     a = op.apply_f(U)
-    op.set_variant(generic=True)
-    b = op.apply_f(U)
-    op.set_variant(vol4=True)
-    c = op.apply_f(U)
-    op.set_variant(serial=True)
-    d = op.apply_f(U)
-    op.set_variant(mma_volume=True)
-    e_ = op.apply_f(U)
-    op.set_variant(volume_first=True)
-    assert torch.allclose(op.apply_f(U), a, rtol=1e-12, atol=1e-12 * float(a.abs().max()))
-    out = torch.empty_like(U)
+    others = []
+    for v in ({"generic": True}, {"tc_volume": True}, {"face_ctas_per_sm": 15},
+              {"face_ctas_per_sm": 1}):
+        op.set_variant(**v)
+        others.append(op.apply_f(U))
     op.set_variant()
-    op.rk_stage(U, U, out, 0.25, 0.5, 1e-3)      # overlapped (out != U)
-    out2 = U.clone()
-    op.rk_stage(U, out2, out2, 0.25, 0.5, 1e-3)   # in place: serial path
-    assert torch.allclose(out, out2, rtol=1e-14, atol=1e-16)
-    for x in (b, c, d, e_):
+    assert torch.equal(op.apply_f(U), a)
+    out = torch.empty_like(U)
+    op.rk_stage(U, U, out, 0.25, 0.5, 1e-3)
+    out2, acc = U.clone(), torch.empty_like(U)
+    op.rk_stage(out2, out2, out2, 0.25, 0.5, 1e-3, acc=acc)   # in place over U and U0
+    assert torch.equal(out, out2)
+    with pytest.raises(ValueError):
+        op.rk_stage(U, U, U.clone(), 0.25, 0.5, 1e-3, acc=U)   # face sums over the input
+    with pytest.raises(ValueError):
+        op.rk_stage(out2, U, out2, 0.25, 0.5, 1e-3)            # acc = out = U0, a != 0
+    for x in others:
         assert rel_l2_per_species(space, a.cpu().numpy(), x.cpu().numpy()).max() <= 1e-13
 
 
@@ -160,7 +132,7 @@ def test_ssprk3_c1_trajectory(golden):
     space = DGSpace(unit_square(32), 1, 6)
     op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
     U = torch.from_numpy(t["c1__U0"]).cuda()
-    work = torch.empty_like(U)
+    work = op.new_work()
     for _ in range(10):
         op.ssprk3_step(U, work, float(t["c1__dt"]))
     err = rel_l2_per_species(space, U.cpu().numpy(), t["c1__U10"])
@@ -172,7 +144,7 @@ def test_ssprk3_3d_trajectory(golden):
     space = DGSpace(unit_cube(3, gamma1_in=None, top_tag=BoundaryTag.NO_FLOW), 2, 6)
     op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
     U = torch.from_numpy(t["cubez3__U0"]).cuda()
-    work = torch.empty_like(U)
+    work = op.new_work()
     for _ in range(3):
         op.ssprk3_step(U, work, 2e-4)
     assert rel_l2_per_species(space, U.cpu().numpy(), t["cubez3__U3"]).max() <= TOL_L2
@@ -183,7 +155,7 @@ def test_rect_trajectory_amplified(golden):
     space = DGSpace(unit_square(16, 4, lengths=(4.0, 1.0)), 2, 6)
     op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
     U = torch.from_numpy(t["rect164__U0"]).cuda()
-    work = torch.empty_like(U)
+    work = op.new_work()
     for _ in range(5):
         op.ssprk3_step(U, work, 2e-5)
     assert rel_l2_per_species(space, U.cpu().numpy(), t["rect164__U5"]).max() <= TOL_L2
@@ -210,7 +182,9 @@ def test_bitwise_reproducible():
     op.set_threads(4, npartitions=7)
     c = op.apply(U)
     assert torch.equal(a, b) and torch.equal(a, c)
-    assert op.audit_face_ownership()["faces_ok"]
+    audit = op.audit_face_ownership()
+    assert audit["faces_ok"] and audit["segments_race_free"] and audit["first_flags_ok"]
+    assert len(audit["faces_per_part"]) == 3          # d+1 colour segments
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
@@ -472,10 +446,10 @@ def test_ssprk3_graph_replay_is_bitwise_equal_to_direct_launches():
     runs = []
     for no_graph in (False, True):
         op.set_variant(no_graph=no_graph)
-        U, W = U0.clone(), torch.empty_like(U0)
+        U, W = U0.clone(), op.new_work()
         for dt in (1e-4, 1e-4, 2e-4, 1e-4):
             op.ssprk3_step(U, W, dt)
-        U2, W2 = U0.clone(), torch.empty_like(U0)      # new buffers
+        U2, W2 = U0.clone(), op.new_work()             # new buffers
         op.ssprk3_step(U2, W2, 1e-4)
         torch.cuda.synchronize()
         runs.append((U.clone(), U2.clone()))
@@ -571,7 +545,7 @@ def test_tiny_meshes_match_oracle(mesh_name, order, scheme):
     model = PlaqueModel(PlaqueParams(**AMPLIFIED))
     U = initial_state(space, 11)
     ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
-    for variant in ({}, {"generic": True}, {"serial": True}, {"face_rows_tc": True}):
+    for variant in ({}, {"generic": True}, {"tc_volume": True}):
         op = _op(space, model, FluxScheme(scheme))
         op.set_variant(**variant)
         got = op.apply_f(U)
@@ -584,13 +558,13 @@ def test_tiny_meshes_match_oracle(mesh_name, order, scheme):
 def test_heat_3d_tensor_core_kernels_match_oracle(scheme, dirichlet, order):
     """3D heat model (Dirichlet mirror faces or zero-flux walls) through the
     transposed tensor-core face and volume kernels (default in 3D) and
-    the element-local DMMA face kernel, vs the oracle
+    the element-local DMMA face kernel (mirror faces), vs the oracle
     (reference operator.py:436-444, tests/oracles.py:192-220)."""
     space = DGSpace(unit_cube(2), order, 1)
     model = DiffusionModel(0.7, dirichlet=0.4 if dirichlet else None)
     U = initial_state(space, 21)
     ref = OracleOperator(space, model, FluxScheme(scheme)).apply(U)
-    for variant in ({}, {"no_tc_faces": True}, {"tc_volume": True}):
+    for variant in ({}, {"generic": True}, {"tc_volume": True}):
         op = _op(space, model, FluxScheme(scheme))
         op.set_variant(**variant)
         got = op.apply(U)
@@ -602,8 +576,9 @@ def test_heat_3d_tensor_core_kernels_match_oracle(scheme, dirichlet, order):
 def test_3d_face_blocks_at_size_match_oracle(order, cells, scheme):
     """The species-rows tensor-core face kernel over many face blocks of
     mixed signatures (all ten Kuhn-cube signatures, blocks cut at 8 faces
-    and at signature changes) and the merged tail mode tile, against the
-    oracle (reference operator.py:253-288) and the faces-as-rows kernel."""
+    and at signature changes, inside 4 colour segments) and the merged tail
+    mode tile, against the oracle (reference operator.py:253-288) and the
+    generic kernels."""
     from paper_1403_1157_b200.mesh import unit_cube
     space = DGSpace(unit_cube(cells), order, 6)
     model = PlaqueModel(PlaqueParams(**AMPLIFIED))
@@ -612,7 +587,7 @@ def test_3d_face_blocks_at_size_match_oracle(order, cells, scheme):
     op = _op(space, model, FluxScheme(scheme))
     got = op.apply_f(U)
     assert rel_l2_per_species(space, got, ref).max() <= 1e-12
-    op.set_variant(face_rows_tc=True)
+    op.set_variant(generic=True)
     other = op.apply_f(U)
     assert rel_l2_per_species(space, got, other).max() <= 1e-13
 
@@ -659,23 +634,20 @@ def test_species_l2_on_device_is_the_parity_metric():
     assert np.allclose(d / n, rel_l2_per_species(space, U, V), rtol=1e-12)
 
 
-@pytest.mark.parametrize("cells,bands,expect,order", [((128, 128), 4, 4, 2), ((16, 8), 4, 1, 2),
-                                                      ((256, 128), 8, 8, 2), ((128, 128), 2, 2, 2),
-                                                      ((128, 128), 4, 4, 3)])
-def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect, order):
-    """tdg_ssprk3_steps_host (per-step copy-in / copy-out, stage wavefront
-    over element bands; none at 16x8; p = 3 runs the tensor-core volume
-    kernel per band) == copy-in, tdg_ssprk3_step, copy-out, bit for bit,
-    over several pipelined steps."""
-    space = DGSpace(unit_square(*cells, lengths=(1.0, 1.0)), order, 6)
-    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"), bands=bands)
-    assert op.tables.n_bands == expect
+@pytest.mark.parametrize("dim,order", [(2, 2), (2, 3), (3, 1), (3, 3)])
+def test_host_steps_bitwise_equal_device_steps(dim, order):
+    """tdg_ssprk3_steps_host (per-step copy-in / copy-out in chunks, the
+    last stage's volume kernel chunk by chunk) == copy-in,
+    tdg_ssprk3_step, copy-out, bit for bit, over several steps."""
+    mesh = unit_square(96, 64) if dim == 2 else unit_cube(6, 5, 4)
+    space = DGSpace(mesh, order, 6)
+    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
     U0 = torch.from_numpy(initial_state(space, 9))
-    dt = 2e-5
+    dt = 2e-5 if dim == 2 else 2e-6
     Uh = U0.clone().pin_memory()
     op.ssprk3_steps_host(Uh, 3, dt)
     torch.cuda.synchronize()
-    Ud, W = U0.cuda(), torch.empty_like(U0).cuda()
+    Ud, W = U0.cuda(), op.new_work()
     for _ in range(3):
         op.ssprk3_step(Ud, W, dt)
     torch.cuda.synchronize()
@@ -687,29 +659,6 @@ def test_host_pipelined_steps_bitwise_equal_device_steps(cells, bands, expect, o
     op.ssprk3_steps_host(Z, 0, dt)                     # zero steps: untouched
     torch.cuda.synchronize()
     assert torch.equal(Z, U0)
-
-
-@pytest.mark.parametrize("k", [1, 2, 3])
-def test_host_pipelined_steps_3d_bitwise_equal_device_steps(k):
-    """3D host-pipelined steps (tensor-core faces over each band's face
-    blocks, tensor-core volume per band, then the face-slot sum) ==
-    copy-in, tdg_ssprk3_step (same kernels, overlapped), copy-out, bit
-    for bit."""
-    from paper_1403_1157_b200.mesh import unit_cube
-    space = DGSpace(unit_cube(16), k, 6)
-    op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"), bands=3)
-    assert op.tables.n_bands == 3
-    U0 = torch.from_numpy(initial_state(space, 4))
-    dt = 2e-6
-    Uh = U0.clone().pin_memory()
-    op.ssprk3_steps_host(Uh, 2, dt)
-    torch.cuda.synchronize()
-    Ud, W = U0.cuda(), torch.empty_like(U0).cuda()
-    for _ in range(2):
-        op.ssprk3_step(Ud, W, dt)
-    torch.cuda.synchronize()
-    assert torch.equal(Uh, Ud.cpu())
-    assert not torch.equal(Uh, U0)
 
 
 def _slab_worker(rank, nranks, port, out):
@@ -765,7 +714,7 @@ def test_two_rank_slab_run_on_one_gpu_matches_global():
     fn = bump_field(2, 6, 3, np.zeros(2), np.asarray(cfg.lengths, float))
     U0 = np.ascontiguousarray(gspace.project(fn).coeffs)
     gop = _op(gspace, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
-    U, W = torch.from_numpy(U0).cuda(), torch.empty(U0.shape, dtype=torch.float64, device="cuda")
+    U, W = torch.from_numpy(U0).cuda(), gop.new_work()
     for _ in range(2):
         gop.ssprk3_step(U, W, 1e-5)
     ref_e = U.cpu().numpy()
