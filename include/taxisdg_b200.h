@@ -241,6 +241,15 @@ TDG_API int tdg_axpy_dev(double s, const double* alpha, const double* x, double*
 TDG_API int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w, int64_t n,
                     double* h, void* stream);
 
+/* One pass of that sweep for slab-decomposed runs, whose dots must be
+ * summed over the ranks between passes: pass i (0 <= i <= j+1) applies the
+ * previous pass's update with the (globally reduced) h[i-1] and writes this
+ * rank's partial of h[i]; the last pass writes w . w (the caller sums over
+ * the ranks and takes the root).  Same kernels, element order and
+ * reduction tree as tdg_mgs. */
+TDG_API int tdg_mgs_pass(tdg_ctx* ctx, const double* V, int64_t ldv, int i, int j, double* w,
+                         int64_t n, double* h, void* stream);
+
 /* GMRES basis vector (reference timeint.py:165,176: V[j+1] = w / hnext):
  * v = w / hnext with ||v|| written to the DEVICE scalar norm_out in the
  * same pass (same reduction tree as tdg_norm2, so bitwise its result); the

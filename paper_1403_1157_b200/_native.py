@@ -64,6 +64,7 @@ def load(path: str = LIB):
     lib.tdg_ssprk3_steps_host.argtypes = [_p, _p, _p, _p, _p, _i64, _d, _d, _p]
     lib.tdg_species_l2.argtypes = [_p, _p, _p, _p, _p]
     lib.tdg_mgs.argtypes = [_p, _p, _i64, ctypes.c_int, _p, _i64, _p, _p]
+    lib.tdg_mgs_pass.argtypes = [_p, _p, _i64, ctypes.c_int, ctypes.c_int, _p, _i64, _p, _p]
     lib.tdg_rk_stage_part.argtypes = [_p, _p, _p, _p, _p, _d, _d, _d, _d, ctypes.c_int, _p]
     lib.tdg_ssprk3_step.argtypes = [_p, _p, _p, _p, _d, _d, _p]
     lib.tdg_color_faces.argtypes = [_i64, _p, _p, _i64, _p, _p]
@@ -80,7 +81,7 @@ def load(path: str = LIB):
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
     lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
-    for name in ("tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    for name in ("tdg_mgs_pass", "tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev", "tdg_scale_norm", "tdg_jv_shift", "tdg_jv_diff"):

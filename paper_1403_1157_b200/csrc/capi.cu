@@ -442,6 +442,16 @@ int tdg_mgs(tdg_ctx* ctx, const double* V, int64_t ldv, int j, double* w, int64_
   return e == cudaSuccess ? TDG_OK : cuda_fail(e, "mgs");
 }
 
+int tdg_mgs_pass(tdg_ctx* ctx, const double* V, int64_t ldv, int i, int j, double* w, int64_t n,
+                 double* h, void* stream) {
+  if (!ctx || !V || !w || !h) return fail(TDG_E_INVALID, "null argument");
+  if (j < 0 || i < 0 || i > j + 1 || n < 0 || ldv < n) return fail(TDG_E_INVALID, "bad mgs sizes");
+  if (!aligned16(V) || !aligned16(w) || (ldv & 1))
+    return fail(TDG_E_INVALID, "mgs operands must be 16-byte aligned (even ldv)");
+  cudaError_t e = launch_mgs_pass(V, ldv, i, j, w, n, h, ctx->part, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "mgs_pass");
+}
+
 int tdg_axpy_dev(double s, const double* alpha, const double* x, double* y, int64_t n,
                  void* stream) {
   if (!alpha || !x || !y) return fail(TDG_E_INVALID, "null argument");

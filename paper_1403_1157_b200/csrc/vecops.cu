@@ -311,6 +311,25 @@ cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n
   return cudaGetLastError();
 }
 
+cudaError_t launch_mgs_pass(const double* V, int64_t ldv, int i, int j, double* w, int64_t n,
+                            double* h, double* part, cudaStream_t st) {
+  // pass i of the sweep ending at j, the dot / norm left un-reduced across
+  // ranks (slab runs all-reduce h[i] before the next pass): i = 0: h[0] =
+  // w . V_0;  0 < i <= j: w -= h[i-1] V_{i-1}, h[i] = w . V_i;  i = j+1:
+  // w -= h[j] V_j, h[j+1] = w . w (the caller takes the root)
+  unsigned* ticket = red_ticket(part);
+  if (i == 0)
+    k_red_partial<0, true><<<kRedBlocks, kRedThreads, 0, st>>>(nullptr, nullptr, w, V, n, part,
+                                                               ticket, h, 0, 0.0);
+  else if (i <= j)
+    k_red_partial<2, true><<<kRedBlocks, kRedThreads, 0, st>>>(
+        h + i - 1, V + (i - 1) * ldv, w, V + i * ldv, n, part, ticket, h + i, 0, 0.0);
+  else
+    k_red_partial<3, true><<<kRedBlocks, kRedThreads, 0, st>>>(h + j, V + j * ldv, w, w, n, part,
+                                                               ticket, h + j + 1, 0, 0.0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scale_norm(const double* w, double hnext, const double* hnext_dev, double* v,
                               int64_t n, double* part, double* norm_out, cudaStream_t st) {
   k_red_partial<4, false><<<kRedBlocks, kRedThreads, 0, st>>>(hnext_dev, nullptr, v, w, n, part,

@@ -19,6 +19,8 @@ cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* part
                        bool norm, cudaStream_t st);
 cudaError_t launch_mgs(const double* V, int64_t ldv, int j, double* w, int64_t n, double* h,
                        double* part, cudaStream_t st);
+cudaError_t launch_mgs_pass(const double* V, int64_t ldv, int i, int j, double* w, int64_t n,
+                            double* h, double* part, cudaStream_t st);
 cudaError_t launch_scale_norm(const double* w, double hnext, const double* hnext_dev, double* v,
                               int64_t n, double* part, double* norm_out, cudaStream_t st);
 cudaError_t launch_jv_shift(const double* U, const double* v, const double* vnorm, double cnum,

@@ -11,6 +11,10 @@ Same constructor, methods and error behaviour as the reference
     .audit_face_ownership()                                  (:231-249)
     attributes .space .model .scheme .mesh
 
+The constructor takes this package's ``DGSpace`` / model / ``FluxScheme``
+or the reference's own ``taxisdg`` objects (``compat.adapt``), so the
+reference's call sites need only the import swapped.
+
 ``apply``/``apply_f`` accept a numpy array or ``DiscreteFunction`` (and
 return a fresh numpy array, like the reference) or a CUDA
 ``torch.Tensor`` of the same shape (and return a CUDA tensor, no host
@@ -32,6 +36,7 @@ import numpy as np
 from . import _native
 from .fespace import DGSpace
 from .flux import FluxScheme
+from .compat import adapt
 from .tables import build_tables, scheme_constants
 
 __all__ = ["DiscreteOperator"]
@@ -73,8 +78,12 @@ class DiscreteOperator:
         if not torch.cuda.is_available():
             raise RuntimeError("DiscreteOperator needs a CUDA device (B200); "
                                "there is no CPU path")
+        # the caller's objects (package or reference taxisdg ones) stay the
+        # public attributes; the device is described from their adapted
+        # package equivalents (compat.adapt)
         self.space, self.model, self.scheme = space, model, scheme
         self.mesh = space.mesh
+        space, model, scheme = adapt(space, model, scheme)
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
@@ -405,6 +414,20 @@ class DiscreteOperator:
             raise ValueError("mgs: inconsistent sizes")
         self._call(self.lib.tdg_mgs, self._ctx, V.data_ptr(), V.stride(0), int(j), w.data_ptr(),
                                        n, h.data_ptr(), self._stream(), what="tdg_mgs")
+        return h
+
+    def mgs_pass(self, V, i: int, j: int, w, h, n: int | None = None):
+        """Pass i of the MGS sweep ending at j over the first ``n`` entries
+        (slab runs: owned rows), leaving h[i] un-reduced across ranks (the
+        caller all-reduces it before the next pass; the last pass leaves
+        w . w)."""
+        n = w.numel() if n is None else int(n)
+        if V.dim() != 2 or not V.is_contiguous() or not w.is_contiguous():
+            raise ValueError("mgs_pass needs a contiguous 2-D V and a contiguous w")
+        if V.shape[1] < n or w.numel() < n or j + 1 > V.shape[0] or h.numel() < j + 2:
+            raise ValueError("mgs_pass: inconsistent sizes")
+        self._call(self.lib.tdg_mgs_pass, self._ctx, V.data_ptr(), V.stride(0), int(i), int(j),
+                   w.data_ptr(), n, h.data_ptr(), self._stream(), what="tdg_mgs_pass")
         return h
 
     def scale_norm(self, w, hnext, v, norm_out):

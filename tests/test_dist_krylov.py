@@ -70,6 +70,14 @@ class _CpuStageOp:
         y.add_(x, alpha=float(s * alpha.reshape(-1)[0]))
         return y
 
+    def mgs_pass(self, V, i, j, w, h, n):
+        """tdg_mgs_pass semantics on the first n entries (CPU double)."""
+        wv = w.reshape(-1)[:n]
+        if i > 0:
+            wv.sub_(V[i - 1, :n] * h[i - 1])
+        h[i] = torch.dot(wv, wv if i == j + 1 else V[i, :n])
+        return h
+
 
 def _problem(rank=None, nranks=None):
     cfg = CONFIGS["c2"]
@@ -110,11 +118,15 @@ def _worker(rank, nranks, port, out):
         dist.destroy_process_group()
 
 
-def test_two_rank_sdirk3_jfnk_matches_single_domain():
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_slab_sdirk3_jfnk_matches_single_domain(nranks):
+    """2 and 4 gloo ranks: the slab SDIRK3 + JFNK path (exchange inside
+    G(V); the MGS sweep pass by pass with every pass's dot all-reduced,
+    SlabReductions.mgs over tdg_mgs_pass semantics) equals the single-domain
+    run with the same GMRES iteration count."""
     op, U, _, _, _ = _problem()
     ref = integrate(op, U, 0.0, 2 * DT, DT, order=3, newton_kwargs=NEWTON)
     Uref = ref.U.numpy()
-    nranks = 2
     mgr = mp.Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(nranks, _free_port(), out), nprocs=nranks,

@@ -136,3 +136,39 @@ def test_quadrature_degree_override():
     assert lo.tables.nq_vol < hi.tables.nq_vol and lo.tables.nq_face < hi.tables.nq_face
     fn = space.project(lambda x: x[..., 0][..., None])
     assert np.allclose(lo.apply(fn.coeffs), hi.apply(fn.coeffs), atol=1e-13)
+
+
+def test_reference_style_stepper_over_numpy_apply_f(golden):
+    """The drop-in at the reference's own call shape: the reference's SDIRK3
+    + JFNK stepper (restated in numpy, oracle.sdirk_integrate, reference
+    timeint.py:137-380) calling the device operator's apply_f(numpy) ->
+    numpy exactly as it calls the reference operator, against the
+    reference's own trajectory."""
+    from oracle import sdirk_integrate
+    t = golden["trajectories"]
+    space = DGSpace(unit_square(4), 2, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    U = sdirk_integrate(op, t["sdirk__U0"], 0.01, 2,
+                        newton_kwargs={"rtol": 1e-11, "atol": 1e-13, "gmres_rtol": 1e-6})
+    err = rel_l2_per_species(space, U, t["sdirk__U2"])
+    assert err.max() <= TOL_L2, err
+
+
+def test_integrate_hands_numpy_to_callbacks():
+    """integrate() with a numpy U0 calls back with numpy states, like the
+    reference (timeint.py:376-378), so reference callbacks such as
+    space.function(U).species_totals() (analysis.conservation_audit,
+    scenarios' balance.csv) work unchanged."""
+    from paper_1403_1157_b200.timeint import integrate
+    space = DGSpace(unit_square(4), 1, 6)
+    op = _op(space, PlaqueModel(), FluxScheme("cdg2"))
+    U0 = _seeded_plaque_state(space)
+    seen = []
+
+    def record(step, t, U):
+        assert isinstance(U, np.ndarray) and U.shape == space.shape
+        seen.append(space.function(U).species_totals())
+
+    res = integrate(op, U0, 0.0, math.inf, 0.01, order=3, n_steps=3, callback=record)
+    assert len(seen) == 3 and isinstance(res.U, np.ndarray)
+    assert np.allclose(seen[-1], space.function(res.U).species_totals(), rtol=0, atol=0)
