@@ -141,6 +141,14 @@ typedef struct tdg_desc {
   const double* face_tc;
   const int32_t* face_blocks;
   int64_t n_face_blocks;
+  /* optional, species-rows face kernel: per face-geometry class (one
+   * (table id, Jinv n) pair) the B fragments paired with the folded
+   * normal-derivative fragments sum_a (Jinv n)_a G_a
+   * (tables.tc_face_fold_tables), and the class of every interior face's
+   * inside / outside side, int32 [nif][2]; both NULL: the kernel folds
+   * Jinv n per face */
+  const double* face_tc_fold;
+  const int32_t* if_fold;
   /* face colour segments, run in order: segment s covers the interior
    * faces [I[s], I[s+1]), the walls [W[s], W[s+1]) and the face blocks
    * [B[s], B[s+1]) with seg_ptr (HOST) = I[n+1] | W[n+1] | B[n+1].  No
@@ -270,7 +278,8 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
  * CTA-staged generic kernels; bit 5: launch tdg_ssprk3_step's kernels
- * directly instead of replaying its cached CUDA graph; bit 12: use the
+ * directly instead of replaying its cached CUDA graph; bit 13: ignore the
+ * face-geometry-class tables (fold Jinv n per face); bit 12: use the
  * transposed tensor-core volume kernel wherever it compiles (default only
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
  * per SM of the 2D register-resident face kernel's grid-stride grid (0 =

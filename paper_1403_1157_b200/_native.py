@@ -38,6 +38,7 @@ class TdgDesc(ctypes.Structure):
         ("bf_elem", _p), ("bf_code", _p), ("bf_geo", _p),
         ("face_mma", _p), ("vol_tc", _p),
         ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64),
+        ("face_tc_fold", _p), ("if_fold", _p),
         ("n_segments", _i32), ("n_segments_cut", _i32), ("seg_ptr", _p),
     ]
 
@@ -49,6 +50,9 @@ def load(path: str = LIB):
     global _lib
     if _lib is not None:
         return _lib
+    # A/B timing of alternative builds (tools/): TDG_LIB names another
+    # in-tree build of the same library
+    path = os.environ.get("TDG_LIB", path)
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `python -m "

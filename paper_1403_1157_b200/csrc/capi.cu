@@ -133,6 +133,8 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.vtc = d.vol_tc;
   p.ftc = d.face_tc;
   p.fblk = d.face_blocks;
+  p.ftf = d.face_tc_fold;
+  p.ffold = d.if_fold;
 
   {
     int dev = 0, sms = 0;
@@ -464,6 +466,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->force_generic = (variant & 1) != 0;
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
   ctx->force_tc = ((variant >> 12) & 1) != 0;
+  ctx->no_fold = ((variant >> 13) & 1) != 0;    // bit 13: no face-geometry-class tables
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;

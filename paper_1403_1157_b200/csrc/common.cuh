@@ -63,6 +63,8 @@ struct OpParams {
   const double* __restrict__ vtc;   // transposed tensor-core volume tables (may be null)
   const double* __restrict__ ftc;   // transposed tensor-core face tables (may be null)
   const int32_t* __restrict__ fblk; // interior-face blocks [n][2] (first, count)
+  const double* __restrict__ ftf;   // face-geometry-class folded tables (may be null)
+  const int32_t* __restrict__ ffold;  // [nif][2] class of the inside / outside side
 };
 
 // code-word layout, mirrors include/taxisdg_b200.h
@@ -87,6 +89,16 @@ __device__ __forceinline__ void acc_put(double* p, double v, bool first) {
 
 // BoundaryTag (mesh.py:46-52)
 enum Tag { GAMMA1 = 1, GAMMA1_IN = 2, GAMMA2 = 3, NO_FLOW = 4 };
+
+// 32-byte read-only global load (sm_100 LDG.E.ENL2.256); p 32-byte aligned
+__device__ __forceinline__ void ld256(const double* p, double* d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
+}
+
+__device__ __forceinline__ void ld128(const double* p, double* d) {
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(d[0]), "=d"(d[1]) : "l"(p));
+}
 
 // Reciprocal to ~1 ulp: MUFU seed + two Newton steps (the operator only
 // needs agreement with the reference to ~1e-15 relative, not IEEE rounding).

@@ -71,6 +71,7 @@ struct tdg_ctx {
   int64_t launches[4] = {0, 0, 0, 0};
   bool force_generic = false;  // testing: pin the CTA-staged kernels
   bool force_tc = false;       // testing: tensor-core volume kernel where the SIMT one fits
+  bool no_fold = false;        // testing: per-face normal-derivative folds despite class tables
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
@@ -107,8 +108,13 @@ int configure(int nqv) {
                            int(WallTile<D, K, M>::smem()));
   if (e != cudaSuccess) return cuda_fail(e, "configure wall");
   if constexpr (TcsFace<D, K, M>::ok) {
-    e = cudaFuncSetAttribute(k_faces_tcs<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_faces_tcs<D, K, M, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(TcsFace<D, K, M>::smem()));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_faces_tcs<D, K, M, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(TcsFace<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcs");
   }
   if constexpr (TcVol<D, K, M>::ok) {
@@ -180,10 +186,14 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
         KernelTimer kt(ctx, 0, st);
         using T = TcsFace<D, K, M>;
         int64_t grid = (sg.b1 - sg.b0 + T::WARPS - 1) / T::WARPS;
-        const int64_t cap = int64_t(ctx->num_sms) * T::MINB * 8;
+        const int64_t cap = int64_t(ctx->num_sms) * T::MINB_FOLD * 8;
         grid = grid < cap ? grid : cap;
-        k_faces_tcs<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, sg.b0, sg.b1,
-                                                                     U, acc);
+        if (p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold)
+          k_faces_tcs<D, K, M, true><<<unsigned(grid), 128, T::smem(), st>>>(
+              p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
+        else
+          k_faces_tcs<D, K, M, false><<<unsigned(grid), 128, T::smem(), st>>>(
+              p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
       }
       if (q.nbf > 0) {
         KernelTimer kt(ctx, 1, st);

@@ -116,10 +116,6 @@ __device__ __forceinline__ void store_row(double* dst, const double* v) {
 // 16-byte piece, in either order depending on its 32-byte alignment.  The
 // face kernel's lanes read / write such rows side by side, so fewer and
 // wider accesses cut the L1 wavefronts of its (saturated) data pipe.
-__device__ __forceinline__ void ld256(const double* p, double* d) {
-  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-      : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
-}
 // coherent 32-byte load (rows this kernel also writes)
 __device__ __forceinline__ void ld256c(const double* p, double* d) {
   asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"

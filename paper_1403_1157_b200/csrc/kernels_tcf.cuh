@@ -23,11 +23,18 @@ struct TcFace {
   static constexpr int KT = (NB + 3) / 4, NBK = 4 * KT;
   static constexpr int NNT = (NB + 7) / 8, NBN = 8 * NNT;
   static constexpr int NCV = 1 + M::NFX;
-  // per-signature table offsets (doubles), see tables.tc_face_tables; every
-  // table is stored fragment-major ([k-step or point tile][...][lane]) so a
-  // warp's B-operand load is 32 consecutive doubles (2 L1 wavefronts)
-  static constexpr int OBT = 0, OGT = OBT + NBK * QP, OBP = OGT + D * NBK * QP,
-                       OGP = OBP + QP * NBN, OWB = OGP + D * QP * NBN, TS = OWB + QP * NBN;
+  // per-signature table offsets (doubles), see tables.tc_face_tables.
+  // Fragment-major ([k-step or point tile][...][lane]); the trace (TR) and
+  // projection (PR) blocks interleave each B fragment with its three
+  // gradient fragments ([...][lane][B, G0, G1, G2]: one 32-byte load per
+  // lane), WB / BT are plain ([...][lane]: one 8-byte load per lane)
+  // (3D: 1 + D = 4 doubles per lane and fragment)
+  static constexpr int OTR = 0, OPR = OTR + (1 + D) * NBK * QP, OWB = OPR + (1 + D) * QP * NBN,
+                       OBT = OWB + QP * NBN, TS = OBT + NBK * QP;
+  // face-geometry-class tables (tables.tc_face_fold_tables): per (table id,
+  // Jinv n) class the B fragment paired with the folded normal-derivative
+  // fragment sum_a jn_a G_a ([...][lane][B, G_n]: one 16-byte load per lane)
+  static constexpr int OTRF = 0, OPRF = OTRF + 2 * NBK * QP, TSF = OPRF + 2 * QP * NBN;
   static constexpr int WARPS = 4;
   static constexpr int PWS = 8 * QP * NCV;  // per-warp point-physics slice
   static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
@@ -87,13 +94,20 @@ struct TcsFace {
   static constexpr int WARPS = 4;
   static constexpr int PWS = 3 * QP * XS + QP * NCV + 1;  // per-warp scratch (doubles)
   static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }
-  // 128 registers (16 warps/SM): 3 -> 4 cut C4 faces 21.6 -> 18.6 ms; 5 spills
+  // 128 registers (16 warps/SM): 3 -> 4 cut C4 faces 21.6 -> 18.6 ms; 5 spills.
+  // p = 3 folding Jinv n per face needs 168 registers (3 CTAs/SM); with the
+  // face-geometry-class tables it fits 128 without spills (64^3 p = 3:
+  // 38.4 ms at 3 CTAs without classes -> 31.6 with -> 30.0 at 4 CTAs)
   static constexpr int MINB = K >= 3 ? 3 : 4;
+  static constexpr int MINB_FOLD = 4;
   static constexpr bool ok = D == 3 && S <= 8 && !M::kMirror && TF::ok && smem() <= 96 * 1024;
 };
 
-template <int D, int K, class M>
-__global__ void __launch_bounds__(128, TcsFace<D, K, M>::MINB)
+// FOLD: the normal-derivative fragments come precomputed per face-geometry
+// class (meshes with few distinct (table, Jinv n) pairs, e.g. the Kuhn
+// cubes: 6 per side); otherwise they are folded per face from jn
+template <int D, int K, class M, bool FOLD>
+__global__ void __launch_bounds__(128, FOLD ? TcsFace<D, K, M>::MINB_FOLD : TcsFace<D, K, M>::MINB)
 k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
             int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ ACC) {
   using T = TcsFace<D, K, M>;
@@ -122,14 +136,21 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
       double jn[2][D];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        jn[0][a] = __ldg(gg + a);
-        jn[1][a] = __ldg(gg + D + a);
+        jn[0][a] = FOLD ? 0.0 : __ldg(gg + a);
+        jn[1][a] = FOLD ? 0.0 : __ldg(gg + D + a);
       }
       const double sfac = __ldg(gg + 2 * D), h = __ldg(gg + 2 * D + 1);
       const double idi = __ldg(gg + 2 * D + 2), ido = __ldg(gg + 2 * D + 3);
       const int sig = code & 1023;
       const double* Ti = tabs + size_t(sig & 31) * TS;
       const double* To = tabs + size_t((sig >> 5) & 31) * TS;
+      const double* Fi = nullptr;
+      const double* Fo = nullptr;
+      if constexpr (FOLD) {
+        const int2 cl = __ldg(reinterpret_cast<const int2*>(p.ffold) + f);
+        Fi = p.ftf + size_t(cl.x) * TF::TSF;
+        Fo = p.ftf + size_t(cl.y) * TF::TSF;
+      }
       // A operands: this face's coefficients, row = species g, k = 4 kt + t
       double ci[KT], co[KT];
 #pragma unroll
@@ -140,8 +161,11 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
       }
       const bool br2 = p.scheme == BR2;
       const bool lift = p.scheme != IP && p.scheme != BO;
-      const bool use_in = lift && (br2 || code_minus_in(code));
-      const bool use_out = lift && (br2 || !code_minus_in(code));
+      // lifting side(s) (operator.py:336-357): K- only (cdg2 / cdg), both
+      // for br2; mi runs on table Tl (K- side, or the inside for br2), mo
+      // on the outside for br2 only -- no predicated-off DMMA chains
+      const bool min_ = code_minus_in(code);
+      const double* Tl = (br2 || min_) ? Ti : To;
 
       // ---- pass 1: traces, transpose, jumps -> modal lifting -------------
       double mi[NNT][2], mo[NNT][2];
@@ -152,16 +176,23 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
         double ui[2] = {0.0, 0.0}, uo[2] = {0.0, 0.0}, di[2] = {0.0, 0.0}, dq[2] = {0.0, 0.0};
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
-          const int ob = (kt * QT + qt) * 32 + lane;
-          dmma(ui[0], ui[1], ci[kt], __ldg(Ti + TF::OBT + ob));
-          dmma(uo[0], uo[1], co[kt], __ldg(To + TF::OBT + ob));
-          double gi = 0.0, go = 0.0;  // dphi/dn fragments (jn folded in)
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const int og = ((a * KT + kt) * QT + qt) * 32 + lane;
-            gi = fma(jn[0][a], __ldg(Ti + TF::OGT + og), gi);
-            go = fma(jn[1][a], __ldg(To + TF::OGT + og), go);
+          double fi[4], fo[4];  // B, G0, G1, G2 fragments of both sides (FOLD: B, G_n)
+          double gi, go;        // dphi/dn fragments (jn folded in)
+          if constexpr (FOLD) {
+            const int ob = 2 * ((kt * QT + qt) * 32 + lane);
+            ld128(Fi + TF::OTRF + ob, fi);
+            ld128(Fo + TF::OTRF + ob, fo);
+            gi = fi[1];
+            go = fo[1];
+          } else {
+            const int ob = 4 * ((kt * QT + qt) * 32 + lane);
+            ld256(Ti + TF::OTR + ob, fi);
+            ld256(To + TF::OTR + ob, fo);
+            gi = fma(jn[0][2], fi[3], fma(jn[0][1], fi[2], jn[0][0] * fi[1]));
+            go = fma(jn[1][2], fo[3], fma(jn[1][1], fo[2], jn[1][0] * fo[1]));
           }
+          dmma(ui[0], ui[1], ci[kt], fi[0]);
+          dmma(uo[0], uo[1], co[kt], fo[0]);
           dmma(di[0], di[1], ci[kt], gi);
           dmma(dq[0], dq[1], co[kt], go);
         }
@@ -182,8 +213,8 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
 #pragma unroll
             for (int nt = 0; nt < NNT; ++nt) {
               const int ow = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
-              if (use_in) dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Ti + TF::OWB + ow));
-              if (use_out) dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + TF::OWB + ow));
+              dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Tl + TF::OWB + ow));
+              if (br2) dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + TF::OWB + ow));
             }
         }
       }
@@ -191,7 +222,8 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
       {
         const double wside = br2 ? 0.5 : 1.0;
         const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac * As;
-        const double ki = use_in ? fac0 * idi : 0.0, ko = use_out ? fac0 * ido : 0.0;
+        const double ki = lift ? fac0 * ((br2 || min_) ? idi : ido) : 0.0;
+        const double ko = br2 ? fac0 * ido : 0.0;
 #pragma unroll
         for (int nt = 0; nt < NNT; ++nt)
 #pragma unroll
@@ -222,8 +254,8 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
           for (int kt = 0; kt < KT; ++kt) {
             const int ob = (kt * QT + qt) * 32 + lane;
             // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
-            if (use_in) dmma(rho[0], rho[1], mi[kt / 2][kt % 2], __ldg(Ti + TF::OBT + ob));
-            if (use_out) dmma(rho[0], rho[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
+            dmma(rho[0], rho[1], mi[kt / 2][kt % 2], __ldg(Tl + TF::OBT + ob));
+            if (br2) dmma(rho[0], rho[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
           }
         }
         double Y[2], X[2];
@@ -257,31 +289,38 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
               // out-side ones (normal-layout lane - 4, sign of Y folded
               // in), so one DMMA pair serves both sides
               const bool oc = (g & 1) != 0;
-              const double* Tx = oc ? To : Ti;
               const int ln = oc ? lane - 4 : lane;
-              const int ob = ((qt * 2 + ks) * NNT + nt) * 32 + ln;
-              double gx = 0.0;
-#pragma unroll
-              for (int a = 0; a < D; ++a) {
-                const int og = (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + ln;
-                gx = fma(oc ? jn[1][a] : jn[0][a], __ldg(Tx + TF::OGP + og), gx);
+              const int of = ((qt * 2 + ks) * NNT + nt) * 32 + ln;
+              double fx[4], gx;
+              if constexpr (FOLD) {
+                ld128((oc ? Fo : Fi) + TF::OPRF + 2 * of, fx);
+                gx = fx[1];
+              } else {
+                ld256((oc ? To : Ti) + TF::OPR + 4 * of, fx);
+                const double* jx = oc ? jn[1] : jn[0];
+                gx = fma(jx[2], fx[3], fma(jx[1], fx[2], jx[0] * fx[1]));
               }
-              const double bx = __ldg(Tx + TF::OBP + ob);
+              const double bx = fx[0];
               dmma(ri[nt][0], ri[nt][1], Y[ks], oc ? -bx : bx);
               dmma(ri[nt][0], ri[nt][1], X[ks], gx);
               continue;
             }
-            const int ob = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
-            double gi = 0.0, go = 0.0;
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-              const int og = (((a * QT + qt) * 2 + ks) * NNT + nt) * 32 + lane;
-              gi = fma(jn[0][a], __ldg(Ti + TF::OGP + og), gi);
-              go = fma(jn[1][a], __ldg(To + TF::OGP + og), go);
+            const int of = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
+            double fi[4], fo[4], gi, go;
+            if constexpr (FOLD) {
+              ld128(Fi + TF::OPRF + 2 * of, fi);
+              ld128(Fo + TF::OPRF + 2 * of, fo);
+              gi = fi[1];
+              go = fo[1];
+            } else {
+              ld256(Ti + TF::OPR + 4 * of, fi);
+              ld256(To + TF::OPR + 4 * of, fo);
+              gi = fma(jn[0][2], fi[3], fma(jn[0][1], fi[2], jn[0][0] * fi[1]));
+              go = fma(jn[1][2], fo[3], fma(jn[1][1], fo[2], jn[1][0] * fo[1]));
             }
-            dmma(ri[nt][0], ri[nt][1], Y[ks], __ldg(Ti + TF::OBP + ob));
+            dmma(ri[nt][0], ri[nt][1], Y[ks], fi[0]);
             dmma(ri[nt][0], ri[nt][1], X[ks], gi);
-            dmma(ro[nt][0], ro[nt][1], -Y[ks], __ldg(To + TF::OBP + ob));
+            dmma(ro[nt][0], ro[nt][1], -Y[ks], fo[0]);
             dmma(ro[nt][0], ro[nt][1], X[ks], go);
           }
       }

@@ -348,19 +348,23 @@ def _frag_kn(A):
 
 
 def tc_face_tables(t: OperatorTables):
-    """Per-signature operand tables of the transposed tensor-core face
-    kernel (csrc/kernels_tcf.cuh), concatenated per table id, each stored
+    """Per-signature operand tables of the 3D species-rows tensor-core face
+    kernel (csrc/kernels_tcf.cuh), concatenated per table id, stored
     fragment-major (``_frag_kq`` / ``_frag_qn``: one warp-wide B-operand
-    load reads 32 consecutive doubles):
+    load is 32 consecutive fragments):
 
-    BT  [NBK][QP]        B[q][k]                 traces u = c B^T, rho = m B^T
-    GT  [d][NBK][QP]     G[q][k][a]              traces d_n u = sum_a (jn_a c) G_a^T
-    BP  [QP][NBN]        B[q][pi(n)]             projection of Y
-    GP  [d][QP][NBN]     G[q][pi(n)][a]          projection of X jn_a
-    WB  [QP][NBN]        w_q B[q][pi(n)]         modal lifting m = dU (w B)
+    TR  [KT][QT][32][4]        (B[q][k], G[q][k][0..2]) B^T / G_a^T fragments:
+                               traces u = c B^T and d_n u = c (sum_a jn_a G_a)^T,
+                               one 32-byte load per lane
+    PR  [QT][2][NNT][32][4]    (B[q][pi(n)], G[q][pi(n)][0..2]): projection of
+                               Y (B) and of X (sum_a jn_a G_a)
+    WB  [QT][2][NNT][32]       w_q B[q][pi(n)]  modal lifting m = dU (w B)
+    BT  [KT][QT][32]           B[q][k]          rho = m B^T
     with QP = ceil8(F), NBK = ceil4(nb), NBN = ceil8(nb).  Returns the flat
     array and the per-signature stride."""
     d, nb, F = t.dim, t.nb, t.nq_face
+    if d != 3:
+        raise ValueError("the species-rows face kernel is 3D only")
     QP, NBK, NBN = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
     pic, ok = _pi_cols(nb)
     parts = []
@@ -371,13 +375,56 @@ def tc_face_tables(t: OperatorTables):
         BP = np.zeros((QP, NBN)); BP[:F] = B[:, pic] * ok
         GP = np.zeros((d, QP, NBN)); GP[:, :F] = G.transpose(2, 0, 1)[:, :, pic] * ok
         WB = np.zeros((QP, NBN)); WB[:F] = (t.face_w[:, None] * B)[:, pic] * ok
-        parts.append(np.concatenate([_frag_kq(BT).ravel()]
-                                    + [_frag_kq(GT[a]).ravel() for a in range(d)]
-                                    + [_frag_qn(BP).ravel()]
-                                    + [_frag_qn(GP[a]).ravel() for a in range(d)]
-                                    + [_frag_qn(WB).ravel()]))
+        TR = np.stack([_frag_kq(BT)] + [_frag_kq(GT[a]) for a in range(d)], axis=-1)
+        PR = np.stack([_frag_qn(BP)] + [_frag_qn(GP[a]) for a in range(d)], axis=-1)
+        parts.append(np.concatenate([TR.ravel(), PR.ravel(), _frag_qn(WB).ravel(),
+                                     _frag_kq(BT).ravel()]))
     stride = len(parts[0])
     return np.ascontiguousarray(np.concatenate(parts)), stride
+
+
+def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
+    """Face-geometry classes of the species-rows face kernel: every
+    interior face side is a (table id, Jinv n) pair; meshes of congruent
+    cells (the Kuhn cubes: 6 classes per side) have few of them, and per
+    class the normal-derivative fragments sum_a (Jinv n)_a G_a can be
+    formed once instead of per face (they are a linear combination of the
+    signature's gradient tables, operator.py:375,386).  Per class:
+
+    TRF [KT][QT][32][2]        (B[q][k], G_n[q][k])        traces
+    PRF [QT][2][NNT][32][2]    (B[q][pi(n)], G_n[q][pi(n)]) projection
+
+    Returns (flat tables, per-class stride, int32 [nif][2] class of the
+    inside / outside side) or None when the mesh has more than
+    ``max_classes`` classes (the kernel then folds per face)."""
+    d, nb, F = t.dim, t.nb, t.nq_face
+    nif = len(t.if_code)
+    if d != 3 or nif == 0 or (t.if_code & CODE_MIRROR).any():
+        return None
+    code = t.if_code.astype(np.int64)
+    tid = np.concatenate([code & 31, (code >> 5) & 31])
+    jn = np.concatenate([t.if_geo[:, 0:3], t.if_geo[:, 3:6]])
+    key = np.concatenate([tid[:, None], jn.view(np.int64)], axis=1)
+    uniq, inv = np.unique(key, axis=0, return_inverse=True)
+    if len(uniq) > max_classes:
+        return None
+    QP, NBK, NBN = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
+    pic, ok = _pi_cols(nb)
+    parts = []
+    for row in uniq:
+        k = int(row[0])
+        jv = row[1:].copy().view(np.float64)
+        B, G = t.face_B[k], t.face_G[k]                     # (F, nb), (F, nb, d)
+        Gn = np.einsum("qia,a->qi", G, jv)
+        BT = np.zeros((NBK, QP)); BT[:nb, :F] = B.T
+        GT = np.zeros((NBK, QP)); GT[:nb, :F] = Gn.T
+        BP = np.zeros((QP, NBN)); BP[:F] = B[:, pic] * ok
+        GP = np.zeros((QP, NBN)); GP[:F] = Gn[:, pic] * ok
+        TRF = np.stack([_frag_kq(BT), _frag_kq(GT)], axis=-1)
+        PRF = np.stack([_frag_qn(BP), _frag_qn(GP)], axis=-1)
+        parts.append(np.concatenate([TRF.ravel(), PRF.ravel()]))
+    cls = np.ascontiguousarray(np.stack([inv[:nif], inv[nif:]], axis=1), dtype=np.int32)
+    return np.ascontiguousarray(np.concatenate(parts)), len(parts[0]), cls
 
 
 def tc_face_blocks(t: OperatorTables, block: int = 8):

@@ -795,3 +795,22 @@ def test_strong_scaling_c5_replica_four_ranks_match_global():
         covered[gids] += 1
         assert np.abs(Ur - ref[gids]).max() <= 1e-13 * np.abs(ref).max()
     assert np.all(covered == 1)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_face_geometry_class_tables_match_per_face_folds(order):
+    """The species-rows face kernel with precomputed per-class
+    normal-derivative fragments (tables.tc_face_fold_tables: the Kuhn cube
+    has 6 (table, Jinv n) classes per side) == the same kernel folding
+    Jinv n per face, and both == the oracle (reference operator.py:375-424)."""
+    space = DGSpace(unit_cube(4, 3, 2), order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme("cdg2"))
+    assert 0 < op.n_face_classes <= 64          # non-cubic cells: more classes
+    U = initial_state(space, 23)
+    a = op.apply_f(U)
+    op.set_variant(no_fold=True)
+    b = op.apply_f(U)
+    assert rel_l2_per_species(space, a, b).max() <= 1e-13
+    ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
+    assert rel_l2_per_species(space, a, ref).max() <= 1e-12
