@@ -286,14 +286,14 @@ int volume(tdg_ctx* ctx, int64_t e0, int64_t e1, const double* U, const double* 
       static int resident = 0;
       if (resident == 0) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_volume_tc<D, K, M>, 128,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_volume_tc<D, K, M>, 32 * T::WARPS,
                                                           T::smem()) != cudaSuccess || nb < 1)
           nb = T::MINB;
         resident = nb;
       }
       const int64_t cap = int64_t(ctx->num_sms) * resident;
       grid = grid < cap ? grid : cap;
-      k_volume_tc<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(p, p.vtc, U, acc, U0, out, a, b,
+      k_volume_tc<D, K, M><<<unsigned(grid), 32 * T::WARPS, T::smem(), st>>>(p, p.vtc, U, acc, U0, out, a, b,
                                                                    c, mode);
     }
   } else {

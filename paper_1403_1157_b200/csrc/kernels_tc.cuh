@@ -36,6 +36,16 @@
 
 namespace tdg {
 
+// species whose values or gradients the volume point physics reads
+template <class M>
+__host__ __device__ constexpr bool quad_species(int s) {
+  for (int k = 0; k < M::NVAL; ++k)
+    if (M::val_sp(k) == s) return true;
+  for (int k = 0; k < M::NGRAD; ++k)
+    if (M::grad_sp(k) == s) return true;
+  return false;
+}
+
 template <int D, int K, class M>
 struct TcVol {
   using Dm = Dims<D, K>;
@@ -53,15 +63,20 @@ struct TcVol {
   static constexpr int OPG = OPP + QP * NBN;             // [D][QP][NBN]
   static constexpr int OKS = OPG + D * QP * NBN;         // [NSYM][NBK][NBN]
   static constexpr int TAB = OKS + NSYM * NBK * NBN;
-  static constexpr int WARPS = 4, EW = 8;
-  static constexpr bool kSmemTables = TAB * 8 <= 64 * 1024;
+  // tables up to 64 KB: 4-warp CTAs, 2 per SM; larger (3D p = 3: 203 KB)
+  // still in shared memory, with one 8-warp CTA per SM (the same 8 warps /
+  // SM the 255-register budget allows), instead of streaming them through
+  // L1 (ncu at p = 3 from global: L1 hit 76 %)
+  static constexpr bool kBig = TAB * 8 > 64 * 1024;
+  static constexpr bool kSmemTables = TAB * 8 <= 220 * 1024;
+  static constexpr int WARPS = kBig ? 12 : 4, EW = 8;
   static constexpr size_t smem() { return kSmemTables ? size_t(TAB) * 8 : 0; }
-  static constexpr int MINB = 2;
+  static constexpr int MINB = kBig ? 1 : 2;
   static constexpr bool ok = S <= kMaxS && D >= 2;
 };
 
 template <int D, int K, class M>
-__global__ void __launch_bounds__(128, TcVol<D, K, M>::MINB)
+__global__ void __launch_bounds__(32 * TcVol<D, K, M>::WARPS, TcVol<D, K, M>::MINB)
 k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
             const double* ACC, const double* U0, double* out, double ca, double cb,
             double cc, int mode) {
@@ -72,7 +87,7 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
   extern __shared__ __align__(16) double sm[];
   const double* tb = tabs;
   if constexpr (T::kSmemTables) {
-    for (int i = threadIdx.x; i < T::TAB; i += 128) sm[i] = __ldg(tabs + i);
+    for (int i = threadIdx.x; i < T::TAB; i += 32 * T::WARPS) sm[i] = __ldg(tabs + i);
     __syncthreads();
     tb = sm;
   }
@@ -91,14 +106,16 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
     double ge[NEG];
 #pragma unroll
     for (int k = 0; k < NEG; ++k) ge[k] = __ldg(p.egeo + ec * NEG + k);
-    // A fragments: every species, every k-step (basis 4 kt + t)
+    // A fragments (basis 4 kt + t): the quadrature species now, the others
+    // only for the epilogue (shorter register live ranges)
     double cf[S][KT];
     const double* urow = U + ec * SN;
 #pragma unroll
     for (int s = 0; s < S; ++s)
+      if (quad_species<M>(s))
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt)
-        cf[s][kt] = (4 * kt + t < NB) ? __ldg(urow + s * NB + 4 * kt + t) : 0.0;
+        for (int kt = 0; kt < KT; ++kt)
+          cf[s][kt] = (4 * kt + t < NB) ? __ldg(urow + s * NB + 4 * kt + t) : 0.0;
 
     double af[NF > 0 ? NF : 1][NNT][2], al[NL > 0 ? NL : 1][NNT][2];
 #pragma unroll
@@ -188,6 +205,12 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
     const double idet = 1.0 / detJ;
     const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
 #pragma unroll
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (!quad_species<M>(s))
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+          cf[s][kt] = (4 * kt + t < NB) ? __ldg(urow + s * NB + 4 * kt + t) : 0.0;
     for (int s = 0; s < S; ++s) {
       double dif[NNT][2];
 #pragma unroll

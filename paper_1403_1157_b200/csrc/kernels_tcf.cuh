@@ -87,7 +87,11 @@ struct TcsFace {
   using TF = TcFace<D, K, M>;
   static constexpr int NB = TF::NB, S = M::S, SN = S * NB, F = TF::F, NFG = TF::NFG;
   static constexpr int QP = TF::QP, QT = TF::QT, KT = TF::KT, NNT = TF::NNT, TS = TF::TS;
-  static constexpr int NCV = TF::NCV, XS = S | 1;
+  // species transpose row stride: lane (g, t) of a pass-1 store hits
+  // double q XS + g with q = 8 qt + 2 t + j; XS = 6 maps each half-warp's
+  // 16 (g, t) onto 16 distinct banks (S | 1 = 7 was 3-way conflicted;
+  // measured time-neutral, less shared memory)
+  static constexpr int NCV = TF::NCV, XS = S == 6 ? 6 : (S | 1);
   // the last mode tile holds at most 4 modes (nb = 10: 2, nb = 20: 4),
   // all in its even columns: both sides' projections share one DMMA pair
   static constexpr bool MERGE = NNT >= 2 && NB - 8 * (NNT - 1) <= 4;
@@ -250,13 +254,22 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
       for (int qt = 0; qt < QT; ++qt) {
         double rho[2] = {0.0, 0.0};
         if (lift) {
+          // two independent accumulator chains (even / odd k-steps): the
+          // flux of this point tile waits on rho, so halve its DMMA chain
+          // (64^3 p = 3: faces 29.7 -> 28.5 ms; splitting pass 1's four
+          // trace chains the same way measured 28.8, and issuing the next
+          // tile's rho ahead of this tile's projection 29.3: 20 B spills)
+          double rb[2] = {0.0, 0.0};
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
             const int ob = (kt * QT + qt) * 32 + lane;
+            double* r = (kt & 1) ? rb : rho;
             // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
-            dmma(rho[0], rho[1], mi[kt / 2][kt % 2], __ldg(Tl + TF::OBT + ob));
-            if (br2) dmma(rho[0], rho[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
+            dmma(r[0], r[1], mi[kt / 2][kt % 2], __ldg(Tl + TF::OBT + ob));
+            if (br2) dmma(r[0], r[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
           }
+          rho[0] += rb[0];
+          rho[1] += rb[1];
         }
         double Y[2], X[2];
 #pragma unroll

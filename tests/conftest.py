@@ -19,4 +19,4 @@ def golden():
     here = os.path.join(ROOT, "tests", "golden")
     return {name: np.load(os.path.join(here, f"{name}.npz"))
             for name in ("tables", "meshes", "operator", "heat",
-                         "trajectories", "trajectories_stated")}
+                         "trajectories", "trajectories_stated", "diagnostics")}

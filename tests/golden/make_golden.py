@@ -363,9 +363,31 @@ def trajectories_stated():
     np.savez_compressed(os.path.join(HERE, "trajectories_stated.npz"), **out)
 
 
+def diagnostics():
+    """Reference output formats for the device diagnostics: a VTK snapshot
+    (vtkio.write_vtk) and species totals (DiscreteFunction.species_totals)
+    of seeded states on a 2D and a 3D mesh."""
+    import tempfile
+    from taxisdg.vtkio import write_vtk
+    out = {}
+    for key, mesh, k in (("sq3", unit_square(3), 2), ("cube1", unit_cube(1), 1)):
+        d = mesh.dim
+        space = DGSpace(mesh, k, n_species=6)
+        U = space.project(bump_field(d, 6, 13, np.zeros(d), np.ones(d))).coeffs
+        fn = space.function(U)
+        with tempfile.TemporaryDirectory() as tmp:
+            path = write_vtk(os.path.join(tmp, "s.vtk"), fn,
+                             names=["n1", "n2", "n3", "c1", "c2", "c3"])
+            text = open(path).read()
+        out[f"{key}__U"] = U
+        out[f"{key}__vtk"] = np.array(text)
+        out[f"{key}__totals"] = fn.species_totals()
+    np.savez_compressed(os.path.join(HERE, "diagnostics.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tables", "meshes", "operators", "heat_cases", "trajectories",
-                             "trajectories_stated"]
+                             "trajectories_stated", "diagnostics"]
     for fn in (globals()[w] for w in which):
         tic = time.perf_counter()
         fn()
