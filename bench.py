@@ -157,7 +157,10 @@ def scaled_config(cfg, world, scaling, cells=None):
     (domain N times as long in x, same cell size)."""
     import dataclasses
     if cells:
-        cfg = dataclasses.replace(cfg, cells=tuple(cells))
+        cfg = dataclasses.replace(
+            cfg, cells=tuple(cells),
+            description=cfg.description + " -- TEST OVERRIDE: " + "x".join(map(str, cells))
+            + " cells (same cell aspect, order, physics)")
     if world == 1 or scaling == "strong":
         return cfg
     cells = (cfg.cells[0] * world,) + tuple(cfg.cells[1:])
@@ -469,8 +472,26 @@ def run_native_arm(args, rank, world, local):
         if dist_on:
             torch.distributed.barrier()
 
+    # full-size property check (size-independent): the lipid
+    # budget c2 + c3 changes only through the GAMMA1_IN influx, at exactly
+    # nu2 sigma |GAMMA1_IN| per unit time (oxidation moves c2 to c3; the
+    # face terms conserve; reference tests/test_operator.py:101-110)
+    def lipid_total(V):
+        tot = op.species_totals(V)
+        if dist_on:
+            torch.distributed.all_reduce(tot)
+        return float(tot[4] + tot[5])
+    gamma1_in = float(op.tables.bf_geo[((op.tables.bf_code >> 11) & 7) == 2].sum()) * \
+        (1.0 if cfg.dim == 2 else 0.5)
+    if dist_on:
+        gi = torch.tensor([gamma1_in], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(gi)
+        gamma1_in = float(gi)
+    lipid0, steps_taken = lipid_total(U), 0
+
     for _ in range(args.warmup):
         stepper.step(U, dt)
+    steps_taken += args.warmup
     torch.cuda.synchronize()
     log("warm-up done")
 
@@ -512,6 +533,17 @@ def run_native_arm(args, rank, world, local):
     torch.cuda.synchronize()
     op.profile(False)
     kt = op.profile_read()
+    steps_taken += args.steps + nprof
+    lipid1 = lipid_total(U)
+    p = model.params
+    expect = steps_taken * dt * p.nu2 * p.sigma * gamma1_in
+    checks = {"lipid_budget_change": lipid1 - lipid0, "expected": expect,
+              "rel_err": abs(lipid1 - lipid0 - expect) / abs(expect) if expect else None,
+              "steps": steps_taken, "finite": bool(torch.isfinite(U[:op.n_owned]).all()),
+              "what": "full-size size-independent check: the c2 + c3 total after the run's "
+                      "SSP-RK3 steps changed by steps * dt * nu2 * sigma * |GAMMA1_IN| "
+                      "(reference tests/test_operator.py:101-110), device totals"}
+    log(f"lipid budget check: rel err {checks['rel_err']}")
     ms_prof = sum(a.elapsed_time(b) for a, b in pevs)
     total_dofs = n_dofs
     if dist_on:  # whole-job DoFs (owned rows of every rank)
@@ -704,6 +736,7 @@ def run_native_arm(args, rank, world, local):
                              "events)",
                        "parallelism": par},
             "roofline": roof, "clocks": clocks, "gpu_launches": launches,
+            "full_size_checks": checks,
             **({"implicit": implicit} if implicit else {}),
         }
         if cpu:

@@ -103,7 +103,7 @@ struct TcsFace {
   // face-geometry-class tables it fits 128 without spills (64^3 p = 3:
   // 38.4 ms at 3 CTAs without classes -> 31.6 with -> 30.0 at 4 CTAs)
   static constexpr int MINB = K >= 3 ? 3 : 4;
-  static constexpr int MINB_FOLD = 4;
+  static constexpr int MINB_FOLD = 4;  // p = 2 at 5 CTAs (96 registers, spills): no gain
   static constexpr bool ok = D == 3 && S <= 8 && !M::kMirror && TF::ok && smem() <= 96 * 1024;
 };
 
