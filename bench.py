@@ -67,7 +67,10 @@ def parse():
     ap.add_argument("--power-iters", type=int, default=200)
     ap.add_argument("--integrator", default="ssprk3", choices=["ssprk3", "sdirk3"],
                     help="sdirk3: the reference's default SDIRK3 + JFNK at --dt")
-    ap.add_argument("--dt", type=float, default=0.01)
+    ap.add_argument("--dt", type=float, default=None,
+                    help="implicit step (default: the reference's 0.01; C3: the stiffness "
+                         "ratio dt a_ii rho = 500, SURVEY 8(d) -- at 0.01 the reference's "
+                         "own GMRES(30) stalls)")
     ap.add_argument("--force-slab", action="store_true",
                     help="use the slab/halo code path even at N=1 (testing)")
     ap.add_argument("--variant", type=int, default=0,
@@ -404,13 +407,26 @@ def log(msg):
 
 
 def _init_dist(args, world, dev):
+    """One process per GPU; NCCL over NVLink for the ghost-row exchange and
+    the Krylov all-reduces.  Logs one line per rank (rank, world, device,
+    backend, NCCL version) so a failing rank is identifiable."""
     import torch
     if world > 1 or "RANK" in os.environ:
         import torch.distributed as dist
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:  # testing only: host-staged exchange, several ranks per GPU
-            dist.init_process_group("gloo")
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        try:
+            if args.dist_backend == "nccl":
+                dist.init_process_group("nccl", device_id=dev)
+            else:  # testing only: host-staged exchange, several ranks per GPU
+                dist.init_process_group("gloo")
+        except Exception as err:  # noqa: BLE001 -- re-raised with the rank attached
+            raise RuntimeError(f"rank {os.environ.get('RANK')}/{world} on {dev}: "
+                               f"{args.dist_backend} process-group init failed: {err}") from err
+        nccl = ".".join(map(str, torch.cuda.nccl.version())) if args.dist_backend == "nccl" \
+            else "-"
+        log(f"rank {dist.get_rank()}/{dist.get_world_size()} on {dev} "
+            f"({torch.cuda.get_device_name(dev)}), backend {dist.get_backend()}, nccl {nccl}, "
+            f"master {os.environ.get('MASTER_ADDR')}:{os.environ.get('MASTER_PORT')}")
     return torch.distributed.is_available() and torch.distributed.is_initialized()
 
 
@@ -682,11 +698,12 @@ def run_native_arm(args, rank, world, local):
         nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
               "gmres_restart": 30, "gmres_maxiter": 200}
         Ui = U.clone()
-        integrate(op, Ui, 0.0, 1.0, 0.01, order=3, n_steps=1, newton_kwargs=nk)  # warm-up
+        args.dt = 0.01 if args.dt is None else args.dt
+        integrate(op, Ui, 0.0, 1.0, args.dt, order=3, n_steps=1, newton_kwargs=nk)  # warm-up
         torch.cuda.synchronize()
         ia, ib = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ia.record()
-        res = integrate(op, Ui, 0.0, 1.0, 0.01, order=3, n_steps=1, newton_kwargs=nk)
+        res = integrate(op, Ui, 0.0, 1.0, args.dt, order=3, n_steps=1, newton_kwargs=nk)
         ib.record()
         ib.synchronize()
         ims = ia.elapsed_time(ib)
@@ -776,6 +793,13 @@ def run_implicit(args, rank, world, local):
         torch.distributed.barrier()
     nk = {"rtol": 1e-8, "atol": 1e-12, "maxiter": 25, "gmres_rtol": 1e-4,
           "gmres_restart": 30, "gmres_maxiter": 200}
+    if args.dt is None:
+        if args.config == "c3":
+            from paper_1403_1157_b200.configs import rho_constant
+            h = float(space.mesh.diameters.min())
+            args.dt = 500.0 / (0.4358665215 * rho_constant(cfg.dim, cfg.order) * 1e-2 / h ** 2)
+        else:
+            args.dt = 0.01
     integrate(op, U, 0.0, 1.0, args.dt, order=3, n_steps=max(1, args.warmup),
               newton_kwargs=nk, halo=halo)
     torch.cuda.synchronize()

@@ -149,11 +149,21 @@ class HaloExchange:
             self._bufs.append(buf)
             ops.append(dist.P2POp(dist.isend, buf, nb))
             ops.append(dist.P2POp(dist.irecv, rv, nb))
-        self._works = dist.batch_isend_irecv(ops) if ops else []
+        try:
+            self._works = dist.batch_isend_irecv(ops) if ops else []
+        except Exception as err:  # noqa: BLE001 -- re-raised with the slab attached
+            raise RuntimeError(f"ghost exchange post failed on rank {s.rank}/{s.nranks} "
+                               f"(neighbours {s.rank - 1}, {s.rank + 1}, backend "
+                               f"{dist.get_backend()}): {err}") from err
 
     def wait(self):
         for w in self._works:
-            w.wait()
+            try:
+                w.wait()
+            except Exception as err:  # noqa: BLE001 -- re-raised with the slab attached
+                s = self.slab
+                raise RuntimeError(f"ghost exchange failed on rank {s.rank}/{s.nranks}: "
+                                   f"{err}") from err
         for dev_rows, host_rows in self._recv:
             dev_rows.copy_(host_rows)
         self._works = []
