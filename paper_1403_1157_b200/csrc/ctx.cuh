@@ -108,13 +108,12 @@ int configure(int nqv) {
                            int(WallTile<D, K, M>::smem()));
   if (e != cudaSuccess) return cuda_fail(e, "configure wall");
   if constexpr (TcsFace<D, K, M>::ok) {
-    e = cudaFuncSetAttribute(k_faces_tcs<D, K, M, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TcsFace<D, K, M>::smem()));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_faces_tcs<D, K, M, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(TcsFace<D, K, M>::smem()));
+    const int sm = int(TcsFace<D, K, M>::smem());
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    for (auto fn : {k_faces_tcs<D, K, M, false, 0>, k_faces_tcs<D, K, M, false, 1>,
+                    k_faces_tcs<D, K, M, false, 2>, k_faces_tcs<D, K, M, true, 0>,
+                    k_faces_tcs<D, K, M, true, 1>, k_faces_tcs<D, K, M, true, 2>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcs");
   }
   if constexpr (TcVol<D, K, M>::ok) {
@@ -188,12 +187,17 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
         int64_t grid = (sg.b1 - sg.b0 + T::WARPS - 1) / T::WARPS;
         const int64_t cap = int64_t(ctx->num_sms) * T::MINB_FOLD * 8;
         grid = grid < cap ? grid : cap;
-        if (p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold)
-          k_faces_tcs<D, K, M, true><<<unsigned(grid), 128, T::smem(), st>>>(
-              p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
+        const bool fold = p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold;
+        const int lm = (p.scheme == IP || p.scheme == BO) ? 0 : (p.scheme == BR2 ? 2 : 1);
+        auto go = [&](auto kernel) {
+          kernel<<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
+        };
+        if (fold)
+          go(lm == 0 ? k_faces_tcs<D, K, M, true, 0>
+                     : (lm == 1 ? k_faces_tcs<D, K, M, true, 1> : k_faces_tcs<D, K, M, true, 2>));
         else
-          k_faces_tcs<D, K, M, false><<<unsigned(grid), 128, T::smem(), st>>>(
-              p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
+          go(lm == 0 ? k_faces_tcs<D, K, M, false, 0>
+                     : (lm == 1 ? k_faces_tcs<D, K, M, false, 1> : k_faces_tcs<D, K, M, false, 2>));
       }
       if (q.nbf > 0) {
         KernelTimer kt(ctx, 1, st);

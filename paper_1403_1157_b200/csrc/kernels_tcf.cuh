@@ -110,7 +110,11 @@ struct TcsFace {
 // FOLD: the normal-derivative fragments come precomputed per face-geometry
 // class (meshes with few distinct (table, Jinv n) pairs, e.g. the Kuhn
 // cubes: 6 per side); otherwise they are folded per face from jn
-template <int D, int K, class M, bool FOLD>
+// LM: lifting sides of the scheme (operator.py:336-357), a compile-time
+// constant so no DMMA chain is issued predicated-off (they still occupy the
+// tensor pipe: 64^3 p = 3 faces 28.5 -> 26.6 ms for the first of them):
+// 0 none (ip, bo), 1 the K- side (cdg2, cdg), 2 both (br2)
+template <int D, int K, class M, bool FOLD, int LM>
 __global__ void __launch_bounds__(128, FOLD ? TcsFace<D, K, M>::MINB_FOLD : TcsFace<D, K, M>::MINB)
 k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restrict__ blocks,
             int64_t blk0, int64_t blk1, const double* __restrict__ U, double* __restrict__ ACC) {
@@ -163,8 +167,8 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
         ci[kt] = in ? __ldg(U + int64_t(el.x) * SN + g * NB + 4 * kt + t) : 0.0;
         co[kt] = in ? __ldg(U + int64_t(el.y) * SN + g * NB + 4 * kt + t) : 0.0;
       }
-      const bool br2 = p.scheme == BR2;
-      const bool lift = p.scheme != IP && p.scheme != BO;
+      constexpr bool br2 = LM == 2;
+      constexpr bool lift = LM > 0;
       // lifting side(s) (operator.py:336-357): K- only (cdg2 / cdg), both
       // for br2; mi runs on table Tl (K- side, or the inside for br2), mo
       // on the outside for br2 only -- no predicated-off DMMA chains
@@ -211,14 +215,22 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
             xs[(2 * QP + q) * XS + g] = 0.5 * (di[j] + dq[j]);
           }
         }
-        if (lift) {
+        if constexpr (lift) {
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
             for (int nt = 0; nt < NNT; ++nt) {
               const int ow = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
               dmma(mi[nt][0], mi[nt][1], du[ks], __ldg(Tl + TF::OWB + ow));
-              if (br2) dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + TF::OWB + ow));
+            }
+        }
+        if constexpr (br2) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < NNT; ++nt) {
+              const int ow = ((qt * 2 + ks) * NNT + nt) * 32 + lane;
+              dmma(mo[nt][0], mo[nt][1], du[ks], __ldg(To + TF::OWB + ow));
             }
         }
       }
@@ -253,7 +265,7 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
 #pragma unroll 1
       for (int qt = 0; qt < QT; ++qt) {
         double rho[2] = {0.0, 0.0};
-        if (lift) {
+        if constexpr (lift) {
           // two independent accumulator chains (even / odd k-steps): the
           // flux of this point tile waits on rho, so halve its DMMA chain
           // (64^3 p = 3: faces 29.7 -> 28.5 ms; splitting pass 1's four
@@ -266,7 +278,14 @@ k_faces_tcs(OpParams p, const double* __restrict__ tabs, const int32_t* __restri
             double* r = (kt & 1) ? rb : rho;
             // m as A operand: k-step kt holds basis 4 kt + t = pi(8 (kt/2) + 2t + kt%2)
             dmma(r[0], r[1], mi[kt / 2][kt % 2], __ldg(Tl + TF::OBT + ob));
-            if (br2) dmma(r[0], r[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
+          }
+          if constexpr (br2) {
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+              const int ob = (kt * QT + qt) * 32 + lane;
+              double* r = (kt & 1) ? rb : rho;
+              dmma(r[0], r[1], mo[kt / 2][kt % 2], __ldg(To + TF::OBT + ob));
+            }
           }
           rho[0] += rb[0];
           rho[1] += rb[1];
