@@ -205,13 +205,29 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
     const double idet = 1.0 / detJ;
     const double scale = mode == 0 ? 1.0 : (mode == 1 ? idet : cc * idet);
 #pragma unroll
-#pragma unroll
     for (int s = 0; s < S; ++s)
       if (!quad_species<M>(s))
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt)
           cf[s][kt] = (4 * kt + t < NB) ? __ldg(urow + s * NB + 4 * kt + t) : 0.0;
+    // species loop unrolled where the registers allow (coefficients stay in
+    // registers instead of a dynamically indexed local array; 3D p = 3
+    // would spill 1.4 KB)
+    constexpr int SUNR = T::kBig ? 1 : S;
+#pragma unroll SUNR
     for (int s = 0; s < S; ++s) {
+      // this species' face sums and U0 entries, loaded ahead of the
+      // diffusion GEMM so their latency hides behind it
+      double facc[NNT][2], fu0[NNT][2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 4 * (2 * nt + j) + t;
+          const int64_t off = ec * SN + s * NB + (i < NB ? i : 0);
+          facc[nt][j] = ACC != nullptr ? __ldcs(ACC + off) : 0.0;
+          fu0[nt][j] = (mode == 2 && ca != 0.0) ? U0[off] : 0.0;
+        }
       double dif[NNT][2];
 #pragma unroll
       for (int nt = 0; nt < NNT; ++nt) dif[nt][0] = dif[nt][1] = 0.0;
@@ -246,11 +262,11 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
             if (li == k) acc += al[k][nt][j];
           double rv = detJ * (acc - As * dif[nt][j] + lin);
           const int64_t off = ec * SN + s * NB + i;
-          if (ACC != nullptr) rv += __ldcs(ACC + off);
+          rv += facc[nt][j];
           double o = scale * rv;
           if (mode == 2) {
             o = fma(cb, cf[s][kt], o);
-            if (ca != 0.0) o = fma(ca, U0[off], o);
+            if (ca != 0.0) o = fma(ca, fu0[nt][j], o);
           }
           if (valid) out[off] = o;
         }

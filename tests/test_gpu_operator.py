@@ -187,15 +187,18 @@ def test_bitwise_reproducible():
     assert len(audit["faces_per_part"]) == 3          # d+1 colour segments
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
 def test_full_size_single_application_vs_oracle(cfg):
     """Spot check of one apply_f at the BASELINE config sizes (C2, C3 at a
-    quarter of its cells, C4 at 1/8) against the CPU oracle."""
+    quarter of its cells, C4 at 1/8, C5 at its cell size and tags on a
+    16x16x16-cell box) against the CPU oracle."""
     if cfg == "c2":
         space = DGSpace(unit_square(512, 128, lengths=(4.0, 1.0)), 2, 6)
     elif cfg == "c3":
         space = DGSpace(unit_square(1024, 256, lengths=(4.0, 1.0), jitter=0.1,
                                     seed=7), 3, 6)
+    elif cfg == "c5":
+        space = DGSpace(unit_cube(16, lengths=(16 / 128, 16 / 128, 16 / 128)), 3, 6)
     else:
         space = DGSpace(unit_cube(32, gamma1_in=None, top_tag=BoundaryTag.NO_FLOW), 2, 6)
     model = PlaqueModel()
