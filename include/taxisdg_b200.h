@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 3
+#define TDG_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -149,9 +149,17 @@ typedef struct tdg_desc {
    * Jinv n per face */
   const double* face_tc_fold;
   const int32_t* if_fold;
+  /* optional, with the class tables: groups of 8/gcd(S,8) interior faces
+   * of one segment sharing both sides' class and the lifting side
+   * (tables.tc_face_groups), int32 [n_face_groups][8/gcd(S,8)] face ids,
+   * -1 past a run's end (they cover every interior face of the segments).
+   * NULL: the one-face species-rows kernel runs the blocks instead */
+  const int32_t* face_groups;
+  int64_t n_face_groups;
   /* face colour segments, run in order: segment s covers the interior
-   * faces [I[s], I[s+1]), the walls [W[s], W[s+1]) and the face blocks
-   * [B[s], B[s+1]) with seg_ptr (HOST) = I[n+1] | W[n+1] | B[n+1].  No
+   * faces [I[s], I[s+1]), the walls [W[s], W[s+1]), the face blocks
+   * [B[s], B[s+1]) and the face groups [G[s], G[s+1]) with seg_ptr (HOST)
+   * = I[n+1] | W[n+1] | B[n+1] | G[n+1].  No
    * element is written twice within a segment, and each element's first
    * written face side (in segment order) carries TDG_CODE_FIRST_IN/OUT and
    * every owned element has at least one face.  The last n_segments_cut
@@ -279,7 +287,8 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
 /* Kernel variant selection (testing / A-B timing).  bit 0: pin the
  * CTA-staged generic kernels; bit 5: launch tdg_ssprk3_step's kernels
  * directly instead of replaying its cached CUDA graph; bit 13: ignore the
- * face-geometry-class tables (fold Jinv n per face); bit 12: use the
+ * face-geometry-class tables (fold Jinv n per face); bit 14: run the
+ * one-face species-rows kernel instead of the face-group kernel; bit 12: use the
  * transposed tensor-core volume kernel wherever it compiles (default only
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
  * per SM of the 2D register-resident face kernel's grid-stride grid (0 =

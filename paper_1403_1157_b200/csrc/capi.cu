@@ -49,7 +49,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   if (d.n_species < 1 || d.n_species > kMaxS) return fail(TDG_E_INVALID, "n_species out of range");
   if (d.scheme < TDG_CDG2 || d.scheme > TDG_BO) return fail(TDG_E_INVALID, "unknown scheme");
   if (d.n_elements < 0 || d.n_ghost < 0 || d.n_int_faces < 0 || d.n_bnd_faces < 0 ||
-      d.n_face_blocks < 0)
+      d.n_face_blocks < 0 || d.n_face_groups < 0)
     return fail(TDG_E_INVALID, "negative size");
   if (d.n_elements + d.n_ghost > (int64_t(1) << 31) - 1)
     return fail(TDG_E_INVALID, "element rows must fit int32");
@@ -75,14 +75,15 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   std::vector<Segment> seg(size_t(d.n_segments));
   if (d.n_segments > 0) {
     const int64_t n1 = d.n_segments + 1;
-    const int64_t *I = d.seg_ptr, *W = I + n1, *B = W + n1;
+    const int64_t *I = d.seg_ptr, *W = I + n1, *B = W + n1, *G = B + n1;
     const bool ends = I[0] == 0 && I[n1 - 1] == d.n_int_faces && W[0] == 0 &&
                       W[n1 - 1] == d.n_bnd_faces && B[0] == 0 &&
-                      B[n1 - 1] == (d.face_blocks ? d.n_face_blocks : 0);
+                      B[n1 - 1] == (d.face_blocks ? d.n_face_blocks : 0) && G[0] == 0 &&
+                      G[n1 - 1] == (d.face_groups ? d.n_face_groups : 0);
     bool mono = true;
     for (int s = 0; s < d.n_segments; ++s) {
-      mono = mono && I[s] <= I[s + 1] && W[s] <= W[s + 1] && B[s] <= B[s + 1];
-      seg[s] = Segment{I[s], I[s + 1], W[s], W[s + 1], B[s], B[s + 1]};
+      mono = mono && I[s] <= I[s + 1] && W[s] <= W[s + 1] && B[s] <= B[s + 1] && G[s] <= G[s + 1];
+      seg[s] = Segment{I[s], I[s + 1], W[s], W[s + 1], B[s], B[s + 1], G[s], G[s + 1]};
     }
     if (!ends || !mono) return fail(TDG_E_INVALID, "inconsistent face segment offsets");
     for (int s = d.n_segments - d.n_segments_cut; s < d.n_segments; ++s)
@@ -135,6 +136,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.fblk = d.face_blocks;
   p.ftf = d.face_tc_fold;
   p.ffold = d.if_fold;
+  p.fgrp = d.face_groups;
 
   {
     int dev = 0, sms = 0;
@@ -467,6 +469,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->use_graph = ((variant >> 5) & 1) == 0;  // bit 5: no CUDA graph for ssprk3
   ctx->force_tc = ((variant >> 12) & 1) != 0;
   ctx->no_fold = ((variant >> 13) & 1) != 0;    // bit 13: no face-geometry-class tables
+  ctx->no_groups = ((variant >> 14) & 1) != 0;  // bit 14: one-face kernel despite face groups
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;

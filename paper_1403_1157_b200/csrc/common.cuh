@@ -65,6 +65,7 @@ struct OpParams {
   const int32_t* __restrict__ fblk; // interior-face blocks [n][2] (first, count)
   const double* __restrict__ ftf;   // face-geometry-class folded tables (may be null)
   const int32_t* __restrict__ ffold;  // [nif][2] class of the inside / outside side
+  const int32_t* __restrict__ fgrp;   // face groups [n][NFQ] (may be null)
 };
 
 // code-word layout, mirrors include/taxisdg_b200.h

@@ -24,6 +24,7 @@
 #include "kernels_mma.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_tcf.cuh"
+#include "kernels_tcg.cuh"
 #include "models.cuh"
 #include "vecops.cuh"
 
@@ -50,9 +51,10 @@ bool pick_reduced(int dim, int order, Impl* out);
 bool pick_diffusion(int dim, int order, Impl* out);
 
 // one colour class: interior faces [f0, f1), walls [w0, w1), face blocks
-// of the 3D tensor-core kernel [b0, b1)
+// of the 3D species-rows kernel [b0, b1), face groups of the 3D face-group
+// kernel [g0, g1)
 struct Segment {
-  int64_t f0, f1, w0, w1, b0, b1;
+  int64_t f0, f1, w0, w1, b0, b1, g0, g1;
 };
 
 }  // namespace tdg
@@ -72,6 +74,7 @@ struct tdg_ctx {
   bool force_generic = false;  // testing: pin the CTA-staged kernels
   bool force_tc = false;       // testing: tensor-core volume kernel where the SIMT one fits
   bool no_fold = false;        // testing: per-face normal-derivative folds despite class tables
+  bool no_groups = false;      // testing: the one-face kernel despite face groups
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
@@ -115,6 +118,13 @@ int configure(int nqv) {
                     k_faces_tcs<D, K, M, true, 1>, k_faces_tcs<D, K, M, true, 2>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcs");
+  }
+  if constexpr (TcgFace<D, K, M>::ok) {
+    const int sm = int(TcgFace<D, K, M>::smem());
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    for (auto fn : {k_faces_tcg<D, K, M, 0>, k_faces_tcg<D, K, M, 1>, k_faces_tcg<D, K, M, 2>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcg");
   }
   if constexpr (TcVol<D, K, M>::ok) {
     e = cudaFuncSetAttribute(k_volume_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -181,14 +191,32 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
   // one signature), walls on the element-local DMMA kernel
   if constexpr (TcsFace<D, K, M>::ok && MmaFace<D, K, M>::ok) {
     if (dflt && p.ftc != nullptr && p.fblk != nullptr && p.fmma != nullptr) {
-      if (sg.b1 > sg.b0) {
+      const bool fold = p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold;
+      const int lm = (p.scheme == IP || p.scheme == BO) ? 0 : (p.scheme == BR2 ? 2 : 1);
+      bool grouped = false;
+      if constexpr (TcgFace<D, K, M>::ok) {
+        grouped = fold && p.fgrp != nullptr && !ctx->no_groups;
+        if (grouped && sg.g1 > sg.g0) {
+          KernelTimer kt(ctx, 0, st);
+          using T = TcgFace<D, K, M>;
+          // persistent: the resident CTAs loop over the segment's groups
+          int64_t grid = sg.g1 - sg.g0;
+          const int64_t cap = int64_t(ctx->num_sms) * T::MINB;
+          grid = grid < cap ? grid : cap;
+          auto go = [&](auto kernel) {
+            kernel<<<unsigned(grid), T::THREADS, T::smem(), st>>>(p, p.ftc, p.fgrp, sg.g0, sg.g1, U,
+                                                                  acc);
+          };
+          go(lm == 0 ? k_faces_tcg<D, K, M, 0>
+                     : (lm == 1 ? k_faces_tcg<D, K, M, 1> : k_faces_tcg<D, K, M, 2>));
+        }
+      }
+      if (!grouped && sg.b1 > sg.b0) {
         KernelTimer kt(ctx, 0, st);
         using T = TcsFace<D, K, M>;
         int64_t grid = (sg.b1 - sg.b0 + T::WARPS - 1) / T::WARPS;
         const int64_t cap = int64_t(ctx->num_sms) * T::MINB_FOLD * 8;
         grid = grid < cap ? grid : cap;
-        const bool fold = p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold;
-        const int lm = (p.scheme == IP || p.scheme == BO) ? 0 : (p.scheme == BR2 ? 2 : 1);
         auto go = [&](auto kernel) {
           kernel<<<unsigned(grid), 128, T::smem(), st>>>(p, p.ftc, p.fblk, sg.b0, sg.b1, U, acc);
         };

@@ -34,7 +34,11 @@ struct TcFace {
   // face-geometry-class tables (tables.tc_face_fold_tables): per (table id,
   // Jinv n) class the B fragment paired with the folded normal-derivative
   // fragment sum_a jn_a G_a ([...][lane][B, G_n]: one 16-byte load per lane)
-  static constexpr int OTRF = 0, OPRF = OTRF + 2 * NBK * QP, TSF = OPRF + 2 * QP * NBN;
+  // plus the projection fragments split by kind ([...][lane]: one 8-byte
+  // load per lane) for the face-group kernel's merged tail tile, which
+  // needs one kind from the inside and the other from the outside lanes
+  static constexpr int OTRF = 0, OPRF = OTRF + 2 * NBK * QP, OPBF = OPRF + 2 * QP * NBN,
+                       OPGF = OPBF + QP * NBN, TSF = OPGF + QP * NBN;
   static constexpr int WARPS = 4;
   static constexpr int PWS = 8 * QP * NCV;  // per-warp point-physics slice
   static constexpr size_t smem() { return size_t(WARPS) * PWS * 8; }

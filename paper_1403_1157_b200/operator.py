@@ -95,7 +95,7 @@ class DiscreteOperator:
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
         from .tables import (mma_face_tables, tc_face_blocks, tc_face_fold_tables,
-                             tc_face_tables, tc_volume_tables)
+                             tc_face_groups, tc_face_tables, tc_volume_tables)
         mma, self._mma_stride = mma_face_tables(t)
         blocks, seg_blk = tc_face_blocks(t)
         fold = tc_face_fold_tables(t)
@@ -103,16 +103,19 @@ class DiscreteOperator:
         self._keep = {"face_mma": dev(mma), "vol_tc": dev(tc_volume_tables(t)),
                       "face_tc": dev(tc_face_tables(t)[0] if t.dim == 3 else np.zeros(4)),
                       "face_blocks": dev(blocks)}
+        groups, seg_grp = np.zeros((0, 1), np.int32), np.zeros(t.n_seg + 1, np.int64)
         if fold is not None:
             self._keep["face_tc_fold"] = dev(fold[0])
             self._keep["if_fold"] = dev(fold[2])
+            groups, seg_grp = tc_face_groups(t, fold[2], t.n_species)
+            self._keep["face_groups"] = dev(groups)
         self._keep.update({name: dev(getattr(t, name)) for name in (
             "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
             "face_Pw", "face_w", "elem_geo", "if_elems", "if_code",
             "if_geo", "bf_elem", "bf_code", "bf_geo")})
         self._host = {
             "seg_ptr": np.ascontiguousarray(np.concatenate(
-                [t.seg_if, t.seg_bf, seg_blk]), dtype=np.int64),
+                [t.seg_if, t.seg_bf, seg_blk, seg_grp]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
             "lin_source": _checked_linear_source(model),
             "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
@@ -142,6 +145,8 @@ class DiscreteOperator:
             face_blocks=ptr(k["face_blocks"]), n_face_blocks=len(blocks),
             face_tc_fold=ptr(k["face_tc_fold"]) if fold is not None else None,
             if_fold=ptr(k["if_fold"]) if fold is not None else None,
+            face_groups=ptr(k["face_groups"]) if fold is not None else None,
+            n_face_groups=len(groups),
             n_segments=t.n_seg, n_segments_cut=t.n_seg_cut,
             seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()
@@ -256,18 +261,20 @@ class DiscreteOperator:
 
     def set_variant(self, generic: bool = False, no_graph: bool = False,
                     tc_volume: bool = False, face_ctas_per_sm: int = 0,
-                    no_fold: bool = False):
+                    no_fold: bool = False, no_groups: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
         kernels directly instead of replaying its CUDA graph; ``tc_volume``
         the tensor-core volume kernel where the SIMT one fits;
         ``face_ctas_per_sm`` caps the grid of the 2D grid-stride face kernel
         (0 default, 15 uncapped); ``no_fold`` makes the 3D face kernel fold
-        Jinv n per face despite face-geometry-class tables.  Defaults:
-        fastest."""
+        Jinv n per face despite face-geometry-class tables; ``no_groups``
+        runs the one-face species-rows kernel instead of the face-group
+        kernel.  Defaults: fastest."""
         self._call(self.lib.tdg_set_variant, self._ctx,
                    int(bool(generic)) | (int(bool(no_graph)) << 5)
                    | (int(bool(tc_volume)) << 12) | (int(bool(no_fold)) << 13)
+                   | (int(bool(no_groups)) << 14)
                    | ((int(face_ctas_per_sm) & 15) << 8),
                    what="tdg_set_variant")
 

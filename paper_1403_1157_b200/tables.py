@@ -393,6 +393,8 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
 
     TRF [KT][QT][32][2]        (B[q][k], G_n[q][k])        traces
     PRF [QT][2][NNT][32][2]    (B[q][pi(n)], G_n[q][pi(n)]) projection
+    PBF [QT][2][NNT][32]       B[q][pi(n)]                  projection, by kind
+    PGF [QT][2][NNT][32]       G_n[q][pi(n)]                (face-group kernel)
 
     Returns (flat tables, per-class stride, int32 [nif][2] class of the
     inside / outside side) or None when the mesh has more than
@@ -422,7 +424,8 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
         GP = np.zeros((QP, NBN)); GP[:F] = Gn[:, pic] * ok
         TRF = np.stack([_frag_kq(BT), _frag_kq(GT)], axis=-1)
         PRF = np.stack([_frag_qn(BP), _frag_qn(GP)], axis=-1)
-        parts.append(np.concatenate([TRF.ravel(), PRF.ravel()]))
+        parts.append(np.concatenate([TRF.ravel(), PRF.ravel(), _frag_qn(BP).ravel(),
+                                     _frag_qn(GP).ravel()]))
     cls = np.ascontiguousarray(np.stack([inv[:nif], inv[nif:]], axis=1), dtype=np.int32)
     return np.ascontiguousarray(np.concatenate(parts)), len(parts[0]), cls
 
@@ -447,6 +450,40 @@ def tc_face_blocks(t: OperatorTables, block: int = 8):
     blocks = np.ascontiguousarray(np.stack([first, cnt], axis=1), dtype=np.int32)
     seg_blk = np.searchsorted(first, t.seg_if, side="left").astype(np.int64)
     return blocks, seg_blk
+
+
+def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):
+    """Face groups of the face-group tensor-core kernel (csrc/kernels_tcg.cuh):
+    runs of NFQ = 8 / gcd(S, 8) interior faces of one colour segment that
+    share the inside and outside face-geometry class (``cls`` from
+    ``tc_face_fold_tables``) and the lifting side (K- flag), so the S NFQ
+    (face, species) rows fill whole DMMA M tiles and share every B operand.
+    The faces keep their segment, so the face-sum order (and every bit of
+    the result) is that of the per-face kernels.  Returns (int32
+    [ngroups][NFQ] face ids, -1 past a run's end; int64 group offsets of the
+    segments [n_seg+1])."""
+    nfq = 8 // int(np.gcd(int(n_species), 8))
+    nif = len(t.if_code)
+    if nif == 0:
+        return np.zeros((0, nfq), np.int32), np.zeros(t.n_seg + 1, np.int64)
+    minus = (t.if_code.astype(np.int64) >> 10) & 1
+    ncls = int(cls.max()) + 1
+    key = ((t.if_seg.astype(np.int64) * ncls + cls[:, 0]) * ncls + cls[:, 1]) * 2 + minus
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    brk = np.flatnonzero(np.diff(ks)) + 1
+    starts = np.concatenate([[0], brk])
+    lens = np.diff(np.concatenate([starts, [nif]]))
+    ng = (lens + nfq - 1) // nfq
+    # slot j of group i of run r holds order[start_r + nfq i + j] inside the run
+    run_of = np.repeat(np.arange(len(starts)), ng)
+    gi = np.arange(ng.sum()) - np.repeat(np.cumsum(ng) - ng, ng)
+    pos = starts[run_of][:, None] + nfq * gi[:, None] + np.arange(nfq)[None, :]
+    inside = pos < (starts + lens)[run_of][:, None]
+    groups = np.where(inside, order[np.minimum(pos, nif - 1)], -1).astype(np.int32)
+    gseg = t.if_seg[order[starts[run_of]]].astype(np.int64)
+    seg_g = np.searchsorted(gseg, np.arange(t.n_seg + 1), side="left").astype(np.int64)
+    return np.ascontiguousarray(groups), seg_g
 
 
 def tc_volume_tables(t: OperatorTables) -> np.ndarray:

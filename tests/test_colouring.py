@@ -11,7 +11,8 @@ from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel, DiffusionMode
 from paper_1403_1157_b200.mesh import unit_cube, unit_square
 from paper_1403_1157_b200.tables import (CODE_FIRST_IN, CODE_FIRST_OUT, CODE_MIRROR,
                                          CODE_SKIP_OUT, build_tables, color_faces,
-                                         tc_face_blocks)
+                                         tc_face_blocks, tc_face_fold_tables,
+                                         tc_face_groups)
 
 
 def _check(t, n_owned):
@@ -91,3 +92,41 @@ def test_slab_cut_faces_run_last():
     for s in range(t.n_seg):
         for f0, n in blocks[seg_blk[s]:seg_blk[s + 1]]:
             assert t.seg_if[s] <= f0 and f0 + n <= t.seg_if[s + 1]
+
+
+@pytest.mark.parametrize("cells,order,scheme,S", [
+    ((3, 3, 3), 3, "cdg2", 6), ((4, 2, 3), 2, "br2", 6), ((4, 3, 2), 1, "ip", 6),
+    ((3, 2, 2), 2, "cdg2", 3)])
+def test_face_groups_cover_each_face_once_within_one_class(cells, order, scheme, S):
+    """tables.tc_face_groups (face-group tensor-core kernel): every interior
+    face sits in exactly one group slot; a group's faces share the colour
+    segment, both sides' face-geometry class and the K- flag; groups hold
+    8 / gcd(S, 8) slots, only a run's last group has empty (-1) slots, and
+    the segment offsets bracket each segment's groups."""
+    from paper_1403_1157_b200 import ReducedModel
+    model = PlaqueModel() if S == 6 else ReducedModel()
+    t = build_tables(DGSpace(unit_cube(*cells), order, S), model, FluxScheme(scheme))
+    fold = tc_face_fold_tables(t)
+    assert fold is not None
+    cls = fold[2]
+    groups, seg_g = tc_face_groups(t, cls, S)
+    nfq = 8 // int(np.gcd(S, 8))
+    assert groups.shape[1] == nfq
+    ids = groups[groups >= 0]
+    assert np.array_equal(np.sort(ids), np.arange(len(t.if_code)))
+    assert (groups[:, 0] >= 0).all()
+    # -1 slots only at the end of a group
+    valid = groups >= 0
+    assert (np.diff(valid.astype(int), axis=1) <= 0).all()
+    f0 = groups[:, :1]
+    g = np.where(valid, groups, f0)
+    minus = (t.if_code >> 10) & 1
+    for arr in (t.if_seg, cls[:, 0], cls[:, 1], minus):
+        assert (arr[g] == arr[f0]).all()
+    assert seg_g[0] == 0 and seg_g[-1] == len(groups)
+    for s in range(t.n_seg):
+        assert (t.if_seg[groups[seg_g[s]:seg_g[s + 1], 0]] == s).all()
+    # a run (same key) has at most one partial group
+    partial = ~valid.all(axis=1)
+    key = t.if_seg[f0[:, 0]] * 10**6 + cls[f0[:, 0], 0] * 10**4 + cls[f0[:, 0], 1] * 10 + minus[f0[:, 0]]
+    assert len(np.unique(key[partial])) == partial.sum()

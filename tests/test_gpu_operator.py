@@ -817,3 +817,23 @@ def test_face_geometry_class_tables_match_per_face_folds(order):
     assert rel_l2_per_species(space, a, b).max() <= 1e-13
     ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
     assert rel_l2_per_species(space, a, ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("scheme", ["cdg2", "br2", "ip", "bo"])
+def test_face_group_kernel_matches_one_face_kernel(order, scheme):
+    """The face-group tensor-core kernel (csrc/kernels_tcg.cuh: four faces
+    of one face-geometry class pair as 24 (face, species) DMMA rows over
+    three warps, the last group of a run partly empty) == the one-face species-rows kernel
+    == the oracle (reference operator.py:253-288, flux.py:92-138), for the
+    lifting on the K- side (cdg2), both sides (br2) and none (ip, bo)."""
+    space = DGSpace(unit_cube(4, 3, 3), order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme(scheme))
+    U = initial_state(space, 29)
+    a = op.apply_f(U)
+    op.set_variant(no_groups=True)
+    b = op.apply_f(U)
+    assert rel_l2_per_species(space, a, b).max() <= 1e-13
+    ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
+    assert rel_l2_per_species(space, a, ref).max() <= 1e-12
