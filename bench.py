@@ -572,9 +572,7 @@ def run_native_arm(args, rank, world, local):
     # per application; every kernel class runs once per colour segment)
     Q, F = t.nq_vol, t.nq_face
     fv, ff, fb = apply_flops(d, nb, Q, F, ne, n_int, n_bnd)
-    names = {"faces": "k_faces_tcs" if d == 3 else "k_faces_fast", "wall": "k_faces_mma"
-             if d == 3 else "k_faces_fast (walls)", "volume": "k_volume_tc"
-             if (d == 3 or t.order == 3) else "k_volume_fast"}
+    names = op.kernel_names()
     per = {}
     for name, flops in (("faces", ff), ("wall", fb), ("volume", fv)):
         tms, nl = kt[name]
@@ -673,7 +671,7 @@ def run_native_arm(args, rank, world, local):
         # f-evaluation (reference operator.py:286; its stepper composes
         # three per SSP-RK3 step), pageable host memory both ways
         if slab is None:
-            Un = Uh.numpy()
+            Un = Uh.numpy().copy()  # pageable, like a user's numpy state
             op.apply_f(Un)
             torch.cuda.synchronize()
             nrep = 1 if big else 5
@@ -684,7 +682,7 @@ def run_native_arm(args, rank, world, local):
             e2e["reference_call_shape"] = {
                 "value": n_dofs / el, "unit": UNIT, "ms_per_apply_f": el * 1e3,
                 "h2d_bytes_per_call": Un.nbytes, "d2h_bytes_per_call": Fh.nbytes,
-                "api": "DiscreteOperator.apply_f(numpy) -> numpy, one f-evaluation per call "
+                "api": "DiscreteOperator.apply_f(numpy) -> numpy (tdg_apply_host: staged copies through pinned buffers), one f-evaluation per call "
                        "(wall clock, pageable host arrays, result allocated per call)"}
             del Fh, Un
         del Uh

@@ -10,6 +10,8 @@
  *   tdg_apply (mass_inverse=0) DiscreteOperator.apply    operator.py:253-284
  *   tdg_apply (mass_inverse=1) DiscreteOperator.apply_f  operator.py:286-288
  *                              + DGSpace.apply_inverse_mass fespace.py:117-118
+ *   tdg_apply_host             the same on host (numpy) arrays, the call shape
+ *                              of the reference's steppers timeint.py:315-333
  *   tdg_rk_stage               one explicit stage  a*U0 + b*U + c*M^-1 L(U)
  *                              (SSP-RK3 composition of apply_f, SURVEY 8(a) a14;
  *                              DIRK stage algebra timeint.py:315-333)
@@ -35,7 +37,9 @@
  * (diffusivity, lin_source, params, seg_ptr) are copied at create time.
  * Streams are `cudaStream_t` passed as `void*` (NULL = legacy default
  * stream).  No call allocates device memory, streams or events after
- * tdg_create (state vectors and work buffers are the caller's).  Every
+ * tdg_create (state vectors and work buffers are the caller's); the one
+ * exception is tdg_apply_host's process-wide pinned host staging, made on
+ * its first call.  Every
  * call returns 0 on success or a negative TDG_E* code; tdg_last_error()
  * gives a message (thread-local).
  *
@@ -61,7 +65,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 4
+#define TDG_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -156,6 +160,17 @@ typedef struct tdg_desc {
    * NULL: the one-face species-rows kernel runs the blocks instead */
   const int32_t* face_groups;
   int64_t n_face_groups;
+  /* optional, tensor-core volume kernel: element-geometry classes
+   * (tables.tc_volume_classes): per class the summed stiffness fragments
+   * [ncls][KT][NNT][32], the elements in class-sorted tasks of 8 (int32
+   * [n_vol_tasks][8] element ids, -1 pads), each task's class (int32
+   * [n_vol_tasks]), and (HOST) the task offsets [9] of the 8 element chunks
+   * [ne k / 8, ne (k+1) / 8); all NULL: per-element metric scaling */
+  const double* vol_cls_tab;
+  const int32_t* vol_perm;
+  const int32_t* vol_task_cls;
+  int64_t n_vol_tasks;
+  const int64_t* vol_chunk_tasks;
   /* face colour segments, run in order: segment s covers the interior
    * faces [I[s], I[s+1]), the walls [W[s], W[s+1]), the face blocks
    * [B[s], B[s+1]) and the face groups [G[s], G[s+1]) with seg_ptr (HOST)
@@ -200,6 +215,18 @@ TDG_API int tdg_rk_stage(tdg_ctx* ctx, const double* U0, const double* U, double
 TDG_API int tdg_rk_stage_part(tdg_ctx* ctx, const double* U0, const double* U, double* out,
                               double* acc, double a, double b, double c, double t, int part,
                               void* stream);
+
+/* tdg_apply on HOST arrays in any (pageable) memory, the reference's own
+ * call shape (apply / apply_f on numpy arrays): U_host (n_elements +
+ * n_ghost rows) -> U_dev, the operator, R_dev -> R_host (n_elements rows),
+ * through process-wide pinned staging buffers (3 x 64 MiB, allocated on
+ * the first call -- the one allocation after tdg_create) that a pool of
+ * host threads fills / drains while the DMA engine moves the neighbouring
+ * piece; the volume kernel runs in element chunks so the copy-out starts
+ * with the first chunk.  Synchronous: R_host is complete on return.  Same
+ * bits as tdg_apply. */
+TDG_API int tdg_apply_host(tdg_ctx* ctx, const double* U_host, double* R_host, double* U_dev,
+                           double* R_dev, double t, int mass_inverse, void* stream);
 
 /* nsteps SSP-RK3 steps of a HOST state (pinned memory, undecomposed
  * mesh), through the device buffers U, w1, w2 (shape of U): every step
@@ -288,7 +315,8 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
  * CTA-staged generic kernels; bit 5: launch tdg_ssprk3_step's kernels
  * directly instead of replaying its cached CUDA graph; bit 13: ignore the
  * face-geometry-class tables (fold Jinv n per face); bit 14: run the
- * one-face species-rows kernel instead of the face-group kernel; bit 12: use the
+ * one-face species-rows kernel instead of the face-group kernel; bit 15:
+ * ignore the element-geometry classes of the volume kernel; bit 12: use the
  * transposed tensor-core volume kernel wherever it compiles (default only
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
  * per SM of the 2D register-resident face kernel's grid-stride grid (0 =

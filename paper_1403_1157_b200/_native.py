@@ -15,7 +15,7 @@ from .build import LIB
 __all__ = ["lib", "TdgDesc", "check", "TDG_OK", "load"]
 
 TDG_OK, TDG_E_INVALID, TDG_E_UNSUPPORTED, TDG_E_CUDA = 0, -1, -2, -3
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double
@@ -40,6 +40,8 @@ class TdgDesc(ctypes.Structure):
         ("face_tc", _p), ("face_blocks", _p), ("n_face_blocks", _i64),
         ("face_tc_fold", _p), ("if_fold", _p),
         ("face_groups", _p), ("n_face_groups", _i64),
+        ("vol_cls_tab", _p), ("vol_perm", _p), ("vol_task_cls", _p), ("n_vol_tasks", _i64),
+        ("vol_chunk_tasks", _p),
         ("n_segments", _i32), ("n_segments_cut", _i32), ("seg_ptr", _p),
     ]
 
@@ -67,6 +69,7 @@ def load(path: str = LIB):
     lib.tdg_rk_stage.argtypes = [_p, _p, _p, _p, _p, _d, _d, _d, _d, _p]
     lib.tdg_species_totals.argtypes = [_p, _p, _p, _p]
     lib.tdg_ssprk3_steps_host.argtypes = [_p, _p, _p, _p, _p, _i64, _d, _d, _p]
+    lib.tdg_apply_host.argtypes = [_p, _p, _p, _p, _p, _d, ctypes.c_int, _p]
     lib.tdg_species_l2.argtypes = [_p, _p, _p, _p, _p]
     lib.tdg_mgs.argtypes = [_p, _p, _i64, ctypes.c_int, _p, _i64, _p, _p]
     lib.tdg_mgs_pass.argtypes = [_p, _p, _i64, ctypes.c_int, ctypes.c_int, _p, _i64, _p, _p]
@@ -86,7 +89,7 @@ def load(path: str = LIB):
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
     lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
-    for name in ("tdg_mgs_pass", "tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    for name in ("tdg_apply_host", "tdg_mgs_pass", "tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev", "tdg_scale_norm", "tdg_jv_shift", "tdg_jv_diff"):

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtaxisdg_b200.so")
-SOURCES = ["capi.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
+SOURCES = ["capi.cu", "hostio.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
            "inst_diffusion.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 

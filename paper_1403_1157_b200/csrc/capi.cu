@@ -49,7 +49,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   if (d.n_species < 1 || d.n_species > kMaxS) return fail(TDG_E_INVALID, "n_species out of range");
   if (d.scheme < TDG_CDG2 || d.scheme > TDG_BO) return fail(TDG_E_INVALID, "unknown scheme");
   if (d.n_elements < 0 || d.n_ghost < 0 || d.n_int_faces < 0 || d.n_bnd_faces < 0 ||
-      d.n_face_blocks < 0 || d.n_face_groups < 0)
+      d.n_face_blocks < 0 || d.n_face_groups < 0 || d.n_vol_tasks < 0)
     return fail(TDG_E_INVALID, "negative size");
   if (d.n_elements + d.n_ghost > (int64_t(1) << 31) - 1)
     return fail(TDG_E_INVALID, "element rows must fit int32");
@@ -90,6 +90,13 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
       if (seg[s].w1 > seg[s].w0) return fail(TDG_E_INVALID, "walls in a cut-face segment");
   } else if (d.n_int_faces + d.n_bnd_faces > 0) {
     return fail(TDG_E_INVALID, "faces without colour segments");
+  }
+
+  if (d.vol_chunk_tasks) {
+    const int64_t* T = d.vol_chunk_tasks;
+    bool ok = T[0] == 0 && T[tdg_ctx::kChunks] == d.n_vol_tasks;
+    for (int k = 0; k < tdg_ctx::kChunks; ++k) ok = ok && T[k] <= T[k + 1];
+    if (!ok) return fail(TDG_E_INVALID, "inconsistent volume-class chunk offsets");
   }
 
   tdg_ctx* ctx = new (std::nothrow) tdg_ctx;
@@ -137,6 +144,13 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.ftf = d.face_tc_fold;
   p.ffold = d.if_fold;
   p.fgrp = d.face_groups;
+  if (d.vol_cls_tab && d.vol_perm && d.vol_task_cls && d.vol_chunk_tasks) {
+    p.vctab = d.vol_cls_tab;
+    p.vperm = d.vol_perm;
+    p.vtcls = d.vol_task_cls;
+    for (int k = 0; k <= tdg_ctx::kChunks; ++k) ctx->vchunk[k] = d.vol_chunk_tasks[k];
+  }
+  ctx->d.vol_chunk_tasks = nullptr;  // copied into ctx->vchunk
 
   {
     int dev = 0, sms = 0;
@@ -470,6 +484,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->force_tc = ((variant >> 12) & 1) != 0;
   ctx->no_fold = ((variant >> 13) & 1) != 0;    // bit 13: no face-geometry-class tables
   ctx->no_groups = ((variant >> 14) & 1) != 0;  // bit 14: one-face kernel despite face groups
+  ctx->no_vcls = ((variant >> 15) & 1) != 0;    // bit 15: no volume element classes
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;

@@ -75,11 +75,13 @@ struct tdg_ctx {
   bool force_tc = false;       // testing: tensor-core volume kernel where the SIMT one fits
   bool no_fold = false;        // testing: per-face normal-derivative folds despite class tables
   bool no_groups = false;      // testing: the one-face kernel despite face groups
+  bool no_vcls = false;        // testing: per-element metric scaling despite volume classes
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
   // per direction (created with the context: no call allocates later)
   static constexpr int kChunks = 8;
+  int64_t vchunk[kChunks + 1] = {};  // volume-class task offsets of the element chunks
   cudaStream_t s_in[2] = {}, s_out[2] = {};
   cudaEvent_t ev_h2d[kChunks] = {}, ev_d2h[kChunks] = {}, ev_vol[kChunks] = {};
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
@@ -127,8 +129,10 @@ int configure(int nqv) {
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcg");
   }
   if constexpr (TcVol<D, K, M>::ok) {
-    e = cudaFuncSetAttribute(k_volume_tc<D, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TcVol<D, K, M>::smem()));
+    for (auto fn : {k_volume_tc<D, K, M, false>, k_volume_tc<D, K, M, true>})
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(TcVol<D, K, M>::smem()));
     if (e != cudaSuccess) return cuda_fail(e, "configure volume_tc");
   }
   if constexpr (MmaFace<D, K, M>::ok) {
@@ -290,6 +294,19 @@ int volume(tdg_ctx* ctx, int64_t e0, int64_t e1, const double* U, const double* 
            const double* acc, double a, double b, double c, int mode, cudaStream_t st) {
   constexpr int SN = SN_of<M, D, K>(), NEG = Dims<D, K>::NEG;
   if (e1 <= e0) return TDG_OK;
+  // element-geometry classes: the range must be a run of whole chunks
+  int64_t ct0 = -1, ct1 = -1;
+  if (ctx->p.vperm != nullptr && !ctx->no_vcls) {
+    constexpr int NCH = tdg_ctx::kChunks;
+    const int64_t ne = ctx->p.ne;
+    for (int k = 0; k <= NCH; ++k) {
+      if (ne * k / NCH == e0 && ct0 < 0) ct0 = ctx->vchunk[k];
+      if (ne * k / NCH == e1) ct1 = ctx->vchunk[k];
+    }
+    if (ct0 < 0 || ct1 < 0) ct0 = ct1 = -1;
+  }
+  const double *U_all = U, *U0_all = U0, *acc_all = acc;
+  double* out_all = out;
   OpParams p = ctx->p;
   p.ne = e1 - e0;
   p.egeo = ctx->p.egeo + e0 * NEG;
@@ -312,21 +329,29 @@ int volume(tdg_ctx* ctx, int64_t e0, int64_t e1, const double* U, const double* 
   } else if (use_tc) {
     if constexpr (tc_ok) {
       using T = TcVol<D, K, M>;
-      const int64_t tasks = (p.ne + T::EW - 1) / T::EW;
+      const bool cls = ct0 >= 0;
+      const int64_t tasks = cls ? ct1 - ct0 : (p.ne + T::EW - 1) / T::EW;
       int64_t grid = (tasks + T::WARPS - 1) / T::WARPS;
       // persistent grid: every CTA slot the registers / shared memory allow
       static int resident = 0;
       if (resident == 0) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_volume_tc<D, K, M>, 32 * T::WARPS,
-                                                          T::smem()) != cudaSuccess || nb < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_volume_tc<D, K, M, true>,
+                                                          32 * T::WARPS, T::smem()) != cudaSuccess ||
+            nb < 1)
           nb = T::MINB;
         resident = nb;
       }
       const int64_t cap = int64_t(ctx->num_sms) * resident;
       grid = grid < cap ? grid : cap;
-      k_volume_tc<D, K, M><<<unsigned(grid), 32 * T::WARPS, T::smem(), st>>>(p, p.vtc, U, acc, U0, out, a, b,
-                                                                   c, mode);
+      if (grid > 0) {
+        if (cls)  // absolute element ids: the unshifted arrays
+          k_volume_tc<D, K, M, true><<<unsigned(grid), 32 * T::WARPS, T::smem(), st>>>(
+              ctx->p, p.vtc, U_all, acc_all, U0_all, out_all, a, b, c, mode, ct0, ct1);
+        else
+          k_volume_tc<D, K, M, false><<<unsigned(grid), 32 * T::WARPS, T::smem(), st>>>(
+              p, p.vtc, U, acc, U0, out, a, b, c, mode, 0, tasks);
+      }
     }
   } else {
     constexpr int TE = VolumeTile<D, K, M>::TE;

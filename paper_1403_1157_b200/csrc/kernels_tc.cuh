@@ -75,11 +75,15 @@ struct TcVol {
   static constexpr bool ok = S <= kMaxS && D >= 2;
 };
 
-template <int D, int K, class M>
+// CLS: the warps visit tasks [task0, task1) of 8 same-class elements
+// (p.vperm, tables.tc_volume_classes) and run the diffusion against the
+// class's summed stiffness (one GEMM per species); otherwise task i is the
+// elements 8i .. 8i+7 of the (range-shifted) arrays
+template <int D, int K, class M, bool CLS>
 __global__ void __launch_bounds__(32 * TcVol<D, K, M>::WARPS, TcVol<D, K, M>::MINB)
 k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restrict__ U,
             const double* ACC, const double* U0, double* out, double ca, double cb,
-            double cc, int mode) {
+            double cc, int mode, int64_t task0, int64_t task1) {
   using T = TcVol<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, NEG = T::NEG, NSYM = T::NSYM;
   constexpr int QT = T::QT, KT = T::KT, NNT = T::NNT;
@@ -96,13 +100,19 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
   mode &= 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t ntask = (p.ne + T::EW - 1) / T::EW;
-
-  for (int64_t task = int64_t(blockIdx.x) * T::WARPS + warp; task < ntask;
+  for (int64_t task = task0 + int64_t(blockIdx.x) * T::WARPS + warp; task < task1;
        task += int64_t(gridDim.x) * T::WARPS) {
-    const int64_t e = task * T::EW + g;
-    const bool valid = e < p.ne;
-    const int64_t ec = valid ? e : p.ne - 1;
+    int64_t e, ec;
+    bool valid;
+    if constexpr (CLS) {
+      e = __ldg(p.vperm + task * T::EW + g);
+      valid = e >= 0;
+      ec = valid ? e : __ldg(p.vperm + task * T::EW);  // a task's first slot is an element
+    } else {
+      e = task * T::EW + g;
+      valid = e < p.ne;
+      ec = valid ? e : p.ne - 1;
+    }
     double ge[NEG];
 #pragma unroll
     for (int k = 0; k < NEG; ++k) ge[k] = __ldg(p.egeo + ec * NEG + k);
@@ -231,16 +241,26 @@ k_volume_tc(OpParams p, const double* __restrict__ tabs, const double* __restric
       double dif[NNT][2];
 #pragma unroll
       for (int nt = 0; nt < NNT; ++nt) dif[nt][0] = dif[nt][1] = 0.0;
+      if constexpr (CLS) {
+        // one GEMM against the class's sum_p M_p KS_p
+        const double* kc = p.vctab + size_t(__ldg(p.vtcls + task)) * (KT * NNT * 32);
 #pragma unroll
-      for (int pq = 0; pq < NSYM; ++pq)
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const double a = cf[s][kt] * ge[1 + pq];
+        for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NNT; ++nt)
-            dmma(dif[nt][0], dif[nt][1], a,
-                 tb[T::OKS + ((pq * KT + kt) * NNT + nt) * 32 + lane]);
-        }
+            dmma(dif[nt][0], dif[nt][1], cf[s][kt], __ldg(kc + (kt * NNT + nt) * 32 + lane));
+      } else {
+#pragma unroll
+        for (int pq = 0; pq < NSYM; ++pq)
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const double a = cf[s][kt] * ge[1 + pq];
+#pragma unroll
+            for (int nt = 0; nt < NNT; ++nt)
+              dmma(dif[nt][0], dif[nt][1], a,
+                   tb[T::OKS + ((pq * KT + kt) * NNT + nt) * 32 + lane]);
+          }
+      }
       const int fi = M::flux_index(s), li = M::nl_index(s);
       const double As = p.A[s];
 #pragma unroll

@@ -95,7 +95,8 @@ class DiscreteOperator:
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
         from .tables import (mma_face_tables, tc_face_blocks, tc_face_fold_tables,
-                             tc_face_groups, tc_face_tables, tc_volume_tables)
+                             tc_face_groups, tc_face_tables, tc_volume_classes,
+                             tc_volume_tables)
         mma, self._mma_stride = mma_face_tables(t)
         blocks, seg_blk = tc_face_blocks(t)
         fold = tc_face_fold_tables(t)
@@ -109,6 +110,14 @@ class DiscreteOperator:
             self._keep["if_fold"] = dev(fold[2])
             groups, seg_grp = tc_face_groups(t, fold[2], t.n_species)
             self._keep["face_groups"] = dev(groups)
+        # element-geometry classes of the tensor-core volume kernel (3D and
+        # 2D p = 3; meshes of congruent cells)
+        vcls = tc_volume_classes(t) if (t.dim == 3 or t.order == 3) else None
+        self.n_volume_classes = 0 if vcls is None else len(np.unique(vcls[2]))
+        if vcls is not None:
+            self._keep["vol_cls_tab"] = dev(vcls[0])
+            self._keep["vol_perm"] = dev(vcls[1])
+            self._keep["vol_task_cls"] = dev(vcls[2])
         self._keep.update({name: dev(getattr(t, name)) for name in (
             "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
             "face_Pw", "face_w", "elem_geo", "if_elems", "if_code",
@@ -118,7 +127,9 @@ class DiscreteOperator:
                 [t.seg_if, t.seg_bf, seg_blk, seg_grp]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
             "lin_source": _checked_linear_source(model),
-            "params": np.ascontiguousarray(model.pack(), dtype=np.float64)}
+            "params": np.ascontiguousarray(model.pack(), dtype=np.float64),
+            "vol_chunk_tasks": np.ascontiguousarray(
+                vcls[3] if vcls is not None else np.zeros(9), dtype=np.int64)}
         chi_e, adj, eta = scheme_constants(space, scheme)
         ptr = lambda x: ctypes.c_void_p(x.data_ptr() if x.numel() else 0)
         hptr = lambda a: ctypes.c_void_p(a.ctypes.data)
@@ -147,6 +158,11 @@ class DiscreteOperator:
             if_fold=ptr(k["if_fold"]) if fold is not None else None,
             face_groups=ptr(k["face_groups"]) if fold is not None else None,
             n_face_groups=len(groups),
+            vol_cls_tab=ptr(k["vol_cls_tab"]) if vcls is not None else None,
+            vol_perm=ptr(k["vol_perm"]) if vcls is not None else None,
+            vol_task_cls=ptr(k["vol_task_cls"]) if vcls is not None else None,
+            n_vol_tasks=len(vcls[2]) if vcls is not None else 0,
+            vol_chunk_tasks=hptr(self._host["vol_chunk_tasks"]) if vcls is not None else None,
             n_segments=t.n_seg, n_segments_cut=t.n_seg_cut,
             seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()
@@ -242,12 +258,27 @@ class DiscreteOperator:
 
     def _apply(self, U, mass_inverse: int, t: float):
         torch = _torch()
-        Ud, is_dev = self._as_device(U)
-        R = torch.empty((self.n_owned, self.space.n_species, self.space.nb),
-                        dtype=torch.float64, device=self.device)
+        rshape = (self.n_owned, self.space.n_species, self.space.nb)
+        if not isinstance(U, torch.Tensor):
+            # host data (numpy / DiscreteFunction), the reference's call
+            # shape: staged copies in and out (tdg_apply_host), a fresh
+            # numpy result like the reference
+            shape = (self.n_rows, self.space.n_species, self.space.nb)
+            Uh = np.ascontiguousarray(np.asarray(getattr(U, "coeffs", U), dtype=float))
+            if Uh.shape != shape:
+                raise ValueError(f"U has shape {Uh.shape}, expected {shape}")
+            Rh = np.empty(rshape)
+            Ud = torch.empty(shape, dtype=torch.float64, device=self.device)
+            Rd = torch.empty(rshape, dtype=torch.float64, device=self.device)
+            self._call(self.lib.tdg_apply_host, self._ctx, Uh.ctypes.data, Rh.ctypes.data,
+                       Ud.data_ptr(), Rd.data_ptr(), float(t), mass_inverse, self._stream(),
+                       what="tdg_apply_host")
+            return Rh
+        Ud, _ = self._as_device(U)
+        R = torch.empty(rshape, dtype=torch.float64, device=self.device)
         self._call(self.lib.tdg_apply, self._ctx, Ud.data_ptr(), R.data_ptr(), float(t),
                    mass_inverse, self._stream(), what="tdg_apply")
-        return R if is_dev else R.cpu().numpy()
+        return R
 
     def apply(self, U, t: float = 0.0):
         return self._apply(U, 0, t)
@@ -259,9 +290,29 @@ class DiscreteOperator:
 
     KERNELS = ("faces", "wall", "volume", "reserved")
 
+    def kernel_names(self) -> dict:
+        """The kernels the default variant launches per kernel class (the
+        library's dispatch rules, ctx.cuh run_segment / volume, for the
+        compiled-in default quadrature)."""
+        t = self.tables
+        if t.dim == 3:
+            if self.n_face_classes and len(self._keep.get("face_groups", ())):
+                faces = "k_faces_tcg"
+            else:
+                faces = "k_faces_tcs"
+            wall = "k_faces_mma"
+        else:
+            faces, wall = "k_faces_fast", "k_faces_fast (walls)"
+        if t.dim == 3 or t.order == 3:
+            volume = "k_volume_tc" + (" (element classes)" if self.n_volume_classes else "")
+        else:
+            volume = "k_volume_fast"
+        return {"faces": faces, "wall": wall, "volume": volume}
+
     def set_variant(self, generic: bool = False, no_graph: bool = False,
                     tc_volume: bool = False, face_ctas_per_sm: int = 0,
-                    no_fold: bool = False, no_groups: bool = False):
+                    no_fold: bool = False, no_groups: bool = False,
+                    no_volume_classes: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
         kernels directly instead of replaying its CUDA graph; ``tc_volume``
@@ -270,11 +321,12 @@ class DiscreteOperator:
         (0 default, 15 uncapped); ``no_fold`` makes the 3D face kernel fold
         Jinv n per face despite face-geometry-class tables; ``no_groups``
         runs the one-face species-rows kernel instead of the face-group
-        kernel.  Defaults: fastest."""
+        kernel; ``no_volume_classes`` scales the volume kernel's diffusion
+        per element despite element-geometry classes.  Defaults: fastest."""
         self._call(self.lib.tdg_set_variant, self._ctx,
                    int(bool(generic)) | (int(bool(no_graph)) << 5)
                    | (int(bool(tc_volume)) << 12) | (int(bool(no_fold)) << 13)
-                   | (int(bool(no_groups)) << 14)
+                   | (int(bool(no_groups)) << 14) | (int(bool(no_volume_classes)) << 15)
                    | ((int(face_ctas_per_sm) & 15) << 8),
                    what="tdg_set_variant")
 

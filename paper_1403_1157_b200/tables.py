@@ -486,6 +486,65 @@ def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):
     return np.ascontiguousarray(groups), seg_g
 
 
+VOL_CHUNKS = 8   # element chunks of the host-data entry points (tdg_ctx::kChunks)
+
+
+def tc_volume_classes(t: OperatorTables, max_classes: int = 16):
+    """Element-geometry classes of the tensor-core volume kernel: meshes of
+    congruent cells (the Kuhn cubes: 6 tetrahedron shapes) have few distinct
+    geometry records (detJ, sym(Jinv Jinv^T)), and per class the exact
+    stiffness sum_p M_p KS_p is one matrix, so a warp of 8 same-class
+    elements runs its diffusion as one GEMM per species instead of
+    d(d+1)/2 metric-scaled ones (reference operator.py:292-324 diffusion
+    term).  Elements keep their rows; the kernel visits them through a
+    permutation, sorted by class inside each of the VOL_CHUNKS element
+    chunks [ne k / 8, ne (k+1) / 8) so chunked launches stay exact.
+
+    Returns (class tables [ncls][KT][NNT][32] fragment-major as
+    ``_frag_kn``, int32 element ids [ntask][8] (-1 pads a class's last
+    task), int32 class of every task [ntask], int64 task offsets of the
+    chunks [VOL_CHUNKS + 1]) or None with more than ``max_classes``."""
+    ne = t.elem_geo.shape[0]
+    if ne == 0:
+        return None
+    uniq, cls = np.unique(np.ascontiguousarray(t.elem_geo).view(np.int64), axis=0,
+                          return_inverse=True)
+    cls = cls.reshape(-1)
+    if len(uniq) > max_classes:
+        return None
+    nb = t.nb
+    NBK, NBN = _ceil(nb, 4), _ceil(nb, 8)
+    pic, ok = _pi_cols(nb)
+    geo = uniq.view(np.float64)
+    tabs = []
+    for g in geo:
+        Kc = np.einsum("p,pij->ij", g[1:], t.vol_stiff)
+        KP = np.zeros((NBK, NBN)); KP[:nb] = Kc[:, pic] * ok
+        tabs.append(_frag_kn(KP).ravel())
+    perm, tcls, toff = [], [], [0]
+    for k in range(VOL_CHUNKS):
+        e0, e1 = ne * k // VOL_CHUNKS, ne * (k + 1) // VOL_CHUNKS
+        c = cls[e0:e1]
+        order = np.argsort(c, kind="stable") + e0
+        cs = cls[order]
+        brk = np.flatnonzero(np.diff(cs)) + 1
+        starts = np.concatenate([[0], brk]) if len(cs) else np.zeros(0, np.int64)
+        lens = np.diff(np.concatenate([starts, [len(cs)]]))
+        ntask = 0
+        for s0, ln in zip(starts, lens):
+            nt = (ln + 7) // 8
+            ids = np.full(nt * 8, -1, np.int64)
+            ids[:ln] = order[s0:s0 + ln]
+            perm.append(ids)
+            tcls.append(np.full(nt, cs[s0], np.int64))
+            ntask += nt
+        toff.append(toff[-1] + ntask)
+    perm = np.concatenate(perm).astype(np.int32)
+    tcls = np.concatenate(tcls).astype(np.int32)
+    return (np.ascontiguousarray(np.concatenate(tabs)), perm.reshape(-1, 8), tcls,
+            np.asarray(toff, dtype=np.int64))
+
+
 def tc_volume_tables(t: OperatorTables) -> np.ndarray:
     """Operand tables of the transposed tensor-core volume kernel
     (csrc/kernels_tc.cuh, k_volume_tc), concatenated, each stored

@@ -130,3 +130,40 @@ def test_face_groups_cover_each_face_once_within_one_class(cells, order, scheme,
     partial = ~valid.all(axis=1)
     key = t.if_seg[f0[:, 0]] * 10**6 + cls[f0[:, 0], 0] * 10**4 + cls[f0[:, 0], 1] * 10 + minus[f0[:, 0]]
     assert len(np.unique(key[partial])) == partial.sum()
+
+
+@pytest.mark.parametrize("cells,order", [((4, 2, 2), 3), ((4, 4, 4), 2), ((3, 3, 3), 1)])
+def test_volume_classes_cover_each_element_once_per_chunk(cells, order):
+    """tables.tc_volume_classes (tensor-core volume kernel): every element
+    sits in exactly one task slot, a task's elements share the geometry
+    record (so one summed stiffness serves the warp), tasks stay inside
+    their element chunk [ne k / 8, ne (k+1) / 8) (chunked host-data
+    launches), and the class tables are sum_p M_p KS_p."""
+    from paper_1403_1157_b200.tables import VOL_CHUNKS, tc_volume_classes
+    t = build_tables(DGSpace(unit_cube(*cells), order, 6), PlaqueModel(), FluxScheme("cdg2"))
+    r = tc_volume_classes(t)
+    assert r is not None
+    tabs, perm, tcls, toff = r
+    ne = t.elem_geo.shape[0]
+    ids = perm[perm >= 0]
+    assert np.array_equal(np.sort(ids), np.arange(ne))
+    assert (perm[:, 0] >= 0).all()
+    assert toff[0] == 0 and toff[-1] == len(perm) and (np.diff(toff) >= 0).all()
+    geo = t.elem_geo
+    for k in range(VOL_CHUNKS):
+        e0, e1 = ne * k // VOL_CHUNKS, ne * (k + 1) // VOL_CHUNKS
+        blk = perm[toff[k]:toff[k + 1]]
+        v = blk[blk >= 0]
+        assert ((v >= e0) & (v < e1)).all() and len(v) == e1 - e0
+    for task in range(len(perm)):
+        v = perm[task][perm[task] >= 0]
+        assert (geo[v] == geo[v[0]]).all()
+    # class table of the first task's class == sum_p M_p KS_p (fragment layout)
+    from paper_1403_1157_b200.tables import _ceil, _frag_kn, _pi_cols
+    nb = t.nb
+    pic, ok = _pi_cols(nb)
+    Kc = np.einsum("p,pij->ij", geo[perm[0, 0], 1:], t.vol_stiff)
+    KP = np.zeros((_ceil(nb, 4), _ceil(nb, 8))); KP[:nb] = Kc[:, pic] * ok
+    stride = len(tabs) // (tcls.max() + 1)
+    assert np.allclose(tabs[tcls[0] * stride:(tcls[0] + 1) * stride], _frag_kn(KP).ravel(),
+                       rtol=0, atol=1e-13 * np.abs(Kc).max())

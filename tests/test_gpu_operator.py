@@ -837,3 +837,46 @@ def test_face_group_kernel_matches_one_face_kernel(order, scheme):
     assert rel_l2_per_species(space, a, b).max() <= 1e-13
     ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
     assert rel_l2_per_species(space, a, ref).max() <= 1e-12
+
+
+def test_host_array_apply_is_bitwise_the_device_apply():
+    """apply / apply_f on numpy arrays (tdg_apply_host: pinned staging
+    pieces filled by host threads, the volume kernel in element chunks with
+    each chunk's copy-out overlapped) == the device-tensor call, bit for
+    bit, on a state of several 64 MiB staging pieces (reference call shape
+    operator.py:253-288)."""
+    import torch
+    space = DGSpace(unit_cube(32, 32, 24), 3, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme("cdg2"))
+    U = initial_state(space, 31)
+    assert U.nbytes > 2 * (64 << 20)
+    Ud = torch.from_numpy(U).cuda()
+    for fn in (op.apply, op.apply_f):
+        host = fn(U)
+        dev = fn(Ud).cpu().numpy()
+        assert isinstance(host, np.ndarray) and host.shape == dev.shape
+        assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_volume_classes_match_per_element_metric(order):
+    """The tensor-core volume kernel over element-geometry classes (tasks of
+    8 same-class elements, diffusion as one GEMM against sum_p M_p KS_p,
+    tables.tc_volume_classes) == the per-element metric-scaled diffusion ==
+    the oracle (reference operator.py:292-324), whole and through the
+    chunked launches of the host-data entry point."""
+    import torch
+    space = DGSpace(unit_cube(4, 4, 2), order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme("cdg2"))
+    assert op.n_volume_classes >= 1
+    U = initial_state(space, 37)
+    a = op.apply_f(torch.from_numpy(U).cuda()).cpu().numpy()
+    h = op.apply_f(U)                       # chunked volume launches
+    op.set_variant(no_volume_classes=True)
+    b = op.apply_f(torch.from_numpy(U).cuda()).cpu().numpy()
+    assert np.array_equal(a, h)
+    assert rel_l2_per_species(space, a, b).max() <= 1e-13
+    ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
+    assert rel_l2_per_species(space, a, ref).max() <= 1e-12
