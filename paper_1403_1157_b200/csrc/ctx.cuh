@@ -204,8 +204,16 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
           KernelTimer kt(ctx, 0, st);
           using T = TcgFace<D, K, M>;
           // persistent: the resident CTAs loop over the segment's groups
+          static int resident = 0;
+          if (resident == 0) {
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_faces_tcg<D, K, M, 1>, T::THREADS,
+                                                              T::smem()) != cudaSuccess || nb < 1)
+              nb = T::MINB;
+            resident = nb;
+          }
           int64_t grid = sg.g1 - sg.g0;
-          const int64_t cap = int64_t(ctx->num_sms) * T::MINB;
+          const int64_t cap = int64_t(ctx->num_sms) * resident;
           grid = grid < cap ? grid : cap;
           auto go = [&](auto kernel) {
             kernel<<<unsigned(grid), T::THREADS, T::smem(), st>>>(p, p.ftc, p.fgrp, sg.g0, sg.g1, U,

@@ -383,6 +383,33 @@ def tc_face_tables(t: OperatorTables):
     return np.ascontiguousarray(np.concatenate(parts)), stride
 
 
+def _row_classes(rows: np.ndarray):
+    """Classes of identical rows of an int64 matrix: (unique rows in order
+    of first appearance, class of every row).  Hash-factorised (O(n), the
+    C5 meshes have 1e8 rows) and verified row by row; falls back to the
+    sorting np.unique on a hash collision."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    h = np.zeros(len(rows), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for j in range(rows.shape[1]):
+            c = rows[:, j].view(np.uint64)
+            h = (h ^ c) * np.uint64(0x9E3779B97F4A7C15) + np.uint64(0x632BE59BD9B4E019 + j)
+            h ^= h >> np.uint64(29)
+    try:
+        import pandas as pd
+        inv, first = pd.factorize(h.view(np.int64), sort=False)
+        inv = inv.astype(np.int64)
+        idx = np.empty(len(first), dtype=np.int64)
+        idx[inv[::-1]] = np.arange(len(rows) - 1, -1, -1)   # first row of each class
+        uniq = rows[idx]
+        if np.array_equal(rows, uniq[inv]):
+            return uniq, inv
+    except ImportError:
+        pass
+    uniq, inv = np.unique(rows, axis=0, return_inverse=True)
+    return uniq, inv.reshape(-1)
+
+
 def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
     """Face-geometry classes of the species-rows face kernel: every
     interior face side is a (table id, Jinv n) pair; meshes of congruent
@@ -407,7 +434,7 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
     tid = np.concatenate([code & 31, (code >> 5) & 31])
     jn = np.concatenate([t.if_geo[:, 0:3], t.if_geo[:, 3:6]])
     key = np.concatenate([tid[:, None], jn.view(np.int64)], axis=1)
-    uniq, inv = np.unique(key, axis=0, return_inverse=True)
+    uniq, inv = _row_classes(key)
     if len(uniq) > max_classes:
         return None
     QP, NBK, NBN = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
@@ -507,9 +534,7 @@ def tc_volume_classes(t: OperatorTables, max_classes: int = 16):
     ne = t.elem_geo.shape[0]
     if ne == 0:
         return None
-    uniq, cls = np.unique(np.ascontiguousarray(t.elem_geo).view(np.int64), axis=0,
-                          return_inverse=True)
-    cls = cls.reshape(-1)
+    uniq, cls = _row_classes(np.ascontiguousarray(t.elem_geo).view(np.int64))
     if len(uniq) > max_classes:
         return None
     nb = t.nb
