@@ -165,7 +165,8 @@ typedef struct tdg_desc {
    * [ncls][KT][NNT][32], the elements in class-sorted tasks of 8 (int32
    * [n_vol_tasks][8] element ids, -1 pads), each task's class (int32
    * [n_vol_tasks]), and (HOST) the task offsets [9] of the 8 element chunks
-   * [ne k / 8, ne (k+1) / 8); all NULL: per-element metric scaling */
+   * (chunk k starts at ne k / 8 rounded down to a multiple of 8 elements,
+   * tables.vol_chunk_bounds); all NULL: per-element metric scaling */
   const double* vol_cls_tab;
   const int32_t* vol_perm;
   const int32_t* vol_task_cls;

@@ -339,7 +339,7 @@ int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, double* U, double* w1, d
   const size_t sn = size_t(ctx->d.n_species) * ctx->d.nb;
   constexpr int NCH = tdg_ctx::kChunks;
   int64_t ck[NCH + 1];
-  for (int k = 0; k <= NCH; ++k) ck[k] = ne * k / NCH;
+  for (int k = 0; k <= NCH; ++k) ck[k] = chunk_start(ne, k);
   cudaEventRecord(ctx->ev_s0, st);
   for (int i = 0; i < 2; ++i) {
     cudaStreamWaitEvent(ctx->s_in[i], ctx->ev_s0, 0);

@@ -100,6 +100,14 @@ struct tdg_ctx {
 
 namespace tdg {
 
+// element chunks of the host-data entry points and of the volume-class
+// task lists (tables.vol_chunk_bounds): chunk k starts at element
+// (ne k / kChunks) rounded down to a multiple of 8, so every chunk's rows
+// keep the 32-byte alignment the vectorised kernels load with
+inline int64_t chunk_start(int64_t ne, int k) {
+  return k >= tdg_ctx::kChunks ? ne : (ne * k / tdg_ctx::kChunks) / 8 * 8;
+}
+
 template <int D, int K, class M>
 int configure(int nqv) {
   cudaError_t e;
@@ -308,8 +316,8 @@ int volume(tdg_ctx* ctx, int64_t e0, int64_t e1, const double* U, const double* 
     constexpr int NCH = tdg_ctx::kChunks;
     const int64_t ne = ctx->p.ne;
     for (int k = 0; k <= NCH; ++k) {
-      if (ne * k / NCH == e0 && ct0 < 0) ct0 = ctx->vchunk[k];
-      if (ne * k / NCH == e1) ct1 = ctx->vchunk[k];
+      if (chunk_start(ne, k) == e0 && ct0 < 0) ct0 = ctx->vchunk[k];
+      if (chunk_start(ne, k) == e1) ct1 = ctx->vchunk[k];
     }
     if (ct0 < 0 || ct1 < 0) ct0 = ct1 = -1;
   }

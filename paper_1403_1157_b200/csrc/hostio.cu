@@ -183,7 +183,7 @@ extern "C" int tdg_apply_host(tdg_ctx* ctx, const double* U_host, double* R_host
   int rc = ctx->impl.run(ctx, U_dev, nullptr, R_dev, R_dev, 0.0, 0.0, 0.0, mode, 3, st);
   constexpr int NCH = tdg_ctx::kChunks;
   int64_t ck[NCH + 1];
-  for (int k = 0; k <= NCH; ++k) ck[k] = ne * k / NCH;
+  for (int k = 0; k <= NCH; ++k) ck[k] = chunk_start(ne, k);
   const bool faces = ctx->p.nif + ctx->p.nbf > 0;
   for (int k = 0; k < NCH && !rc; ++k) {
     rc = ctx->impl.volume(ctx, ck[k], ck[k + 1], U_dev, nullptr, R_dev, faces ? R_dev : nullptr,

@@ -516,6 +516,13 @@ def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):
 VOL_CHUNKS = 8   # element chunks of the host-data entry points (tdg_ctx::kChunks)
 
 
+def vol_chunk_bounds(ne: int):
+    """Element chunk boundaries of the host-data entry points (ctx.cuh
+    chunk_start): ne k / 8 rounded down to a multiple of 8 elements."""
+    return [ne if k >= VOL_CHUNKS else (ne * k // VOL_CHUNKS) // 8 * 8
+            for k in range(VOL_CHUNKS + 1)]
+
+
 def tc_volume_classes(t: OperatorTables, max_classes: int = 16):
     """Element-geometry classes of the tensor-core volume kernel: meshes of
     congruent cells (the Kuhn cubes: 6 tetrahedron shapes) have few distinct
@@ -525,7 +532,7 @@ def tc_volume_classes(t: OperatorTables, max_classes: int = 16):
     d(d+1)/2 metric-scaled ones (reference operator.py:292-324 diffusion
     term).  Elements keep their rows; the kernel visits them through a
     permutation, sorted by class inside each of the VOL_CHUNKS element
-    chunks [ne k / 8, ne (k+1) / 8) so chunked launches stay exact.
+    chunks (``vol_chunk_bounds``) so chunked launches stay exact.
 
     Returns (class tables [ncls][KT][NNT][32] fragment-major as
     ``_frag_kn``, int32 element ids [ntask][8] (-1 pads a class's last
@@ -547,8 +554,9 @@ def tc_volume_classes(t: OperatorTables, max_classes: int = 16):
         KP = np.zeros((NBK, NBN)); KP[:nb] = Kc[:, pic] * ok
         tabs.append(_frag_kn(KP).ravel())
     perm, tcls, toff = [], [], [0]
+    cb = vol_chunk_bounds(ne)
     for k in range(VOL_CHUNKS):
-        e0, e1 = ne * k // VOL_CHUNKS, ne * (k + 1) // VOL_CHUNKS
+        e0, e1 = cb[k], cb[k + 1]
         c = cls[e0:e1]
         order = np.argsort(c, kind="stable") + e0
         cs = cls[order]

@@ -139,7 +139,7 @@ def test_volume_classes_cover_each_element_once_per_chunk(cells, order):
     record (so one summed stiffness serves the warp), tasks stay inside
     their element chunk [ne k / 8, ne (k+1) / 8) (chunked host-data
     launches), and the class tables are sum_p M_p KS_p."""
-    from paper_1403_1157_b200.tables import VOL_CHUNKS, tc_volume_classes
+    from paper_1403_1157_b200.tables import VOL_CHUNKS, tc_volume_classes, vol_chunk_bounds
     t = build_tables(DGSpace(unit_cube(*cells), order, 6), PlaqueModel(), FluxScheme("cdg2"))
     r = tc_volume_classes(t)
     assert r is not None
@@ -150,8 +150,10 @@ def test_volume_classes_cover_each_element_once_per_chunk(cells, order):
     assert (perm[:, 0] >= 0).all()
     assert toff[0] == 0 and toff[-1] == len(perm) and (np.diff(toff) >= 0).all()
     geo = t.elem_geo
+    cb = vol_chunk_bounds(ne)
+    assert all(b % 8 == 0 for b in cb[:-1]) and cb[-1] == ne
     for k in range(VOL_CHUNKS):
-        e0, e1 = ne * k // VOL_CHUNKS, ne * (k + 1) // VOL_CHUNKS
+        e0, e1 = cb[k], cb[k + 1]
         blk = perm[toff[k]:toff[k + 1]]
         v = blk[blk >= 0]
         assert ((v >= e0) & (v < e1)).all() and len(v) == e1 - e0
