@@ -50,7 +50,9 @@ struct TcgFace {
                        CWS = OY0 + MT * QT * 2 * 32;
   static constexpr size_t smem() { return size_t(CWS) * 8; }
   // up to 16 warps / SM at 128 registers
-  static constexpr int MINB = 16 / MT;
+  // p = 3: 5 CTAs (15 warps) at 128 registers; 6 CTAs at 96 registers
+  // measured 23.3 against 22.4 ms (64^3), at p = 2 11.6 against 12.2 ms
+  static constexpr int MINB = K >= 3 ? 16 / MT : 6;
   static constexpr bool ok = D == 3 && MT >= 1 && MT <= 4 && !M::kMirror && TF::ok &&
                              smem() * MINB <= 200 * 1024;
 };
