@@ -433,7 +433,7 @@ def _init_dist(args, world, dev):
 def run_native_arm(args, rank, world, local):
     import torch
     from paper_1403_1157_b200.operator import DiscreteOperator
-    from paper_1403_1157_b200.roofline import apply_bytes, apply_flops, executed_flops
+    from paper_1403_1157_b200.roofline import apply_bytes, apply_flops, executed_split
 
     local = local % max(torch.cuda.device_count(), 1)  # testing: ranks may share a GPU
     torch.cuda.set_device(local)
@@ -574,15 +574,21 @@ def run_native_arm(args, rank, world, local):
     fv, ff, fb = apply_flops(d, nb, Q, F, ne, n_int, n_bnd)
     names = op.kernel_names()
     per = {}
-    for name, flops in (("faces", ff), ("wall", fb), ("volume", fv)):
+    xv, xf, xb = executed_split(d, nb, Q, F, ne, n_int, n_bnd,
+                                face_classes=op.n_face_classes > 0,
+                                vol_classes=op.n_volume_classes > 0)
+    peak = fp64_peak(op)
+    for name, flops, xfl in (("faces", ff, xf), ("wall", fb, xb), ("volume", fv, xv)):
         tms, nl = kt[name]
         if nl:
             apps = 3 * nprof
+            sec = tms / apps * 1e-3
             per[name] = {"kernel": names[name], "ms_per_application": tms / apps,
                          "launches_per_application": nl / apps,
-                         "algorithmic_tflops": flops / (tms / apps * 1e-3) / 1e12,
+                         "algorithmic_tflops": flops / sec / 1e12,
+                         "executed_tflops": xfl / sec / 1e12,
+                         "executed_frac": xfl / sec / 1e12 / peak,
                          "share_of_step": tms / ms_prof}
-    peak = fp64_peak(op)
     pk = measured_peaks()
     dom = max(per, key=lambda k: per[k]["share_of_step"])
     traffic = None
@@ -615,8 +621,10 @@ def run_native_arm(args, rank, world, local):
             "per_kernel": per,
             "step_algorithmic_tflops": step_flops / step_s / 1e12,
             "step_frac": step_flops / step_s / 1e12 / peak,
-            "step_executed_tflops": 3 * executed_flops(d, nb, Q, F, ne, n_int, n_bnd)
-            / step_s / 1e12,
+            "step_executed_tflops": 3 * (xv + xf + xb) / step_s / 1e12,
+            "executed_note": "executed = the kernels' reformulated sequence without tensor-core "
+                             "padding (roofline.executed_split); the frac above uses the "
+                             "reference's algorithmic sequence, which is larger",
             "step_hbm_gbs_compulsory": 3 * apply_bytes(d, n_dofs, ne, n_int, n_bnd) / step_s / 1e9,
             "hbm_peak_gbs": pk.get("hbm_gbs")}
 

@@ -12,7 +12,7 @@ face traces) is credited with the reference's work, and
 from __future__ import annotations
 
 __all__ = ["vol_flops", "face_flops", "bface_flops", "apply_flops",
-           "apply_bytes", "executed_flops"]
+           "apply_bytes", "executed_flops", "executed_split"]
 
 
 def vol_flops(d, nb, Q, S=6):
@@ -44,16 +44,26 @@ def apply_bytes(d, n_dofs, ne, n_int, n_bnd, rk_stage=True):
     return b
 
 
-def executed_flops(d, nb, Q, F, ne, n_int, n_bnd, S=6):
-    """Flops of the reformulated sequence the kernels run (plaque model):
+def executed_split(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False,
+                   vol_classes=False):
+    """(volume, interior faces, boundary faces) flops of the reformulated
+    sequence the kernels run (plaque model), without tensor-core padding:
     volume: values of 4 species and reference gradients of 3 at every
     point, 2 pulled-back flux rows + the bilinear source projected, exact
-    stiffness diffusion and modal linear source; faces: u and d_n u per
-    side and species, lifting on one side, projection to both sides."""
+    stiffness diffusion (d(d+1)/2 metric-scaled GEMMs, or one per species
+    against the element class's summed stiffness) and the modal linear
+    source; faces: u and d_n u per side and species (Jinv n folded into the
+    gradient tables per face, or precomputed per face-geometry class),
+    lifting on one side, projection to both sides."""
     nsym = d * (d + 1) // 2
     vol = (Q * (2 * nb * (4 + 3 * d) + 2 * 3 * d * d + 40 + 2 * (2 * d * nb + nb))
-           + S * nb * 2 * nb * (nsym + 1) + S * nb * 2 * S)
-    face = (2 * 2 * F * nb * d + 2 * 2 * 2 * F * nb * S + 2 * F * F * S + F * 120
-            + 2 * 2 * 2 * F * nb * S)
+           + S * nb * 2 * nb * (1 if vol_classes else nsym + 1) + S * nb * 2 * S)
+    face = ((0 if face_classes else 2 * 2 * F * nb * d) + 2 * 2 * 2 * F * nb * S
+            + 2 * F * F * S + F * 120 + 2 * 2 * 2 * F * nb * S)
     bface = 2 * F * nb + 2 * F * nb * S
-    return ne * vol + n_int * face + n_bnd * bface
+    return ne * vol, n_int * face, n_bnd * bface
+
+
+def executed_flops(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False, vol_classes=False):
+    """Sum of ``executed_split``."""
+    return sum(executed_split(d, nb, Q, F, ne, n_int, n_bnd, S, face_classes, vol_classes))

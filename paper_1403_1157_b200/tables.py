@@ -424,8 +424,9 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
     PGF [QT][2][NNT][32]       G_n[q][pi(n)]                (face-group kernel)
 
     Returns (flat tables, per-class stride, int32 [nif][2] class of the
-    inside / outside side) or None when the mesh has more than
-    ``max_classes`` classes (the kernel then folds per face)."""
+    inside / outside side, [(table id, Jinv n)] per class) or None when the
+    mesh has more than ``max_classes`` classes (the kernel then folds per
+    face)."""
     d, nb, F = t.dim, t.nb, t.nq_face
     nif = len(t.if_code)
     if d != 3 or nif == 0 or (t.if_code & CODE_MIRROR).any():
@@ -454,7 +455,8 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
         parts.append(np.concatenate([TRF.ravel(), PRF.ravel(), _frag_qn(BP).ravel(),
                                      _frag_qn(GP).ravel()]))
     cls = np.ascontiguousarray(np.stack([inv[:nif], inv[nif:]], axis=1), dtype=np.int32)
-    return np.ascontiguousarray(np.concatenate(parts)), len(parts[0]), cls
+    keys = [(int(row[0]), row[1:].copy().view(np.float64)) for row in uniq]
+    return np.ascontiguousarray(np.concatenate(parts)), len(parts[0]), cls, keys
 
 
 def tc_face_blocks(t: OperatorTables, block: int = 8):
@@ -477,6 +479,66 @@ def tc_face_blocks(t: OperatorTables, block: int = 8):
     blocks = np.ascontiguousarray(np.stack([first, cnt], axis=1), dtype=np.int32)
     seg_blk = np.searchsorted(first, t.seg_if, side="left").astype(np.int64)
     return blocks, seg_blk
+
+
+def _o_basis(A: np.ndarray, rank: int) -> np.ndarray:
+    """Orthonormal basis of the column space of A (F x m), which must have
+    numerical rank ``rank`` (the face rules have negative weights, so the
+    basis is orthonormal in the plain inner product and W enters through
+    small Gram matrices)."""
+    U, s, _ = np.linalg.svd(A, full_matrices=False)
+    if len(s) > rank and s[rank] > 1e-11 * s[0]:
+        raise ValueError(f"trace space rank above {rank}: singular values {s[:rank + 2]}")
+    if s[rank - 1] < 1e-8 * s[0]:
+        raise ValueError(f"trace space rank below {rank}")
+    return U[:, :rank]
+
+
+def modal_face_factors(t: OperatorTables, fold):
+    """Low-rank factors of the 3D face operator (the face-group kernel's
+    modal formulation).  On a face the traces of the degree-k volume basis
+    span P_k of the face triangle, (k+1)(k+2)/2 functions, and the traces of
+    a directional derivative (Jinv n fixed per face-geometry class) span
+    P_{k-1}, k(k+1)/2 functions: with orthonormal bases Bf (F x nfm) and
+    Bd (F x ndm) of those spaces at the face points,
+
+        face_B[tab]  = Bf T[tab],     T[tab]  = Bf^T face_B[tab]
+        G_n[class]   = Bd Td[class],  Td[class] = Bd^T G_n[class]
+
+    exactly (to roundoff).  With W = diag(face weights), Mff = Bf^T W Bf and
+    Mfd = Bf^T W Bd, the face terms of reference operator.py:326-424 reduce
+    to modal algebra except the pointwise LLF flux (a_j = T_in c_in -
+    T_out c_out, g = (Td_in c_in + Td_out c_out) / 2):
+
+        B^T W rho,  rho = B (B^T W dU)   ->  T^T (Mff T_l T_l^T Mff) a_j
+        B^T W (A gav)                    ->  A T^T Mfd g
+        G_n^T W X,  X ~ dU               ->  Td^T Mfd^T a_j
+        B^T W (eta/h A dU)  (ip)         ->  eta/h A T^T Mff a_j
+
+    ``fold`` is ``tc_face_fold_tables``'s result (class keys come from it).
+    Returns dict(Bf, Bd, T [ntab][nfm][nb], Td [ncls][ndm][nb],
+    L [ntab][nfm][nfm] = Mff T T^T Mff, Mff, Mfd, nfm, ndm)."""
+    d, k, nb = t.dim, t.order, t.nb
+    if d != 3:
+        raise ValueError("the modal face factors are 3D")
+    nfm, ndm = (k + 1) * (k + 2) // 2, k * (k + 1) // 2
+    w = t.face_w
+    B = t.face_B                                     # (ntab, F, nb)
+    Bf = _o_basis(np.concatenate(list(B), axis=1), nfm)
+    T = np.einsum("qm,tqi->tmi", Bf, B)
+    cls_keys = fold[3]
+    Gn = np.stack([np.einsum("qia,a->qi", t.face_G[int(tab)], jv) for tab, jv in cls_keys])
+    if ndm > 0:
+        Bd = _o_basis(np.concatenate(list(Gn), axis=1), ndm)
+        Td = np.einsum("qm,cqi->cmi", Bd, Gn)
+    else:
+        Bd = np.zeros((len(w), 0))
+        Td = np.zeros((len(Gn), 0, nb))
+    Mff = np.einsum("qm,q,qn->mn", Bf, w, Bf)
+    Mfd = np.einsum("qm,q,qn->mn", Bf, w, Bd)
+    L = np.einsum("mk,tki,tli,ln->tmn", Mff, T, T, Mff)
+    return {"Bf": Bf, "Bd": Bd, "T": T, "Td": Td, "L": L, "Mff": Mff, "Mfd": Mfd,
+            "nfm": nfm, "ndm": ndm}
 
 
 def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):
