@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 5
+#define TDG_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -160,6 +160,12 @@ typedef struct tdg_desc {
    * NULL: the one-face species-rows kernel runs the blocks instead */
   const int32_t* face_groups;
   int64_t n_face_groups;
+  /* optional, with the face groups: operand tables of the modal face
+   * kernel (tables.modal_face_tables: face-trace factors face_B = Bf T,
+   * G_n = Bd Td), layout from the compiled sizes, per signature and per
+   * face-geometry class); NULL: the face-group kernel evaluates the full
+   * traces */
+  const double* face_modal;
   /* optional, tensor-core volume kernel: element-geometry classes
    * (tables.tc_volume_classes): per class the summed stiffness fragments
    * [ncls][KT][NNT][32], the elements in class-sorted tasks of 8 (int32
@@ -316,7 +322,8 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
  * CTA-staged generic kernels; bit 5: launch tdg_ssprk3_step's kernels
  * directly instead of replaying its cached CUDA graph; bit 13: ignore the
  * face-geometry-class tables (fold Jinv n per face); bit 14: run the
- * one-face species-rows kernel instead of the face-group kernel; bit 15:
+ * one-face species-rows kernel instead of the face-group kernel; bit 16:
+ * the face-group kernel on full traces instead of the modal one; bit 15:
  * ignore the element-geometry classes of the volume kernel; bit 12: use the
  * transposed tensor-core volume kernel wherever it compiles (default only
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs

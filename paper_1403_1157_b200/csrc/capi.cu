@@ -144,6 +144,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.ftf = d.face_tc_fold;
   p.ffold = d.if_fold;
   p.fgrp = d.face_groups;
+  p.fmod = d.face_modal;
   if (d.vol_cls_tab && d.vol_perm && d.vol_task_cls && d.vol_chunk_tasks) {
     p.vctab = d.vol_cls_tab;
     p.vperm = d.vol_perm;
@@ -485,6 +486,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->no_fold = ((variant >> 13) & 1) != 0;    // bit 13: no face-geometry-class tables
   ctx->no_groups = ((variant >> 14) & 1) != 0;  // bit 14: one-face kernel despite face groups
   ctx->no_vcls = ((variant >> 15) & 1) != 0;    // bit 15: no volume element classes
+  ctx->no_modal = ((variant >> 16) & 1) != 0;   // bit 16: face groups on full traces
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;

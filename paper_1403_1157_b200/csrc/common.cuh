@@ -66,6 +66,7 @@ struct OpParams {
   const double* __restrict__ ftf;   // face-geometry-class folded tables (may be null)
   const int32_t* __restrict__ ffold;  // [nif][2] class of the inside / outside side
   const int32_t* __restrict__ fgrp;   // face groups [n][NFQ] (may be null)
+  const double* __restrict__ fmod;    // modal face tables (may be null)
   const double* __restrict__ vctab;   // volume element-class stiffness tables (may be null)
   const int32_t* __restrict__ vperm;  // [ntask][8] class-sorted element ids
   const int32_t* __restrict__ vtcls;  // [ntask] class of each task

@@ -25,6 +25,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_tcf.cuh"
 #include "kernels_tcg.cuh"
+#include "kernels_tcm.cuh"
 #include "models.cuh"
 #include "vecops.cuh"
 
@@ -76,6 +77,7 @@ struct tdg_ctx {
   bool no_fold = false;        // testing: per-face normal-derivative folds despite class tables
   bool no_groups = false;      // testing: the one-face kernel despite face groups
   bool no_vcls = false;        // testing: per-element metric scaling despite volume classes
+  bool no_modal = false;       // testing: face groups on full traces despite modal tables
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
@@ -135,6 +137,13 @@ int configure(int nqv) {
     for (auto fn : {k_faces_tcg<D, K, M, 0>, k_faces_tcg<D, K, M, 1>, k_faces_tcg<D, K, M, 2>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcg");
+  }
+  if constexpr (TcmFace<D, K, M>::ok) {
+    const int sm = int(TcmFace<D, K, M>::smem());
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    for (auto fn : {k_faces_tcm<D, K, M, 0>, k_faces_tcm<D, K, M, 1>, k_faces_tcm<D, K, M, 2>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
+    if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcm");
   }
   if constexpr (TcVol<D, K, M>::ok) {
     for (auto fn : {k_volume_tc<D, K, M, false>, k_volume_tc<D, K, M, true>})
@@ -205,10 +214,38 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
     if (dflt && p.ftc != nullptr && p.fblk != nullptr && p.fmma != nullptr) {
       const bool fold = p.ftf != nullptr && p.ffold != nullptr && !ctx->no_fold;
       const int lm = (p.scheme == IP || p.scheme == BO) ? 0 : (p.scheme == BR2 ? 2 : 1);
+      // face groups: the modal kernel, else the full-trace group kernel,
+      // else the one-face kernel over blocks
       bool grouped = false;
-      if constexpr (TcgFace<D, K, M>::ok) {
-        grouped = fold && p.fgrp != nullptr && !ctx->no_groups;
+      if constexpr (TcmFace<D, K, M>::ok) {
+        grouped = fold && p.fgrp != nullptr && p.fmod != nullptr && !ctx->no_groups &&
+                  !ctx->no_modal;
         if (grouped && sg.g1 > sg.g0) {
+          KernelTimer kt(ctx, 0, st);
+          using T = TcmFace<D, K, M>;
+          static int resident = 0;
+          if (resident == 0) {
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_faces_tcm<D, K, M, 1>, T::THREADS,
+                                                              T::smem()) != cudaSuccess || nb < 1)
+              nb = T::MINB;
+            resident = nb;
+          }
+          int64_t grid = sg.g1 - sg.g0;
+          const int64_t cap = int64_t(ctx->num_sms) * resident;
+          grid = grid < cap ? grid : cap;
+          auto go = [&](auto kernel) {
+            kernel<<<unsigned(grid), T::THREADS, T::smem(), st>>>(p, p.fmod, p.fgrp, sg.g0, sg.g1, U,
+                                                                  acc);
+          };
+          go(lm == 0 ? k_faces_tcm<D, K, M, 0>
+                     : (lm == 1 ? k_faces_tcm<D, K, M, 1> : k_faces_tcm<D, K, M, 2>));
+        }
+      }
+      if constexpr (TcgFace<D, K, M>::ok) {
+        const bool use = !grouped && fold && p.fgrp != nullptr && !ctx->no_groups;
+        grouped = grouped || use;
+        if (use && sg.g1 > sg.g0) {
           KernelTimer kt(ctx, 0, st);
           using T = TcgFace<D, K, M>;
           // persistent: the resident CTAs loop over the segment's groups

@@ -1,0 +1,327 @@
+// Interior faces on the FP64 tensor cores (3D) in the MODAL face space.
+// On a face the traces of the degree-k volume basis span P_k of the face
+// triangle (nfm = (k+1)(k+2)/2 functions) and the traces of a directional
+// derivative (Jinv n, fixed per face-geometry class) span P_{k-1} (ndm =
+// k(k+1)/2): face_B = Bf T, G_n = Bd Td with orthonormal Bf, Bd at the face
+// points (tables.modal_face_factors).  The face terms of reference
+// operator.py:326-424 then need point values only for the nonlinear LLF
+// flux; everything else is small modal algebra (a_j = T_in c_in - T_out
+// c_out, g = (Td_in c_in + Td_out c_out) / 2, W = face weights):
+//
+//   R_in  =  sfac (T_in^T  Ybr + Td_in^T  Xbr)
+//   R_out =  sfac (-T_out^T Ybr + Td_out^T Xbr)
+//   Ybr   =  A Mfd g - ki L_l a_j - Bf^T W cnv      (ip: - eta/h A Mff a_j)
+//   Xbr   =  adj/2 A Mfd^T a_j
+//   cnv   =  lambda/2 du + (F_in + F_out).n / 2     pointwise, du = Bf a_j
+//
+// with L = Mff T T^T Mff the lifting (B (B^T W dU) in modal form).  At
+// p = 3 this is 157 DMMAs per 8 (face, species) rows against 357 for the
+// one-face kernel's 6 rows.  The CTA runs a face group of
+// tables.tc_face_groups (4 faces sharing both sides' classes and the
+// lifting side: every B operand is shared), one warp per 8 rows, like
+// k_faces_tcg:
+//
+//   A  (modal)     a_in, a_out, d_in, d_out from the coefficients
+//   B1 (points)    du, u_in, gav per point tile -> physics slots of xs
+//   physics        LLF wave speed / taxis flux normals, CTA-wide
+//   B2 (points)    cnv -> p = Bf^T W cnv
+//   C  (modal)     Ybr, Xbr -> both sides' contributions
+//
+// The 96-entry point loops are unrolled (du stays in registers).
+// Operand tables: tables.modal_face_tables (fragment-major, pi-permuted
+// output columns so a GEMM's accumulator is the next GEMM's A operand).
+#pragma once
+
+#include "common.cuh"
+#include "kernels_mma.cuh"
+#include "kernels_tcf.cuh"
+#include "models.cuh"
+
+namespace tdg {
+
+// slot of species s among the physics (value) species, -1 if none
+template <class M>
+__host__ __device__ constexpr int mval_slot(int s) {
+  for (int i = 0; i < M::NVAL; ++i)
+    if (M::val_sp(i) == s) return i;
+  return -1;
+}
+template <class M>
+__host__ __device__ constexpr int mgrad_slot(int s) {
+  for (int i = 0; i < M::NGRAD; ++i)
+    if (M::grad_sp(i) == s) return i;
+  return -1;
+}
+__host__ __device__ constexpr int gcd_m(int a, int b) { return b == 0 ? a : gcd_m(b, a % b); }
+
+template <int D, int K, class M>
+struct TcmFace {
+  using Dm = Dims<D, K>;
+  static constexpr int NB = Dm::NB, S = M::S, SN = S * NB, F = Dm::NQF, NFG = Dm::NFG;
+  static constexpr int NT = Dm::NT;  // trace-table signatures
+  static constexpr int QP = ceil_to(F, 8), QT = QP / 8;
+  static constexpr int KT = (NB + 3) / 4, NNT = (NB + 7) / 8;
+  static constexpr int NFM = (K + 1) * (K + 2) / 2, NDM0 = K * (K + 1) / 2,
+                       NDM = NDM0 > 0 ? NDM0 : 1;
+  static constexpr int KTF = (NFM + 3) / 4, NNF = (NFM + 7) / 8;
+  static constexpr int KTD = (NDM + 3) / 4, NND = (NDM + 7) / 8;
+  // table offsets (doubles), tables.modal_face_tables
+  static constexpr int OBF = 0, OBD = OBF + KTF * QT * 32, OWB = OBD + KTD * QT * 32,
+                       OMFD = OWB + QT * 2 * NNF * 32, OMDF = OMFD + KTD * NNF * 32,
+                       OMFF = OMDF + KTF * NND * 32, GLOB = OMFF + KTF * NNF * 32;
+  static constexpr int OT1 = 0, OT4 = OT1 + KT * NNF * 32, OL = OT4 + KTF * NNT * 32,
+                       TABS = OL + KTF * NNF * 32;
+  static constexpr int OD1 = 0, OD4 = OD1 + KT * NND * 32, CLS = OD4 + KTD * NNT * 32;
+  static constexpr int OCLS = GLOB + NT * TABS;  // first class block
+  static constexpr int NCV = 1 + M::NFX;
+  static constexpr int NFQ = 8 / gcd_m(S, 8), MT = S * NFQ / 8, THREADS = 32 * MT;
+  // physics slots per (face, point): u_in, u_out of the value species, gav
+  // of the gradient species (odd stride: conflict-free physics reads)
+  static constexpr int NSL = 2 * M::NVAL + M::NGRAD, XS = NSL | 1;
+  static constexpr int OXS = 0, OCV = OXS + NFQ * QP * XS, CWS = OCV + NFQ * QP * NCV;
+  static constexpr size_t smem() { return size_t(CWS) * 8; }
+  static constexpr int MINB = 16 / MT;
+  static constexpr bool ok = D == 3 && M::kConv && !M::kMirror && MT >= 1 && MT <= 4 &&
+                             F <= 64 && smem() * MINB <= 200 * 1024;
+};
+
+// LM: lifting sides (operator.py:336-357): 0 none (ip, bo), 1 the K- side
+// (cdg2, cdg), 2 both (br2)
+template <int D, int K, class M, int LM>
+__global__ void __launch_bounds__(TcmFace<D, K, M>::THREADS, TcmFace<D, K, M>::MINB)
+k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict__ groups,
+            int64_t g0, int64_t g1, const double* __restrict__ U, double* __restrict__ ACC) {
+  using T = TcmFace<D, K, M>;
+  constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG, QP = T::QP;
+  constexpr int QT = T::QT, KT = T::KT, NNT = T::NNT;
+  constexpr int KTF = T::KTF, NNF = T::NNF, KTD = T::KTD, NND = T::NND;
+  constexpr int NCV = T::NCV, XS = T::XS, NFQ = T::NFQ;
+  constexpr bool br2 = LM == 2, lift = LM > 0;
+  extern __shared__ __align__(16) double sm[];
+  double* xs = sm + T::OXS;   // [NFQ][QP][XS] physics slots
+  double* cvs = sm + T::OCV;  // [NFQ][QP][NCV]
+  const int lane = threadIdx.x & 31, mt = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int fq = (8 * mt + g) / S, sp = (8 * mt + g) % S;
+  const double As = p.A[sp];
+  // this row's physics slots (-1: none)
+  int slv = -1, slg = -1;
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (sp == s) {
+      slv = mval_slot<M>(s);
+      slg = mgrad_slot<M>(s);
+    }
+  const double* tg = tm;  // global block
+
+  for (int64_t grp = g0 + blockIdx.x; grp < g1; grp += gridDim.x) {
+    const int32_t* gf = groups + grp * NFQ;
+    const int f0 = __ldg(gf);
+    const int code0 = __ldg(p.ifcode + f0);
+    const int2 cl = __ldg(reinterpret_cast<const int2*>(p.ffold) + f0);
+    const int sig = code0 & 1023;
+    const double* Ti = tm + T::GLOB + size_t(sig & 31) * T::TABS;
+    const double* To = tm + T::GLOB + size_t((sig >> 5) & 31) * T::TABS;
+    const double* Ci = tm + T::OCLS + size_t(cl.x) * T::CLS;
+    const double* Co = tm + T::OCLS + size_t(cl.y) * T::CLS;
+    const bool min_ = code_minus_in(code0);  // one lifting side per group
+    const int fid = __ldg(gf + fq);
+    const bool fv = fid >= 0;
+    const int fs = fv ? fid : f0;
+    const double* gg = p.ifgeo + int64_t(fs) * NFG;
+    const double sfac = fv ? __ldg(gg + 2 * D) : 0.0;
+    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + fs);
+
+    // ---- A: face modes / d-modes of both sides ----------------------------
+    double aI[NNF][2], aO[NNF][2], dI[NND][2], dO[NND][2];
+#pragma unroll
+    for (int n = 0; n < NNF; ++n) aI[n][0] = aI[n][1] = aO[n][0] = aO[n][1] = 0.0;
+#pragma unroll
+    for (int n = 0; n < NND; ++n) dI[n][0] = dI[n][1] = dO[n][0] = dO[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const bool in = fv && 4 * kt + t < NB;
+      const double ci = in ? __ldg(U + int64_t(el.x) * SN + sp * NB + 4 * kt + t) : 0.0;
+      const double co = in ? __ldg(U + int64_t(el.y) * SN + sp * NB + 4 * kt + t) : 0.0;
+#pragma unroll
+      for (int n = 0; n < NNF; ++n) {
+        const int o = T::OT1 + (kt * NNF + n) * 32 + lane;
+        dmma(aI[n][0], aI[n][1], ci, __ldg(Ti + o));
+        dmma(aO[n][0], aO[n][1], co, __ldg(To + o));
+      }
+#pragma unroll
+      for (int n = 0; n < NND; ++n) {
+        const int o = T::OD1 + (kt * NND + n) * 32 + lane;
+        dmma(dI[n][0], dI[n][1], ci, __ldg(Ci + o));
+        dmma(dO[n][0], dO[n][1], co, __ldg(Co + o));
+      }
+    }
+    // A fragments of the modal vectors: k-step kt holds mode 4 kt + t =
+    // pi(8 (kt/2) + 2t + kt%2), i.e. accumulator entry [kt/2][kt%2]
+    double aJ[NNF][2], gm[NND][2];
+#pragma unroll
+    for (int n = 0; n < NNF; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) aJ[n][j] = aI[n][j] - aO[n][j];
+#pragma unroll
+    for (int n = 0; n < NND; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) gm[n][j] = 0.5 * (dI[n][j] + dO[n][j]);
+
+    // ---- B1: point values -> physics slots; du kept in registers -------
+    double du[QT][2];
+#pragma unroll
+    for (int qt = 0; qt < QT; ++qt) {
+      double d0[2] = {0.0, 0.0}, u0[2] = {0.0, 0.0}, gv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int kt = 0; kt < KTF; ++kt) {
+        const double b = __ldg(tg + T::OBF + (kt * QT + qt) * 32 + lane);
+        dmma(d0[0], d0[1], aJ[kt / 2][kt % 2], b);
+        dmma(u0[0], u0[1], aI[kt / 2][kt % 2], b);
+      }
+#pragma unroll
+      for (int kt = 0; kt < KTD; ++kt)  // (warp-wide: every row, used by the gradient species)
+        dmma(gv[0], gv[1], gm[kt / 2][kt % 2], __ldg(tg + T::OBD + (kt * QT + qt) * 32 + lane));
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        du[qt][j] = d0[j];
+        if (slv >= 0) {
+          double* x = xs + (fq * QP + 8 * qt + 2 * t + j) * XS;
+          x[slv] = u0[j];
+          x[M::NVAL + slv] = u0[j] - d0[j];
+          if (slg >= 0) x[2 * M::NVAL + slg] = gv[j];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- physics, once per (face, point), CTA-wide -------------------------
+    for (int i = threadIdx.x; i < NFQ * F; i += T::THREADS) {
+      const int f = i / F, q = i - f * F;
+      const double* xq = xs + (f * QP + q) * XS;
+      auto fetch = [xq](int kind, int s2) {
+        return kind == 0 ? xq[mval_slot<M>(s2)]
+                         : (kind == 1 ? xq[M::NVAL + mval_slot<M>(s2)]
+                                      : xq[2 * M::NVAL + mgrad_slot<M>(s2)]);
+      };
+      M::face_point(p.P, fetch, cvs + (f * QP + q) * NCV);
+    }
+    __syncthreads();
+    // ---- B2: p = Bf^T W cnv ------------------------------------------------
+    double pw[NNF][2];
+#pragma unroll
+    for (int n = 0; n < NNF; ++n) pw[n][0] = pw[n][1] = 0.0;
+#pragma unroll
+    for (int qt = 0; qt < QT; ++qt) {
+      double cn[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = 8 * qt + 2 * t + j;
+        double v = 0.0;
+        if (q < F) {
+          const double* c = cvs + (fq * QP + q) * NCV;
+          v = 0.5 * c[0] * du[qt][j];
+#pragma unroll
+          for (int k = 0; k < M::NFX; ++k)
+            if (sp == k) v = fma(0.5, c[1 + k], v);
+        }
+        cn[j] = v;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int n = 0; n < NNF; ++n)
+          dmma(pw[n][0], pw[n][1], cn[ks], __ldg(tg + T::OWB + ((qt * 2 + ks) * NNF + n) * 32 + lane));
+    }
+    // ---- C: modal brackets, both sides ---------------------------------------
+    // Ybr = A Mfd g - ki L a_j - p  (ip: - eta/h A Mff a_j)
+    double yb[NNF][2], xb[NND][2];
+#pragma unroll
+    for (int n = 0; n < NNF; ++n) yb[n][0] = -pw[n][0], yb[n][1] = -pw[n][1];
+#pragma unroll
+    for (int n = 0; n < NND; ++n) xb[n][0] = xb[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KTD; ++kt)
+#pragma unroll
+      for (int n = 0; n < NNF; ++n)
+        dmma(yb[n][0], yb[n][1], As * gm[kt / 2][kt % 2],
+             __ldg(tg + T::OMFD + (kt * NNF + n) * 32 + lane));
+    if constexpr (lift) {
+      const double wside = br2 ? 0.5 : 1.0;
+      const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac * As;
+      const double ki = fac0 * __ldg(gg + 2 * D + ((br2 || min_) ? 2 : 3));
+      const double ko = br2 ? fac0 * __ldg(gg + 2 * D + 3) : 0.0;
+      const double* Tl = (br2 || min_) ? Ti : To;
+#pragma unroll
+      for (int kt = 0; kt < KTF; ++kt)
+#pragma unroll
+        for (int n = 0; n < NNF; ++n) {
+          const int o = T::OL + (kt * NNF + n) * 32 + lane;
+          dmma(yb[n][0], yb[n][1], -ki * aJ[kt / 2][kt % 2], __ldg(Tl + o));
+          if constexpr (br2) dmma(yb[n][0], yb[n][1], -ko * aJ[kt / 2][kt % 2], __ldg(To + o));
+        }
+    } else {
+      if (p.scheme == IP) {
+        const double kip = -p.eta / __ldg(gg + 2 * D + 1) * As;
+#pragma unroll
+        for (int kt = 0; kt < KTF; ++kt)
+#pragma unroll
+          for (int n = 0; n < NNF; ++n)
+            dmma(yb[n][0], yb[n][1], kip * aJ[kt / 2][kt % 2],
+                 __ldg(tg + T::OMFF + (kt * NNF + n) * 32 + lane));
+      }
+    }
+    {  // Xbr = adj/2 A Mfd^T a_j
+      const double kx = 0.5 * p.adj * As;
+#pragma unroll
+      for (int kt = 0; kt < KTF; ++kt)
+#pragma unroll
+        for (int n = 0; n < NND; ++n)
+          dmma(xb[n][0], xb[n][1], kx * aJ[kt / 2][kt % 2],
+               __ldg(tg + T::OMDF + (kt * NND + n) * 32 + lane));
+    }
+    // R_in = sfac (T_in^T Ybr + Td_in^T Xbr), R_out = sfac (-T_out^T Ybr + Td_out^T Xbr)
+    double ri[NNT][2], ro[NNT][2];
+#pragma unroll
+    for (int nt = 0; nt < NNT; ++nt) ri[nt][0] = ri[nt][1] = ro[nt][0] = ro[nt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KTF; ++kt) {
+      const double a = sfac * yb[kt / 2][kt % 2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) {
+        const int o = T::OT4 + (kt * NNT + nt) * 32 + lane;
+        dmma(ri[nt][0], ri[nt][1], a, __ldg(Ti + o));
+        dmma(ro[nt][0], ro[nt][1], -a, __ldg(To + o));
+      }
+    }
+#pragma unroll
+    for (int kt = 0; kt < KTD; ++kt) {
+      const double a = sfac * xb[kt / 2][kt % 2];
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt) {
+        const int o = T::OD4 + (kt * NNT + nt) * 32 + lane;
+        dmma(ri[nt][0], ri[nt][1], a, __ldg(Ci + o));
+        dmma(ro[nt][0], ro[nt][1], a, __ldg(Co + o));
+      }
+    }
+    // face-sum rows: lane entries (face fq, species sp, basis 4 (2nt + j) + t)
+    if (fv) {
+      const int code = __ldg(p.ifcode + fid);
+      const bool skip_out = code_skip_out(code);
+      const bool fin = code_first_in(code), fout = code_first_out(code);
+      double* fci = ACC + int64_t(el.x) * SN + sp * NB;
+      double* fco = ACC + int64_t(el.y) * SN + sp * NB;
+#pragma unroll
+      for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 4 * (2 * nt + j) + t;
+          if (i < NB) {
+            acc_put(fci + i, ri[nt][j], fin);
+            if (!skip_out) acc_put(fco + i, ro[nt][j], fout);
+          }
+        }
+    }
+  }
+}
+
+}  // namespace tdg

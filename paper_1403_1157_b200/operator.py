@@ -96,7 +96,7 @@ class DiscreteOperator:
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
         from .tables import (mma_face_tables, tc_face_blocks, tc_face_fold_tables,
                              tc_face_groups, tc_face_tables, tc_volume_classes,
-                             tc_volume_tables)
+                             tc_volume_tables, modal_face_tables)
         mma, self._mma_stride = mma_face_tables(t)
         blocks, seg_blk = tc_face_blocks(t)
         fold = tc_face_fold_tables(t)
@@ -110,6 +110,7 @@ class DiscreteOperator:
             self._keep["if_fold"] = dev(fold[2])
             groups, seg_grp = tc_face_groups(t, fold[2], t.n_species)
             self._keep["face_groups"] = dev(groups)
+            self._keep["face_modal"] = dev(modal_face_tables(t, fold))
         # element-geometry classes of the tensor-core volume kernel (3D and
         # 2D p = 3; meshes of congruent cells)
         vcls = tc_volume_classes(t) if (t.dim == 3 or t.order == 3) else None
@@ -158,6 +159,7 @@ class DiscreteOperator:
             if_fold=ptr(k["if_fold"]) if fold is not None else None,
             face_groups=ptr(k["face_groups"]) if fold is not None else None,
             n_face_groups=len(groups),
+            face_modal=ptr(k["face_modal"]) if fold is not None else None,
             vol_cls_tab=ptr(k["vol_cls_tab"]) if vcls is not None else None,
             vol_perm=ptr(k["vol_perm"]) if vcls is not None else None,
             vol_task_cls=ptr(k["vol_task_cls"]) if vcls is not None else None,
@@ -297,7 +299,7 @@ class DiscreteOperator:
         t = self.tables
         if t.dim == 3:
             if self.n_face_classes and len(self._keep.get("face_groups", ())):
-                faces = "k_faces_tcg"
+                faces = "k_faces_tcm" if "face_modal" in self._keep else "k_faces_tcg"
             else:
                 faces = "k_faces_tcs"
             wall = "k_faces_mma"
@@ -312,7 +314,7 @@ class DiscreteOperator:
     def set_variant(self, generic: bool = False, no_graph: bool = False,
                     tc_volume: bool = False, face_ctas_per_sm: int = 0,
                     no_fold: bool = False, no_groups: bool = False,
-                    no_volume_classes: bool = False):
+                    no_volume_classes: bool = False, no_modal: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
         kernels directly instead of replaying its CUDA graph; ``tc_volume``
@@ -322,11 +324,14 @@ class DiscreteOperator:
         Jinv n per face despite face-geometry-class tables; ``no_groups``
         runs the one-face species-rows kernel instead of the face-group
         kernel; ``no_volume_classes`` scales the volume kernel's diffusion
-        per element despite element-geometry classes.  Defaults: fastest."""
+        per element despite element-geometry classes; ``no_modal`` runs the
+        face-group kernel on full traces instead of the modal face space.
+        Defaults: fastest."""
         self._call(self.lib.tdg_set_variant, self._ctx,
                    int(bool(generic)) | (int(bool(no_graph)) << 5)
                    | (int(bool(tc_volume)) << 12) | (int(bool(no_fold)) << 13)
                    | (int(bool(no_groups)) << 14) | (int(bool(no_volume_classes)) << 15)
+                   | (int(bool(no_modal)) << 16)
                    | ((int(face_ctas_per_sm) & 15) << 8),
                    what="tdg_set_variant")
 

@@ -525,7 +525,19 @@ def modal_face_factors(t: OperatorTables, fold):
     w = t.face_w
     B = t.face_B                                     # (ntab, F, nb)
     Bf = _o_basis(np.concatenate(list(B), axis=1), nfm)
-    T = np.einsum("qm,tqi->tmi", Bf, B)
+    # T = Bf^+ B in extended precision, kept as a double-double pair (T,
+    # Tlo): the jump T_in c_in - T_out c_out of a continuous field cancels
+    # to roundoff only if both tables carry B to well below one ulp (the
+    # fp64-rounded T alone leaves ~1e-14 |c| in the jump, which the 1/h
+    # penalties amplify)
+    Bl = Bf.astype(np.longdouble)
+    G = np.linalg.inv((Bf.T @ Bf).astype(np.float64)).astype(np.longdouble)
+    eye = np.eye(nfm, dtype=np.longdouble)
+    for _ in range(3):
+        G = G + G @ (eye - (Bl.T @ Bl) @ G)
+    Tx = np.stack([G @ (Bl.T @ B[k].astype(np.longdouble)) for k in range(len(B))])
+    T = Tx.astype(np.float64)
+    Tlo = (Tx - T.astype(np.longdouble)).astype(np.float64)
     cls_keys = fold[3]
     Gn = np.stack([np.einsum("qia,a->qi", t.face_G[int(tab)], jv) for tab, jv in cls_keys])
     if ndm > 0:
@@ -537,8 +549,59 @@ def modal_face_factors(t: OperatorTables, fold):
     Mff = np.einsum("qm,q,qn->mn", Bf, w, Bf)
     Mfd = np.einsum("qm,q,qn->mn", Bf, w, Bd)
     L = np.einsum("mk,tki,tli,ln->tmn", Mff, T, T, Mff)
-    return {"Bf": Bf, "Bd": Bd, "T": T, "Td": Td, "L": L, "Mff": Mff, "Mfd": Mfd,
+    return {"Bf": Bf, "Bd": Bd, "T": T, "Tlo": Tlo, "Td": Td, "L": L, "Mff": Mff, "Mfd": Mfd,
             "nfm": nfm, "ndm": ndm}
+
+
+def _pi_mat(M: np.ndarray, rows: int, ncols: int):
+    """[rows][8 ceil(ncols/8)] with column n holding M[:, pi(n)] (zero past
+    ncols) -- the output-column permutation of the DMMA kernels."""
+    pic, ok = _pi_cols(ncols)
+    out = np.zeros((rows, len(pic)))
+    out[:M.shape[0]] = M[:, pic] * ok
+    return out
+
+
+def modal_face_tables(t: OperatorTables, fold):
+    """Operand tables of the modal face-group kernel (csrc/kernels_tcm.cuh)
+    from ``modal_face_factors``, fragment-major, concatenated as
+
+      global     BF  [KTF][QT][32]        Bf^T          point values of face modes
+                 BD  [KTD][QT][32]        Bd^T          of d-modes
+                 WB  [QT][2][NNF][32]     w Bf (pi)     projection of the pointwise flux
+                 MFD [KTD][NNF][32]       Mfd^T (pi)    A gav term
+                 MDF [KTF][NND][32]       Mfd (pi)      adjoint term
+                 MFF [KTF][NNF][32]       Mff (pi)      ip penalty
+      per table  T1  [KT][NNF][32]        T^T (pi)      face modes of the coefficients
+                 T4  [KTF][NNT][32]       T (pi)        back to the volume modes
+                 L   [KTF][NNF][32]       L^T (pi)      lifting (Mff T T^T Mff)
+      per class  D1  [KT][NND][32]        Td^T (pi)     d-modes of the coefficients
+                 D4  [KTD][NNT][32]       Td (pi)       back to the volume modes
+
+    with nfm / ndm face / d-modes, KTF = ceil(nfm/4), NNF = ceil(nfm/8),
+    KTD, NND likewise, KT = ceil(nb/4), NNT = ceil(nb/8), QT = ceil(F/8).
+    Returns the flat array."""
+    mf = modal_face_factors(t, fold)
+    nb, F = t.nb, t.nq_face
+    nfm, ndm = mf["nfm"], mf["ndm"]
+    KTF, KTD, KT = -(-nfm // 4), -(-max(ndm, 1) // 4), -(-nb // 4)
+    QP = _ceil(F, 8)
+    Bf = np.zeros((QP, 4 * KTF)); Bf[:F, :nfm] = mf["Bf"]
+    Bd = np.zeros((QP, 4 * KTD)); Bd[:F, :ndm] = mf["Bd"]
+    w = np.zeros(QP); w[:F] = t.face_w
+    parts = [_frag_kq(Bf.T), _frag_kq(Bd.T),
+             _frag_qn(_pi_mat(w[:, None] * Bf[:, :nfm], QP, nfm)),
+             _frag_kn(_pi_mat(mf["Mfd"].T, 4 * KTD, nfm)),
+             _frag_kn(_pi_mat(mf["Mfd"], 4 * KTF, ndm)),
+             _frag_kn(_pi_mat(mf["Mff"].T, 4 * KTF, nfm))]
+    for k in range(t.face_B.shape[0]):
+        T = mf["T"][k]
+        parts += [_frag_kn(_pi_mat(T.T, 4 * KT, nfm)), _frag_kn(_pi_mat(T, 4 * KTF, nb)),
+                  _frag_kn(_pi_mat(mf["L"][k].T, 4 * KTF, nfm))]
+    for c in range(mf["Td"].shape[0]):
+        Td = mf["Td"][c]
+        parts += [_frag_kn(_pi_mat(Td.T, 4 * KT, max(ndm, 1))), _frag_kn(_pi_mat(Td, 4 * KTD, nb))]
+    return np.ascontiguousarray(np.concatenate([p.ravel() for p in parts]))
 
 
 def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):

@@ -31,7 +31,7 @@ def _modal_face(em, mf, cls_in, cls_out, U, code, ein, eout, g):
     ci, co = U[ein], U[eout]
     a_in, a_out = ci @ T[tin].T, co @ T[tout].T           # (S, nfm)
     d_in, d_out = ci @ Td[cls_in].T, co @ Td[cls_out].T   # (S, ndm)
-    a_j = a_in - a_out
+    a_j = a_in - a_out + (ci @ mf["Tlo"][tin].T - co @ mf["Tlo"][tout].T)
     gm = 0.5 * (d_in + d_out)
     ui, uo = a_in @ Bf.T, a_out @ Bf.T                    # (S, F) physics inputs
     gn = gm @ Bd.T
