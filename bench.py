@@ -576,7 +576,8 @@ def run_native_arm(args, rank, world, local):
     per = {}
     xv, xf, xb = executed_split(d, nb, Q, F, ne, n_int, n_bnd,
                                 face_classes=op.n_face_classes > 0,
-                                vol_classes=op.n_volume_classes > 0)
+                                vol_classes=op.n_volume_classes > 0,
+                                modal_order=t.order if names["faces"] == "k_faces_tcm" else None)
     peak = fp64_peak(op)
     for name, flops, xfl in (("faces", ff, xf), ("wall", fb, xb), ("volume", fv, xv)):
         tms, nl = kt[name]

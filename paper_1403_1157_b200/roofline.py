@@ -12,7 +12,7 @@ face traces) is credited with the reference's work, and
 from __future__ import annotations
 
 __all__ = ["vol_flops", "face_flops", "bface_flops", "apply_flops",
-           "apply_bytes", "executed_flops", "executed_split"]
+           "apply_bytes", "executed_flops", "executed_split", "modal_face_flops"]
 
 
 def vol_flops(d, nb, Q, S=6):
@@ -44,8 +44,20 @@ def apply_bytes(d, n_dofs, ne, n_int, n_bnd, rk_stage=True):
     return b
 
 
+def modal_face_flops(d, k, nb, F, S=6):
+    """Flops per interior face of the modal face kernel (csrc/kernels_tcm.cuh):
+    face / d-modes of both sides, point values of the jump, u_in and gav,
+    the LLF physics, the projection of the pointwise flux, the modal
+    brackets (A Mfd g, lifting, adjoint term) and the back-projection to
+    both sides' volume modes (no tensor-core padding)."""
+    nfm, ndm = (k + 1) * (k + 2) // 2, k * (k + 1) // 2
+    per_species = (4 * (nfm + ndm) * nb + 2 * F * (2 * nfm + ndm) + 2 * F * nfm
+                   + 4 * nfm * ndm + 2 * nfm * nfm + 4 * (nfm + ndm) * nb)
+    return S * per_species + 120 * F
+
+
 def executed_split(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False,
-                   vol_classes=False):
+                   vol_classes=False, modal_order=None):
     """(volume, interior faces, boundary faces) flops of the reformulated
     sequence the kernels run (plaque model), without tensor-core padding:
     volume: values of 4 species and reference gradients of 3 at every
@@ -60,10 +72,14 @@ def executed_split(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False,
            + S * nb * 2 * nb * (1 if vol_classes else nsym + 1) + S * nb * 2 * S)
     face = ((0 if face_classes else 2 * 2 * F * nb * d) + 2 * 2 * 2 * F * nb * S
             + 2 * F * F * S + F * 120 + 2 * 2 * 2 * F * nb * S)
+    if modal_order is not None:   # the modal face kernel
+        face = modal_face_flops(d, modal_order, nb, F, S)
     bface = 2 * F * nb + 2 * F * nb * S
     return ne * vol, n_int * face, n_bnd * bface
 
 
-def executed_flops(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False, vol_classes=False):
+def executed_flops(d, nb, Q, F, ne, n_int, n_bnd, S=6, face_classes=False, vol_classes=False,
+                   modal_order=None):
     """Sum of ``executed_split``."""
-    return sum(executed_split(d, nb, Q, F, ne, n_int, n_bnd, S, face_classes, vol_classes))
+    return sum(executed_split(d, nb, Q, F, ne, n_int, n_bnd, S, face_classes, vol_classes,
+                              modal_order))
