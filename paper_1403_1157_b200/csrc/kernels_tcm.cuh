@@ -61,17 +61,19 @@ struct TcmFace {
   static constexpr int NT = Dm::NT;  // trace-table signatures
   static constexpr int QP = ceil_to(F, 8), QT = QP / 8;
   static constexpr int KT = (NB + 3) / 4, NNT = (NB + 7) / 8;
-  static constexpr int NFM = (K + 1) * (K + 2) / 2, NDM0 = K * (K + 1) / 2,
-                       NDM = NDM0 > 0 ? NDM0 : 1;
-  static constexpr int KTF = (NFM + 3) / 4, NNF = (NFM + 7) / 8;
-  static constexpr int KTD = (NDM + 3) / 4, NND = (NDM + 7) / 8;
-  // table offsets (doubles), tables.modal_face_tables
-  static constexpr int OBF = 0, OBD = OBF + KTF * QT * 32, OWB = OBD + KTD * QT * 32,
-                       OMFD = OWB + QT * 2 * NNF * 32, OMDF = OMFD + KTD * NNF * 32,
-                       OMFF = OMDF + KTF * NND * 32, GLOB = OMFF + KTF * NNF * 32;
-  static constexpr int OT1 = 0, OT4 = OT1 + KT * NNF * 32, OL = OT4 + KTF * NNT * 32,
-                       TABS = OL + KTF * NNF * 32;
-  static constexpr int OD1 = 0, OD4 = OD1 + KT * NND * 32, CLS = OD4 + KTD * NNT * 32;
+  static constexpr int NFM = (K + 1) * (K + 2) / 2, NDM = K * (K + 1) / 2, NV = NFM + NDM;
+  // the modal vector v = (a | d) of a row: k-steps [0, KA) hold the a part,
+  // [KD0, KTV) the d part; output tiles [0, NAT) the a part, [NAT0, NNV)
+  // the d part (tables.modal_face_tables)
+  static constexpr int KA = (NFM + 3) / 4, KTV = (NV + 3) / 4, KD0 = NFM / 4;
+  static constexpr int NNV = (NV + 7) / 8, NAT = (NFM + 7) / 8, NAT0 = NFM / 8;
+  // table offsets (doubles)
+  static constexpr int OBF = 0, OBD = OBF + KA * QT * 32, OWB = OBD + (KTV - KD0) * QT * 32,
+                       OMFD = OWB + QT * 2 * NAT * 32, OMDF = OMFD + (KTV - KD0) * NAT * 32,
+                       OMFF = OMDF + KA * (NNV - NAT0) * 32, GLOB = OMFF + KA * NAT * 32;
+  static constexpr int OL = 0, TABS = KA * NAT * 32;
+  static constexpr int OTD1 = 0, OTD4 = OTD1 + KT * NNV * 32, OTD4M = OTD4 + KTV * NNT * 32,
+                       CLS = OTD4M + KTV * NNT * 32;
   static constexpr int OCLS = GLOB + NT * TABS;  // first class block
   static constexpr int NCV = 1 + M::NFX;
   static constexpr int NFQ = 8 / gcd_m(S, 8), MT = S * NFQ / 8, THREADS = 32 * MT;
@@ -83,8 +85,8 @@ struct TcmFace {
   // 80 registers (small spills) -> 8 CTAs / 24 warps per SM: 64^3 p = 3
   // faces 10.8 -> 10.3 ms, p = 2 6.2 -> 5.1 ms against 128 registers
   static constexpr int MINB = 7;
-  static constexpr bool ok = D == 3 && M::kConv && !M::kMirror && MT >= 1 && MT <= 4 &&
-                             F <= 64 && smem() * MINB <= 200 * 1024;
+  static constexpr bool ok = D == 3 && K >= 1 && M::kConv && !M::kMirror && MT >= 1 &&
+                             MT <= 4 && F <= 64 && smem() * MINB <= 200 * 1024;
 };
 
 // LM: lifting sides (operator.py:336-357): 0 none (ip, bo), 1 the K- side
@@ -96,7 +98,8 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
   using T = TcmFace<D, K, M>;
   constexpr int NB = T::NB, S = T::S, SN = T::SN, F = T::F, NFG = T::NFG, QP = T::QP;
   constexpr int QT = T::QT, KT = T::KT, NNT = T::NNT;
-  constexpr int KTF = T::KTF, NNF = T::NNF, KTD = T::KTD, NND = T::NND;
+  constexpr int KA = T::KA, KTV = T::KTV, KD0 = T::KD0, NNV = T::NNV, NAT = T::NAT,
+                NAT0 = T::NAT0;
   constexpr int NCV = T::NCV, XS = T::XS, NFQ = T::NFQ;
   constexpr bool br2 = LM == 2, lift = LM > 0;
   extern __shared__ __align__(16) double sm[];
@@ -134,41 +137,34 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
     const double sfac = fv ? __ldg(gg + 2 * D) : 0.0;
     const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + fs);
 
-    // ---- A: face modes / d-modes of both sides ----------------------------
-    double aI[NNF][2], aO[NNF][2], dI[NND][2], dO[NND][2];
+    // ---- A: modal vectors v = (a | d) of both sides -----------------------
+    double vI[NNV][2], vO[NNV][2];
 #pragma unroll
-    for (int n = 0; n < NNF; ++n) aI[n][0] = aI[n][1] = aO[n][0] = aO[n][1] = 0.0;
-#pragma unroll
-    for (int n = 0; n < NND; ++n) dI[n][0] = dI[n][1] = dO[n][0] = dO[n][1] = 0.0;
+    for (int n = 0; n < NNV; ++n) vI[n][0] = vI[n][1] = vO[n][0] = vO[n][1] = 0.0;
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       const bool in = fv && 4 * kt + t < NB;
       const double ci = in ? __ldg(U + int64_t(el.x) * SN + sp * NB + 4 * kt + t) : 0.0;
       const double co = in ? __ldg(U + int64_t(el.y) * SN + sp * NB + 4 * kt + t) : 0.0;
 #pragma unroll
-      for (int n = 0; n < NNF; ++n) {
-        const int o = T::OT1 + (kt * NNF + n) * 32 + lane;
-        dmma(aI[n][0], aI[n][1], ci, __ldg(Ti + o));
-        dmma(aO[n][0], aO[n][1], co, __ldg(To + o));
-      }
-#pragma unroll
-      for (int n = 0; n < NND; ++n) {
-        const int o = T::OD1 + (kt * NND + n) * 32 + lane;
-        dmma(dI[n][0], dI[n][1], ci, __ldg(Ci + o));
-        dmma(dO[n][0], dO[n][1], co, __ldg(Co + o));
+      for (int n = 0; n < NNV; ++n) {
+        const int o = T::OTD1 + (kt * NNV + n) * 32 + lane;
+        dmma(vI[n][0], vI[n][1], ci, __ldg(Ci + o));
+        dmma(vO[n][0], vO[n][1], co, __ldg(Co + o));
       }
     }
-    // A fragments of the modal vectors: k-step kt holds mode 4 kt + t =
-    // pi(8 (kt/2) + 2t + kt%2), i.e. accumulator entry [kt/2][kt%2]
-    double aJ[NNF][2], gm[NND][2];
+    // A fragments: k-step kt holds combined mode 4 kt + t = pi(8 (kt/2) +
+    // 2t + kt%2), i.e. accumulator entry [kt/2][kt%2].  aJ's a part is the
+    // jump a_in - a_out, gm's d part the average (d_in + d_out) / 2 (the
+    // other parts meet zero table rows)
+    double aJ[NNV][2], gm[NNV][2];
 #pragma unroll
-    for (int n = 0; n < NNF; ++n)
+    for (int n = 0; n < NNV; ++n)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) aJ[n][j] = aI[n][j] - aO[n][j];
-#pragma unroll
-    for (int n = 0; n < NND; ++n)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) gm[n][j] = 0.5 * (dI[n][j] + dO[n][j]);
+      for (int j = 0; j < 2; ++j) {
+        aJ[n][j] = vI[n][j] - vO[n][j];
+        gm[n][j] = 0.5 * (vI[n][j] + vO[n][j]);
+      }
 
     // ---- B1: point values -> physics slots; du kept in registers -------
     double du[QT][2];
@@ -176,14 +172,15 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
     for (int qt = 0; qt < QT; ++qt) {
       double d0[2] = {0.0, 0.0}, u0[2] = {0.0, 0.0}, gv[2] = {0.0, 0.0};
 #pragma unroll
-      for (int kt = 0; kt < KTF; ++kt) {
+      for (int kt = 0; kt < KA; ++kt) {
         const double b = __ldg(tg + T::OBF + (kt * QT + qt) * 32 + lane);
         dmma(d0[0], d0[1], aJ[kt / 2][kt % 2], b);
-        dmma(u0[0], u0[1], aI[kt / 2][kt % 2], b);
+        dmma(u0[0], u0[1], vI[kt / 2][kt % 2], b);
       }
 #pragma unroll
-      for (int kt = 0; kt < KTD; ++kt)  // (warp-wide: every row, used by the gradient species)
-        dmma(gv[0], gv[1], gm[kt / 2][kt % 2], __ldg(tg + T::OBD + (kt * QT + qt) * 32 + lane));
+      for (int kt = KD0; kt < KTV; ++kt)  // (warp-wide: every row, used by the gradient species)
+        dmma(gv[0], gv[1], gm[kt / 2][kt % 2],
+             __ldg(tg + T::OBD + ((kt - KD0) * QT + qt) * 32 + lane));
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         du[qt][j] = d0[j];
@@ -208,10 +205,12 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
       M::face_point(p.P, fetch, cvs + (f * QP + q) * NCV);
     }
     __syncthreads();
-    // ---- B2: p = Bf^T W cnv ------------------------------------------------
-    double pw[NNF][2];
+    // ---- B2 + C: the row's modal bracket yb = (Ybr | Xbr) ---------------
+    //   Ybr = A Mfd g - ki L a_j - Bf^T W cnv  (ip: - eta/h A Mff a_j)
+    //   Xbr = adj/2 A Mfd^T a_j
+    double yb[NNV][2];
 #pragma unroll
-    for (int n = 0; n < NNF; ++n) pw[n][0] = pw[n][1] = 0.0;
+    for (int n = 0; n < NNV; ++n) yb[n][0] = yb[n][1] = 0.0;
 #pragma unroll
     for (int qt = 0; qt < QT; ++qt) {
       double cn[2];
@@ -226,27 +225,20 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
           for (int k = 0; k < M::NFX; ++k)
             if (sp == k) v = fma(0.5, c[1 + k], v);
         }
-        cn[j] = v;
+        cn[j] = -v;  // Ybr carries - Bf^T W cnv
       }
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-        for (int n = 0; n < NNF; ++n)
-          dmma(pw[n][0], pw[n][1], cn[ks], __ldg(tg + T::OWB + ((qt * 2 + ks) * NNF + n) * 32 + lane));
+        for (int n = 0; n < NAT; ++n)
+          dmma(yb[n][0], yb[n][1], cn[ks], __ldg(tg + T::OWB + ((qt * 2 + ks) * NAT + n) * 32 + lane));
     }
-    // ---- C: modal brackets, both sides ---------------------------------------
-    // Ybr = A Mfd g - ki L a_j - p  (ip: - eta/h A Mff a_j)
-    double yb[NNF][2], xb[NND][2];
 #pragma unroll
-    for (int n = 0; n < NNF; ++n) yb[n][0] = -pw[n][0], yb[n][1] = -pw[n][1];
+    for (int kt = KD0; kt < KTV; ++kt)
 #pragma unroll
-    for (int n = 0; n < NND; ++n) xb[n][0] = xb[n][1] = 0.0;
-#pragma unroll
-    for (int kt = 0; kt < KTD; ++kt)
-#pragma unroll
-      for (int n = 0; n < NNF; ++n)
+      for (int n = 0; n < NAT; ++n)
         dmma(yb[n][0], yb[n][1], As * gm[kt / 2][kt % 2],
-             __ldg(tg + T::OMFD + (kt * NNF + n) * 32 + lane));
+             __ldg(tg + T::OMFD + ((kt - KD0) * NAT + n) * 32 + lane));
     if constexpr (lift) {
       const double wside = br2 ? 0.5 : 1.0;
       const double fac0 = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * wside * 0.5 * sfac * As;
@@ -254,10 +246,10 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
       const double ko = br2 ? fac0 * __ldg(gg + 2 * D + 3) : 0.0;
       const double* Tl = (br2 || min_) ? Ti : To;
 #pragma unroll
-      for (int kt = 0; kt < KTF; ++kt)
+      for (int kt = 0; kt < KA; ++kt)
 #pragma unroll
-        for (int n = 0; n < NNF; ++n) {
-          const int o = T::OL + (kt * NNF + n) * 32 + lane;
+        for (int n = 0; n < NAT; ++n) {
+          const int o = T::OL + (kt * NAT + n) * 32 + lane;
           dmma(yb[n][0], yb[n][1], -ki * aJ[kt / 2][kt % 2], __ldg(Tl + o));
           if constexpr (br2) dmma(yb[n][0], yb[n][1], -ko * aJ[kt / 2][kt % 2], __ldg(To + o));
         }
@@ -265,44 +257,33 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
       if (p.scheme == IP) {
         const double kip = -p.eta / __ldg(gg + 2 * D + 1) * As;
 #pragma unroll
-        for (int kt = 0; kt < KTF; ++kt)
+        for (int kt = 0; kt < KA; ++kt)
 #pragma unroll
-          for (int n = 0; n < NNF; ++n)
+          for (int n = 0; n < NAT; ++n)
             dmma(yb[n][0], yb[n][1], kip * aJ[kt / 2][kt % 2],
-                 __ldg(tg + T::OMFF + (kt * NNF + n) * 32 + lane));
+                 __ldg(tg + T::OMFF + (kt * NAT + n) * 32 + lane));
       }
     }
-    {  // Xbr = adj/2 A Mfd^T a_j
+    {
       const double kx = 0.5 * p.adj * As;
 #pragma unroll
-      for (int kt = 0; kt < KTF; ++kt)
+      for (int kt = 0; kt < KA; ++kt)
 #pragma unroll
-        for (int n = 0; n < NND; ++n)
-          dmma(xb[n][0], xb[n][1], kx * aJ[kt / 2][kt % 2],
-               __ldg(tg + T::OMDF + (kt * NND + n) * 32 + lane));
+        for (int n = NAT0; n < NNV; ++n)
+          dmma(yb[n][0], yb[n][1], kx * aJ[kt / 2][kt % 2],
+               __ldg(tg + T::OMDF + (kt * (NNV - NAT0) + n - NAT0) * 32 + lane));
     }
-    // R_in = sfac (T_in^T Ybr + Td_in^T Xbr), R_out = sfac (-T_out^T Ybr + Td_out^T Xbr)
+    // R_in = sfac (T_in ; Td_in)^T yb, R_out = sfac (-T_out ; Td_out)^T yb
     double ri[NNT][2], ro[NNT][2];
 #pragma unroll
     for (int nt = 0; nt < NNT; ++nt) ri[nt][0] = ri[nt][1] = ro[nt][0] = ro[nt][1] = 0.0;
 #pragma unroll
-    for (int kt = 0; kt < KTF; ++kt) {
+    for (int kt = 0; kt < KTV; ++kt) {
       const double a = sfac * yb[kt / 2][kt % 2];
 #pragma unroll
       for (int nt = 0; nt < NNT; ++nt) {
-        const int o = T::OT4 + (kt * NNT + nt) * 32 + lane;
-        dmma(ri[nt][0], ri[nt][1], a, __ldg(Ti + o));
-        dmma(ro[nt][0], ro[nt][1], -a, __ldg(To + o));
-      }
-    }
-#pragma unroll
-    for (int kt = 0; kt < KTD; ++kt) {
-      const double a = sfac * xb[kt / 2][kt % 2];
-#pragma unroll
-      for (int nt = 0; nt < NNT; ++nt) {
-        const int o = T::OD4 + (kt * NNT + nt) * 32 + lane;
-        dmma(ri[nt][0], ri[nt][1], a, __ldg(Ci + o));
-        dmma(ro[nt][0], ro[nt][1], a, __ldg(Co + o));
+        dmma(ri[nt][0], ri[nt][1], a, __ldg(Ci + T::OTD4 + (kt * NNT + nt) * 32 + lane));
+        dmma(ro[nt][0], ro[nt][1], a, __ldg(Co + T::OTD4M + (kt * NNT + nt) * 32 + lane));
       }
     }
     // face-sum rows: lane entries (face fq, species sp, basis 4 (2nt + j) + t)

@@ -564,43 +564,75 @@ def _pi_mat(M: np.ndarray, rows: int, ncols: int):
 
 def modal_face_tables(t: OperatorTables, fold):
     """Operand tables of the modal face-group kernel (csrc/kernels_tcm.cuh)
-    from ``modal_face_factors``, fragment-major, concatenated as
+    from ``modal_face_factors``.  The kernel keeps one modal vector per row,
+    v = (face modes a | d-modes d), nv = nfm + ndm entries (16 at p = 3), in
+    the DMMA accumulator layout with pi-permuted columns; a GEMM over the a
+    (d) part uses the k-steps that hold them and zero table rows for the
+    other part.  Fragment-major, concatenated as
 
-      global     BF  [KTF][QT][32]        Bf^T          point values of face modes
-                 BD  [KTD][QT][32]        Bd^T          of d-modes
-                 WB  [QT][2][NNF][32]     w Bf (pi)     projection of the pointwise flux
-                 MFD [KTD][NNF][32]       Mfd^T (pi)    A gav term
-                 MDF [KTF][NND][32]       Mfd (pi)      adjoint term
-                 MFF [KTF][NNF][32]       Mff (pi)      ip penalty
-      per table  T1  [KT][NNF][32]        T^T (pi)      face modes of the coefficients
-                 T4  [KTF][NNT][32]       T (pi)        back to the volume modes
-                 L   [KTF][NNF][32]       L^T (pi)      lifting (Mff T T^T Mff)
-      per class  D1  [KT][NND][32]        Td^T (pi)     d-modes of the coefficients
-                 D4  [KTD][NNT][32]       Td (pi)       back to the volume modes
+      global     BF  [KA][QT][32]           Bf^T         point values of the a part
+                 BD  [KTV-KD0][QT][32]      Bd^T         of the d part
+                 WB  [QT][2][NAT][32]       w Bf (pi)    projection of the pointwise flux
+                 MFD [KTV-KD0][NAT][32]     Mfd (pi)     A gav term   (d -> a)
+                 MDF [KA][NNV-NAT0][32]     Mfd^T (pi)   adjoint term (a -> d)
+                 MFF [KA][NAT][32]          Mff (pi)     ip penalty   (a -> a)
+      per table  L   [KA][NAT][32]          L (pi)       lifting (Mff T T^T Mff)
+      per class  TD1 [KT][NNV][32]          (T | Td)^T   v of the coefficients
+                 TD4 [KTV][NNT][32]         (T ; Td)     back to the volume modes (inside)
+                 TD4M[KTV][NNT][32]         (-T ; Td)    (outside: the flux changes sign)
 
-    with nfm / ndm face / d-modes, KTF = ceil(nfm/4), NNF = ceil(nfm/8),
-    KTD, NND likewise, KT = ceil(nb/4), NNT = ceil(nb/8), QT = ceil(F/8).
+    KA = ceil(nfm/4) k-steps hold the a part, k-steps KD0 = floor(nfm/4) ..
+    KTV = ceil(nv/4) the d part; NNV = ceil(nv/8) output tiles, the a part in
+    tiles [0, NAT = ceil(nfm/8)), the d part in [NAT0 = floor(nfm/8), NNV).
     Returns the flat array."""
     mf = modal_face_factors(t, fold)
     nb, F = t.nb, t.nq_face
     nfm, ndm = mf["nfm"], mf["ndm"]
-    KTF, KTD, KT = -(-nfm // 4), -(-max(ndm, 1) // 4), -(-nb // 4)
+    nv = nfm + ndm
+    KT, KA, KTV, KD0 = -(-nb // 4), -(-nfm // 4), -(-nv // 4), nfm // 4
+    NNV, NAT, NAT0 = -(-nv // 8), -(-nfm // 8), nfm // 8
     QP = _ceil(F, 8)
-    Bf = np.zeros((QP, 4 * KTF)); Bf[:F, :nfm] = mf["Bf"]
-    Bd = np.zeros((QP, 4 * KTD)); Bd[:F, :ndm] = mf["Bd"]
+    pv, okv = _pi_cols(nv)                 # combined output columns
+    pv = np.where(okv, pv, nv)             # out of range -> the zero column
     w = np.zeros(QP); w[:F] = t.face_w
-    parts = [_frag_kq(Bf.T), _frag_kq(Bd.T),
-             _frag_qn(_pi_mat(w[:, None] * Bf[:, :nfm], QP, nfm)),
-             _frag_kn(_pi_mat(mf["Mfd"].T, 4 * KTD, nfm)),
-             _frag_kn(_pi_mat(mf["Mfd"], 4 * KTF, ndm)),
-             _frag_kn(_pi_mat(mf["Mff"].T, 4 * KTF, nfm))]
+    Bf = np.zeros((QP, nv + 1)); Bf[:F, :nfm] = mf["Bf"]       # columns: combined modes
+    Bd = np.zeros((QP, nv + 1)); Bd[:F, nfm:nv] = mf["Bd"][:, :ndm]
+    Mfd = mf["Mfd"][:, :ndm]
+    # square operators on the combined index, zero-padded by one
+    def comb(rows_a, rows_d, Xaa=None, Xad=None, Xda=None):
+        M = np.zeros((nv + 1, nv + 1))
+        if Xaa is not None: M[:nfm, :nfm] = Xaa
+        if Xad is not None: M[:nfm, nfm:nv] = Xad
+        if Xda is not None: M[nfm:nv, :nfm] = Xda
+        return M
+    def kn(M, k0, k1, n0, n1):
+        """B operand [k][n]: rows = combined k in [4 k0, 4 k1), columns
+        tiles [n0, n1) of the pi-permuted combined outputs, M[k][out]."""
+        rows = np.arange(4 * k0, 4 * k1)
+        rows = np.where(rows < nv, rows, nv)
+        cols = pv[8 * n0:8 * n1]
+        return _frag_kn(M[np.ix_(rows, cols)])
+    BFr = Bf[:, np.where(np.arange(4 * KA) < nfm, np.arange(4 * KA), nv)]
+    BDr = Bd[:, np.where(np.arange(4 * KD0, 4 * KTV) < nv, np.arange(4 * KD0, 4 * KTV), nv)]
+    WB = (w[:, None] * Bf)[:, pv[:8 * NAT]]
+    parts = [_frag_kq(BFr.T), _frag_kq(BDr.T), _frag_qn(WB),
+             kn(comb(0, 0, Xda=Mfd.T), KD0, KTV, 0, NAT),        # out_a += Mfd d
+             kn(comb(0, 0, Xad=Mfd), 0, KA, NAT0, NNV),           # out_d += Mfd^T a
+             kn(comb(0, 0, Xaa=mf["Mff"]), 0, KA, 0, NAT)]        # out_a += Mff a
     for k in range(t.face_B.shape[0]):
-        T = mf["T"][k]
-        parts += [_frag_kn(_pi_mat(T.T, 4 * KT, nfm)), _frag_kn(_pi_mat(T, 4 * KTF, nb)),
-                  _frag_kn(_pi_mat(mf["L"][k].T, 4 * KTF, nfm))]
-    for c in range(mf["Td"].shape[0]):
-        Td = mf["Td"][c]
-        parts += [_frag_kn(_pi_mat(Td.T, 4 * KT, max(ndm, 1))), _frag_kn(_pi_mat(Td, 4 * KTD, nb))]
+        parts.append(kn(comb(0, 0, Xaa=mf["L"][k].T), 0, KA, 0, NAT))
+    # the class's table id comes from the class key (tc_face_fold_tables)
+    for c, (tab, _jv) in enumerate(fold[3]):
+        T, Td = mf["T"][tab], mf["Td"][c][:ndm]
+        V = np.zeros((nb, nv + 1)); V[:, :nfm] = T.T; V[:, nfm:nv] = Td.T   # (T | Td)^T
+        TD1 = V[np.where(np.arange(4 * KT) < nb, np.arange(4 * KT), nb - 1)][:, pv[:8 * NNV]]
+        TD1[np.arange(4 * KT) >= nb] = 0.0
+        pic, ok = _pi_cols(nb)
+        R = np.zeros((4 * KTV, len(pic)))
+        R[:nfm] = T[:, pic] * ok
+        R[nfm:nv] = Td[:, pic] * ok
+        RM = R.copy(); RM[:nfm] *= -1.0
+        parts += [_frag_kn(TD1), _frag_kn(R), _frag_kn(RM)]
     return np.ascontiguousarray(np.concatenate([p.ravel() for p in parts]))
 
 
