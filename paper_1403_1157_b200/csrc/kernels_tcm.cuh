@@ -61,6 +61,9 @@ struct TcmFace {
   static constexpr int NT = Dm::NT;  // trace-table signatures
   static constexpr int QP = ceil_to(F, 8), QT = QP / 8;
   static constexpr int KT = (NB + 3) / 4, NNT = (NB + 7) / 8;
+  // P_k / P_{k-1} on the face triangle (3D only: on 2D's tiny segments a
+  // group's work is too small for the CTA's two barriers; the register-
+  // resident k_faces_fast stays faster at C2)
   static constexpr int NFM = (K + 1) * (K + 2) / 2, NDM = K * (K + 1) / 2, NV = NFM + NDM;
   // the modal vector v = (a | d) of a row: k-steps [0, KA) hold the a part,
   // [KD0, KTV) the d part; output tiles [0, NAT) the a part, [NAT0, NNV)

@@ -410,6 +410,29 @@ def _row_classes(rows: np.ndarray):
     return uniq, inv.reshape(-1)
 
 
+def face_classes(t: OperatorTables, max_classes: int = 512):
+    """Face-geometry classes: every interior face side is a (trace-table id,
+    Jinv n) pair; meshes of congruent cells have few of them (Kuhn cubes: 6
+    per side; the structured triangles likewise).  Returns (int32 [nif][2]
+    class of the inside / outside side, [(table id, Jinv n)] per class) or
+    None (no interior faces, Dirichlet mirror faces, or more than
+    ``max_classes`` classes)."""
+    d = t.dim
+    nif = len(t.if_code)
+    if nif == 0 or (t.if_code & CODE_MIRROR).any():
+        return None
+    code = t.if_code.astype(np.int64)
+    tid = np.concatenate([code & 31, (code >> 5) & 31])
+    jn = np.ascontiguousarray(np.concatenate([t.if_geo[:, 0:d], t.if_geo[:, d:2 * d]]))
+    key = np.concatenate([tid[:, None], jn.view(np.int64)], axis=1)
+    uniq, inv = _row_classes(key)
+    if len(uniq) > max_classes:
+        return None
+    cls = np.ascontiguousarray(np.stack([inv[:nif], inv[nif:]], axis=1), dtype=np.int32)
+    keys = [(int(row[0]), row[1:].copy().view(np.float64)) for row in uniq]
+    return cls, keys
+
+
 def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
     """Face-geometry classes of the species-rows face kernel: every
     interior face side is a (table id, Jinv n) pair; meshes of congruent
@@ -428,22 +451,16 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
     mesh has more than ``max_classes`` classes (the kernel then folds per
     face)."""
     d, nb, F = t.dim, t.nb, t.nq_face
-    nif = len(t.if_code)
-    if d != 3 or nif == 0 or (t.if_code & CODE_MIRROR).any():
+    if d != 3:
         return None
-    code = t.if_code.astype(np.int64)
-    tid = np.concatenate([code & 31, (code >> 5) & 31])
-    jn = np.concatenate([t.if_geo[:, 0:3], t.if_geo[:, 3:6]])
-    key = np.concatenate([tid[:, None], jn.view(np.int64)], axis=1)
-    uniq, inv = _row_classes(key)
-    if len(uniq) > max_classes:
+    fc = face_classes(t, max_classes)
+    if fc is None:
         return None
+    cls, keys = fc
     QP, NBK, NBN = _ceil(F, 8), _ceil(nb, 4), _ceil(nb, 8)
     pic, ok = _pi_cols(nb)
     parts = []
-    for row in uniq:
-        k = int(row[0])
-        jv = row[1:].copy().view(np.float64)
+    for k, jv in keys:
         B, G = t.face_B[k], t.face_G[k]                     # (F, nb), (F, nb, d)
         Gn = np.einsum("qia,a->qi", G, jv)
         BT = np.zeros((NBK, QP)); BT[:nb, :F] = B.T
@@ -454,8 +471,6 @@ def tc_face_fold_tables(t: OperatorTables, max_classes: int = 512):
         PRF = np.stack([_frag_qn(BP), _frag_qn(GP)], axis=-1)
         parts.append(np.concatenate([TRF.ravel(), PRF.ravel(), _frag_qn(BP).ravel(),
                                      _frag_qn(GP).ravel()]))
-    cls = np.ascontiguousarray(np.stack([inv[:nif], inv[nif:]], axis=1), dtype=np.int32)
-    keys = [(int(row[0]), row[1:].copy().view(np.float64)) for row in uniq]
     return np.ascontiguousarray(np.concatenate(parts)), len(parts[0]), cls, keys
 
 
@@ -515,13 +530,13 @@ def modal_face_factors(t: OperatorTables, fold):
         G_n^T W X,  X ~ dU               ->  Td^T Mfd^T a_j
         B^T W (eta/h A dU)  (ip)         ->  eta/h A T^T Mff a_j
 
-    ``fold`` is ``tc_face_fold_tables``'s result (class keys come from it).
+    ``fold``: ``face_classes``' (cls, keys) or ``tc_face_fold_tables``'
+    result (the class keys are its last entry).
     Returns dict(Bf, Bd, T [ntab][nfm][nb], Td [ncls][ndm][nb],
     L [ntab][nfm][nfm] = Mff T T^T Mff, Mff, Mfd, nfm, ndm)."""
     d, k, nb = t.dim, t.order, t.nb
-    if d != 3:
-        raise ValueError("the modal face factors are 3D")
-    nfm, ndm = (k + 1) * (k + 2) // 2, k * (k + 1) // 2
+    # P_k / P_{k-1} on the face: a triangle (3D) or a segment (2D)
+    nfm, ndm = ((k + 1) * (k + 2) // 2, k * (k + 1) // 2) if d == 3 else (k + 1, k)
     w = t.face_w
     B = t.face_B                                     # (ntab, F, nb)
     Bf = _o_basis(np.concatenate(list(B), axis=1), nfm)
@@ -538,7 +553,7 @@ def modal_face_factors(t: OperatorTables, fold):
     Tx = np.stack([G @ (Bl.T @ B[k].astype(np.longdouble)) for k in range(len(B))])
     T = Tx.astype(np.float64)
     Tlo = (Tx - T.astype(np.longdouble)).astype(np.float64)
-    cls_keys = fold[3]
+    cls_keys = fold[-1]
     Gn = np.stack([np.einsum("qia,a->qi", t.face_G[int(tab)], jv) for tab, jv in cls_keys])
     if ndm > 0:
         Bd = _o_basis(np.concatenate(list(Gn), axis=1), ndm)
@@ -622,7 +637,7 @@ def modal_face_tables(t: OperatorTables, fold):
     for k in range(t.face_B.shape[0]):
         parts.append(kn(comb(0, 0, Xaa=mf["L"][k].T), 0, KA, 0, NAT))
     # the class's table id comes from the class key (tc_face_fold_tables)
-    for c, (tab, _jv) in enumerate(fold[3]):
+    for c, (tab, _jv) in enumerate(fold[-1]):
         T, Td = mf["T"][tab], mf["Td"][c][:ndm]
         V = np.zeros((nb, nv + 1)); V[:, :nfm] = T.T; V[:, nfm:nv] = Td.T   # (T | Td)^T
         TD1 = V[np.where(np.arange(4 * KT) < nb, np.arange(4 * KT), nb - 1)][:, pv[:8 * NNV]]

@@ -8,9 +8,9 @@ import numpy as np
 import pytest
 
 from paper_1403_1157_b200 import DGSpace, FluxScheme, PlaqueModel, PlaqueParams
-from paper_1403_1157_b200.mesh import unit_cube
-from paper_1403_1157_b200.tables import (build_tables, modal_face_factors, scheme_constants,
-                                         tc_face_fold_tables)
+from paper_1403_1157_b200.mesh import unit_cube, unit_square
+from paper_1403_1157_b200.tables import (build_tables, face_classes, modal_face_factors,
+                                         scheme_constants)
 from paper_1403_1157_b200.fields import initial_state
 
 from _cases import AMPLIFIED
@@ -57,14 +57,15 @@ def _modal_face(em, mf, cls_in, cls_out, U, code, ein, eout, g):
     return ri, ro
 
 
+@pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("order", [1, 2, 3])
 @pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
-def test_modal_face_terms_match_direct(order, scheme):
-    space = DGSpace(unit_cube(2, 2, 2), order, 6)
+def test_modal_face_terms_match_direct(dim, order, scheme):
+    space = DGSpace(unit_cube(2, 2, 2) if dim == 3 else unit_square(4, 3), order, 6)
     model = PlaqueModel(PlaqueParams(**AMPLIFIED))
     sch = FluxScheme(scheme)
     t = build_tables(space, model, sch)
-    fold = tc_face_fold_tables(t)
+    fold = face_classes(t)
     mf = modal_face_factors(t, fold)
     chi_e, adj, eta = scheme_constants(space, sch)
     em = DeviceEmulator(t, model, sch.id, chi_e, adj, eta)
@@ -74,24 +75,25 @@ def test_modal_face_terms_match_direct(order, scheme):
         code = int(t.if_code[f])
         ein, eout = t.if_elems[f]
         ri, ro = em.face_contrib(U, code, ein, eout, t.if_geo[f])
-        mi, mo = _modal_face(em, mf, fold[2][f, 0], fold[2][f, 1], U, code, ein, eout,
+        mi, mo = _modal_face(em, mf, fold[0][f, 0], fold[0][f, 1], U, code, ein, eout,
                              t.if_geo[f])
         scale = max(np.abs(ri).max(), np.abs(ro).max())
         worst = max(worst, np.abs(mi - ri).max() / scale, np.abs(mo - ro).max() / scale)
     assert worst <= 1e-12, worst
 
 
+@pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("order", [1, 2, 3])
-def test_modal_factors_reconstruct_the_tables(order):
+def test_modal_factors_reconstruct_the_tables(dim, order):
     """Bf T = face_B and Bd Td = the folded normal-derivative tables, with
     orthonormal Bf, Bd (tables.modal_face_factors)."""
-    space = DGSpace(unit_cube(2, 2, 2), order, 6)
+    space = DGSpace(unit_cube(2, 2, 2) if dim == 3 else unit_square(4, 3), order, 6)
     t = build_tables(space, PlaqueModel(), FluxScheme("cdg2"))
-    fold = tc_face_fold_tables(t)
+    fold = face_classes(t)
     mf = modal_face_factors(t, fold)
     assert np.allclose(mf["Bf"].T @ mf["Bf"], np.eye(mf["nfm"]), atol=1e-13)
     for k in range(t.face_B.shape[0]):
         assert np.abs(mf["Bf"] @ mf["T"][k] - t.face_B[k]).max() <= 1e-14 * np.abs(t.face_B[k]).max()
-    for c, (tab, jv) in enumerate(fold[3]):
+    for c, (tab, jv) in enumerate(fold[1]):
         Gn = np.einsum("qia,a->qi", t.face_G[tab], jv)
         assert np.abs(mf["Bd"] @ mf["Td"][c] - Gn).max() <= 1e-12 * max(1, np.abs(Gn).max())
