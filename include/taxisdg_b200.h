@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 6
+#define TDG_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -166,6 +166,15 @@ typedef struct tdg_desc {
    * face-geometry class); NULL: the face-group kernel evaluates the full
    * traces */
   const double* face_modal;
+  /* optional point data of the diffusion model (x-dependent closures,
+   * reference tests/test_operator.py:31-70): Dirichlet values at the face
+   * points of the mirror faces, [n_int_faces][nq_face][S] (entries of the
+   * non-mirror faces unused), and prescribed wall fluxes at the points,
+   * [n_bnd_faces][nq_face][S]; either forces the CTA-staged generic face
+   * kernels.  Device pointers, caller-owned, may change between calls
+   * (time-dependent data) */
+  const double* if_bval;
+  const double* bf_qval;
   /* optional, tensor-core volume kernel: element-geometry classes
    * (tables.tc_volume_classes): per class the summed stiffness fragments
    * [ncls][KT][NNT][32], the elements in class-sorted tasks of 8 (int32

@@ -16,7 +16,8 @@ descriptions, which the operator packs for the device:
 * model: ``PlaqueModel`` / ``ReducedModel`` by class, their
   ``PlaqueParams`` copied field by field; the reference's heat test
   models (``tests/oracles.py:192-220``: insulated walls, or constant
-  Dirichlet data) become ``DiffusionModel``;
+  Dirichlet data) become ``DiffusionModel``, subclasses with x- or
+  normal-dependent ``dirichlet_value`` / ``boundary_flux`` with point data;
 * scheme: name and ``ip_eta0``.
 
 Models whose physics is not compiled for the device (the manufactured
@@ -81,6 +82,15 @@ def _params(p) -> PlaqueParams:
     return PlaqueParams(**{f.name: float(getattr(p, f.name)) for f in fields(PlaqueParams)})
 
 
+def _overrides(model, base_name: str, method: str) -> bool:
+    """True when a subclass of the reference class ``base_name`` redefines
+    ``method``."""
+    for cls in type(model).__mro__:
+        if cls.__name__ == base_name:
+            return getattr(type(model), method) is not getattr(cls, method)
+    return False
+
+
 def adapt_model(model):
     if _is_ours(model, (PlaqueModel, ReducedModel, DiffusionModel)):
         return model
@@ -91,8 +101,15 @@ def adapt_model(model):
     if "ReducedModel" in mro:
         return ReducedModel(_params(model.params))
     if "ZeroFluxHeat" in mro:
+        # a subclass overriding boundary_flux (x / normal-dependent walls,
+        # reference tests/test_operator.py:31-51) keeps its data as point data
+        if _overrides(model, "ZeroFluxHeat", "boundary_flux"):
+            return DiffusionModel(float(model.kappa), wall_flux_fn=model.boundary_flux)
         return DiffusionModel(float(model.kappa))
     if "ConstantDirichletHeat" in mro:
+        # likewise an overridden dirichlet_value (tests/test_operator.py:54-70)
+        if _overrides(model, "ConstantDirichletHeat", "dirichlet_value"):
+            return DiffusionModel(float(model.kappa), dirichlet_fn=model.dirichlet_value)
         return DiffusionModel(float(model.kappa), dirichlet=float(model.value))
     raise ValueError(f"model {name!r} has no device implementation (plaque, reduced, "
                      "zero-flux or constant-Dirichlet diffusion)")

@@ -145,6 +145,9 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.ffold = d.if_fold;
   p.fgrp = d.face_groups;
   p.fmod = d.face_modal;
+  p.ifbv = d.if_bval;
+  p.bfqv = d.bf_qval;
+  ctx->point_data = d.if_bval != nullptr || d.bf_qval != nullptr;
   if (d.vol_cls_tab && d.vol_perm && d.vol_task_cls && d.vol_chunk_tasks) {
     p.vctab = d.vol_cls_tab;
     p.vperm = d.vol_perm;

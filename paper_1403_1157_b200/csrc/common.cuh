@@ -67,6 +67,8 @@ struct OpParams {
   const int32_t* __restrict__ ffold;  // [nif][2] class of the inside / outside side
   const int32_t* __restrict__ fgrp;   // face groups [n][NFQ] (may be null)
   const double* __restrict__ fmod;    // modal face tables (may be null)
+  const double* __restrict__ ifbv;    // [nif][nqf][S] Dirichlet values at mirror-face points (may be null)
+  const double* __restrict__ bfqv;    // [nbf][nqf][S] prescribed wall fluxes at the points (may be null)
   const double* __restrict__ vctab;   // volume element-class stiffness tables (may be null)
   const int32_t* __restrict__ vperm;  // [ntask][8] class-sorted element ids
   const int32_t* __restrict__ vtcls;  // [ntask] class of each task

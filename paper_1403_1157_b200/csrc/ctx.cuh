@@ -78,6 +78,7 @@ struct tdg_ctx {
   bool no_groups = false;      // testing: the one-face kernel despite face groups
   bool no_vcls = false;        // testing: per-element metric scaling despite volume classes
   bool no_modal = false;       // testing: face groups on full traces despite modal tables
+  bool point_data = false;     // boundary point data: the generic face kernels
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
@@ -206,8 +207,10 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
   q.bfel = p.bfel + sg.w0;
   q.bfcode = p.bfcode + sg.w0;
   q.bfgeo = p.bfgeo + sg.w0;
+  if (p.ifbv) q.ifbv = p.ifbv + sg.f0 * p.nqf * M::S;
+  if (p.bfqv) q.bfqv = p.bfqv + sg.w0 * p.nqf * M::S;
   if (q.nif + q.nbf == 0) return;
-  const bool dflt = p.nqf == Dims<D, K>::NQF && !ctx->force_generic;
+  const bool dflt = p.nqf == Dims<D, K>::NQF && !ctx->force_generic && !ctx->point_data;
   // 3D: interior faces on the species-rows tensor-core kernel (blocks of
   // one signature), walls on the element-local DMMA kernel
   if constexpr (TcsFace<D, K, M>::ok && MmaFace<D, K, M>::ok) {

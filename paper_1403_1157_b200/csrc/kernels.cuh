@@ -265,7 +265,8 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ ACC) {
       ui[s] = tu_in[s * F + q];
       const double gi = tg_in[s * F + q];
       if (mirror) {
-        uo[s] = 2.0 * M::mirror_value(p.P, s) - ui[s];
+        const double gd = p.ifbv ? p.ifbv[((f0 + f) * nqf + q) * S + s] : M::mirror_value(p.P, s);
+        uo[s] = 2.0 * gd - ui[s];
         gn[s] = gi;
       } else {
         uo[s] = tu_out[s * F + q];
@@ -296,7 +297,10 @@ k_faces(OpParams p, const double* __restrict__ U, double* __restrict__ ACC) {
         for (int s = 0; s < S; ++s) {
           double a = 0.0;
           for (int pp = 0; pp < nqf; ++pp) {
-            const double du = mirror ? 2.0 * (tu_in[s * F + pp] - M::mirror_value(p.P, s))
+            const double gd = !mirror ? 0.0
+                              : (p.ifbv ? p.ifbv[((f0 + f) * nqf + pp) * S + s]
+                                        : M::mirror_value(p.P, s));
+            const double du = mirror ? 2.0 * (tu_in[s * F + pp] - gd)
                                      : tu_in[s * F + pp] - tu_out[s * F + pp];
             a = fma(__ldg(pw + pp), du, a);
           }
@@ -383,6 +387,10 @@ k_wall(OpParams p, const double* __restrict__ U, double* __restrict__ ACC) {
     for (int i = 0; i < NB; ++i) c1 = fma(__ldg(b + i), cw[f * NB + i], c1);
     double qv[S];
     M::wall(p.P, code_tag(code), c1, qv);
+    if (p.bfqv) {  // prescribed point data (heat models with x-dependent walls)
+#pragma unroll
+      for (int s = 0; s < S; ++s) qv[s] = p.bfqv[((f0 + f) * nqf + q) * S + s];
+    }
     const double w = -__ldg(p.fw + q) * sf[f];
 #pragma unroll
     for (int s = 0; s < S; ++s) yw[(f * S + s) * F + q] = w * qv[s];

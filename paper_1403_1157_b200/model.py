@@ -157,19 +157,42 @@ class ReducedModel:
 class DiffusionModel:
     """dU/dt = div(kappa grad U), no source.  ``dirichlet`` None closes
     the walls with zero prescribed flux; a float (or per-species array)
-    imposes that constant through the mirrored trace u_out = 2 g - u_in."""
+    imposes that constant through the mirrored trace u_out = 2 g - u_in.
+
+    Point data (the reference's x-dependent test models,
+    tests/test_operator.py:31-70): ``dirichlet_fn(x, t)`` -> (..., S)
+    Dirichlet values at physical points (reference ``dirichlet_value``,
+    model.py:273), or ``wall_flux_fn(tag, u, normal, t)`` -> (n, S)
+    prescribed fluxes in the inward-normal convention (reference
+    ``boundary_flux``, operator.py:446-458) that must not depend on u (the
+    operator evaluates them with u = 0 at the wall points).  Both are
+    evaluated on the host at the face quadrature points, at t = 0 and again
+    whenever an application passes another t (``time_dependent``)."""
 
     has_convection = False
     model_id = MODEL_DIFFUSION
 
-    def __init__(self, kappa=1.0, n_species: int = 1, dirichlet=None):
+    def __init__(self, kappa=1.0, n_species: int = 1, dirichlet=None, dirichlet_fn=None,
+                 wall_flux_fn=None, time_dependent: bool = False):
         self.n_species = int(n_species)
         self.species = tuple(f"u{i}" for i in range(self.n_species))
         self.kappa = np.broadcast_to(np.asarray(kappa, dtype=float),
                                      (self.n_species,)).copy()
+        if dirichlet is not None and dirichlet_fn is not None:
+            raise ValueError("give either constant Dirichlet data or dirichlet_fn")
+        if wall_flux_fn is not None and (dirichlet is not None or dirichlet_fn is not None):
+            raise ValueError("wall fluxes and Dirichlet data are exclusive closures")
         self.dirichlet = (None if dirichlet is None else np.broadcast_to(
             np.asarray(dirichlet, dtype=float), (self.n_species,)).copy())
-        self.boundary_kind = "flux" if dirichlet is None else "dirichlet"
+        self.dirichlet_fn = dirichlet_fn
+        self.wall_flux_fn = wall_flux_fn
+        self.time_dependent = bool(time_dependent)
+        self.boundary_kind = ("dirichlet" if dirichlet is not None or dirichlet_fn is not None
+                              else "flux")
+
+    @property
+    def has_point_data(self) -> bool:
+        return self.dirichlet_fn is not None or self.wall_flux_fn is not None
 
     def diffusivity(self) -> np.ndarray:
         return self.kappa.copy()

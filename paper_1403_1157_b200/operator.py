@@ -123,6 +123,16 @@ class DiscreteOperator:
             "vol_phi", "vol_grad", "vol_w", "vol_stiff", "face_B", "face_G",
             "face_Pw", "face_w", "elem_geo", "if_elems", "if_code",
             "if_geo", "bf_elem", "bf_code", "bf_geo")})
+        # point data of the diffusion model's x-dependent closures
+        self._pd_t = None
+        if getattr(model, "has_point_data", False):
+            nq, S = t.nq_face, t.n_species
+            self._keep["if_bval"] = torch.zeros((max(len(t.if_code), 1), nq, S),
+                                                dtype=torch.float64, device=self.device)
+            self._keep["bf_qval"] = torch.zeros((max(len(t.bf_code), 1), nq, S),
+                                                dtype=torch.float64, device=self.device)
+            self._pd_model = model
+            self._set_point_data(0.0)
         self._host = {
             "seg_ptr": np.ascontiguousarray(np.concatenate(
                 [t.seg_if, t.seg_bf, seg_blk, seg_grp]), dtype=np.int64),
@@ -165,6 +175,8 @@ class DiscreteOperator:
             vol_task_cls=ptr(k["vol_task_cls"]) if vcls is not None else None,
             n_vol_tasks=len(vcls[2]) if vcls is not None else 0,
             vol_chunk_tasks=hptr(self._host["vol_chunk_tasks"]) if vcls is not None else None,
+            if_bval=ptr(k["if_bval"]) if "if_bval" in k else None,
+            bf_qval=ptr(k["bf_qval"]) if "bf_qval" in k else None,
             n_segments=t.n_seg, n_segments_cut=t.n_seg_cut,
             seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()
@@ -258,8 +270,49 @@ class DiscreteOperator:
             raise ValueError(f"U has shape {U.shape}, expected {shape}")
         return torch.from_numpy(np.ascontiguousarray(U)).to(self.device), False
 
+    def _set_point_data(self, t: float):
+        """Evaluate the model's x-dependent boundary closures at the face
+        quadrature points (reference operator.py:436-458) and upload them."""
+        tb, model, mesh = self.tables, self._pd_model, self.space.mesh
+        d, nq, S = tb.dim, tb.nq_face, tb.n_species
+        nperm = 2 if d == 2 else 6
+        from .fespace import face_reference_points
+        J, _, _ = mesh.jacobians()
+        if model.dirichlet_fn is not None:
+            vals = np.zeros((max(len(tb.if_code), 1), nq, S))
+            mirror = np.flatnonzero(tb.if_code & (1 << 14))
+            tin = tb.if_code[mirror] & 31
+            for tid in np.unique(tin):
+                sel = mirror[tin == tid]
+                e = tb.if_elems[sel, 0]
+                xi = face_reference_points(d, int(tid) // nperm, int(tid) % nperm, tb.face_pts)
+                X = mesh.vertices[mesh.elements[e, 0]][:, None, :] + np.einsum(
+                    "fij,qj->fqi", J[e], xi)
+                vals[sel] = np.asarray(model.dirichlet_fn(X.reshape(-1, d), t),
+                                       dtype=float).reshape(len(sel), nq, S)
+            self._keep["if_bval"].copy_(_torch().from_numpy(vals))
+        if model.wall_flux_fn is not None and len(tb.bf_code):
+            vals = np.zeros((len(tb.bf_code), nq, S))
+            tags = mesh.face_tags[tb.bf_fid]
+            for tag in np.unique(tags):
+                sel = np.flatnonzero(tags == tag)
+                nrm = np.repeat(mesh.face_normals[tb.bf_fid[sel]], nq, axis=0)
+                q = model.wall_flux_fn(int(tag), np.zeros((len(sel) * nq, S)), nrm, t)
+                vals[sel] = np.asarray(q, dtype=float).reshape(len(sel), nq, S)
+            self._keep["bf_qval"].copy_(_torch().from_numpy(vals))
+        self._pd_t = float(t)
+
+    def _point_data_at(self, t: float, entry: str):
+        if self._pd_t is None or not self._pd_model.time_dependent or float(t) == self._pd_t:
+            return
+        if entry != "apply":
+            raise ValueError("time-dependent boundary data: step through apply / apply_f "
+                             "(the reference's stepper call shape)")
+        self._set_point_data(t)
+
     def _apply(self, U, mass_inverse: int, t: float):
         torch = _torch()
+        self._point_data_at(t, "apply")
         rshape = (self.n_owned, self.space.n_species, self.space.nb)
         if not isinstance(U, torch.Tensor):
             # host data (numpy / DiscreteFunction), the reference's call
@@ -371,6 +424,7 @@ class DiscreteOperator:
         """out = a U0 + b U + c M^-1 L(U) in one fused pass.  The face sums
         accumulate in ``acc`` (default: ``out``), which must not alias U
         (nor U0 when a != 0)."""
+        self._point_data_at(t, "rk_stage")
         self._check_vec("U", U, self.n_rows)
         self._check_vec("out", out)
         if U0 is not None:
@@ -445,6 +499,10 @@ class DiscreteOperator:
         """One Shu-Osher SSP-RK3 step in place on U (undecomposed meshes;
         slab runs use ``stepping.SSPRK3`` with the halo exchange).  ``work``
         = two work vectors (``new_work()``)."""
+        if self._pd_t is not None and self._pd_model.time_dependent:
+            # the three stages need the data at three times
+            raise ValueError("time-dependent boundary data: step through apply / apply_f "
+                             "(the reference's stepper call shape)")
         if self.n_rows != self.n_owned:
             raise ValueError("ssprk3_step needs an undecomposed mesh; use "
                              "stepping.SSPRK3(op, halo) for slab runs")

@@ -89,6 +89,9 @@ class OperatorTables:
     # host-only: element-local face index per side (audit, emulator)
     if_lf: np.ndarray = None
     bf_lf: np.ndarray = None
+    if_fid: np.ndarray = None   # mesh face id of every interior (+ mirror) face
+    bf_fid: np.ndarray = None   # mesh face id of every wall face
+    face_pts: np.ndarray = None  # face rule points (reference face coordinates)
 
 
 def _face_tables(space: DGSpace, frule):
@@ -200,6 +203,7 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
                          axis=1)
     el = np.stack([ein, eout], axis=1)
     lfs = np.stack([fl[fi, 0], fl[fi, 1]], axis=1)
+    fids = fi.astype(np.int64)
     bmask = ~interior & owned(fe[:, 0])
     if dirichlet:
         bi = np.flatnonzero(bmask)
@@ -215,6 +219,7 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         el = np.concatenate([el, np.stack([be, np.full(len(bi), -1)], axis=1)])
         lfs = np.concatenate([lfs, np.stack([fl[bi, 0], np.full(len(bi), -1)],
                                             axis=1)])
+        fids = np.concatenate([fids, bi.astype(np.int64)])
         nbf = np.zeros(0, dtype=np.int64)
     else:
         nbf = np.flatnonzero(bmask)
@@ -243,6 +248,7 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
     # interior faces by (segment, signature); walls by (segment, table, tag)
     order = np.lexsort((code & 1023, seg_f))
     code, geo, el, lfs, seg_f = code[order], geo[order], el[order], lfs[order], seg_f[order]
+    fids = fids[order]
     btag = mesh.face_tags[nbf].astype(np.int64)
     border = np.lexsort((btag, tid[nbf, 0], seg_w))
     nbf, btag, seg_w = nbf[border], btag[border], seg_w[border]
@@ -275,7 +281,8 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         bf_elem=i32(fe[nbf, 0]), bf_code=i32(bcode), bf_geo=c64(sfac_all[nbf]),
         n_cut=n_cut, n_seg=int(n_seg), n_seg_cut=int(nc2),
         seg_if=seg_if.astype(np.int64), seg_bf=seg_bf.astype(np.int64),
-        if_seg=seg_f.astype(np.int32), if_lf=i32(lfs), bf_lf=i32(fl[nbf, 0]))
+        if_seg=seg_f.astype(np.int32), if_lf=i32(lfs), bf_lf=i32(fl[nbf, 0]),
+        if_fid=fids, bf_fid=nbf.astype(np.int64), face_pts=np.asarray(fr.points, dtype=float))
 
 
 def _ceil(x, m):

@@ -98,3 +98,38 @@ def test_package_objects_pass_through():
     m, s = PlaqueModel(), FluxScheme("cdg2")
     a = adapt(space, m, s)
     assert a[0] is space and a[1] is m and a[2] is s
+
+
+def test_x_dependent_heat_models_adapt_with_point_data():
+    """The reference's linear-field test models (tests/test_operator.py:31-70:
+    a ZeroFluxHeat with a normal-dependent boundary_flux, a
+    ConstantDirichletHeat with an x-dependent dirichlet_value) adapt to
+    DiffusionModel with point data, evaluated through the reference's own
+    methods."""
+    class LinearWall(oracles.ZeroFluxHeat):
+        def __init__(self):
+            super().__init__(kappa=0.8)
+
+        def boundary_flux(self, tag, U, normal, t):
+            qn = -self.kappa * (normal @ np.array([2.0, -1.0]))
+            return np.broadcast_to(qn[:, None], U.shape).copy()
+
+    class LinearDirichlet(oracles.ConstantDirichletHeat):
+        def __init__(self):
+            super().__init__(0.0, kappa=0.8)
+
+        def dirichlet_value(self, x, t):
+            return (0.3 + 2.0 * x[..., 0] - 1.0 * x[..., 1])[..., None]
+
+    space = T.fespace.DGSpace(T.mesh.unit_square(3), 2)
+    _, wall, _ = adapt(space, LinearWall(), T.flux.FluxScheme("cdg2"))
+    assert isinstance(wall, DiffusionModel) and wall.wall_flux_fn is not None
+    n = np.array([[0.0, -1.0], [1.0, 0.0]])
+    assert np.allclose(wall.wall_flux_fn(1, np.zeros((2, 1)), n, 0.0)[:, 0],
+                       -0.8 * (n @ np.array([2.0, -1.0])))
+    _, dmod, _ = adapt(space, LinearDirichlet(), T.flux.FluxScheme("cdg2"))
+    assert dmod.boundary_kind == "dirichlet" and dmod.dirichlet_fn is not None
+    assert np.allclose(dmod.dirichlet_fn(np.array([[0.5, 0.25]]), 0.0), [[1.05]])
+    _, plain, _ = adapt(space, oracles.ConstantDirichletHeat(0.4, kappa=0.8),
+                        T.flux.FluxScheme("cdg2"))
+    assert plain.dirichlet_fn is None and plain.dirichlet[0] == 0.4

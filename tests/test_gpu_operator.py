@@ -918,3 +918,56 @@ def test_volume_classes_match_per_element_metric(order):
     assert rel_l2_per_species(space, a, b).max() <= 1e-13
     ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
     assert rel_l2_per_species(space, a, ref).max() <= 1e-12
+
+
+SCHEMES = ["cdg2", "cdg", "br2", "ip", "bo"]
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_linear_field_with_x_dependent_walls_is_harmonic(dim):
+    """Reference tests/test_operator.py:31-51 on the device: a globally
+    linear state with matching (normal-dependent) prescribed wall fluxes has
+    zero jumps, a constant gradient and zero Laplacian, so L_h(U) is
+    roundoff (< 1e-11) for every scheme (point data through the generic
+    face kernels)."""
+    grad = np.array([2.0, -1.0, 0.5][:dim])
+    kappa = 0.8
+
+    def wall(tag, U, normal, t):
+        qn = -kappa * (normal @ grad)
+        return np.broadcast_to(qn[:, None], U.shape).copy()
+
+    mesh = unit_square(3) if dim == 2 else unit_cube(2)
+    space = DGSpace(mesh, 2, 1)
+    fn = space.project(lambda x: (0.3 + x @ grad)[..., None])
+    for name in SCHEMES:
+        op = _op(space, DiffusionModel(kappa, wall_flux_fn=wall), FluxScheme(name))
+        r = op.apply(fn.coeffs, 0.0)
+        assert np.abs(r).max() < 1e-11, name
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_linear_field_with_x_dependent_dirichlet_data(dim):
+    """Reference tests/test_operator.py:54-70 on the device: Dirichlet data
+    equal to a linear field (mirror faces with pointwise values) leaves it
+    steady for every scheme; with time-dependent data the values follow
+    the t of the call (the reference re-evaluates dirichlet_value(x, t))."""
+    grad = np.array([2.0, -1.0, 0.5][:dim])
+    mesh = unit_square(3) if dim == 2 else unit_cube(2)
+    space = DGSpace(mesh, 2, 1)
+    fn = space.project(lambda x: (0.3 + x @ grad)[..., None])
+    for name in SCHEMES:
+        op = _op(space, DiffusionModel(0.8, dirichlet_fn=lambda x, t: (0.3 + x @ grad)[..., None]),
+                 FluxScheme(name))
+        r = op.apply(fn.coeffs, 0.0)
+        assert np.abs(r).max() < 1e-11, name
+    moving = DiffusionModel(0.8, dirichlet_fn=lambda x, t: (0.3 + t + x @ grad)[..., None],
+                            time_dependent=True)
+    op = _op(space, moving, FluxScheme("cdg2"))
+    fn1 = space.project(lambda x: (1.3 + x @ grad)[..., None])
+    assert np.abs(op.apply(fn1.coeffs, 1.0)).max() < 1e-11
+    assert np.abs(op.apply(fn1.coeffs, 0.0)).max() > 1e-3
+    with pytest.raises(ValueError):
+        import torch
+        U = torch.from_numpy(fn1.coeffs).cuda()
+        op.ssprk3_step(U, op.new_work(), 1e-4)
