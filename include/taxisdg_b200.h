@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 7
+#define TDG_ABI_VERSION 8
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -175,6 +175,19 @@ typedef struct tdg_desc {
    * (time-dependent data) */
   const double* if_bval;
   const double* bf_qval;
+  /* optional, host-data stepping (tdg_ssprk3_steps_host): within every
+   * segment the faces, walls, blocks and groups are ordered by element
+   * chunk (chunk k = elements from ne k / 8 rounded down to a multiple of
+   * eight, and a face belongs to the later chunk of its elements); seg_chunk_ptr
+   * (HOST) = 4 offset arrays of n_segments * 8 + 1 entries (faces | walls |
+   * blocks | groups), run (s, c) = [o[8 s + c], o[8 s + c + 1]); and the
+   * code words with the TDG_CODE_FIRST_* bits cleared (device).  With them
+   * the first stage of every host step runs chunk by chunk as the state
+   * arrives (volume terms first, face sums added, then M^-1 and the stage
+   * combination); NULL: whole-state stages */
+  const int64_t* seg_chunk_ptr;
+  const int32_t* if_code_add;
+  const int32_t* bf_code_add;
   /* optional, tensor-core volume kernel: element-geometry classes
    * (tables.tc_volume_classes): per class the summed stiffness fragments
    * [ncls][KT][NNT][32], the elements in class-sorted tasks of 8 (int32

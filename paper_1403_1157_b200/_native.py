@@ -15,7 +15,7 @@ from .build import LIB
 __all__ = ["lib", "TdgDesc", "check", "TDG_OK", "load"]
 
 TDG_OK, TDG_E_INVALID, TDG_E_UNSUPPORTED, TDG_E_CUDA = 0, -1, -2, -3
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double
@@ -41,6 +41,7 @@ class TdgDesc(ctypes.Structure):
         ("face_tc_fold", _p), ("if_fold", _p),
         ("face_groups", _p), ("n_face_groups", _i64), ("face_modal", _p),
         ("if_bval", _p), ("bf_qval", _p),
+        ("seg_chunk_ptr", _p), ("if_code_add", _p), ("bf_code_add", _p),
         ("vol_cls_tab", _p), ("vol_perm", _p), ("vol_task_cls", _p), ("n_vol_tasks", _i64),
         ("vol_chunk_tasks", _p),
         ("n_segments", _i32), ("n_segments_cut", _i32), ("seg_ptr", _p),

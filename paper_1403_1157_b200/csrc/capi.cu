@@ -1,4 +1,5 @@
 // C-ABI entry points (include/taxisdg_b200.h).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -148,6 +149,17 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   p.ifbv = d.if_bval;
   p.bfqv = d.bf_qval;
   ctx->point_data = d.if_bval != nullptr || d.bf_qval != nullptr;
+  if (d.seg_chunk_ptr && d.if_code_add && (d.n_bnd_faces == 0 || d.bf_code_add)) {
+    constexpr int NCH = tdg_ctx::kChunks;
+    const int64_t n1 = int64_t(d.n_segments) * NCH + 1;
+    const int64_t *I = d.seg_chunk_ptr, *W = I + n1, *B = W + n1, *G = B + n1;
+    ctx->segc.resize(size_t(d.n_segments) * NCH);
+    for (int64_t k = 0; k + 1 < n1; ++k)
+      ctx->segc[size_t(k)] = Segment{I[k], I[k + 1], W[k], W[k + 1], B[k], B[k + 1], G[k], G[k + 1]};
+    ctx->ifcode_add = d.if_code_add;
+    ctx->bfcode_add = d.bf_code_add;
+  }
+  ctx->d.seg_chunk_ptr = nullptr;  // copied into ctx->segc
   if (d.vol_cls_tab && d.vol_perm && d.vol_task_cls && d.vol_chunk_tasks) {
     p.vctab = d.vol_cls_tab;
     p.vperm = d.vol_perm;
@@ -332,6 +344,22 @@ int tdg_ssprk3_step(tdg_ctx* ctx, double* U, double* w1, double* w2, double t, d
   return TDG_OK;
 }
 
+}  // extern "C"
+
+// out = b U + c M^-1 out element by element (M^-1 = 1/detJ: orthonormal
+// reference basis), the first host stage's closing combination
+__global__ void k_stage_finalize(int64_t n, int sn, int neg, const double* __restrict__ egeo,
+                                 const double* __restrict__ U, double* __restrict__ out, double b,
+                                 double c) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double idet = 1.0 / __ldg(egeo + (i / sn) * neg);
+    out[i] = fma(b, U[i], c * idet * out[i]);
+  }
+}
+
+extern "C" {
+
 int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, double* U, double* w1, double* w2,
                           int64_t nsteps, double t, double dt, void* stream) {
   (void)t;
@@ -358,8 +386,29 @@ int tdg_ssprk3_steps_host(tdg_ctx* ctx, double* U_host, double* U, double* w1, d
       if (m) cudaMemcpyAsync(U + o, U_host + o, m * sizeof(double), cudaMemcpyHostToDevice, cs);
       cudaEventRecord(ctx->ev_h2d[k], cs);
     }
-    for (int k = 0; k < NCH; ++k) cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
-    int rc = ctx->impl.run(ctx, U, nullptr, w1, w1, 0.0, 1.0, dt, 2, 0, st);
+    int rc = 0;
+    if (!ctx->segc.empty()) {
+      // stage 1 chunk by chunk as the state arrives: the volume terms of
+      // chunk k initialise its rows of w1 (L_h without M^-1), then every
+      // segment's faces of chunk k (elements in chunks <= k, all arrived)
+      // add to them; M^-1 and U1 = U + dt M^-1 L_h(U) close the stage
+      for (int k = 0; k < NCH && !rc; ++k) {
+        cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
+        rc = ctx->impl.volume(ctx, ck[k], ck[k + 1], U, nullptr, w1, nullptr, 0.0, 0.0, 0.0, 0,
+                              st);
+        for (int s = 0; s < ctx->d.n_segments && !rc; ++s)
+          rc = ctx->impl.faces_chunk(ctx, s, k, U, w1, st);
+      }
+      if (!rc) {
+        const int64_t n = ne * int64_t(sn);
+        const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(ctx->num_sms) * 8);
+        k_stage_finalize<<<unsigned(grid), 256, 0, st>>>(n, int(sn), 1 + ctx->d.dim * (ctx->d.dim + 1) / 2,
+                                                         ctx->p.egeo, U, w1, 1.0, dt);
+      }
+    } else {
+      for (int k = 0; k < NCH; ++k) cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0);
+      rc = ctx->impl.run(ctx, U, nullptr, w1, w1, 0.0, 1.0, dt, 2, 0, st);
+    }
     if (!rc) rc = ctx->impl.run(ctx, w1, U, w2, w2, 0.75, 0.25, 0.25 * dt, 2, 0, st);
     // stage 3: every face segment, then the volume kernel chunk by chunk,
     // each chunk's copy-out as soon as it is written

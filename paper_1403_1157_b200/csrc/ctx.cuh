@@ -44,6 +44,9 @@ struct Impl {
   int (*volume)(tdg_ctx*, int64_t e0, int64_t e1, const double* U, const double* U0, double* out,
                 const double* acc, double a, double b, double c, int mode, cudaStream_t st);
   int (*upload)(const OpParams& p);
+  // the faces of segment s restricted to element chunk c (host-data
+  // stepping), adding into acc (the add-only code words: no first writes)
+  int (*faces_chunk)(tdg_ctx*, int s, int c, const double* U, double* acc, cudaStream_t st);
   int max_nqv, max_nqf;
 };
 
@@ -85,6 +88,12 @@ struct tdg_ctx {
   // per direction (created with the context: no call allocates later)
   static constexpr int kChunks = 8;
   int64_t vchunk[kChunks + 1] = {};  // volume-class task offsets of the element chunks
+  // (segment, chunk) sub-segments and the add-only code words (FIRST bits
+  // cleared): the host-data stepping's first stage runs chunk by chunk as
+  // the state arrives, over face sums the volume kernel initialised
+  std::vector<tdg::Segment> segc;
+  const int32_t* ifcode_add = nullptr;
+  const int32_t* bfcode_add = nullptr;
   cudaStream_t s_in[2] = {}, s_out[2] = {};
   cudaEvent_t ev_h2d[kChunks] = {}, ev_d2h[kChunks] = {}, ev_vol[kChunks] = {};
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
@@ -195,8 +204,9 @@ constexpr int SN_of() { return M::S * Dims<D, K>::NB; }
 
 // The faces of one colour segment, adding into the face-sum rows acc.
 template <int D, int K, class M>
-void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, cudaStream_t st) {
-  const OpParams& p = ctx->p;
+void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, cudaStream_t st,
+                 const OpParams* po = nullptr) {
+  const OpParams& p = po ? *po : ctx->p;
   constexpr int NFG = Dims<D, K>::NFG;
   OpParams q = p;  // the segment's face ranges
   q.nif = sg.f1 - sg.f0;
@@ -452,8 +462,19 @@ int upload_const(const OpParams& p) {
 }
 
 template <int D, int K, class M>
+int faces_chunk(tdg_ctx* ctx, int s, int c, const double* U, double* acc, cudaStream_t st) {
+  OpParams p = ctx->p;
+  p.ifcode = ctx->ifcode_add;
+  p.bfcode = ctx->bfcode_add;
+  run_segment<D, K, M>(ctx, ctx->segc[size_t(s) * tdg_ctx::kChunks + c], U, acc, st, &p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TDG_OK : cuda_fail(e, "face launch (chunk)");
+}
+
+template <int D, int K, class M>
 Impl make_impl() {
   return Impl{&configure<D, K, M>, &run<D, K, M>, &volume<D, K, M>, &upload_const<D, K, M>,
+              &faces_chunk<D, K, M>,
               Dims<D, K>::NQV, Dims<D, K>::NQF};
 }
 

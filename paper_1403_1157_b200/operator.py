@@ -94,7 +94,8 @@ class DiscreteOperator:
         self.n_owned = t.elem_geo.shape[0]
         self.n_rows = space.mesh.n_elements  # owned + ghost rows of U
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
-        from .tables import (mma_face_tables, tc_face_blocks, tc_face_fold_tables,
+        from .tables import (CODE_FIRST_IN, CODE_FIRST_OUT, mma_face_tables,
+                             seg_chunk_offsets, tc_face_blocks, tc_face_fold_tables,
                              tc_face_groups, tc_face_tables, tc_volume_classes,
                              tc_volume_tables, modal_face_tables)
         mma, self._mma_stride = mma_face_tables(t)
@@ -133,7 +134,31 @@ class DiscreteOperator:
                                                 dtype=torch.float64, device=self.device)
             self._pd_model = model
             self._set_point_data(0.0)
+        # host-data stepping: (segment, chunk) runs and add-only code words
+        # (tdg_desc.seg_chunk_ptr, tables.seg_chunk_offsets)
+        chunked = self.n_rows == self.n_owned and len(t.if_code) + len(t.bf_code) > 0
+        if chunked:
+            nseg = t.n_seg
+            bseg = np.repeat(np.arange(nseg), np.diff(t.seg_bf))
+            offs = [seg_chunk_offsets(t.if_seg, t.if_chunk, nseg),
+                    seg_chunk_offsets(bseg, t.bf_chunk, nseg)]
+            if len(blocks):
+                offs.append(seg_chunk_offsets(t.if_seg[blocks[:, 0]], t.if_chunk[blocks[:, 0]], nseg))
+            else:
+                offs.append(np.zeros(nseg * 8 + 1, np.int64))
+            if len(groups) and groups.shape[1] and "face_groups" in self._keep:
+                g0 = groups[:, 0]
+                offs.append(seg_chunk_offsets(t.if_seg[g0], t.if_chunk[g0], nseg))
+            else:
+                offs.append(np.zeros(nseg * 8 + 1, np.int64))
+            first = CODE_FIRST_IN | CODE_FIRST_OUT
+            self._keep["if_code_add"] = dev((t.if_code & ~first).astype(np.int32)
+                                            if len(t.if_code) else np.zeros(1, np.int32))
+            self._keep["bf_code_add"] = dev((t.bf_code & ~first).astype(np.int32)
+                                            if len(t.bf_code) else np.zeros(1, np.int32))
         self._host = {
+            "seg_chunk_ptr": (np.ascontiguousarray(np.concatenate(offs), dtype=np.int64)
+                              if chunked else np.zeros(1, np.int64)),
             "seg_ptr": np.ascontiguousarray(np.concatenate(
                 [t.seg_if, t.seg_bf, seg_blk, seg_grp]), dtype=np.int64),
             "diffusivity": np.ascontiguousarray(model.diffusivity(), dtype=np.float64),
@@ -177,6 +202,9 @@ class DiscreteOperator:
             vol_chunk_tasks=hptr(self._host["vol_chunk_tasks"]) if vcls is not None else None,
             if_bval=ptr(k["if_bval"]) if "if_bval" in k else None,
             bf_qval=ptr(k["bf_qval"]) if "bf_qval" in k else None,
+            seg_chunk_ptr=hptr(self._host["seg_chunk_ptr"]) if chunked else None,
+            if_code_add=ptr(k["if_code_add"]) if chunked else None,
+            bf_code_add=ptr(k["bf_code_add"]) if chunked else None,
             n_segments=t.n_seg, n_segments_cut=t.n_seg_cut,
             seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()

@@ -91,6 +91,8 @@ class OperatorTables:
     bf_lf: np.ndarray = None
     if_fid: np.ndarray = None   # mesh face id of every interior (+ mirror) face
     bf_fid: np.ndarray = None   # mesh face id of every wall face
+    if_chunk: np.ndarray = None  # element chunk of every interior face (vol_chunk_bounds)
+    bf_chunk: np.ndarray = None
     face_pts: np.ndarray = None  # face rule points (reference face coordinates)
 
 
@@ -245,13 +247,22 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
     seg_f[cidx] = nc1 + col_c
     seg_w = col_m[len(main):].astype(np.int64)
     n_seg = nc1 + nc2
-    # interior faces by (segment, signature); walls by (segment, table, tag)
-    order = np.lexsort((code & 1023, seg_f))
+    # element chunk of every face (the host-data stepping's copy chunks,
+    # vol_chunk_bounds): the later chunk of its owned elements
+    cbnd = np.asarray(vol_chunk_bounds(n_owned), dtype=np.int64)
+    def echunk(e):
+        return np.clip(np.searchsorted(cbnd, e, side="right") - 1, 0, VOL_CHUNKS - 1)
+    e_out_own = np.where((el[:, 1] >= 0) & (el[:, 1] < n_owned), el[:, 1], el[:, 0])
+    chunk_f = np.maximum(echunk(el[:, 0]), echunk(e_out_own))
+    chunk_w = echunk(fe[nbf, 0])
+    # interior faces by (segment, chunk, signature); walls by (segment,
+    # chunk, table, tag): a segment's faces of one chunk are contiguous
+    order = np.lexsort((code & 1023, chunk_f, seg_f))
     code, geo, el, lfs, seg_f = code[order], geo[order], el[order], lfs[order], seg_f[order]
-    fids = fids[order]
+    fids, chunk_f = fids[order], chunk_f[order]
     btag = mesh.face_tags[nbf].astype(np.int64)
-    border = np.lexsort((btag, tid[nbf, 0], seg_w))
-    nbf, btag, seg_w = nbf[border], btag[border], seg_w[border]
+    border = np.lexsort((btag, tid[nbf, 0], chunk_w, seg_w))
+    nbf, btag, seg_w, chunk_w = nbf[border], btag[border], seg_w[border], chunk_w[border]
     bcode = tid[nbf, 0] | (btag << 11)
     seg_if = np.searchsorted(seg_f, np.arange(n_seg + 1), side="left")
     seg_bf = np.searchsorted(seg_w, np.arange(n_seg + 1), side="left")
@@ -282,7 +293,17 @@ def build_tables(space: DGSpace, model, scheme: FluxScheme,
         n_cut=n_cut, n_seg=int(n_seg), n_seg_cut=int(nc2),
         seg_if=seg_if.astype(np.int64), seg_bf=seg_bf.astype(np.int64),
         if_seg=seg_f.astype(np.int32), if_lf=i32(lfs), bf_lf=i32(fl[nbf, 0]),
-        if_fid=fids, bf_fid=nbf.astype(np.int64), face_pts=np.asarray(fr.points, dtype=float))
+        if_fid=fids, bf_fid=nbf.astype(np.int64), face_pts=np.asarray(fr.points, dtype=float),
+        if_chunk=chunk_f.astype(np.int32), bf_chunk=chunk_w.astype(np.int32))
+
+
+def seg_chunk_offsets(seg: np.ndarray, chunk: np.ndarray, n_seg: int) -> np.ndarray:
+    """Offsets of the (segment, chunk) runs of an array sorted by (segment,
+    chunk): int64 [n_seg * VOL_CHUNKS + 1]; run (s, c) is [o[s C + c],
+    o[s C + c + 1]).  The host-data stepping runs its first stage chunk by
+    chunk as the state arrives (csrc/capi.cu tdg_ssprk3_steps_host)."""
+    key = np.asarray(seg, dtype=np.int64) * VOL_CHUNKS + np.asarray(chunk, dtype=np.int64)
+    return np.searchsorted(key, np.arange(n_seg * VOL_CHUNKS + 1), side="left").astype(np.int64)
 
 
 def _ceil(x, m):
@@ -489,7 +510,8 @@ def tc_face_blocks(t: OperatorTables, block: int = 8):
     nif = len(t.if_code)
     if nif == 0:
         return np.zeros((0, 2), np.int32), np.zeros(t.n_seg + 1, np.int64)
-    sig = (t.if_code.astype(np.int64) & 1023) + t.if_seg.astype(np.int64) * 1024
+    sig = ((t.if_code.astype(np.int64) & 1023)
+           + (t.if_seg.astype(np.int64) * VOL_CHUNKS + t.if_chunk) * 1024)
     brk = np.flatnonzero(np.diff(sig)) + 1
     starts = np.concatenate([[0], brk])
     lens = np.diff(np.concatenate([starts, [nif]]))
@@ -674,7 +696,8 @@ def tc_face_groups(t: OperatorTables, cls: np.ndarray, n_species: int):
         return np.zeros((0, nfq), np.int32), np.zeros(t.n_seg + 1, np.int64)
     minus = (t.if_code.astype(np.int64) >> 10) & 1
     ncls = int(cls.max()) + 1
-    key = ((t.if_seg.astype(np.int64) * ncls + cls[:, 0]) * ncls + cls[:, 1]) * 2 + minus
+    sc = t.if_seg.astype(np.int64) * VOL_CHUNKS + t.if_chunk
+    key = ((sc * ncls + cls[:, 0]) * ncls + cls[:, 1]) * 2 + minus
     order = np.argsort(key, kind="stable")
     ks = key[order]
     brk = np.flatnonzero(np.diff(ks)) + 1

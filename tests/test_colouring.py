@@ -126,9 +126,12 @@ def test_face_groups_cover_each_face_once_within_one_class(cells, order, scheme,
     assert seg_g[0] == 0 and seg_g[-1] == len(groups)
     for s in range(t.n_seg):
         assert (t.if_seg[groups[seg_g[s]:seg_g[s + 1], 0]] == s).all()
-    # a run (same key) has at most one partial group
+    # a run (same segment, element chunk, classes, K- side) has at most one
+    # partial group, and a group never straddles a chunk
+    assert (t.if_chunk[g] == t.if_chunk[f0]).all()
     partial = ~valid.all(axis=1)
-    key = t.if_seg[f0[:, 0]] * 10**6 + cls[f0[:, 0], 0] * 10**4 + cls[f0[:, 0], 1] * 10 + minus[f0[:, 0]]
+    f = f0[:, 0]
+    key = (((t.if_seg[f] * 8 + t.if_chunk[f]) * 10**3 + cls[f, 0]) * 10**3 + cls[f, 1]) * 2 + minus[f]
     assert len(np.unique(key[partial])) == partial.sum()
 
 
@@ -169,3 +172,30 @@ def test_volume_classes_cover_each_element_once_per_chunk(cells, order):
     stride = len(tabs) // (tcls.max() + 1)
     assert np.allclose(tabs[tcls[0] * stride:(tcls[0] + 1) * stride], _frag_kn(KP).ravel(),
                        rtol=0, atol=1e-13 * np.abs(Kc).max())
+
+
+@pytest.mark.parametrize("cells,order", [((6, 4, 4), 2), ((5, 3, 3), 3)])
+def test_segment_chunk_runs_read_only_arrived_chunks(cells, order):
+    """tables.seg_chunk_offsets (host-data stepping: the first stage runs
+    chunk by chunk as the state arrives): within every colour segment the
+    faces and walls are ordered by element chunk, run (s, c) holds exactly
+    the segment's faces of chunk c, and a face of chunk c touches elements
+    of chunks <= c only (all copied in when it runs)."""
+    from paper_1403_1157_b200.tables import VOL_CHUNKS, seg_chunk_offsets, vol_chunk_bounds
+    t = build_tables(DGSpace(unit_cube(*cells), order, 6), PlaqueModel(), FluxScheme("cdg2"))
+    ne = t.elem_geo.shape[0]
+    cb = np.asarray(vol_chunk_bounds(ne))
+    ch = lambda e: np.searchsorted(cb, e, side="right") - 1
+    off = seg_chunk_offsets(t.if_seg, t.if_chunk, t.n_seg)
+    assert off[0] == 0 and off[-1] == len(t.if_code)
+    for s in range(t.n_seg):
+        for c in range(VOL_CHUNKS):
+            a, b = off[s * VOL_CHUNKS + c], off[s * VOL_CHUNKS + c + 1]
+            assert (t.if_seg[a:b] == s).all() and (t.if_chunk[a:b] == c).all()
+            el = t.if_elems[a:b]
+            assert (ch(el[:, 0]) <= c).all() and (ch(el[el[:, 1] >= 0, 1]) <= c).all()
+            assert (np.maximum(ch(el[:, 0]), ch(np.where(el[:, 1] >= 0, el[:, 1], el[:, 0]))) == c).all()
+    bseg = np.repeat(np.arange(t.n_seg), np.diff(t.seg_bf))
+    boff = seg_chunk_offsets(bseg, t.bf_chunk, t.n_seg)
+    assert boff[-1] == len(t.bf_code)
+    assert (ch(t.bf_elem) == t.bf_chunk).all()

@@ -668,10 +668,12 @@ def test_species_l2_on_device_is_the_parity_metric():
 
 
 @pytest.mark.parametrize("dim,order", [(2, 2), (2, 3), (3, 1), (3, 3)])
-def test_host_steps_bitwise_equal_device_steps(dim, order):
-    """tdg_ssprk3_steps_host (per-step copy-in / copy-out in chunks, the
-    last stage's volume kernel chunk by chunk) == copy-in,
-    tdg_ssprk3_step, copy-out, bit for bit, over several steps."""
+def test_host_steps_match_device_steps(dim, order):
+    """tdg_ssprk3_steps_host (per-step copy-in / copy-out in chunks; the
+    first stage chunk by chunk as the state arrives -- volume terms first,
+    face sums added -- and the last stage's volume kernel chunk by chunk)
+    == copy-in, tdg_ssprk3_step, copy-out over several steps, to roundoff
+    (the first stage sums in another order)."""
     mesh = unit_square(96, 64) if dim == 2 else unit_cube(6, 5, 4)
     space = DGSpace(mesh, order, 6)
     op = _op(space, PlaqueModel(PlaqueParams(**AMPLIFIED)), FluxScheme("cdg2"))
@@ -684,7 +686,7 @@ def test_host_steps_bitwise_equal_device_steps(dim, order):
     for _ in range(3):
         op.ssprk3_step(Ud, W, dt)
     torch.cuda.synchronize()
-    assert torch.equal(Uh, Ud.cpu())
+    assert rel_l2_per_species(space, Uh.numpy(), Ud.cpu().numpy()).max() <= 1e-14
     assert not torch.equal(Uh, U0)
     with pytest.raises(ValueError):
         op.ssprk3_steps_host(U0.clone(), 1, dt)        # not pinned
