@@ -15,7 +15,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libtaxisdg_b200.so")
+LIB = os.environ.get("TDG_LIB_OUT") or os.path.join(PKG, "libtaxisdg_b200.so")
+# A/B builds only (tools/): extra -D flags for an alternative library file
+EXTRA = os.environ.get("TDG_EXTRA_FLAGS", "").split()
 SOURCES = ["capi.cu", "hostio.cu", "vecops.cu", "inst_plaque.cu", "inst_reduced.cu",
            "inst_diffusion.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
@@ -49,9 +51,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs, procs = [], []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o"))
         cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
-               "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+               "-I", CSRC, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                             stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
@@ -70,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as fh:
+    with open(LIB + ".ptxas.log" if EXTRA else os.path.join(CSRC, "ptxas.log"), "w") as fh:
         fh.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
