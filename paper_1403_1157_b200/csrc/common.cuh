@@ -97,6 +97,14 @@ __device__ __forceinline__ void acc_put(double* p, double v, bool first) {
 // BoundaryTag (mesh.py:46-52)
 enum Tag { GAMMA1 = 1, GAMMA1_IN = 2, GAMMA2 = 3, NO_FLOW = 4 };
 
+// read-only global load that does not allocate in L1 (streamed state rows:
+// L1 stays for the operand tables)
+__device__ __forceinline__ double ld_na(const double* p) {
+  double d;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(d) : "l"(p));
+  return d;
+}
+
 // 32-byte read-only global load (sm_100 LDG.E.ENL2.256); p 32-byte aligned
 __device__ __forceinline__ void ld256(const double* p, double* d) {
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"

@@ -151,8 +151,13 @@ int configure(int nqv) {
   if constexpr (TcmFace<D, K, M>::ok) {
     const int sm = int(TcmFace<D, K, M>::smem());
     const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    for (auto fn : {k_faces_tcm<D, K, M, 0>, k_faces_tcm<D, K, M, 1>, k_faces_tcm<D, K, M, 2>})
+    for (auto fn : {k_faces_tcm<D, K, M, 0>, k_faces_tcm<D, K, M, 1>, k_faces_tcm<D, K, M, 2>}) {
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, attr, sm);
+#if TDG_TCM_CARVE
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, TDG_TCM_CARVE);
+#endif
+    }
     if (e != cudaSuccess) return cuda_fail(e, "configure faces_tcm");
   }
   if constexpr (TcVol<D, K, M>::ok) {

@@ -32,6 +32,10 @@
 // output columns so a GEMM's accumulator is the next GEMM's A operand).
 #pragma once
 
+#ifndef TDG_TCM_MINB
+#define TDG_TCM_MINB 8
+#endif
+
 #include "common.cuh"
 #include "kernels_mma.cuh"
 #include "kernels_tcf.cuh"
@@ -83,11 +87,19 @@ struct TcmFace {
   // physics slots per (face, point): u_in, u_out of the value species, gav
   // of the gradient species (odd stride: conflict-free physics reads)
   static constexpr int NSL = 2 * M::NVAL + M::NGRAD, XS = NSL | 1;
-  static constexpr int OXS = 0, OCV = OXS + NFQ * QP * XS, CWS = OCV + NFQ * QP * NCV;
+  // p >= 3: the point physics writes its NCV results over the slots it has
+  // read (face_point reads every input first), so there is no separate cv
+  // array and 8 CTAs leave L1 room for the class tables a group streams
+  // (64^3 p = 3 faces 9.25 -> 8.73 ms; at p = 2 the extra barrier costs more
+  // than the L1 gains: 5.27 -> 5.36 ms)
+  static constexpr bool ALIAS = K >= 3;
+  static_assert(!ALIAS || NCV <= XS, "cv slots alias the physics slots");
+  static constexpr int OXS = 0, OCV = ALIAS ? OXS : OXS + NFQ * QP * XS,
+                       CWS = OCV + (ALIAS ? NFQ * QP * XS : NFQ * QP * NCV);
   static constexpr size_t smem() { return size_t(CWS) * 8; }
   // 80 registers (small spills) -> 8 CTAs / 24 warps per SM: 64^3 p = 3
   // faces 10.8 -> 10.3 ms, p = 2 6.2 -> 5.1 ms against 128 registers
-  static constexpr int MINB = 7;
+  static constexpr int MINB = K >= 3 ? TDG_TCM_MINB : 7;
   static constexpr bool ok = D == 3 && K >= 1 && M::kConv && !M::kMirror && MT >= 1 &&
                              MT <= 4 && F <= 64 && smem() * MINB <= 200 * 1024;
 };
@@ -169,6 +181,7 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
         gm[n][j] = 0.5 * (vI[n][j] + vO[n][j]);
       }
 
+    if constexpr (T::ALIAS) __syncthreads();  // the previous group's B2 has read its cv slots
     // ---- B1: point values -> physics slots; du kept in registers -------
     double du[QT][2];
 #pragma unroll
@@ -205,7 +218,14 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
                          : (kind == 1 ? xq[M::NVAL + mval_slot<M>(s2)]
                                       : xq[2 * M::NVAL + mgrad_slot<M>(s2)]);
       };
-      M::face_point(p.P, fetch, cvs + (f * QP + q) * NCV);
+      if constexpr (T::ALIAS) {
+        double cv[NCV];
+        M::face_point(p.P, fetch, cv);
+#pragma unroll
+        for (int k = 0; k < NCV; ++k) xs[(f * QP + q) * XS + k] = cv[k];
+      } else {
+        M::face_point(p.P, fetch, cvs + (f * QP + q) * NCV);
+      }
     }
     __syncthreads();
     // ---- B2 + C: the row's modal bracket yb = (Ybr | Xbr) ---------------
@@ -222,7 +242,7 @@ k_faces_tcm(OpParams p, const double* __restrict__ tm, const int32_t* __restrict
         const int q = 8 * qt + 2 * t + j;
         double v = 0.0;
         if (q < F) {
-          const double* c = cvs + (fq * QP + q) * NCV;
+          const double* c = T::ALIAS ? xs + (fq * QP + q) * XS : cvs + (fq * QP + q) * NCV;
           v = 0.5 * c[0] * du[qt][j];
 #pragma unroll
           for (int k = 0; k < M::NFX; ++k)
