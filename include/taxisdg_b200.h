@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define TDG_ABI_VERSION 8
+#define TDG_ABI_VERSION 9
 
 #if defined(__GNUC__)
 #define TDG_API __attribute__((visibility("default")))
@@ -350,9 +350,20 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
  * transposed tensor-core volume kernel wherever it compiles (default only
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
  * per SM of the 2D register-resident face kernel's grid-stride grid (0 =
- * default, 15 = uncapped, one face group per warp).  0 (default) lets the
- * library pick the fastest compiled-in kernels. */
+ * default, 15 = uncapped, one face group per warp); bit 17: the 2D faces on
+ * the shared-memory-table kernel instead of the signature-run kernel.  0
+ * (default) lets the library pick the fastest compiled-in kernels. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
+
+/* 2D signature runs (k_faces_sig): tdg_create cuts the interior faces into
+ * maximal runs of one (inside, outside) trace-table signature and launches
+ * each run with its tables as kernel parameters; a run whose faces all carry
+ * the same Jinv n on both sides has it folded into the tables.  Returns the
+ * number of runs (0: the kernel is not used: 3D, Dirichlet mirror models,
+ * non-default face rule, boundary point data, or faces not sorted into few
+ * runs) and how many are folded.  Replaces nothing in the reference (launch
+ * bookkeeping of operator.py:262-284's face loop). */
+TDG_API int tdg_face_runs(const tdg_ctx* ctx, int64_t* n_runs, int64_t* n_folded);
 
 /* Per-kernel device timing: with profiling enabled every operator kernel
  * launch is bracketed by CUDA events on its own stream;

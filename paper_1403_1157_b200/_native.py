@@ -15,7 +15,7 @@ from .build import LIB
 __all__ = ["lib", "TdgDesc", "check", "TDG_OK", "load"]
 
 TDG_OK, TDG_E_INVALID, TDG_E_UNSUPPORTED, TDG_E_CUDA = 0, -1, -2, -3
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double
@@ -88,10 +88,11 @@ def load(path: str = LIB):
     lib.tdg_profile.argtypes = [_p, ctypes.c_int]
     lib.tdg_set_variant.argtypes = [_p, ctypes.c_int]
     lib.tdg_profile_read.argtypes = [_p, ctypes.POINTER(_d), ctypes.POINTER(_i64)]
+    lib.tdg_face_runs.argtypes = [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
     lib.tdg_fp64_probe.argtypes = [_p, _i64, _p]
     lib.tdg_fp64_probe_threads.restype = _i64
     lib.tdg_dmma_probe.argtypes = [_p, _i64, _p]
-    for name in ("tdg_apply_host", "tdg_mgs_pass", "tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
+    for name in ("tdg_face_runs", "tdg_apply_host", "tdg_mgs_pass", "tdg_color_faces", "tdg_ssprk3_steps_host", "tdg_species_l2", "tdg_mgs", "tdg_species_totals", "tdg_rk_stage_part", "tdg_dmma_probe", "tdg_set_variant", "tdg_profile", "tdg_profile_read", "tdg_fp64_probe",
                  "tdg_create", "tdg_destroy", "tdg_apply", "tdg_rk_stage",
                  "tdg_ssprk3_step", "tdg_dot", "tdg_norm2", "tdg_axpby",
                  "tdg_axpy_dev", "tdg_scale_norm", "tdg_jv_shift", "tdg_jv_diff"):

@@ -177,6 +177,7 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
   }
   int rc = impl.configure(d.nq_vol);
   if (rc == TDG_OK) rc = impl.upload(p);
+  if (rc == TDG_OK) rc = impl.prepare(ctx);
   if (rc != TDG_OK) {
     delete ctx;
     return rc;
@@ -539,6 +540,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->no_groups = ((variant >> 14) & 1) != 0;  // bit 14: one-face kernel despite face groups
   ctx->no_vcls = ((variant >> 15) & 1) != 0;    // bit 15: no volume element classes
   ctx->no_modal = ((variant >> 16) & 1) != 0;   // bit 16: face groups on full traces
+  ctx->no_sig = ((variant >> 17) & 1) != 0;     // bit 17: k_faces_fast despite signature runs
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;
@@ -547,6 +549,14 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
     cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;
   }
+  return TDG_OK;
+}
+
+int tdg_face_runs(const tdg_ctx* ctx, int64_t* n_runs, int64_t* n_folded) {
+  if (!ctx || !n_runs || !n_folded) return fail(TDG_E_INVALID, "null argument");
+  *n_runs = int64_t(ctx->sig_runs.size());
+  *n_folded = 0;
+  for (const SigRun& r : ctx->sig_runs) *n_folded += r.fold ? 1 : 0;
   return TDG_OK;
 }
 

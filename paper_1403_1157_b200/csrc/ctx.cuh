@@ -13,6 +13,8 @@
 // segments (part 2 of a split stage).
 #pragma once
 
+#include <cmath>
+#include <cstring>
 #include <string>
 #include <utility>
 #include <vector>
@@ -44,6 +46,9 @@ struct Impl {
   int (*volume)(tdg_ctx*, int64_t e0, int64_t e1, const double* U, const double* U0, double* out,
                 const double* acc, double a, double b, double c, int mode, cudaStream_t st);
   int (*upload)(const OpParams& p);
+  // host-side launch data made once at tdg_create (signature runs of the
+  // 2D face kernel)
+  int (*prepare)(tdg_ctx*);
   // the faces of segment s restricted to element chunk c (host-data
   // stepping), adding into acc (the add-only code words: no first writes)
   int (*faces_chunk)(tdg_ctx*, int s, int c, const double* U, double* acc, cudaStream_t st);
@@ -59,6 +64,15 @@ bool pick_diffusion(int dim, int order, Impl* out);
 // kernel [g0, g1)
 struct Segment {
   int64_t f0, f1, w0, w1, b0, b1, g0, g1;
+};
+
+// maximal run of interior faces [f0, f1) with one (inside, outside)
+// trace-table signature (k_faces_sig)
+struct SigRun {
+  int64_t f0, f1;
+  int tin, tout;
+  bool fold;        // every face has the same Jinv n on both sides
+  double jn[2][3];  // ... these
 };
 
 }  // namespace tdg
@@ -82,6 +96,12 @@ struct tdg_ctx {
   bool no_vcls = false;        // testing: per-element metric scaling despite volume classes
   bool no_modal = false;       // testing: face groups on full traces despite modal tables
   bool point_data = false;     // boundary point data: the generic face kernels
+  bool no_sig = false;         // testing: k_faces_fast despite signature runs
+  // 2D: signature runs over the interior faces (sorted by f0) and host
+  // copies of the face tables their kernel parameters are built from;
+  // empty when the faces are not sorted into few runs
+  std::vector<tdg::SigRun> sig_runs;
+  std::vector<double> h_fB, h_fG, h_fPw, h_fw;
   int num_sms = 148;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
@@ -204,6 +224,12 @@ struct KernelTimer {
   }
 };
 
+// k_faces_sig: at most this many signature runs over all interior faces /
+// launches per segment; meshes whose faces are not sorted into few runs
+// stay on k_faces_fast
+constexpr int kMaxSigRuns = 4096;
+constexpr size_t kMaxSigRunsPerSegment = 8;
+
 template <class M, int D, int K>
 constexpr int SN_of() { return M::S * Dims<D, K>::NB; }
 
@@ -324,6 +350,78 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
       const int64_t grid = (warps + T::WARPS - 1) / T::WARPS;
       k_faces_mma<D, K, M><<<unsigned(grid), 128, T::smem(), st>>>(q, q.fmma, U, acc);
       return;
+    }
+  }
+  // 2D: the interior faces of the segment's signature runs with their
+  // tables as kernel parameters; the last run's launch takes the walls
+  if constexpr (SigFace<D, K, M>::ok) {
+    if (dflt && !ctx->no_sig && !ctx->sig_runs.empty() && q.nif > 0) {
+      // runs overlapping [f0, f1) (the chunked sub-segments cut runs)
+      size_t r0 = 0, r1 = ctx->sig_runs.size();
+      while (r0 < r1 && ctx->sig_runs[r0].f1 <= sg.f0) ++r0;
+      size_t re = r0;
+      while (re < r1 && ctx->sig_runs[re].f0 < sg.f1) ++re;
+      if (re - r0 <= kMaxSigRunsPerSegment) {
+        using T = SigFace<D, K, M>;
+        constexpr int F = Dims<D, K>::NQF, NB = Dims<D, K>::NB;
+        static int resident = 0;
+        if (resident == 0) {
+          int nb = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_faces_sig<D, K, M, D>, 128, 0) !=
+                  cudaSuccess || nb < 1)
+            nb = T::MINB;
+          resident = nb;
+        }
+        for (size_t k = r0; k < re; ++k) {
+          const SigRun& rr = ctx->sig_runs[k];
+          const int64_t a = rr.f0 > sg.f0 ? rr.f0 : sg.f0, b = rr.f1 < sg.f1 ? rr.f1 : sg.f1;
+          if (b <= a) continue;
+          OpParams r = q;
+          r.nif = b - a;
+          r.ifel = p.ifel + 2 * a;
+          r.ifcode = p.ifcode + a;
+          r.ifgeo = p.ifgeo + a * NFG;
+          if (k + 1 < re) r.nbf = 0;  // the walls go with the last run
+          KernelTimer kt(ctx, 0, st);
+          const int64_t groups = (r.nif + T::FPW - 1) / T::FPW;
+          const int64_t wgroups = (r.nbf + T::FPW - 1) / T::FPW;
+          int64_t grid = (groups + wgroups + T::WARPS - 1) / T::WARPS;
+          if (ctx->face_ctas_per_sm >= 0) {
+            const int per = ctx->face_ctas_per_sm > 0 ? ctx->face_ctas_per_sm : resident;
+            const int64_t cap = int64_t(ctx->num_sms) * per;
+            grid = grid < cap ? grid : cap;
+          }
+          auto fill = [&](auto& tb, bool fold) {
+            for (int side = 0; side < 2; ++side) {
+              const int t = side ? rr.tout : rr.tin;
+              std::memcpy(tb.B[side], ctx->h_fB.data() + size_t(t) * F * NB, sizeof(tb.B[side]));
+              std::memcpy(tb.Pw[side], ctx->h_fPw.data() + size_t(t) * F * F, sizeof(tb.Pw[side]));
+              const double* g = ctx->h_fG.data() + size_t(t) * F * NB * D;
+              double* o = &tb.G[side][0][0][0];
+              for (int j = 0; j < F * NB; ++j) {
+                if (fold) {  // d_n phi = G . (Jinv n), k_faces_fast's order
+                  double v = 0.0;
+                  for (int c = 0; c < D; ++c) v = std::fma(g[j * D + c], rr.jn[side][c], v);
+                  o[j] = v;
+                } else {
+                  for (int c = 0; c < D; ++c) o[j * D + c] = g[j * D + c];
+                }
+              }
+            }
+            std::memcpy(tb.w, ctx->h_fw.data(), sizeof(tb.w));
+          };
+          if (rr.fold && !ctx->no_fold) {
+            FaceSigTab<D, K, 1> tb;
+            fill(tb, true);
+            k_faces_sig<D, K, M, 1><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+          } else {
+            FaceSigTab<D, K, D> tb;
+            fill(tb, false);
+            k_faces_sig<D, K, M, D><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+          }
+        }
+        return;
+      }
     }
   }
   // 2D: register-resident kernel, interior faces and walls in one launch
@@ -466,6 +564,72 @@ int upload_const(const OpParams& p) {
   return TDG_OK;
 }
 
+// Signature runs of the interior faces and host copies of the face tables
+// (k_faces_sig builds its kernel-parameter tables from them).  The face
+// arrays are device memory: read back once, here.
+template <int D, int K, class M>
+int prepare(tdg_ctx* ctx) {
+  if constexpr (SigFace<D, K, M>::ok) {
+    const OpParams& p = ctx->p;
+    if (p.nqf != Dims<D, K>::NQF || p.nif == 0 || ctx->point_data) return TDG_OK;
+    constexpr int F = Dims<D, K>::NQF, NB = Dims<D, K>::NB, NT = Dims<D, K>::NT;
+    std::vector<int32_t> code(size_t(p.nif));
+    ctx->h_fB.resize(size_t(NT) * F * NB);
+    ctx->h_fG.resize(size_t(NT) * F * NB * D);
+    ctx->h_fPw.resize(size_t(NT) * F * F);
+    ctx->h_fw.resize(F);
+    cudaError_t e = cudaMemcpy(code.data(), p.ifcode, code.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    auto back = [&e](std::vector<double>& h, const double* d) {
+      if (e == cudaSuccess) e = cudaMemcpy(h.data(), d, h.size() * sizeof(double), cudaMemcpyDeviceToHost);
+    };
+    back(ctx->h_fB, p.fB);
+    back(ctx->h_fG, p.fG);
+    back(ctx->h_fPw, p.fPw);
+    back(ctx->h_fw, p.fw);
+    if (e != cudaSuccess) return cuda_fail(e, "face tables -> host");
+    std::vector<SigRun> runs;
+    bool ok = true;
+    for (int64_t f = 0; f < p.nif && ok; ++f) {
+      const int c = code[size_t(f)];
+      const int tin = c & 31, tout = (c >> 5) & 31;
+      ok = !((c >> 14) & 1) && tin < NT && tout < NT;  // no mirror faces
+      if (runs.empty() || runs.back().tin != tin || runs.back().tout != tout) {
+        runs.push_back(SigRun{f, f + 1, tin, tout, false, {}});
+        ok = ok && runs.size() <= size_t(kMaxSigRuns);
+      } else {
+        runs.back().f1 = f + 1;
+      }
+    }
+    if (ok) {
+      // runs whose faces all carry the same Jinv n (bitwise) fold it into
+      // the tables; the face records are read back in pieces
+      constexpr int NFG = Dims<D, K>::NFG;
+      constexpr int64_t PIECE = int64_t(1) << 18;
+      std::vector<double> geo(size_t(PIECE) * NFG);
+      for (SigRun& r : runs) {
+        r.fold = true;
+        bool have = false;
+        for (int64_t f0 = r.f0; f0 < r.f1 && r.fold; f0 += PIECE) {
+          const int64_t n = r.f1 - f0 < PIECE ? r.f1 - f0 : PIECE;
+          e = cudaMemcpy(geo.data(), p.ifgeo + f0 * NFG, size_t(n) * NFG * sizeof(double),
+                         cudaMemcpyDeviceToHost);
+          if (e != cudaSuccess) return cuda_fail(e, "face records -> host");
+          if (!have) {
+            for (int side = 0; side < 2; ++side)
+              for (int c = 0; c < D; ++c) r.jn[side][c] = geo[size_t(side) * D + c];
+            have = true;
+          }
+          for (int64_t f = 0; f < n && r.fold; ++f)
+            for (int j = 0; j < 2 * D; ++j)
+              r.fold = r.fold && geo[size_t(f) * NFG + j] == r.jn[j / D][j % D];
+        }
+      }
+      ctx->sig_runs = std::move(runs);
+    }
+  }
+  return TDG_OK;
+}
+
 template <int D, int K, class M>
 int faces_chunk(tdg_ctx* ctx, int s, int c, const double* U, double* acc, cudaStream_t st) {
   OpParams p = ctx->p;
@@ -479,7 +643,7 @@ int faces_chunk(tdg_ctx* ctx, int s, int c, const double* U, double* acc, cudaSt
 template <int D, int K, class M>
 Impl make_impl() {
   return Impl{&configure<D, K, M>, &run<D, K, M>, &volume<D, K, M>, &upload_const<D, K, M>,
-              &faces_chunk<D, K, M>,
+              &prepare<D, K, M>, &faces_chunk<D, K, M>,
               Dims<D, K>::NQV, Dims<D, K>::NQF};
 }
 

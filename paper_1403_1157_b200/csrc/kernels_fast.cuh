@@ -25,6 +25,15 @@
 #include "kernels.cuh"
 #include "models.cuh"
 
+// A/B builds: resident CTAs per SM the signature-run face kernel is
+// compiled for (0 = the default of its struct)
+#ifndef TDG_SIG_MINB
+#define TDG_SIG_MINB 0
+#endif
+#ifndef TDG_SIG_NARROW
+#define TDG_SIG_NARROW 0
+#endif
+
 namespace tdg {
 
 template <int D, int K, class M>
@@ -493,6 +502,287 @@ k_faces_fast(OpParams p, const double* __restrict__ U, double* __restrict__ ACC,
       acc_row_wide<NB>(ACC + int64_t(eout) * SN + s * NB, ro, code_first_out(code));
   }
   __syncwarp();  // the warp's scratch is rewritten by the next group
+  }
+}
+
+// ------------------------------------------------- signature-run face kernel
+//
+// k_faces_sig  the interior faces of one run of a colour segment that share
+//              their (inside, outside) trace-table signature.  The run's
+//              tables (B, reference gradients, Pw of both sides, weights)
+//              travel as a __grid_constant__ kernel parameter, so every
+//              table entry reaches its DFMA through the constant bank /
+//              uniform registers: no table loads on the L1 data path at
+//              all.  k_faces_fast reads one 16-byte shared-memory row piece
+//              per two DFMAs and is bound by the L1 return path (ncu:
+//              l1tex 80-88%, FP64 pipe 32-35%).
+//              NG = D: the normal derivative is taken after the contraction
+//              (jn . (G c) instead of (G jn) . c), D-1 more DFMAs per entry
+//              but no per-face table.  NG = 1: every face of the run has
+//              the same Jinv n on both sides (structured meshes with
+//              exactly representable cell sizes), and the host folds it
+//              into the tables (G holds d_n phi).
+//              Same lane mapping, physics transpose, penalty and face-sum
+//              updates as k_faces_fast.  Structured and jittered triangle
+//              meshes have one signature pair per colour segment.  Groups
+//              past the interior ones are the segment's prescribed-flux
+//              walls (k_faces_fast's wall branch, trace rows from global
+//              memory), so a segment is one launch.
+template <int D, int K, int NG>
+struct FaceSigTab {
+  static constexpr int F = Dims<D, K>::NQF, NB = Dims<D, K>::NB;
+  double B[2][F][NB];      // trace tables: inside / outside signature
+  double G[2][F][NB][NG];  // reference gradients (NG = D) or d_n phi (NG = 1) at the face points
+  double Pw[2][F][F];      // lifting tables
+  double w[F];             // face weights
+};
+
+template <int D, int K, class M>
+struct SigFace {
+  using T = FastFace<D, K, M>;
+  static constexpr int NB = T::NB, S = T::S, F = T::F, XS = T::XS, NCV = T::NCV, FPW = T::FPW;
+  static constexpr int WARPS = 4;
+  // per-face scratch: the species transpose and the coupled point results;
+  // stride = 6 (mod 16) doubles as in k_faces_fast
+  static constexpr int PF0 = (3 * XS * F + F * NCV + 1) & ~1;
+  static constexpr int PF = PF0 + ((6 - PF0 % 16) + 16) % 16;
+  static constexpr bool ok = T::ok && !M::kMirror && D == 2 &&
+                             sizeof(FaceSigTab<D, K, D>) + sizeof(OpParams) <= 16 * 1024;
+  // k <= 2: 5 CTAs (20 warps) per SM at 96 registers; k = 3: 4 CTAs at
+  // 128 (no spills).  Measured at C2 / jittered C3-quarter sizes: 3 CTAs
+  // - / 626 us, 4: 79 / 576, 5: 78 / 594, 6: 76 / 672
+  static constexpr int MINB = TDG_SIG_MINB > 0 ? TDG_SIG_MINB : (NB <= 6 ? 5 : 4);
+};
+
+// row accesses of the signature-run kernel: the 32-byte pieces of
+// k_faces_fast (fewer L1 wavefronts, alignment selects) or plain 16-byte
+// pieces (TDG_SIG_NARROW: fewer instructions)
+template <int NB>
+__device__ __forceinline__ void sig_load_row(const double* src, double* dst) {
+#if TDG_SIG_NARROW
+  load_row<NB>(src, dst);
+#else
+  load_row_wide<NB>(src, dst);
+#endif
+}
+template <int NB>
+__device__ __forceinline__ void sig_acc_row(double* dst, const double* v, bool first) {
+#if TDG_SIG_NARROW
+  if (!first) {
+    double o[NB];
+    smem_row<NB>(dst, o);  // plain (coherent) 16-byte loads
+#pragma unroll
+    for (int i = 0; i < NB; ++i) o[i] += v[i];
+    store_row<NB>(dst, o);
+  } else {
+    store_row<NB>(dst, v);
+  }
+#else
+  acc_row_wide<NB>(dst, v, first);
+#endif
+}
+
+template <int D, int K, class M, int NG>
+__global__ void __launch_bounds__(128, SigFace<D, K, M>::MINB)
+k_faces_sig(const __grid_constant__ OpParams p, const __grid_constant__ FaceSigTab<D, K, NG> tb,
+            const double* __restrict__ U, double* __restrict__ ACC, int64_t ngroups,
+            int64_t nwgroups) {
+  using T = SigFace<D, K, M>;
+  constexpr int NB = T::NB, S = T::S, SN = S * NB, F = T::F, FPW = T::FPW, NCV = T::NCV;
+  constexpr int NFG = Dims<D, K>::NFG;
+  __shared__ __align__(16) double sm[T::WARPS * FPW * T::PF];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / S, s = lane - grp * S, base = grp * S;
+  const bool lane_ok = grp < FPW;
+  double* xch = sm + (warp * FPW + (lane_ok ? grp : 0)) * T::PF;  // [3][F][XS]
+  double* cvs = xch + 3 * T::XS * F;                              // [F][NCV]
+  const double As = p.A[s];
+
+  for (int64_t gw = int64_t(blockIdx.x) * T::WARPS + warp; gw < ngroups + nwgroups;
+       gw += int64_t(gridDim.x) * T::WARPS) {
+    if (gw >= ngroups) {
+      // prescribed wall flux: only the gate species' trace is needed
+      const int64_t b = (gw - ngroups) * FPW + grp;
+      const bool active = lane_ok && b < p.nbf;
+      const int64_t bc = b < p.nbf ? b : p.nbf - 1;
+      const int code = __ldg(p.bfcode + bc);
+      const int ein = __ldg(p.bfel + bc);
+      const double sfac = __ldg(p.bfgeo + bc);
+      double ci[NB], ri[NB];
+      load_row<NB>(U + int64_t(ein) * SN + s * NB, ci);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) ri[i] = 0.0;
+      const double* Bi = p.fB + code_tin(code) * F * NB;
+      const int tag = code_tag(code);
+#pragma unroll
+      for (int q = 0; q < F; ++q) {
+        double bi[NB];
+        load_row<NB>(Bi + q * NB, bi);
+        double u = 0.0;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) u = fma(bi[i], ci[i], u);
+        const double c1 = __shfl_sync(0xffffffffu, u, base + M::WALL_SP);
+        const double Y = -tb.w[q] * sfac * M::wall_lane(p.P, tag, s, c1);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) ri[i] = fma(Y, bi[i], ri[i]);
+      }
+      if (active) sig_acc_row<NB>(ACC + int64_t(ein) * SN + s * NB, ri, code_first_in(code));
+      continue;
+    }
+    // face record and the two coefficient rows of species s (lanes past the
+    // end recompute the last face and never store)
+    const int64_t f = gw * FPW + grp;
+    const bool active = lane_ok && f < p.nif;
+    const int64_t fc = f < p.nif ? f : p.nif - 1;
+    const int code = __ldg(p.ifcode + fc);
+    const int2 el = __ldg(reinterpret_cast<const int2*>(p.ifel) + fc);
+    double jn[2][D], sfac, h, idi, ido;
+    {
+      static_assert(NFG == 8, "2D face record");
+      const double* g = p.ifgeo + fc * NFG;
+      double w[4];
+      if constexpr (NG == D) {
+        ld256(g, w);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          jn[0][a] = w[a];
+          jn[1][a] = w[D + a];
+        }
+      }
+      ld256(g + 4, w);
+      sfac = w[0];
+      h = w[1];
+      idi = w[2];
+      ido = w[3];
+    }
+    double ci[NB], co[NB];
+    sig_load_row<NB>(U + int64_t(el.x) * SN + s * NB, ci);
+    sig_load_row<NB>(U + int64_t(el.y) * SN + s * NB, co);
+    // traces of both sides, jump and averaged normal derivative
+    double dU[F], gav[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) {
+      double u = 0.0, v = 0.0, gi[NG], go[NG];
+#pragma unroll
+      for (int a = 0; a < NG; ++a) gi[a] = go[a] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        u = fma(tb.B[0][q][i], ci[i], u);
+        v = fma(tb.B[1][q][i], co[i], v);
+#pragma unroll
+        for (int a = 0; a < NG; ++a) {
+          gi[a] = fma(tb.G[0][q][i][a], ci[i], gi[a]);
+          go[a] = fma(tb.G[1][q][i][a], co[i], go[a]);
+        }
+      }
+      double x = gi[0], y = go[0];
+      if constexpr (NG == D) {
+        x = y = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          x = fma(jn[0][a], gi[a], x);
+          y = fma(jn[1][a], go[a], y);
+        }
+      }
+      dU[q] = u - v;
+      gav[q] = 0.5 * (x + y);
+      if constexpr (M::kConv) {
+        if (lane_ok) {
+          xch[(0 * F + q) * T::XS + s] = u;
+          xch[(1 * F + q) * T::XS + s] = v;
+          xch[(2 * F + q) * T::XS + s] = gav[q];
+        }
+      }
+    }
+    // coupled convective physics once per face point (smem transpose)
+    double fl[F];  // penalty + convective flux per point
+#pragma unroll
+    for (int q = 0; q < F; ++q) fl[q] = 0.0;
+    if constexpr (M::kConv) {
+      __syncwarp();
+      if (lane_ok) {
+        for (int q = s; q < F; q += S) {
+          const double* xq = xch + q * T::XS;
+          auto fetch = [xq](int kind, int sp) { return xq[kind * F * T::XS + sp]; };
+          M::face_point(p.P, fetch, cvs + q * NCV);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < F; ++q) {
+        double c = 0.5 * cvs[q * NCV] * dU[q];
+#pragma unroll
+        for (int k = 0; k < M::NFX; ++k)
+          if (s == k) c = fma(0.5, cvs[q * NCV + 1 + k], c);
+        fl[q] = c;
+      }
+    }
+    // penalty A_hat . n (operator.py:336-357), lifting on the needed side(s)
+    if (p.scheme == IP) {
+      const double c = p.eta / h * As;
+#pragma unroll
+      for (int q = 0; q < F; ++q) fl[q] = fma(c, dU[q], fl[q]);
+    } else if (p.scheme != BO) {
+      const bool br2 = p.scheme == BR2;
+      const bool use_in = br2 || code_minus_in(code);
+      const bool use_out = br2 || !code_minus_in(code);
+      const double fac = (p.scheme == CDG ? 4.0 : 2.0) * p.chi_e * As * (br2 ? 0.5 : 1.0) * 0.5 * sfac;
+      if (use_in) {
+        const double fi = fac * idi;
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int pp = 0; pp < F; ++pp) a = fma(tb.Pw[0][q][pp], dU[pp], a);
+          fl[q] = fma(fi, a, fl[q]);
+        }
+      }
+      if (use_out) {
+        const double fo = fac * ido;
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int pp = 0; pp < F; ++pp) a = fma(tb.Pw[1][q][pp], dU[pp], a);
+          fl[q] = fma(fo, a, fl[q]);
+        }
+      }
+    }
+    // projection onto both sides' test functions
+    double ri[NB], ro[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) ri[i] = ro[i] = 0.0;
+    const double hadj = 0.5 * p.adj * As;
+#pragma unroll
+    for (int q = 0; q < F; ++q) {
+      const double wq = tb.w[q] * sfac;
+      const double Y = wq * (As * gav[q] - fl[q]);
+      const double X = wq * hadj * dU[q];
+      double Xi[NG], Xo[NG];
+#pragma unroll
+      for (int a = 0; a < NG; ++a) {
+        Xi[a] = NG == D ? X * jn[0][a] : X;
+        Xo[a] = NG == D ? X * jn[1][a] : X;
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        double a = fma(Y, tb.B[0][q][i], ri[i]);
+        double b = fma(-Y, tb.B[1][q][i], ro[i]);
+#pragma unroll
+        for (int c = 0; c < NG; ++c) {
+          a = fma(Xi[c], tb.G[0][q][i][c], a);
+          b = fma(Xo[c], tb.G[1][q][i][c], b);
+        }
+        ri[i] = a;
+        ro[i] = b;
+      }
+    }
+    if (active) {
+      sig_acc_row<NB>(ACC + int64_t(el.x) * SN + s * NB, ri, code_first_in(code));
+      if (!code_skip_out(code))
+        sig_acc_row<NB>(ACC + int64_t(el.y) * SN + s * NB, ro, code_first_out(code));
+    }
+    __syncwarp();  // the warp's scratch is rewritten by the next group
   }
 }
 

@@ -384,6 +384,8 @@ class DiscreteOperator:
             else:
                 faces = "k_faces_tcs"
             wall = "k_faces_mma"
+        elif self.face_runs()[0]:
+            faces = wall = "k_faces_sig"     # walls ride in the last run's launch
         else:
             faces, wall = "k_faces_fast", "k_faces_fast (walls)"
         if t.dim == 3 or t.order == 3:
@@ -392,10 +394,19 @@ class DiscreteOperator:
             volume = "k_volume_fast"
         return {"faces": faces, "wall": wall, "volume": volume}
 
+    def face_runs(self) -> tuple:
+        """(signature runs, folded runs) of the 2D signature-run face kernel
+        ``k_faces_sig``; (0, 0) when the library does not use it."""
+        n, nf = ctypes.c_int64(0), ctypes.c_int64(0)
+        self._call(self.lib.tdg_face_runs, self._ctx, ctypes.byref(n), ctypes.byref(nf),
+                   what="tdg_face_runs")
+        return int(n.value), int(nf.value)
+
     def set_variant(self, generic: bool = False, no_graph: bool = False,
                     tc_volume: bool = False, face_ctas_per_sm: int = 0,
                     no_fold: bool = False, no_groups: bool = False,
-                    no_volume_classes: bool = False, no_modal: bool = False):
+                    no_volume_classes: bool = False, no_modal: bool = False,
+                    no_sig: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
         kernels directly instead of replaying its CUDA graph; ``tc_volume``
@@ -406,13 +417,15 @@ class DiscreteOperator:
         runs the one-face species-rows kernel instead of the face-group
         kernel; ``no_volume_classes`` scales the volume kernel's diffusion
         per element despite element-geometry classes; ``no_modal`` runs the
-        face-group kernel on full traces instead of the modal face space.
+        face-group kernel on full traces instead of the modal face space;
+        ``no_sig`` runs the 2D faces on ``k_faces_fast`` (tables in shared
+        memory) instead of the signature-run kernel ``k_faces_sig``.
         Defaults: fastest."""
         self._call(self.lib.tdg_set_variant, self._ctx,
                    int(bool(generic)) | (int(bool(no_graph)) << 5)
                    | (int(bool(tc_volume)) << 12) | (int(bool(no_fold)) << 13)
                    | (int(bool(no_groups)) << 14) | (int(bool(no_volume_classes)) << 15)
-                   | (int(bool(no_modal)) << 16)
+                   | (int(bool(no_modal)) << 16) | (int(bool(no_sig)) << 17)
                    | ((int(face_ctas_per_sm) & 15) << 8),
                    what="tdg_set_variant")
 

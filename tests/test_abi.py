@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
     lib.tdg_version.restype = ctypes.c_int
-    assert lib.tdg_version() == 8
+    assert lib.tdg_version() == 9
 
 
 def test_create_rejects_bad_descriptor_without_gpu():

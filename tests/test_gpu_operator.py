@@ -973,3 +973,57 @@ def test_linear_field_with_x_dependent_dirichlet_data(dim):
         import torch
         U = torch.from_numpy(fn1.coeffs).cuda()
         op.ssprk3_step(U, op.new_work(), 1e-4)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("scheme", ["cdg2", "cdg", "br2", "ip", "bo"])
+@pytest.mark.parametrize("mesh_kind", ["pow2", "thirds", "jitter"])
+def test_signature_run_face_kernel(order, scheme, mesh_kind):
+    """The 2D signature-run face kernel k_faces_sig (a run's trace / gradient
+    / lifting tables as kernel parameters, walls in the same launch) == the
+    shared-memory-table kernel k_faces_fast == the oracle (reference
+    operator.py:326-424), with Jinv n folded into the tables where a run's
+    faces all share it (power-of-two cells: exactly representable), per face
+    otherwise (cells of size 1/3, jittered vertices)."""
+    if mesh_kind == "pow2":
+        mesh = unit_square(16, 4, lengths=(4.0, 1.0))
+    elif mesh_kind == "thirds":
+        mesh = unit_square(12, 6, lengths=(4.0, 1.0))
+    else:
+        mesh = unit_square(12, 5, lengths=(4.0, 1.0), jitter=0.1, seed=5)
+    space = DGSpace(mesh, order, 6)
+    model = PlaqueModel(PlaqueParams(**AMPLIFIED))
+    op = _op(space, model, FluxScheme(scheme))
+    runs, folded = op.face_runs()
+    assert runs >= 3 and op.kernel_names()["faces"] == "k_faces_sig"
+    assert (folded == runs) if mesh_kind == "pow2" else (folded < runs)
+    U = initial_state(space, 31)
+    a = op.apply_f(U)
+    op.set_variant(no_fold=True)
+    b = op.apply_f(U)                   # Jinv n per face
+    op.set_variant(no_sig=True)
+    c = op.apply_f(U)                   # k_faces_fast
+    ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
+    assert rel_l2_per_species(space, a, c).max() <= 1e-13
+    assert rel_l2_per_species(space, b, c).max() <= 1e-13
+    assert rel_l2_per_species(space, a, ref).max() <= 1e-12
+
+
+def test_signature_run_kernel_reduced_model_and_fallback():
+    """k_faces_sig on the three-species reduced model; the Dirichlet mirror
+    models and a non-default face rule stay on the other kernels."""
+    from paper_1403_1157_b200 import ReducedModel
+    space = DGSpace(unit_square(8, 8), 2, 3)
+    model = ReducedModel()
+    op = _op(space, model, FluxScheme("cdg2"))
+    assert op.face_runs()[0] >= 3
+    U = initial_state(space, 3)
+    a = op.apply_f(U)
+    op.set_variant(no_sig=True)
+    assert rel_l2_per_species(space, a, op.apply_f(U)).max() <= 1e-13
+    ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
+    assert rel_l2_per_species(space, a, ref).max() <= 1e-12
+    heat = _op(DGSpace(unit_square(4), 2), DiffusionModel(0.7, dirichlet=0.4), FluxScheme("cdg2"))
+    assert heat.face_runs() == (0, 0)
+    over = _op(DGSpace(unit_square(4), 2, 6), PlaqueModel(), FluxScheme("cdg2"), face_degree=4)
+    assert over.face_runs() == (0, 0)
