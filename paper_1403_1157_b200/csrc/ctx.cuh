@@ -561,6 +561,21 @@ int upload_const(const OpParams& p) {
                              size_t(CL::OW) * sizeof(double), cudaMemcpyDeviceToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "face tables -> constant memory");
   }
+#if TDG_VOL_CONST
+  if constexpr (FastVol<D, K, M>::ok && VolConstLayout<D, K>::fits) {
+    if (p.nqv != Dims<D, K>::NQV) return TDG_OK;
+    using VL = VolConstLayout<D, K>;
+    auto put = [](const double* src, int off, int n) {
+      return cudaMemcpyToSymbol(c_vol_tab<D, K>, src, size_t(n) * sizeof(double),
+                                size_t(off) * sizeof(double), cudaMemcpyDeviceToDevice);
+    };
+    cudaError_t e = put(p.phi, VL::OPHI, VL::OGR - VL::OPHI);
+    if (e == cudaSuccess) e = put(p.grad, VL::OGR, VL::OW - VL::OGR);
+    if (e == cudaSuccess) e = put(p.wv, VL::OW, VL::OKS - VL::OW);
+    if (e == cudaSuccess) e = put(p.ks, VL::OKS, VL::N - VL::OKS);
+    if (e != cudaSuccess) return cuda_fail(e, "volume tables -> constant memory");
+  }
+#endif
   return TDG_OK;
 }
 

@@ -33,6 +33,13 @@
 #ifndef TDG_SIG_NARROW
 #define TDG_SIG_NARROW 0
 #endif
+// k_volume_fast: tables from constant memory instead of shared memory
+#ifndef TDG_VOL_CONST
+#define TDG_VOL_CONST 1
+#endif
+#ifndef TDG_VOL_MINB
+#define TDG_VOL_MINB 0
+#endif
 
 namespace tdg {
 
@@ -855,9 +862,29 @@ struct FastVol {
   static constexpr int TPHI = Q * NB, TGR = Q * NB * D, TKS = NSYM * NB * NB;
   static constexpr int TAB = TPHI + TGR + Q + TKS;
   static constexpr bool ok = SN <= 36 && TAB * 8 <= 24 * 1024;
-  static constexpr int MINB = 4;  // CTAs/SM the register budget targets
-  static constexpr size_t smem() { return size_t(TAB + 2 * TE * SNP) * 8; }
+  // CTAs/SM the register budget targets.  Measured with the tables in
+  // constant memory, C2 (p = 2) / 1024x256 p = 1: 4 CTAs 55.5 / 74.4 us,
+  // 5-6: 51.5 / 74.2, 7-8: 60.2 (spills) / 70.1; 3D instantiations stay at 4
+  static constexpr int MINB = TDG_VOL_MINB > 0 ? TDG_VOL_MINB : (D == 3 ? 4 : (NB <= 3 ? 8 : 5));
+  static constexpr int STAB = TDG_VOL_CONST ? 0 : TAB;  // tables staged in shared memory
+  static constexpr size_t smem() { return size_t(STAB + 2 * TE * SNP) * 8; }
 };
+
+// Volume tables (Phi, grad Phi, weights, stiffness blocks at the default
+// rule) in constant memory: reference-element data, identical for every
+// mesh of one (d, k).  The quadrature loop's table reads become
+// uniform-register operands (LDCU with a uniform index) instead of
+// shared-memory broadcasts.
+template <int D, int K>
+struct VolConstLayout {
+  using Dm = Dims<D, K>;
+  static constexpr int NSYM = D * (D + 1) / 2;
+  static constexpr int OPHI = 0, OGR = Dm::NQV * Dm::NB, OW = OGR + Dm::NQV * Dm::NB * D,
+                       OKS = OW + Dm::NQV, N = OKS + NSYM * Dm::NB * Dm::NB;
+  static constexpr bool fits = N * 8 <= 24 * 1024;
+};
+template <int D, int K>
+__constant__ double c_vol_tab[VolConstLayout<D, K>::fits ? VolConstLayout<D, K>::N : 1];
 
 template <int D, int K, class M>
 __global__ void __launch_bounds__(FastVol<D, K, M>::TE, FastVol<D, K, M>::MINB)
@@ -867,11 +894,19 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* ACC,
   constexpr int NB = T::NB, S = T::S, SN = T::SN, SNP = T::SNP, Q = T::Q, TE = T::TE;
   constexpr int NEG = T::NEG, NSYM = T::NSYM;
   extern __shared__ __align__(16) double sm[];
+#if TDG_VOL_CONST
+  using VL = VolConstLayout<D, K>;
+  const double* tphi = c_vol_tab<D, K> + VL::OPHI;
+  const double* tgr = c_vol_tab<D, K> + VL::OGR;
+  const double* tw = c_vol_tab<D, K> + VL::OW;
+  const double* tks = c_vol_tab<D, K> + VL::OKS;
+#else
   double* tphi = sm;
   double* tgr = tphi + T::TPHI;
   double* tw = tgr + T::TGR;
   double* tks = tw + Q;
-  double* bufA = sm + T::TAB;
+#endif
+  double* bufA = sm + T::STAB;
   double* bufB = bufA + TE * SNP;
   // ACC: the face-sum rows (null: no faces); ACC and U0 may alias out
   mode &= 3;
@@ -879,10 +914,12 @@ k_volume_fast(OpParams p, const double* __restrict__ U, const double* ACC,
   const int64_t e0 = int64_t(blockIdx.x) * TE;
   const int nt = int(p.ne - e0 < TE ? p.ne - e0 : TE);
 
+#if !TDG_VOL_CONST
   for (int i = tid; i < T::TPHI; i += TE) tphi[i] = p.phi[i];
   for (int i = tid; i < T::TGR; i += TE) tgr[i] = p.grad[i];
   for (int i = tid; i < Q; i += TE) tw[i] = p.wv[i];
   for (int i = tid; i < T::TKS; i += TE) tks[i] = p.ks[i];
+#endif
   // the face-sum tile and U0 are consumed after the quadrature loop: start
   // pulling them into L2 now (bulk prefetch, one thread per tile)
   if (tid <= 1) {
