@@ -328,7 +328,8 @@ def host_cpu():
     return int(cores), model
 
 
-def cpu_reference(cfg_name, scheme_name, steps, warmup, dt=None, repeats=1, cells=None):
+def cpu_reference(cfg_name, scheme_name, steps, warmup, dt=None, repeats=1, cells=None,
+                  budget_s=None):
     """Time the CPU oracle port on a bounded sample of the config, under
     the reference's own scaling protocol (analysis.scaling_study,
     reference analysis.py:211-242: BLAS pinned to one thread, one worker
@@ -355,12 +356,19 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, dt=None, repeats=1, cell
         U = U0.copy()
         for _ in range(warmup):
             U = step(U)
-        for _ in range(max(1, repeats)):
+        done, spent = 0, 0.0
+        while done < max(1, repeats):
             tic = time.perf_counter()
             for _ in range(steps):
                 U = step(U)
             el = time.perf_counter() - tic
             best = el if best is None else min(best, el)
+            done += 1
+            spent += el
+            # best of `repeats`, cut short when another pass would push the
+            # whole timing leg past the budget
+            if budget_s is not None and spent + el > budget_s:
+                break
     return space.n_dofs * 3 * steps / best, best, cfg.cells, space.n_dofs, cores, cpu_model
 
 
@@ -369,11 +377,14 @@ def cpu_reference(cfg_name, scheme_name, steps, warmup, dt=None, repeats=1, cell
 def run_reference_arm(args, rank):
     if rank != 0:
         return
-    steps = max(1, args.steps if args.config != "c5" else 1)
-    warm = min(args.warmup, 1)
+    # the driver's --steps K --warmup W, as given: each step is one SSP-RK3
+    # step of the bounded sample (a few seconds on 16 cores at C5), best of
+    # up to 3 passes within about two minutes
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
     cells = tuple(int(c) for c in args.cells.split("x")) if args.cells else None
     val, el, scells, ndofs, cores, cpu_model = cpu_reference(
-        args.config, args.scheme, steps, warm, repeats=3, cells=cells)
+        args.config, args.scheme, steps, warm, repeats=3, cells=cells, budget_s=120.0)
     from paper_1403_1157_b200.configs import CONFIGS
     cfg = scaled_config(CONFIGS[args.config], 1, "strong", cells)
     where = ("the full " + args.config + " mesh" if tuple(scells) == tuple(cfg.cells) else
@@ -385,14 +396,19 @@ def run_reference_arm(args, rank):
         "ms_per_step": el / steps * 1e3, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian bumps, L2-projected)",
-        "config": {"workload": cfg.description
-                   + f", {args.scheme}, SSP-RK3 steps (3 f-evals each)",
-                   "n_dofs_sample": ndofs},
+        # the same workload string as the native arm's line; the CPU arm times
+        # a bounded sample of it (cpu_baseline.sample)
+        "config": {"workload": cfg.description + f", {args.scheme}, SSP-RK3 "
+                   "steps (3 fused f-evals + stage updates each)",
+                   "n_elements": int(np.prod(cfg.cells)) * (2 if cfg.dim == 2 else 6),
+                   "n_dofs_sample": ndofs,
+                   "parallelism": f"{cores} host threads (reference CPU path)"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
                          "cpu_model": cpu_model,
                          "sample": f"{steps} SSP-RK3 step(s) of {where}, numpy oracle port "
                                    f"of the reference (oracle/), {cores} worker threads "
-                                   f"(physical cores), BLAS pinned to 1 thread, best of 3"},
+                                   f"(physical cores), BLAS pinned to 1 thread, best of up "
+                                   f"to 3 passes"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
