@@ -351,8 +351,10 @@ TDG_API int tdg_jv_diff(double* r, const double* GU, const double* eps, int64_t 
  * where the one-thread-per-element kernel does not fit); bits 8-11: CTAs
  * per SM of the 2D register-resident face kernel's grid-stride grid (0 =
  * default, 15 = uncapped, one face group per warp); bit 17: the 2D faces on
- * the shared-memory-table kernel instead of the signature-run kernel.  0
- * (default) lets the library pick the fastest compiled-in kernels. */
+ * the shared-memory-table kernel instead of the signature-run kernel; bit 18:
+ * the cp.async-staged signature-run kernel on states of any size (default:
+ * only states larger than half the L2).  0 (default) lets the library pick
+ * the fastest compiled-in kernels. */
 TDG_API int tdg_set_variant(tdg_ctx* ctx, int variant);
 
 /* 2D signature runs (k_faces_sig): tdg_create cuts the interior faces into

@@ -173,6 +173,9 @@ int tdg_create(const tdg_desc* desc, tdg_ctx** out) {
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
       ctx->num_sms = sms;
+    int l2 = 0;
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) == cudaSuccess && l2 > 0)
+      ctx->l2_bytes = size_t(l2);
     cudaGetLastError();
   }
   int rc = impl.configure(d.nq_vol);
@@ -541,6 +544,7 @@ int tdg_set_variant(tdg_ctx* ctx, int variant) {
   ctx->no_vcls = ((variant >> 15) & 1) != 0;    // bit 15: no volume element classes
   ctx->no_modal = ((variant >> 16) & 1) != 0;   // bit 16: face groups on full traces
   ctx->no_sig = ((variant >> 17) & 1) != 0;     // bit 17: k_faces_fast despite signature runs
+  ctx->sig_async = ((variant >> 18) & 1) != 0;  // bit 18: cp.async-staged k_faces_sig at any size
   // bits 8-11: CTAs per SM of the 2D face kernel's grid-stride grid (0 =
   // the resident count; 15 = one group per warp, no grid cap)
   const int f = (variant >> 8) & 15;

@@ -97,12 +97,14 @@ struct tdg_ctx {
   bool no_modal = false;       // testing: face groups on full traces despite modal tables
   bool point_data = false;     // boundary point data: the generic face kernels
   bool no_sig = false;         // testing: k_faces_fast despite signature runs
+  bool sig_async = false;      // testing: the cp.async-staged k_faces_sig on small states too
   // 2D: signature runs over the interior faces (sorted by f0) and host
   // copies of the face tables their kernel parameters are built from;
   // empty when the faces are not sorted into few runs
   std::vector<tdg::SigRun> sig_runs;
   std::vector<double> h_fB, h_fG, h_fPw, h_fw;
   int num_sms = 148;
+  size_t l2_bytes = size_t(126) << 20;
   int face_ctas_per_sm = 0;    // 2D face-kernel grid cap per SM: 0 = resident CTAs, -1 = none
   // host-data stepping: copies in kChunks element chunks on two streams
   // per direction (created with the context: no call allocates later)
@@ -410,14 +412,28 @@ void run_segment(tdg_ctx* ctx, const Segment& sg, const double* U, double* acc, 
             }
             std::memcpy(tb.w, ctx->h_fw.data(), sizeof(tb.w));
           };
+          // states larger than the L2 (C3): the cp.async-staged variant
+          // hides the record -> rows round trips to DRAM (C3 faces 2.22 ->
+          // 1.91 ms); on L2-resident states (C2) it is 2% slower
+          const bool async_ = TDG_SIG_FORCE_ASYNC >= 0
+                                  ? TDG_SIG_FORCE_ASYNC != 0
+                                  : ctx->sig_async ||
+                                    size_t(ctx->d.n_elements + ctx->d.n_ghost) * SN_of<M, D, K>() * 8 >
+                                        ctx->l2_bytes / 2;
           if (rr.fold && !ctx->no_fold) {
             FaceSigTab<D, K, 1> tb;
             fill(tb, true);
-            k_faces_sig<D, K, M, 1><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+            if (async_)
+              k_faces_sig_async<D, K, M, 1><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+            else
+              k_faces_sig<D, K, M, 1><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
           } else {
             FaceSigTab<D, K, D> tb;
             fill(tb, false);
-            k_faces_sig<D, K, M, D><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+            if (async_)
+              k_faces_sig_async<D, K, M, D><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
+            else
+              k_faces_sig<D, K, M, D><<<unsigned(grid), 128, 0, st>>>(r, tb, U, acc, groups, wgroups);
           }
         }
         return;

@@ -406,7 +406,7 @@ class DiscreteOperator:
                     tc_volume: bool = False, face_ctas_per_sm: int = 0,
                     no_fold: bool = False, no_groups: bool = False,
                     no_volume_classes: bool = False, no_modal: bool = False,
-                    no_sig: bool = False):
+                    no_sig: bool = False, sig_async: bool = False):
         """Kernel selection for testing / A-B timing: ``generic`` pins the
         CTA-staged generic kernels; ``no_graph`` launches ``ssprk3_step``'s
         kernels directly instead of replaying its CUDA graph; ``tc_volume``
@@ -419,13 +419,16 @@ class DiscreteOperator:
         per element despite element-geometry classes; ``no_modal`` runs the
         face-group kernel on full traces instead of the modal face space;
         ``no_sig`` runs the 2D faces on ``k_faces_fast`` (tables in shared
-        memory) instead of the signature-run kernel ``k_faces_sig``.
+        memory) instead of the signature-run kernel ``k_faces_sig``;
+        ``sig_async`` runs its cp.async-staged variant (the default only for
+        states larger than half the L2) at any size.
         Defaults: fastest."""
         self._call(self.lib.tdg_set_variant, self._ctx,
                    int(bool(generic)) | (int(bool(no_graph)) << 5)
                    | (int(bool(tc_volume)) << 12) | (int(bool(no_fold)) << 13)
                    | (int(bool(no_groups)) << 14) | (int(bool(no_volume_classes)) << 15)
                    | (int(bool(no_modal)) << 16) | (int(bool(no_sig)) << 17)
+                   | (int(bool(sig_async)) << 18)
                    | ((int(face_ctas_per_sm) & 15) << 8),
                    what="tdg_set_variant")
 

@@ -1001,6 +1001,10 @@ def test_signature_run_face_kernel(order, scheme, mesh_kind):
     a = op.apply_f(U)
     op.set_variant(no_fold=True)
     b = op.apply_f(U)                   # Jinv n per face
+    op.set_variant(sig_async=True)
+    assert np.array_equal(op.apply_f(U), a)     # cp.async-staged operands: same arithmetic
+    op.set_variant(sig_async=True, no_fold=True)
+    assert np.array_equal(op.apply_f(U), b)
     op.set_variant(no_sig=True)
     c = op.apply_f(U)                   # k_faces_fast
     ref = OracleOperator(space, model, FluxScheme(scheme)).apply_f(U)
