@@ -1,6 +1,6 @@
-"""A/B of the 2D face kernels (k_faces_sig vs k_faces_fast): parity of one
-application against the oracle on a small mesh and between the two kernels
-at full size, then ms per application per kernel class.
+"""A/B of the 2D face kernels (k_faces_sig vs k_faces_fast): ms per
+application per kernel class and the difference between the two kernels at
+size (parity against the oracle: tests/test_gpu_operator.py).
 usage: python tools/face2d_bench.py [nx ny] [k] [reps] [jitter]"""
 import os
 import sys
@@ -11,7 +11,6 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1403_1157_b200 import (DGSpace, FluxScheme, PlaqueModel, PlaqueParams,  # noqa: E402
                                   unit_square)
-from paper_1403_1157_b200.fields import initial_state  # noqa: E402
 from paper_1403_1157_b200.operator import DiscreteOperator  # noqa: E402
 from paper_1403_1157_b200.roofline import apply_flops  # noqa: E402
 
@@ -30,20 +29,6 @@ def mesh(nx, ny):
         kw.update(jitter=jit, seed=3)
     return unit_square(nx, ny, **kw)
 
-
-if os.environ.get("TDG_ORACLE", "1") == "1":
-    from oracle import OracleOperator
-    for sch in ("cdg2", "cdg", "br2", "ip", "bo"):
-        sp = DGSpace(mesh(12, 6), k, 6)
-        U0 = initial_state(sp, seed=1)
-        op = DiscreteOperator(sp, model, FluxScheme(sch))
-        ref = OracleOperator(sp, model, FluxScheme(sch)).apply(U0)
-        r1 = op.apply(U0)
-        op.set_variant(no_sig=True)
-        r0 = op.apply(U0)
-        sc = np.abs(ref).max()
-        print(f"{sch:5s} k={k} sig vs oracle {np.abs(r1 - ref).max() / sc:.2e}  fast vs oracle "
-              f"{np.abs(r0 - ref).max() / sc:.2e}")
 
 space = DGSpace(mesh(nx, ny), k, 6)
 op = DiscreteOperator(space, model, FluxScheme("cdg2"))
