@@ -50,11 +50,14 @@ TDG_SIG_KERNEL(const __grid_constant__ OpParams p, const __grid_constant__ FaceS
     cp_row(rst + T::RHALF, U + int64_t(e.y) * SN + s * NB);
   };
   auto issue_geo = [&](int64_t fc) {
-    if (lane_ok && s < NFG / 2)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
-                       unsigned(__cvta_generic_to_shared(gst + 2 * s))),
-                   "l"(p.ifgeo + fc * NFG + 2 * s)
-                   : "memory");
+    // the face's S lanes share its record: lane s copies 16-byte pieces
+    // s, s + S, ... (S may be smaller than the piece count)
+    if (lane_ok)
+      for (int k = s; k < NFG / 2; k += S)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                         unsigned(__cvta_generic_to_shared(gst + 2 * k))),
+                     "l"(p.ifgeo + fc * NFG + 2 * k)
+                     : "memory");
   };
   auto face_of = [&](int64_t gw) {
     const int64_t f = gw * FPW + grp;

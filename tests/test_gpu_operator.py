@@ -1023,6 +1023,8 @@ def test_signature_run_kernel_reduced_model_and_fallback():
     assert op.face_runs()[0] >= 3
     U = initial_state(space, 3)
     a = op.apply_f(U)
+    op.set_variant(sig_async=True)      # three lanes per face copy the 64-byte record
+    assert np.array_equal(op.apply_f(U), a)
     op.set_variant(no_sig=True)
     assert rel_l2_per_species(space, a, op.apply_f(U)).max() <= 1e-13
     ref = OracleOperator(space, model, FluxScheme("cdg2")).apply_f(U)
