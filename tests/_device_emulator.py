@@ -33,7 +33,11 @@ def _heav(s, eps):
 
 
 class DeviceEmulator:
-    def __init__(self, tables, model, scheme, chi_e, adj, eta):
+    def __init__(self, tables, model, scheme, chi_e, adj, eta, normal_after=False):
+        # normal_after: the signature-run kernel's order (k_faces_sig): the
+        # normal derivative after the contraction, jn . (G c), and the adjoint
+        # term projected with (X jn) . G instead of a per-face d_n phi table
+        self.normal_after = normal_after
         self.t, self.model, self.scheme = tables, model, scheme
         self.chi_e, self.adj, self.eta = chi_e, adj, eta
         self.A = model.diffusivity()
@@ -153,6 +157,9 @@ class DeviceEmulator:
             ci = U[ein]
             ui = ci @ t.face_B[tin].T          # (S, F)
             gi = ci @ dpi.T
+            after = self.normal_after and not mirror
+            if after:
+                gi = np.einsum("sqa,a->sq", np.einsum("si,qia->sqa", ci, t.face_G[tin]), jin)
             if mirror:
                 gval = self.P[:S]
                 uo = 2 * gval[:, None] - ui
@@ -162,6 +169,9 @@ class DeviceEmulator:
                 co = U[eout]
                 uo = co @ t.face_B[tout].T
                 go = co @ dpo.T
+                if after:
+                    go = np.einsum("sqa,a->sq",
+                                   np.einsum("si,qia->sqa", co, t.face_G[tout]), jout)
             dU = ui - uo
             gn = 0.5 * (gi + go)
             qv = np.zeros((F, S))
@@ -184,6 +194,12 @@ class DeviceEmulator:
             wq = t.face_w * sfac
             Y = wq[None, :] * (self.A[:, None] * gn - qv.T)
             X = wq[None, :] * 0.5 * self.adj * self.A[:, None] * dU
+            if after:
+                ri = Y @ t.face_B[tin] + np.einsum("sqa,qia->si", X[:, :, None] * jin,
+                                                   t.face_G[tin])
+                ro = -Y @ t.face_B[tout] + np.einsum("sqa,qia->si", X[:, :, None] * jout,
+                                                     t.face_G[tout])
+                return ri, ro
             ri = Y @ t.face_B[tin] + X @ dpi
             ro = None if mirror else -Y @ t.face_B[tout] + X @ dpo
             return ri, ro

@@ -14,9 +14,9 @@ from _device_emulator import DeviceEmulator
 from test_oracle_golden import _golden_names
 
 
-def _emulate(space, model, scheme, U):
+def _emulate(space, model, scheme, U, **kw):
     t = build_tables(space, model, scheme)
-    em = DeviceEmulator(t, model, scheme.id, *scheme_constants(space, scheme))
+    em = DeviceEmulator(t, model, scheme.id, *scheme_constants(space, scheme), **kw)
     return em.apply(U)
 
 
@@ -24,6 +24,19 @@ def _emulate(space, model, scheme, U):
 def test_emulated_kernels_match_reference(golden, name):
     space, model, scheme, U, R, _ = operator_case(golden, name)
     got = _emulate(space, model, scheme, U)
+    assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
+
+
+@pytest.mark.parametrize("name", [n for n in _golden_names()
+                                  if "_p0_" not in n and n.startswith(("sq", "jit", "rect"))])
+def test_emulated_signature_run_order_matches_reference(golden, name):
+    """The 2D signature-run kernel's operation order (csrc/kernels_sig_body.cuh:
+    normal derivative after the contraction, adjoint term projected with
+    (X jn) . grad phi) against the same golden outputs."""
+    space, model, scheme, U, R, _ = operator_case(golden, name)
+    if space.mesh.dim != 2:
+        pytest.skip("2D kernel")
+    got = _emulate(space, model, scheme, U, normal_after=True)
     assert np.abs(got - R).max() <= 1e-12 * np.abs(R).max()
 
 
