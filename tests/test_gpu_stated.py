@@ -172,3 +172,43 @@ def test_integrate_hands_numpy_to_callbacks():
     res = integrate(op, U0, 0.0, math.inf, 0.01, order=3, n_steps=3, callback=record)
     assert len(seen) == 3 and isinstance(res.U, np.ndarray)
     assert np.allclose(seen[-1], space.function(res.U).species_totals(), rtol=0, atol=0)
+
+
+def test_c2_full_size_against_oracle_port():
+    """Full-size C2 (512x128 cells, p=2, 4.7M DoFs): SSP-RK3 steps on the
+    device against the same steps of the pinned CPU oracle port
+    (oracle/taxis_oracle.py, checked against the reference's golden outputs
+    in tests/test_oracle_golden.py; reference operator.py:253-288).  20 steps
+    by default (about half a minute of CPU work on 16 cores); TDG_LONG=1
+    runs the config's stated 100 steps (three minutes: 1 passed in 185.7 s
+    on the B200 box, profiles/r02_c2_full_100_steps.log)."""
+    import os
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleOperator
+    from paper_1403_1157_b200.fields import initial_state
+    space = DGSpace(unit_square(512, 128, lengths=(4.0, 1.0)), 2, 6)
+    model, scheme = PlaqueModel(), FluxScheme("cdg2")
+    U0 = initial_state(space, 2)
+    dt = 1.43e-5                      # SURVEY 8(d): 0.8 * 2.51 / rho at C2
+    steps = 100 if os.environ.get("TDG_LONG") == "1" else 20
+    op = _op(space, model, scheme)
+    U = torch.from_numpy(U0).cuda()
+    work = op.new_work()
+    for _ in range(steps):
+        op.ssprk3_step(U, work, dt)
+    got = U.cpu().numpy()
+    try:
+        import psutil
+        cores = psutil.cpu_count(logical=False) or os.cpu_count() or 1
+    except ImportError:
+        cores = os.cpu_count() or 1
+    ref_op = OracleOperator(space, model, scheme, nthreads=max(1, min(cores, 32)))
+    V = U0.copy()
+    with threadpool_limits(1):
+        for _ in range(steps):
+            V1 = V + dt * ref_op.apply_f(V)
+            V2 = 0.75 * V + 0.25 * (V1 + dt * ref_op.apply_f(V1))
+            V = V / 3.0 + (2.0 / 3.0) * (V2 + dt * ref_op.apply_f(V2))
+    err = rel_l2_per_species(space, got, V)
+    assert err.max() <= TOL_L2, err
+    assert rel_l2_per_species(space, U0, V).max() > 1e3 * TOL_L2
