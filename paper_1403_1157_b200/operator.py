@@ -209,6 +209,9 @@ class DiscreteOperator:
             seg_ptr=hptr(self._host["seg_ptr"]))
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
+            # tdg_create reads some device tables back (signature runs) and copies others
+            # to constant memory on the default stream: the uploads above must be done
+            torch.cuda.current_stream(self.device).synchronize()
             _native.check(self.lib.tdg_create(ctypes.byref(desc), ctypes.byref(handle)),
                           "tdg_create")
             self._dev_index = torch.cuda.current_device()
