@@ -219,6 +219,13 @@ typedef struct tdg_ctx tdg_ctx;
 TDG_API int tdg_version(void);
 TDG_API const char* tdg_last_error(void);
 
+/* Builds the context for one operator (reference DiscreteOperator.__init__,
+ * operator.py:85-140: tables, face SoA, K- flags).  The device arrays of the
+ * descriptor must be complete when this is called (no upload pending on
+ * another stream): tdg_create copies reference-element tables to constant
+ * memory and, for the 2D signature-run kernel, reads the face code words,
+ * face tables and face records back once, on the default stream.  It creates
+ * every stream, event and workspace the later calls use. */
 TDG_API int tdg_create(const tdg_desc* desc, tdg_ctx** out);
 TDG_API int tdg_destroy(tdg_ctx* ctx);
 
