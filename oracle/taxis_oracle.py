@@ -183,7 +183,8 @@ def _physics(model):
 class OracleOperator:
     """CPU restatement of ``DiscreteOperator`` (operator.py:77-458).
 
-    ``nthreads`` > 1 splits elements into contiguous parts; each worker
+    ``nthreads`` > 1 splits the elements by recursive coordinate bisection
+    like the reference (mesh.py:432-456); each worker
     assembles the volume terms of its elements and every term of the
     faces whose inside element it owns into a private buffer, merged in
     part order (the reference's owner-computes scheme,
@@ -243,9 +244,11 @@ class OracleOperator:
         interior = fe[:, 1] >= 0
         P = self.nthreads
         ne = m.n_elements
-        self.parts = [np.arange(ne * p // P, ne * (p + 1) // P)
-                      for p in range(P)]
-        owner = np.minimum((fe[:, 0] * P) // max(ne, 1), P - 1)
+        # the reference's partition: recursive coordinate bisection of the
+        # element centroids (mesh.py:432-456), one part per worker
+        part_of = m.partition(P) if P > 1 else np.zeros(ne, dtype=np.int64)
+        self.parts = [np.flatnonzero(part_of == p) for p in range(P)]
+        owner = part_of[fe[:, 0]]
         key = np.where(interior,
                        ((fl[:, 0] * 8 + fp[:, 0]) * 8 + fl[:, 1]) * 8 + fp[:, 1],
                        100000 + (fl[:, 0] * 8 + fp[:, 0]) * 8
