@@ -388,7 +388,12 @@ class DiscreteOperator:
                 faces = "k_faces_tcs"
             wall = "k_faces_mma"
         elif self.face_runs()[0]:
-            faces = wall = "k_faces_sig"     # walls ride in the last run's launch
+            # walls ride in the last run's launch; states larger than half the
+            # L2 take the cp.async-staged variant (ctx.cuh run_segment)
+            import torch
+            l2 = torch.cuda.get_device_properties(self.device).L2_cache_size
+            rows = self.space.mesh.n_elements * t.n_species * t.nb * 8
+            faces = wall = "k_faces_sig_async" if rows > l2 // 2 else "k_faces_sig"
         else:
             faces, wall = "k_faces_fast", "k_faces_fast (walls)"
         if t.dim == 3 or t.order == 3:
