@@ -576,6 +576,15 @@ def run_native_arm(args, rank, world, local):
                       "SSP-RK3 steps changed by steps * dt * nu2 * sigma * |GAMMA1_IN| "
                       "(reference tests/test_operator.py:101-110), device totals"}
     log(f"lipid budget check: rel err {checks['rel_err']}")
+    if slab is None and stepper._work is not None:
+        # bitwise run-to-run reproducibility at full size (the reference's
+        # determinism contract, tests/test_operator.py:113-119): one fused
+        # stage evaluated twice into the two work vectors
+        W = stepper._work
+        op.rk_stage(U, U, W[0], 0.75, 0.25, 0.25 * dt)
+        op.rk_stage(U, U, W[1], 0.75, 0.25, 0.25 * dt)
+        checks["stage_bitwise_reproducible"] = bool(torch.equal(W[0], W[1]))
+        log(f"stage reproducibility check: {checks['stage_bitwise_reproducible']}")
     ms_prof = sum(a.elapsed_time(b) for a, b in pevs)
     total_dofs = n_dofs
     if dist_on:  # whole-job DoFs (owned rows of every rank)
